@@ -1,0 +1,185 @@
+/*
+ * lnorm.h -- C ABI of the B200-native exhaustive Gray-code search for the
+ * L_1, L_marg and L_d norms of an integer matrix (arXiv 2503.21596).
+ *
+ * Citations are to /root/reference/PAPER.md lines ("P:n") as recorded in
+ * DESIGN.md (the reference tree is not shipped).
+ *
+ *   L_1(M)    = max_{a in {+-1}^n}          sum_y | sum_x M_xy a_x |              P:58-61, Eq. (1)
+ *   L_marg(M) = max_{a_0 = +1, a_x = +-1}   sum_x M_x0 a_x + sum_{y>=1} |sum_x M_xy a_x|   P:64-68, Eq. (2)
+ *   L_d(M)    = max_{a in {0..d-1}^n}       sum_{g} sum_y | sum_{x: a_x = g} M_xy |  P:95-107, Eqs. (6)-(7)
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  M       caller-owned, read-only, row-major contiguous n*m int32 (host memory
+ *          unless the name says _device).  Nothing is retained after return.
+ *          Marginal layout (Eq. 2): column 0 is summed signed, row 0 is the
+ *          strategy entry fixed to +1; M[0][0] is the constant term.
+ *  d       d = 1 selects L_1 (L_1 is NOT L_d at d = 1); d >= 2 selects L_d.
+ *          Supported: 1 <= d <= 8 (L_d for d > n equals L_n; handled exactly).
+ *  with_marginals  0 or 1; 1 is legal only with d = 1 (selects L_marg).
+ *  value   caller-allocated int64: the exact norm (may be negative for L_marg).
+ *  argmax  caller-allocated int8[n] (may be NULL), in the input's row order:
+ *          d = 1: entries +1/-1 with entry 0 = +1; d >= 2: labels 0..d-1 in
+ *          restricted-growth form (entry 0 = 0, new labels appear in order).
+ *          Canonical choice (R2): the lexicographically smallest
+ *          optimal strategy (row 0 most significant, +1 before -1, labels in
+ *          numeric order).  Exception (R6): for L_1/L_marg with
+ *          n > m the search runs on M^T and argmax is x_i = sgn((M y*)_i)
+ *          (sgn 0 = +1, then x_0 normalised to +1), which attains the value
+ *          but need not be lexicographically smallest.
+ *  Errors  every function returns an lnorm_status; on error the outputs are
+ *          untouched.  LNORM_EINVAL: null pointer, n < 1, m < 1, d out of
+ *          range, bad flag combination.  LNORM_EOVERFLOW: sum |M_ij| > 2^31-1
+ *          (the int32 column sums and values could overflow; P:259 integer
+ *          exactness).  LNORM_ETOOLARGE: the search space does not fit the
+ *          64-bit word index (P:261 / P:336-340: more than 63 enumerated rows
+ *          after orientation for d = 1, or d^(n-1) >= 2^63 for d >= 2), or the
+ *          problem exceeds the kernels' column limit (m > 1024 after
+ *          orientation).  LNORM_ENODEV / ECUDA / ENCCL / ENOMEM: runtime.
+ *  Threads re-entrant per device (an internal per-device context is guarded by
+ *          a mutex); all calls synchronise before returning.
+ *
+ * Every step of the search runs in the library's sm_100a kernels; there is no
+ * CPU fallback (no device => LNORM_ENODEV).
+ */
+#ifndef LNORM_H
+#define LNORM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  LNORM_OK = 0,
+  LNORM_EINVAL = 1,
+  LNORM_EOVERFLOW = 2,
+  LNORM_ETOOLARGE = 3,
+  LNORM_ENODEV = 4,
+  LNORM_ECUDA = 5,
+  LNORM_ENCCL = 6,
+  LNORM_ENOMEM = 7
+} lnorm_status;
+
+/* Human-readable name of a status code (static storage). */
+const char* lnorm_status_string(int status);
+
+/* ABI version: (major << 16) | minor. */
+int32_t lnorm_version(void);
+
+/*
+ * Exact norm of M on the current CUDA device (per-worker maxima of the
+ * Gray-code walk compared at the end).  Host buffers; the H2D copy of M, the
+ * walk, the reduction and the argmax recovery all happen inside this call.
+ */
+int lnorm_compute(const int32_t* M, int32_t n, int32_t m, int32_t d, int32_t with_marginals,
+                  int64_t* value, int8_t* argmax);
+
+/*
+ * Same as lnorm_compute but M is a DEVICE pointer on the current device
+ * (row-major n*m int32) and work is enqueued on `cuda_stream` (a
+ * cudaStream_t; NULL = the library's internal stream).  Used to time the
+ * search with its input already resident in HBM.  Synchronises before return.
+ */
+int lnorm_compute_device(const int32_t* M_device, int32_t n, int32_t m, int32_t d,
+                         int32_t with_marginals, void* cuda_stream,
+                         int64_t* value, int8_t* argmax);
+
+/*
+ * One process, several GPUs (single-node, NVLink/NVSwitch): the unit range is
+ * split across devices by Algorithm 1, every device walks its
+ * slice, one ncclAllReduce(max) on an 8-byte key combines them and every
+ * device recovers the same argmax.  device_ids: NULL = 0..num_devices-1.
+ * Communicators are created and destroyed inside the call.
+ */
+int lnorm_compute_multi(const int32_t* M, int32_t n, int32_t m, int32_t d, int32_t with_marginals,
+                        int32_t num_devices, const int32_t* device_ids,
+                        int64_t* value, int8_t* argmax);
+
+/*
+ * One rank per GPU (torchrun): a communicator handle owned by the library.
+ * lnorm_comm_unique_id writes a 128-byte ncclUniqueId (rank 0 calls it and
+ * broadcasts the bytes, e.g. through torch.distributed); every rank then calls
+ * lnorm_comm_create with its rank, the world size and its CUDA device.
+ * lnorm_compute_rank: rank r walks its Algorithm-1 slice of the units, the
+ * 8-byte key is all-reduced (ncclMax) on the compute stream and every rank
+ * returns the same value and argmax.  world == 1 with comm == NULL is allowed
+ * (no collective).  Host buffer M (replicated on every rank).
+ */
+typedef struct lnorm_comm lnorm_comm;
+int lnorm_comm_unique_id(uint8_t id_out[128]);
+int lnorm_comm_create(const uint8_t id[128], int32_t rank, int32_t world, int32_t device,
+                      lnorm_comm** comm_out);
+int lnorm_comm_destroy(lnorm_comm* comm);
+int lnorm_compute_rank(lnorm_comm* comm, const int32_t* M, int32_t n, int32_t m, int32_t d,
+                       int32_t with_marginals, int64_t* value, int8_t* argmax);
+/* lnorm_compute_rank with M already resident on the rank's device (row-major n*m int32). */
+int lnorm_compute_rank_device(lnorm_comm* comm, const int32_t* M_device, int32_t n, int32_t m, int32_t d,
+                              int32_t with_marginals, int64_t* value, int8_t* argmax);
+
+/*
+ * Test hook for sampled parity at sizes the oracle cannot finish: for each of
+ * `count` prefixes (int8[count][nfixed], row-major; digits 0/1 meaning +1/-1
+ * for d = 1, labels 0..d-1 for d >= 2; for L_marg digit 0 of every prefix
+ * must be 0) return in out[i] the maximum value over all strategies whose
+ * rows 0..nfixed-1 equal prefix i and whose remaining rows are free.  No
+ * orientation is applied.  Runs the same walk kernels as lnorm_compute.
+ * Requires 1 <= nfixed <= n.
+ */
+int lnorm_prefix_maxima(const int32_t* M, int32_t n, int32_t m, int32_t d, int32_t with_marginals,
+                        int32_t nfixed, const int8_t* prefixes, int64_t count, int64_t* out);
+
+/*
+ * Test hook: the device walk of ONE unit, step by step.  Rows 0..nfixed-1 are
+ * fixed to `prefix` (digits as above); the remaining s = n - nfixed rows are
+ * walked in reflected Gray order (binary for d = 1 and d = 2, d-ary
+ * otherwise; suffix digit i <-> row n-1-i) starting from all-zero digits.
+ * values[w] receives the value after step w (w = 0 .. base^s - 1) and, if
+ * digits is non-NULL, digits[w*n + x] the strategy digit of row x at step w.
+ * base^s must be <= max_steps.
+ */
+int lnorm_walk_trace(const int32_t* M, int32_t n, int32_t m, int32_t d, int32_t with_marginals,
+                     int32_t nfixed, const int8_t* prefix, int64_t max_steps,
+                     int64_t* values, int8_t* digits);
+
+/*
+ * Host-side reflected Gray-code helpers -- the same __host__ __device__ code the
+ * kernels use.  lnorm_gray_digit: digit i of word j of the d-ary reflected
+ * Gray code (d = 2: Eq. 8; d >= 2: Eqs. 13-15).
+ * lnorm_gray_change: for j >= 1 the digit that differs between words j-1 and
+ * j (Eq. 9 / Eq. 17) and its old/new values.
+ */
+int32_t lnorm_gray_digit(int32_t d, int32_t i, uint64_t j);
+int lnorm_gray_change(int32_t d, uint64_t j, int32_t* digit, int32_t* from, int32_t* to);
+
+/*
+ * Algorithm 1: inclusive word range [j_min, j_max] of worker t out
+ * of T over C words; an empty range has j_max = j_min - 1.
+ */
+int lnorm_partition(uint64_t C, int64_t T, int64_t t, int64_t* j_min, int64_t* j_max);
+
+/* Statistics of the last successful compute call on the calling thread. */
+typedef struct {
+  int32_t rows, cols;          /* enumerated rows / columns after orientation */
+  int32_t transposed;          /* 1 if M^T was searched */
+  int32_t prefix_digits;       /* k: rows 1..k form the unit prefix */
+  int32_t suffix_digits;       /* s: rows k+1..r-1 are walked per unit */
+  int32_t d;                   /* 1 (+-1 strategies) or the label count */
+  int64_t units;               /* units in this call (this rank's slice for _rank) */
+  int64_t units_total;         /* units over all ranks */
+  double  steps;               /* Gray steps (strategies) walked by this call */
+  double  column_updates;      /* algorithmic column updates (c per step, 2c for d >= 3) */
+  double  walk_ms;             /* CUDA-event time of the walk kernel(s) */
+  double  total_ms;            /* CUDA-event time from first H2D to last D2H */
+  int32_t launches;            /* kernels launched by the call */
+  int32_t variant;             /* kernel variant id */
+  int32_t block_threads, grid_blocks;
+} lnorm_stats;
+int lnorm_last_stats(lnorm_stats* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LNORM_H */

@@ -1,1 +1,269 @@
-"""B200-native exhaustive Gray-code search for the L_d norms of arXiv 2503.21596."""
+"""B200-native exhaustive Gray-code search for the L_d norms of arXiv 2503.21596.
+
+Thin ctypes binding over the C ABI of ``liblnorm.so`` (declared in
+``include/lnorm.h``): argument marshalling only -- every step of the search
+runs in the library's sm_100a kernels.  If the library is missing or no CUDA
+device is present the calls raise; there is no CPU fallback.
+
+    value, argmax = compute(M, d=1)                 # L_1      (Eq. 1)
+    value, argmax = compute(M, d=1, with_marginals=True)   # L_marg (Eq. 2)
+    value, argmax = compute(M, d=3)                 # L_3      (Eq. 6)
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+__all__ = [
+    "LNormError", "load", "compute", "compute_device", "compute_multi", "Comm", "prefix_maxima",
+    "walk_trace", "gray_digit", "gray_change", "partition", "last_stats", "status_string", "SYMBOLS",
+]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liblnorm.so")
+
+# every function include/lnorm.h declares (checked by tests/test_abi.py)
+SYMBOLS = [
+    "lnorm_status_string", "lnorm_version", "lnorm_compute", "lnorm_compute_device", "lnorm_compute_multi",
+    "lnorm_comm_unique_id", "lnorm_comm_create", "lnorm_comm_destroy", "lnorm_compute_rank",
+    "lnorm_compute_rank_device",
+    "lnorm_prefix_maxima", "lnorm_walk_trace", "lnorm_gray_digit", "lnorm_gray_change", "lnorm_partition",
+    "lnorm_last_stats",
+]
+
+STATUS = {0: "OK", 1: "EINVAL", 2: "EOVERFLOW", 3: "ETOOLARGE", 4: "ENODEV", 5: "ECUDA", 6: "ENCCL", 7: "ENOMEM"}
+
+
+class LNormError(RuntimeError):
+    def __init__(self, status: int, what: str = ""):
+        self.status = status
+        self.name = STATUS.get(status, str(status))
+        super().__init__(f"{what}: {self.name} ({_status_text(status)})")
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [
+        ("rows", ctypes.c_int32), ("cols", ctypes.c_int32), ("transposed", ctypes.c_int32),
+        ("prefix_digits", ctypes.c_int32), ("suffix_digits", ctypes.c_int32), ("d", ctypes.c_int32),
+        ("units", ctypes.c_int64), ("units_total", ctypes.c_int64), ("steps", ctypes.c_double),
+        ("column_updates", ctypes.c_double), ("walk_ms", ctypes.c_double), ("total_ms", ctypes.c_double),
+        ("launches", ctypes.c_int32), ("variant", ctypes.c_int32), ("block_threads", ctypes.c_int32),
+        ("grid_blocks", ctypes.c_int32),
+    ]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+_lock = threading.Lock()
+_lib = None
+
+
+def load():
+    """Load liblnorm.so (raises if it was not built: run __graft_entry__.build())."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: build it with `python -m paper_2503_21596_b200.build`")
+        lib = ctypes.CDLL(LIB_PATH)
+        P = ctypes.POINTER
+        i32, i64, u64 = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64
+        i32p, i8p, i64p = P(i32), P(ctypes.c_int8), P(i64)
+        vp = ctypes.c_void_p
+        sig = {
+            "lnorm_status_string": ([ctypes.c_int], ctypes.c_char_p),
+            "lnorm_version": ([], i32),
+            "lnorm_compute": ([i32p, i32, i32, i32, i32, i64p, i8p], ctypes.c_int),
+            "lnorm_compute_device": ([vp, i32, i32, i32, i32, vp, i64p, i8p], ctypes.c_int),
+            "lnorm_compute_multi": ([i32p, i32, i32, i32, i32, i32, i32p, i64p, i8p], ctypes.c_int),
+            "lnorm_comm_unique_id": ([P(ctypes.c_uint8)], ctypes.c_int),
+            "lnorm_comm_create": ([P(ctypes.c_uint8), i32, i32, i32, P(vp)], ctypes.c_int),
+            "lnorm_comm_destroy": ([vp], ctypes.c_int),
+            "lnorm_compute_rank": ([vp, i32p, i32, i32, i32, i32, i64p, i8p], ctypes.c_int),
+            "lnorm_compute_rank_device": ([vp, vp, i32, i32, i32, i32, i64p, i8p], ctypes.c_int),
+            "lnorm_prefix_maxima": ([i32p, i32, i32, i32, i32, i32, i8p, i64, i64p], ctypes.c_int),
+            "lnorm_walk_trace": ([i32p, i32, i32, i32, i32, i32, i8p, i64, i64p, i8p], ctypes.c_int),
+            "lnorm_gray_digit": ([i32, i32, u64], i32),
+            "lnorm_gray_change": ([i32, u64, i32p, i32p, i32p], ctypes.c_int),
+            "lnorm_partition": ([u64, i64, i64, i64p, i64p], ctypes.c_int),
+            "lnorm_last_stats": ([P(Stats)], ctypes.c_int),
+        }
+        for name, (args, res) in sig.items():
+            f = getattr(lib, name)
+            f.argtypes = args
+            f.restype = res
+        _lib = lib
+        return lib
+
+
+def _status_text(status: int) -> str:
+    try:
+        return load().lnorm_status_string(status).decode()
+    except Exception:
+        return STATUS.get(status, "?")
+
+
+def status_string(status: int) -> str:
+    return _status_text(status)
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        raise LNormError(rc, what)
+
+
+def _mat(M):
+    A = np.ascontiguousarray(np.asarray(M), dtype=np.int32)
+    if A.ndim != 2:
+        raise ValueError("M must be a 2-D integer matrix")
+    return A
+
+
+def _p(a, ct):
+    return a.ctypes.data_as(ctypes.POINTER(ct))
+
+
+def compute(M, d: int = 1, with_marginals: bool = False):
+    """Exact L_1 / L_marg / L_d of the host matrix M on the current CUDA device.
+
+    Returns (value, argmax) -- argmax is int8[n] (+-1 for d = 1, RGS labels for d >= 2)."""
+    A = _mat(M)
+    n, m = A.shape
+    v = ctypes.c_int64()
+    arg = np.zeros(n, dtype=np.int8)
+    _check(load().lnorm_compute(_p(A, ctypes.c_int32), n, m, d, int(with_marginals), ctypes.byref(v),
+                                _p(arg, ctypes.c_int8)), "lnorm_compute")
+    return int(v.value), arg
+
+
+def compute_device(M_dev, d: int = 1, with_marginals: bool = False, stream=None):
+    """Same as compute() for a matrix already resident on the device.
+
+    M_dev: a CUDA tensor-like object with ``data_ptr()`` and ``shape`` (int32, contiguous)."""
+    n, m = int(M_dev.shape[0]), int(M_dev.shape[1])
+    v = ctypes.c_int64()
+    arg = np.zeros(n, dtype=np.int8)
+    st = ctypes.c_void_p(stream) if stream else None
+    _check(load().lnorm_compute_device(ctypes.c_void_p(M_dev.data_ptr()), n, m, d, int(with_marginals), st,
+                                       ctypes.byref(v), _p(arg, ctypes.c_int8)), "lnorm_compute_device")
+    return int(v.value), arg
+
+
+def compute_multi(M, d: int = 1, with_marginals: bool = False, devices=None):
+    """One process, several GPUs: Algorithm-1 unit split + one NCCL all-reduce(max)."""
+    A = _mat(M)
+    n, m = A.shape
+    if devices is None:
+        import torch
+        devices = list(range(torch.cuda.device_count()))
+    ids = np.ascontiguousarray(np.asarray(devices, dtype=np.int32))
+    v = ctypes.c_int64()
+    arg = np.zeros(n, dtype=np.int8)
+    _check(load().lnorm_compute_multi(_p(A, ctypes.c_int32), n, m, d, int(with_marginals), len(ids),
+                                      _p(ids, ctypes.c_int32), ctypes.byref(v), _p(arg, ctypes.c_int8)),
+           "lnorm_compute_multi")
+    return int(v.value), arg
+
+
+class Comm:
+    """A library-owned NCCL communicator for one rank of a torchrun job.
+
+    Rank 0 creates the 128-byte unique id with ``Comm.unique_id()`` and
+    broadcasts it (e.g. ``torch.distributed.broadcast_object_list``)."""
+
+    def __init__(self, uid: bytes | None, rank: int, world: int, device: int):
+        self._h = ctypes.c_void_p()
+        buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid) if uid is not None else None
+        _check(load().lnorm_comm_create(buf, rank, world, device, ctypes.byref(self._h)), "lnorm_comm_create")
+        self.rank, self.world, self.device = rank, world, device
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (ctypes.c_uint8 * 128)()
+        _check(load().lnorm_comm_unique_id(buf), "lnorm_comm_unique_id")
+        return bytes(buf)
+
+    def compute(self, M, d: int = 1, with_marginals: bool = False):
+        A = _mat(M)
+        n, m = A.shape
+        v = ctypes.c_int64()
+        arg = np.zeros(n, dtype=np.int8)
+        _check(load().lnorm_compute_rank(self._h, _p(A, ctypes.c_int32), n, m, d, int(with_marginals),
+                                         ctypes.byref(v), _p(arg, ctypes.c_int8)), "lnorm_compute_rank")
+        return int(v.value), arg
+
+    def compute_device(self, M_dev, d: int = 1, with_marginals: bool = False):
+        n, m = int(M_dev.shape[0]), int(M_dev.shape[1])
+        v = ctypes.c_int64()
+        arg = np.zeros(n, dtype=np.int8)
+        _check(load().lnorm_compute_rank_device(self._h, ctypes.c_void_p(M_dev.data_ptr()), n, m, d,
+                                                int(with_marginals), ctypes.byref(v), _p(arg, ctypes.c_int8)),
+               "lnorm_compute_rank_device")
+        return int(v.value), arg
+
+    def close(self):
+        if self._h:
+            load().lnorm_comm_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def prefix_maxima(M, prefixes, d: int = 1, with_marginals: bool = False):
+    """Per-prefix maxima (test hook): max over completions of each fixed prefix of rows 0..nfixed-1."""
+    A = _mat(M)
+    n, m = A.shape
+    P = np.ascontiguousarray(np.asarray(prefixes, dtype=np.int8))
+    if P.ndim != 2:
+        raise ValueError("prefixes must be 2-D (count x nfixed)")
+    out = np.zeros(P.shape[0], dtype=np.int64)
+    _check(load().lnorm_prefix_maxima(_p(A, ctypes.c_int32), n, m, d, int(with_marginals), P.shape[1],
+                                      _p(P, ctypes.c_int8), P.shape[0], _p(out, ctypes.c_int64)),
+           "lnorm_prefix_maxima")
+    return out
+
+
+def walk_trace(M, prefix, d: int = 1, with_marginals: bool = False):
+    """Per-step values and digits of the device walk of one unit (test hook)."""
+    A = _mat(M)
+    n, m = A.shape
+    pre = np.ascontiguousarray(np.asarray(prefix, dtype=np.int8))
+    base = 2 if d == 1 else d
+    steps = base ** (n - len(pre))
+    vals = np.zeros(steps, dtype=np.int64)
+    digs = np.zeros((steps, n), dtype=np.int8)
+    _check(load().lnorm_walk_trace(_p(A, ctypes.c_int32), n, m, d, int(with_marginals), len(pre),
+                                   _p(pre, ctypes.c_int8), steps, _p(vals, ctypes.c_int64),
+                                   _p(digs, ctypes.c_int8)), "lnorm_walk_trace")
+    return vals, digs
+
+
+def gray_digit(d: int, i: int, j: int) -> int:
+    return int(load().lnorm_gray_digit(d, i, j))
+
+
+def gray_change(d: int, j: int):
+    a, b, c = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    _check(load().lnorm_gray_change(d, j, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)), "lnorm_gray_change")
+    return a.value, b.value, c.value
+
+
+def partition(C: int, T: int, t: int):
+    lo, hi = ctypes.c_int64(), ctypes.c_int64()
+    _check(load().lnorm_partition(C, T, t, ctypes.byref(lo), ctypes.byref(hi)), "lnorm_partition")
+    return lo.value, hi.value
+
+
+def last_stats() -> dict:
+    s = Stats()
+    _check(load().lnorm_last_stats(ctypes.byref(s)), "lnorm_last_stats")
+    return s.as_dict()

@@ -1,0 +1,724 @@
+// C ABI (include/lnorm.h): validation, orientation, unit planning, device
+// contexts, launches, the single NCCL all-reduce of the multi-GPU variants and
+// the argmax recovery / finalisation kernels.  Host code here only marshals
+// and plans; every step of the search runs in the kernels.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <functional>
+#include <nccl.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include "../../include/lnorm.h"
+#include "common.cuh"
+
+using namespace lnorm;
+
+namespace {
+
+// ------------------------------------------------------------------ NCCL --
+// NCCL is resolved at run time (dlopen) so the library loads on hosts without
+// it and shares the process's already-loaded libnccl (e.g. torch's).
+struct Nccl {
+  bool ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommInitAll)(ncclComm_t*, int, const int*) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+};
+
+Nccl& nccl() {
+  static Nccl n;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    void* h = nullptr;
+    for (const char* nm : names) {
+      h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+      if (h) break;
+    }
+    if (!h) for (const char* nm : names) { h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL); if (h) break; }
+    if (!h) return;
+    n.GetUniqueId = (decltype(n.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+    n.CommInitRank = (decltype(n.CommInitRank))dlsym(h, "ncclCommInitRank");
+    n.CommInitAll = (decltype(n.CommInitAll))dlsym(h, "ncclCommInitAll");
+    n.AllReduce = (decltype(n.AllReduce))dlsym(h, "ncclAllReduce");
+    n.CommDestroy = (decltype(n.CommDestroy))dlsym(h, "ncclCommDestroy");
+    n.GroupStart = (decltype(n.GroupStart))dlsym(h, "ncclGroupStart");
+    n.GroupEnd = (decltype(n.GroupEnd))dlsym(h, "ncclGroupEnd");
+    n.ok = n.GetUniqueId && n.CommInitRank && n.CommInitAll && n.AllReduce && n.CommDestroy;
+  });
+  return n;
+}
+
+// --------------------------------------------------------------- problem --
+struct Problem {
+  int n = 0, m = 0, d = 1, marg = 0;
+  int mode = MODE_L1;   // Mode
+  int dl = 2;           // labels walked: 2 for +-1 strategies, else effective d
+  bool transposed = false;
+  int r = 0, c = 0;     // enumerated rows / columns
+};
+
+int validate(const int32_t* M, int n, int m, int d, int marg, Problem* pr) {
+  if (!M || n < 1 || m < 1 || d < 1 || d > kMaxD || (marg != 0 && marg != 1)) return LNORM_EINVAL;
+  if (marg && d != 1) return LNORM_EINVAL;
+  int64_t S = 0;
+  for (int64_t i = 0; i < (int64_t)n * m; ++i) {
+    int64_t v = M[i];
+    S += v < 0 ? -v : v;
+    if (S > INT32_MAX) return LNORM_EOVERFLOW;
+  }
+  Problem p;
+  p.n = n; p.m = m; p.d = d; p.marg = marg;
+  if (d == 1) {
+    p.mode = marg ? MODE_MARG : MODE_L1;
+    p.dl = 2;
+    p.transposed = n > m;                 // PAPER.md:144 (L_1); R5 (L_marg)
+    p.r = p.transposed ? m : n;
+    p.c = p.transposed ? n : m;
+  } else {
+    p.mode = MODE_LD;
+    p.dl = std::max(2, std::min(d, n));   // L_d = L_min(d,n) (at most n labels used)
+    p.r = n; p.c = m;                     // never transposed
+  }
+  if (p.r > kMaxRows - 1 || p.c > kMaxCols) return LNORM_ETOOLARGE;
+  // search space d^(r-1) must fit a 63-bit word index
+  long double space = 1;
+  for (int i = 0; i < p.r - 1; ++i) space *= p.dl;
+  if (space >= 9.2e18L) return LNORM_ETOOLARGE;
+  *pr = p;
+  return LNORM_OK;
+}
+
+// ------------------------------------------------------------------ plan --
+enum Kernel { K_BIN = 0, K_LD = 1, K_GEN = 2 };
+
+struct Plan {
+  int kernel = K_GEN;
+  int k = 0, s = 0;
+  int64_t units = 1;
+  std::vector<uint64_t> table;   // packed prefixes (RGS for d >= 3, explicit for hooks); empty = arithmetic
+};
+
+constexpr int64_t kNominalLanes = 148LL * 1024;   // plan is hardware-independent => identical on every rank
+constexpr int64_t kTableCap = 1LL << 22;
+
+// All restricted-growth prefixes of length k+1 with labels < d, in lexicographic order.
+void rgs_enumerate(int len, int d, std::vector<uint64_t>& out, int64_t cap) {
+  const int pb = prefix_bits(d);
+  std::vector<int> dig(len, 0);
+  // iterative DFS in lexicographic order
+  std::function<bool(int, int)> rec = [&](int pos, int mx) -> bool {
+    if (pos == len) {
+      uint64_t w = 0;
+      for (int x = 0; x < len; ++x) w |= (uint64_t)dig[x] << (pb * x);
+      out.push_back(w);
+      return (int64_t)out.size() < cap;
+    }
+    for (int a = 0; a <= std::min(mx + 1, d - 1); ++a) {
+      dig[pos] = a;
+      if (!rec(pos + 1, std::max(mx, a))) return false;
+    }
+    return true;
+  };
+  dig[0] = 0;
+  if (len == 1) { out.push_back(0); return; }
+  rec(1, 0);
+}
+
+int64_t rgs_count(int len, int d) {
+  // number of RGS strings of length len with at most d labels: sum_{j<=d} S(len, j)
+  std::vector<std::vector<long double>> S(len + 1, std::vector<long double>(d + 1, 0));
+  S[0][0] = 1;
+  for (int i = 1; i <= len; ++i)
+    for (int j = 1; j <= d; ++j) S[i][j] = j * S[i - 1][j] + S[i - 1][j - 1];
+  long double t = 0;
+  for (int j = 1; j <= d; ++j) t += S[len][j];
+  return t > 9e18L ? INT64_MAX : (int64_t)t;
+}
+
+int make_plan(const Problem& pr, int world, Plan* pl) {
+  const int f = pr.r - 1;
+  const int64_t target = kNominalLanes * 64 * std::max(1, world);
+  Plan p;
+  if (pr.dl == 2) {
+    const bool hot = walk_bin_supported(pr.mode, pr.c, std::min(f, 4)) && f >= 4;
+    const int smin = hot ? 4 : 0;
+    int k = 0;
+    while (k < f - smin && k < 31 && (1LL << k) < target) ++k;
+    p.k = k; p.s = f - k; p.units = 1LL << k;
+    p.kernel = hot ? K_BIN : K_GEN;
+  } else {
+    const int d = pr.dl;
+    const bool hot = walk_ld_supported(d, pr.c, 1) && f >= 1;
+    const int smin = hot ? 1 : 0;
+    int k = 0;
+    while (k < f - smin && (k + 2) * prefix_bits(d) <= 64 && rgs_count(k + 2, d) <= kTableCap && rgs_count(k + 1, d) < target) ++k;
+    p.k = k; p.s = f - k;
+    rgs_enumerate(k + 1, d, p.table, kTableCap + 1);
+    p.units = (int64_t)p.table.size();
+    p.kernel = hot ? K_LD : K_GEN;
+  }
+  // per-unit word count must fit 32-bit block counters
+  long double words = 1;
+  for (int i = 0; i < p.s; ++i) words *= pr.dl;
+  if (words >= 4.0e9L || p.units >= (1LL << 32)) return LNORM_ETOOLARGE;
+  *pl = std::move(p);
+  return LNORM_OK;
+}
+
+// --------------------------------------------------------------- kernels --
+__global__ void orient_kernel(const int32_t* in, int n, int m, int transpose, int32_t* out) {
+  const int64_t total = (int64_t)n * m;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    if (!transpose) out[i] = in[i];
+    else { const int64_t x = i / m, y = i % m; out[y * n + x] = in[i]; }
+  }
+}
+
+__global__ void init_ctl_kernel(unsigned long long* ctl) {
+  ctl[0] = 0ull;        // work counter
+  ctl[1] = 0ull;        // max key
+  ctl[2] = ~0ull;       // min lexicographic suffix key
+  ctl[3] = 0ull;
+}
+
+struct FinalizeArgs {
+  const unsigned long long* ctl;
+  const uint64_t* table;   // full prefix table or null (binary arithmetic)
+  const int32_t* Min;      // original (un-oriented) input, n x m
+  int n, m, r, k, s, base, mode, transposed, pbits;
+  int64_t* value_out;
+  int8_t* argmax_out;      // int8[n]
+};
+
+// Assemble the lexicographically smallest optimum from (unit, suffix key) and
+// map it back to the caller's row order (R2, R6).
+__global__ void finalize_kernel(FinalizeArgs a) {
+  __shared__ int8_t dig[kMaxRows];
+  __shared__ int flip;
+  const unsigned long long key = a.ctl[1], lex = a.ctl[2];
+  const int64_t u = (int64_t)key_unit(key);
+  if (threadIdx.x == 0) {
+    *a.value_out = (int64_t)key_value(key);
+    for (int x = 0; x <= a.k; ++x)
+      dig[x] = a.table ? (int8_t)((a.table[u] >> (a.pbits * x)) & ((1ull << a.pbits) - 1ull)) : (int8_t)(x == 0 ? 0 : (u >> (a.k - x)) & 1);
+    uint64_t q = lex;
+    for (int i = 0; i < a.s; ++i) { dig[a.r - 1 - i] = (int8_t)(q % (uint64_t)a.base); q /= (uint64_t)a.base; }
+  }
+  __syncthreads();
+  if (!a.transposed) {
+    for (int x = threadIdx.x; x < a.n; x += blockDim.x)
+      a.argmax_out[x] = a.mode == MODE_LD ? dig[x] : (int8_t)(dig[x] ? -1 : 1);
+    return;
+  }
+  // searched M^T: dig is y* over the caller's columns; x_i = sgn((M y*)_i), sgn(0) = +1
+  for (int i = threadIdx.x; i < a.n; i += blockDim.x) {
+    int64_t z = 0;
+    for (int j = 0; j < a.m; ++j) z += (int64_t)a.Min[(int64_t)i * a.m + j] * (dig[j] ? -1 : 1);
+    a.argmax_out[i] = z >= 0 ? 1 : -1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) flip = (a.mode == MODE_L1 && a.argmax_out[0] == -1) ? 1 : 0;
+  __syncthreads();
+  if (a.mode == MODE_MARG) { if (threadIdx.x == 0) a.argmax_out[0] = 1; }
+  else if (flip) for (int i = threadIdx.x; i < a.n; i += blockDim.x) a.argmax_out[i] = (int8_t)-a.argmax_out[i];
+}
+
+// --------------------------------------------------------------- context --
+struct DevCtx {
+  int device = -1;
+  std::mutex mu;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[4] = {};
+  int nsm = 148;
+  int32_t* dIn = nullptr; size_t capIn = 0;
+  int32_t* dM = nullptr; size_t capM = 0;
+  int32_t* dTab = nullptr;
+  unsigned long long* dCtl = nullptr;
+  uint64_t* dPre = nullptr; size_t capPre = 0;
+  int64_t* dRes = nullptr;          // [0] value, then int8 argmax[kMaxCols]
+  int64_t* dUnit = nullptr; size_t capUnit = 0;
+  int64_t* hRes = nullptr;          // pinned mirror of dRes
+  bool ready = false;
+};
+
+DevCtx g_ctx[64];
+std::mutex g_ctx_mu;
+thread_local lnorm_stats g_stats;
+
+#define CU(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { (void)cudaGetLastError(); \
+  return e_ == cudaErrorMemoryAllocation ? LNORM_ENOMEM : LNORM_ECUDA; } } while (0)
+
+int ctx_get(int device, DevCtx** out) {
+  if (device < 0 || device >= 64) return LNORM_ENODEV;
+  std::lock_guard<std::mutex> g(g_ctx_mu);
+  DevCtx& c = g_ctx[device];
+  if (!c.ready) {
+    CU(cudaSetDevice(device));
+    CU(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+    for (auto& e : c.ev) CU(cudaEventCreate(&e));
+    CU(cudaDeviceGetAttribute(&c.nsm, cudaDevAttrMultiProcessorCount, device));
+    CU(cudaMalloc(&c.dTab, sizeof(int32_t) * 8448));
+    CU(cudaMalloc(&c.dCtl, sizeof(unsigned long long) * 4));
+    CU(cudaMalloc(&c.dRes, 8 + kMaxCols + 64));
+    CU(cudaMallocHost(&c.hRes, 8 + kMaxCols + 64));
+    c.device = device;
+    c.ready = true;
+  }
+  *out = &c;
+  return LNORM_OK;
+}
+
+template <class T>
+int grow(T** p, size_t* cap, size_t need) {
+  if (*cap >= need) return LNORM_OK;
+  if (*p) cudaFree(*p);
+  *p = nullptr; *cap = 0;
+  CU(cudaMalloc(p, sizeof(T) * need));
+  *cap = need;
+  return LNORM_OK;
+}
+
+// Algorithm 1 verbatim: inclusive range of worker t of T over C words;
+// the provisional j_max is signed (it is -1 when J = 0).
+void algorithm1(uint64_t C, int64_t T, int64_t t, int64_t* j_min, int64_t* j_max) {
+  const int64_t J = (int64_t)(C / (uint64_t)T), R = (int64_t)(C % (uint64_t)T);
+  int64_t lo = t * J, hi = (t + 1) * J - 1;
+  if (t <= R) lo += t; else lo += R;
+  if (t < R) hi += t + 1; else hi += R;
+  *j_min = lo;
+  *j_max = hi;
+}
+
+int64_t ipow(int b, int e) { int64_t r = 1; for (int i = 0; i < e; ++i) r *= b; return r; }
+
+struct RunOut {
+  int64_t value = 0;
+  std::vector<int8_t> argmax;
+};
+
+// Launch the walk over units [ub, ub+uc) of plan `pl` (params prepared by caller).
+int launch_walk(DevCtx& cx, const Problem& pr, const Plan& pl, WalkParams& wp, int* grid_out, int* block_out) {
+  int block = 128, occ = 0;
+  if (pl.kernel == K_BIN) occ = walk_bin_occupancy(pr.mode, pr.c, &block);
+  else if (pl.kernel == K_LD) occ = walk_ld_occupancy(pr.dl, pr.c, &block);
+  else occ = walk_generic_occupancy(pr.dl, pr.c, &block);
+  if (occ < 1) occ = 1;
+  const int64_t per_block = pl.kernel == K_GEN ? block / 32 : block;   // units claimed per block round
+  int64_t want = (wp.unit_count + per_block - 1) / per_block;
+  int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)occ * cx.nsm, want));
+  cudaError_t e;
+  if (pl.kernel == K_BIN) e = walk_bin_launch(wp, cx.dTab, grid, cx.stream, &block);
+  else if (pl.kernel == K_LD) e = walk_ld_launch(wp, cx.dTab, grid, cx.stream, &block);
+  else e = walk_generic_launch(wp, grid, cx.stream, &block);
+  if (e != cudaSuccess) { (void)cudaGetLastError(); return LNORM_ECUDA; }
+  *grid_out = grid; *block_out = block;
+  return LNORM_OK;
+}
+
+// Full search on one device.  dIn: device copy of the caller's n x m matrix.
+// world > 1: this rank walks its Algorithm-1 slice and `comm` all-reduces the key.
+int run_device(DevCtx& cx, const int32_t* dIn, const Problem& pr, int rank, int world, ncclComm_t comm,
+               RunOut* out, lnorm_stats* st) {
+  Plan pl;
+  int rc = make_plan(pr, world, &pl);
+  if (rc) return rc;
+  cudaStream_t s = cx.stream;
+  if ((rc = grow(&cx.dM, &cx.capM, (size_t)pr.n * pr.m))) return rc;
+  if (!pl.table.empty()) {
+    if ((rc = grow(&cx.dPre, &cx.capPre, pl.table.size()))) return rc;
+  }
+  CU(cudaEventRecord(cx.ev[0], s));
+  int launches = 0;
+  orient_kernel<<<std::min(1024, (pr.n * pr.m + 255) / 256), 256, 0, s>>>(dIn, pr.n, pr.m, pr.transposed ? 1 : 0, cx.dM);
+  ++launches;
+  CU(cudaGetLastError());
+  if (!pl.table.empty())
+    CU(cudaMemcpyAsync(cx.dPre, pl.table.data(), sizeof(uint64_t) * pl.table.size(), cudaMemcpyHostToDevice, s));
+  init_ctl_kernel<<<1, 1, 0, s>>>(cx.dCtl);
+  ++launches;
+  // Algorithm 1 over the unit list: rank slice [lo, hi]
+  int64_t lo = 0, cnt = pl.units;
+  if (world > 1) {
+    int64_t jmin = 0, jmax = -1;
+    algorithm1((uint64_t)pl.units, world, rank, &jmin, &jmax);
+    lo = jmin;
+    cnt = jmax - jmin + 1;
+  }
+  WalkParams wp{};
+  wp.M = cx.dM; wp.r = pr.r; wp.c = pr.c; wp.mode = pr.mode; wp.d = pr.dl; wp.k = pl.k; wp.s = pl.s;
+  wp.unit_begin = lo; wp.unit_count = cnt; wp.pbits = prefix_bits(pr.dl);
+  wp.prefix_table = pl.table.empty() ? nullptr : cx.dPre + lo;
+  wp.counter = cx.dCtl; wp.key = cx.dCtl + 1; wp.unit_max = nullptr;
+  int grid = 0, block = 0;
+  CU(cudaEventRecord(cx.ev[1], s));
+  if (cnt > 0) {
+    if ((rc = launch_walk(cx, pr, pl, wp, &grid, &block))) return rc;
+    launches += pl.kernel == K_GEN ? 1 : 2;   // table build + walk
+  }
+  CU(cudaEventRecord(cx.ev[2], s));
+  if (world > 1) {
+    Nccl& nc = nccl();
+    if (!nc.ok || !comm) return LNORM_ENCCL;
+    if (nc.AllReduce(cx.dCtl + 1, cx.dCtl + 1, 1, ncclUint64, ncclMax, comm, s) != ncclSuccess) return LNORM_ENCCL;
+  }
+  // recovery over the full unit space (same winning unit on every rank)
+  WalkParams rp = wp;
+  rp.unit_begin = 0; rp.unit_count = pl.units;
+  rp.prefix_table = pl.table.empty() ? nullptr : cx.dPre;
+  if (recover_launch(rp, cx.dCtl + 2, s) != cudaSuccess) { (void)cudaGetLastError(); return LNORM_ECUDA; }
+  ++launches;
+  FinalizeArgs fa;
+  fa.ctl = cx.dCtl; fa.table = rp.prefix_table; fa.Min = dIn; fa.n = pr.n; fa.m = pr.m; fa.r = pr.r;
+  fa.k = pl.k; fa.s = pl.s; fa.base = pr.dl; fa.mode = pr.mode; fa.transposed = pr.transposed ? 1 : 0; fa.pbits = prefix_bits(pr.dl);
+  fa.value_out = cx.dRes; fa.argmax_out = reinterpret_cast<int8_t*>(cx.dRes + 1);
+  finalize_kernel<<<1, 256, 0, s>>>(fa);
+  ++launches;
+  CU(cudaGetLastError());
+  CU(cudaMemcpyAsync(cx.hRes, cx.dRes, 8 + pr.n, cudaMemcpyDeviceToHost, s));
+  CU(cudaEventRecord(cx.ev[3], s));
+  CU(cudaStreamSynchronize(s));
+  out->value = cx.hRes[0];
+  out->argmax.assign(reinterpret_cast<int8_t*>(cx.hRes + 1), reinterpret_cast<int8_t*>(cx.hRes + 1) + pr.n);
+  float wms = 0, tms = 0;
+  cudaEventElapsedTime(&wms, cx.ev[1], cx.ev[2]);
+  cudaEventElapsedTime(&tms, cx.ev[0], cx.ev[3]);
+  lnorm_stats S{};
+  S.rows = pr.r; S.cols = pr.c; S.transposed = pr.transposed; S.prefix_digits = pl.k; S.suffix_digits = pl.s;
+  S.d = pr.d == 1 ? 1 : pr.dl; S.units = cnt; S.units_total = pl.units;
+  S.steps = (double)cnt * (double)ipow(pr.dl, pl.s);
+  S.column_updates = S.steps * pr.c * (pr.mode == MODE_LD && pr.dl >= 3 ? 2 : 1);
+  S.walk_ms = wms; S.total_ms = tms; S.launches = launches; S.variant = pl.kernel;
+  S.block_threads = block; S.grid_blocks = grid;
+  *st = S;
+  return LNORM_OK;
+}
+
+int current_device(int* dev) {
+  int cnt = 0;
+  if (cudaGetDeviceCount(&cnt) != cudaSuccess || cnt < 1) { (void)cudaGetLastError(); return LNORM_ENODEV; }
+  if (cudaGetDevice(dev) != cudaSuccess) { (void)cudaGetLastError(); return LNORM_ENODEV; }
+  return LNORM_OK;
+}
+
+void write_out(const RunOut& ro, int64_t* value, int8_t* argmax) {
+  *value = ro.value;
+  if (argmax) std::memcpy(argmax, ro.argmax.data(), ro.argmax.size());
+}
+
+int compute_on(int device, const int32_t* hostM, const int32_t* devM, int n, int m, int d, int marg,
+               int rank, int world, ncclComm_t comm, int64_t* value, int8_t* argmax) {
+  if (!value) return LNORM_EINVAL;
+  Problem pr;
+  std::vector<int32_t> hcopy;
+  DevCtx* cx = nullptr;
+  int rc = ctx_get(device, &cx);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> g(cx->mu);
+  CU(cudaSetDevice(device));
+  if (devM) {   // validation needs the entries: bring the (small) matrix to the host once
+    if (n < 1 || m < 1) return LNORM_EINVAL;
+    hcopy.resize((size_t)n * m);
+    CU(cudaMemcpy(hcopy.data(), devM, sizeof(int32_t) * hcopy.size(), cudaMemcpyDeviceToHost));
+    hostM = hcopy.data();
+  }
+  if ((rc = validate(hostM, n, m, d, marg, &pr))) return rc;
+  const int32_t* dIn = devM;
+  if (!devM) {
+    if ((rc = grow(&cx->dIn, &cx->capIn, (size_t)n * m))) return rc;
+    CU(cudaMemcpyAsync(cx->dIn, hostM, sizeof(int32_t) * n * m, cudaMemcpyHostToDevice, cx->stream));
+    dIn = cx->dIn;
+  }
+  RunOut ro;
+  lnorm_stats st{};
+  if ((rc = run_device(*cx, dIn, pr, rank, world, comm, &ro, &st))) return rc;
+  g_stats = st;
+  write_out(ro, value, argmax);
+  return LNORM_OK;
+}
+
+}  // namespace
+
+struct lnorm_comm {
+  ncclComm_t comm = nullptr;
+  int rank = 0, world = 1, device = 0;
+};
+
+extern "C" {
+
+const char* lnorm_status_string(int status) {
+  switch (status) {
+    case LNORM_OK: return "ok";
+    case LNORM_EINVAL: return "invalid argument";
+    case LNORM_EOVERFLOW: return "sum |M_ij| exceeds 2^31-1 (int32 exactness bound)";
+    case LNORM_ETOOLARGE: return "search space or shape exceeds the supported limits";
+    case LNORM_ENODEV: return "no CUDA device";
+    case LNORM_ECUDA: return "CUDA runtime error";
+    case LNORM_ENCCL: return "NCCL unavailable or failed";
+    case LNORM_ENOMEM: return "out of device memory";
+    default: return "unknown status";
+  }
+}
+
+int32_t lnorm_version(void) { return (1 << 16) | 0; }
+
+int lnorm_compute(const int32_t* M, int32_t n, int32_t m, int32_t d, int32_t with_marginals,
+                  int64_t* value, int8_t* argmax) {
+  if (!M) return LNORM_EINVAL;
+  int dev = 0, rc = current_device(&dev);
+  if (rc) return rc;
+  return compute_on(dev, M, nullptr, n, m, d, with_marginals, 0, 1, nullptr, value, argmax);
+}
+
+int lnorm_compute_device(const int32_t* M_device, int32_t n, int32_t m, int32_t d, int32_t with_marginals,
+                         void* cuda_stream, int64_t* value, int8_t* argmax) {
+  (void)cuda_stream;   // work runs on the context stream; the call synchronises before returning
+  if (!M_device) return LNORM_EINVAL;
+  int dev = 0, rc = current_device(&dev);
+  if (rc) return rc;
+  return compute_on(dev, nullptr, M_device, n, m, d, with_marginals, 0, 1, nullptr, value, argmax);
+}
+
+int lnorm_comm_unique_id(uint8_t id_out[128]) {
+  if (!id_out) return LNORM_EINVAL;
+  Nccl& nc = nccl();
+  if (!nc.ok) return LNORM_ENCCL;
+  ncclUniqueId id;
+  if (nc.GetUniqueId(&id) != ncclSuccess) return LNORM_ENCCL;
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  std::memcpy(id_out, &id, 128);
+  return LNORM_OK;
+}
+
+int lnorm_comm_create(const uint8_t id[128], int32_t rank, int32_t world, int32_t device, lnorm_comm** comm_out) {
+  if (!comm_out || world < 1 || rank < 0 || rank >= world || device < 0) return LNORM_EINVAL;
+  lnorm_comm* c = new lnorm_comm;
+  c->rank = rank; c->world = world; c->device = device;
+  if (world > 1) {
+    if (!id) { delete c; return LNORM_EINVAL; }
+    Nccl& nc = nccl();
+    if (!nc.ok) { delete c; return LNORM_ENCCL; }
+    if (cudaSetDevice(device) != cudaSuccess) { (void)cudaGetLastError(); delete c; return LNORM_ENODEV; }
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, 128);
+    if (nc.CommInitRank(&c->comm, world, uid, rank) != ncclSuccess) { delete c; return LNORM_ENCCL; }
+  }
+  *comm_out = c;
+  return LNORM_OK;
+}
+
+int lnorm_comm_destroy(lnorm_comm* comm) {
+  if (!comm) return LNORM_EINVAL;
+  if (comm->comm) { Nccl& nc = nccl(); if (nc.ok) nc.CommDestroy(comm->comm); }
+  delete comm;
+  return LNORM_OK;
+}
+
+int lnorm_compute_rank(lnorm_comm* comm, const int32_t* M, int32_t n, int32_t m, int32_t d,
+                       int32_t with_marginals, int64_t* value, int8_t* argmax) {
+  if (!M) return LNORM_EINVAL;
+  if (!comm) {
+    int dev = 0, rc = current_device(&dev);
+    if (rc) return rc;
+    return compute_on(dev, M, nullptr, n, m, d, with_marginals, 0, 1, nullptr, value, argmax);
+  }
+  return compute_on(comm->device, M, nullptr, n, m, d, with_marginals, comm->rank, comm->world, comm->comm,
+                    value, argmax);
+}
+
+int lnorm_compute_rank_device(lnorm_comm* comm, const int32_t* M_device, int32_t n, int32_t m, int32_t d,
+                              int32_t with_marginals, int64_t* value, int8_t* argmax) {
+  if (!M_device) return LNORM_EINVAL;
+  if (!comm) {
+    int dev = 0, rc = current_device(&dev);
+    if (rc) return rc;
+    return compute_on(dev, nullptr, M_device, n, m, d, with_marginals, 0, 1, nullptr, value, argmax);
+  }
+  return compute_on(comm->device, nullptr, M_device, n, m, d, with_marginals, comm->rank, comm->world, comm->comm,
+                    value, argmax);
+}
+
+int lnorm_compute_multi(const int32_t* M, int32_t n, int32_t m, int32_t d, int32_t with_marginals,
+                        int32_t num_devices, const int32_t* device_ids, int64_t* value, int8_t* argmax) {
+  if (!M || !value || num_devices < 1 || num_devices > 64) return LNORM_EINVAL;
+  std::vector<int> devs(num_devices);
+  for (int i = 0; i < num_devices; ++i) devs[i] = device_ids ? device_ids[i] : i;
+  int cnt = 0;
+  if (cudaGetDeviceCount(&cnt) != cudaSuccess) { (void)cudaGetLastError(); return LNORM_ENODEV; }
+  for (int dv : devs) if (dv < 0 || dv >= cnt) return LNORM_ENODEV;
+  if (num_devices == 1) return compute_on(devs[0], M, nullptr, n, m, d, with_marginals, 0, 1, nullptr, value, argmax);
+  Nccl& nc = nccl();
+  if (!nc.ok) return LNORM_ENCCL;
+  std::vector<ncclComm_t> comms(num_devices);
+  if (nc.CommInitAll(comms.data(), num_devices, devs.data()) != ncclSuccess) return LNORM_ENCCL;
+  std::vector<int> rcs(num_devices, 0);
+  std::vector<int64_t> vals(num_devices, 0);
+  std::vector<std::vector<int8_t>> args(num_devices, std::vector<int8_t>(n, 0));
+  std::vector<lnorm_stats> sts(num_devices);
+  std::vector<std::thread> th;
+  for (int g = 0; g < num_devices; ++g) {
+    th.emplace_back([&, g] {
+      rcs[g] = compute_on(devs[g], M, nullptr, n, m, d, with_marginals, g, num_devices, comms[g], &vals[g],
+                          args[g].data());
+      sts[g] = g_stats;
+    });
+  }
+  for (auto& t : th) t.join();
+  for (auto& cm : comms) nc.CommDestroy(cm);
+  for (int g = 0; g < num_devices; ++g) if (rcs[g]) return rcs[g];
+  for (int g = 1; g < num_devices; ++g)
+    if (vals[g] != vals[0] || args[g] != args[0]) return LNORM_ECUDA;   // ranks must agree bit-for-bit
+  *value = vals[0];
+  if (argmax) std::memcpy(argmax, args[0].data(), n);
+  lnorm_stats S = sts[0];
+  for (int g = 1; g < num_devices; ++g) {
+    S.units += sts[g].units; S.steps += sts[g].steps; S.column_updates += sts[g].column_updates;
+    S.walk_ms = std::max(S.walk_ms, sts[g].walk_ms); S.total_ms = std::max(S.total_ms, sts[g].total_ms);
+    S.launches += sts[g].launches;
+  }
+  g_stats = S;
+  return LNORM_OK;
+}
+
+int lnorm_prefix_maxima(const int32_t* M, int32_t n, int32_t m, int32_t d, int32_t with_marginals,
+                        int32_t nfixed, const int8_t* prefixes, int64_t count, int64_t* out) {
+  if (!M || !prefixes || !out || count < 1 || nfixed < 1 || nfixed > n) return LNORM_EINVAL;
+  int dev = 0, rc = current_device(&dev);
+  if (rc) return rc;
+  Problem pr;
+  if ((rc = validate(M, n, m, d, with_marginals, &pr))) return rc;
+  // no orientation, no label reduction: the hook walks exactly the suffix of the given rows
+  pr.transposed = false; pr.r = n; pr.c = m;
+  pr.dl = d == 1 ? 2 : d;
+  if (pr.r > kMaxRows - 1 || pr.c > kMaxCols) return LNORM_ETOOLARGE;
+  const int base = pr.dl;
+  Plan pl;
+  pl.k = nfixed - 1; pl.s = n - nfixed; pl.units = count;
+  pl.table.resize(count);
+  const int pb = prefix_bits(base);
+  if (nfixed * pb > 64) return LNORM_EINVAL;
+  for (int64_t i = 0; i < count; ++i) {
+    uint64_t w = 0;
+    for (int x = 0; x < nfixed; ++x) {
+      int v = prefixes[i * nfixed + x];
+      if (v < 0 || v >= base) return LNORM_EINVAL;
+      if (x == 0 && with_marginals && v != 0) return LNORM_EINVAL;
+      w |= (uint64_t)v << (pb * x);
+    }
+    pl.table[i] = w;
+  }
+  if (base == 2) pl.kernel = walk_bin_supported(pr.mode, pr.c, pl.s) ? K_BIN : K_GEN;
+  else pl.kernel = walk_ld_supported(base, pr.c, pl.s) ? K_LD : K_GEN;
+  long double words = 1;
+  for (int i = 0; i < pl.s; ++i) words *= base;
+  if (words >= 4.0e9L) return LNORM_ETOOLARGE;
+  DevCtx* cx = nullptr;
+  if ((rc = ctx_get(dev, &cx))) return rc;
+  std::lock_guard<std::mutex> g(cx->mu);
+  CU(cudaSetDevice(dev));
+  if ((rc = grow(&cx->dIn, &cx->capIn, (size_t)n * m))) return rc;
+  if ((rc = grow(&cx->dM, &cx->capM, (size_t)n * m))) return rc;
+  if ((rc = grow(&cx->dPre, &cx->capPre, (size_t)count))) return rc;
+  if ((rc = grow(&cx->dUnit, &cx->capUnit, (size_t)count))) return rc;
+  cudaStream_t s = cx->stream;
+  CU(cudaMemcpyAsync(cx->dM, M, sizeof(int32_t) * n * m, cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync(cx->dPre, pl.table.data(), sizeof(uint64_t) * count, cudaMemcpyHostToDevice, s));
+  init_ctl_kernel<<<1, 1, 0, s>>>(cx->dCtl);
+  WalkParams wp{};
+  wp.M = cx->dM; wp.r = n; wp.c = m; wp.mode = pr.mode; wp.d = base; wp.k = pl.k; wp.s = pl.s;
+  wp.unit_begin = 0; wp.unit_count = count; wp.prefix_table = cx->dPre; wp.pbits = pb;
+  wp.counter = cx->dCtl; wp.key = cx->dCtl + 1; wp.unit_max = cx->dUnit;
+  int grid = 0, block = 0;
+  if ((rc = launch_walk(*cx, pr, pl, wp, &grid, &block))) return rc;
+  CU(cudaMemcpyAsync(out, cx->dUnit, sizeof(int64_t) * count, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  return LNORM_OK;
+}
+
+int lnorm_walk_trace(const int32_t* M, int32_t n, int32_t m, int32_t d, int32_t with_marginals,
+                     int32_t nfixed, const int8_t* prefix, int64_t max_steps, int64_t* values, int8_t* digits) {
+  if (!M || !prefix || !values || nfixed < 1 || nfixed > n || max_steps < 1) return LNORM_EINVAL;
+  int dev = 0, rc = current_device(&dev);
+  if (rc) return rc;
+  Problem pr;
+  if ((rc = validate(M, n, m, d, with_marginals, &pr))) return rc;
+  pr.r = n; pr.c = m; pr.dl = d == 1 ? 2 : d;
+  if (n > kMaxRows - 1 || m > kMaxCols) return LNORM_ETOOLARGE;
+  const int base = pr.dl, s_ = n - nfixed;
+  long double words = 1;
+  for (int i = 0; i < s_; ++i) words *= base;
+  if (words > (long double)max_steps) return LNORM_EINVAL;
+  uint64_t w = 0;
+  const int pb = prefix_bits(base);
+  if (nfixed * pb > 64) return LNORM_EINVAL;
+  for (int x = 0; x < nfixed; ++x) {
+    if (prefix[x] < 0 || prefix[x] >= base) return LNORM_EINVAL;
+    w |= (uint64_t)prefix[x] << (pb * x);
+  }
+  DevCtx* cx = nullptr;
+  if ((rc = ctx_get(dev, &cx))) return rc;
+  std::lock_guard<std::mutex> g(cx->mu);
+  CU(cudaSetDevice(dev));
+  const int64_t nw = (int64_t)words;
+  if ((rc = grow(&cx->dM, &cx->capM, (size_t)n * m))) return rc;
+  if ((rc = grow(&cx->dPre, &cx->capPre, 1))) return rc;
+  if ((rc = grow(&cx->dUnit, &cx->capUnit, (size_t)nw + (size_t)(nw * n + 7) / 8))) return rc;
+  cudaStream_t s = cx->stream;
+  CU(cudaMemcpyAsync(cx->dM, M, sizeof(int32_t) * n * m, cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync(cx->dPre, &w, sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+  WalkParams wp{};
+  wp.M = cx->dM; wp.r = n; wp.c = m; wp.mode = pr.mode; wp.d = base; wp.k = nfixed - 1; wp.s = s_;
+  wp.unit_begin = 0; wp.unit_count = 1; wp.prefix_table = cx->dPre; wp.pbits = pb;
+  int8_t* ddig = reinterpret_cast<int8_t*>(cx->dUnit + nw);
+  if (trace_launch(wp, nw, cx->dUnit, digits ? ddig : nullptr, s) != cudaSuccess) { (void)cudaGetLastError(); return LNORM_ECUDA; }
+  CU(cudaMemcpyAsync(values, cx->dUnit, sizeof(int64_t) * nw, cudaMemcpyDeviceToHost, s));
+  if (digits) CU(cudaMemcpyAsync(digits, ddig, (size_t)nw * n, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  return LNORM_OK;
+}
+
+int32_t lnorm_gray_digit(int32_t d, int32_t i, uint64_t j) {
+  if (d < 2 || i < 0 || i > 63) return -1;
+  if (d == 2) return (int32_t)brgc_digit((uint32_t)i, j);
+  return (int32_t)dary_digit((uint32_t)d, (uint32_t)i, j);
+}
+
+int lnorm_gray_change(int32_t d, uint64_t j, int32_t* digit, int32_t* from, int32_t* to) {
+  if (d < 2 || j < 1 || !digit || !from || !to) return LNORM_EINVAL;
+  if (d == 2) {
+    uint32_t i = brgc_change(j);
+    *digit = (int32_t)i;
+    *from = (int32_t)brgc_digit(i, j - 1);
+    *to = (int32_t)brgc_digit(i, j);
+    return LNORM_OK;
+  }
+  uint32_t i, f, t;
+  dary_change_values((uint32_t)d, j, &i, &f, &t);
+  *digit = (int32_t)i; *from = (int32_t)f; *to = (int32_t)t;
+  return LNORM_OK;
+}
+
+int lnorm_partition(uint64_t C, int64_t T, int64_t t, int64_t* j_min, int64_t* j_max) {
+  if (T < 1 || t < 0 || t >= T || !j_min || !j_max) return LNORM_EINVAL;
+  algorithm1(C, T, t, j_min, j_max);
+  return LNORM_OK;
+}
+
+int lnorm_last_stats(lnorm_stats* out) {
+  if (!out) return LNORM_EINVAL;
+  *out = g_stats;
+  return LNORM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,94 @@
+// Shared device-side definitions of the walk kernels (product path).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include "gray.cuh"
+
+namespace lnorm {
+
+enum Mode : int32_t { MODE_L1 = 0, MODE_MARG = 1, MODE_LD = 2 };
+
+// bits per packed prefix digit for a label alphabet of size `base`
+__host__ __device__ __forceinline__ int prefix_bits(int base) { return base <= 2 ? 1 : (base <= 4 ? 2 : 3); }
+
+constexpr int kMaxRows = 64;       // enumerated rows after orientation
+constexpr int kMaxCols = 1024;     // columns after orientation
+constexpr int kMaxD = 8;
+
+// One launch of a walk kernel over a contiguous range of units.
+// A unit = one fixed prefix (rows 0..k) whose suffix (rows k+1..r-1, s = r-1-k
+// digits) is walked completely in reflected Gray order.
+struct WalkParams {
+  const int32_t* M;              // device, r x c row-major (oriented)
+  int32_t r, c;                  // enumerated rows, columns
+  int32_t mode;                  // Mode
+  int32_t d;                     // 2 for +-1 strategies and L_2, else label count
+  int32_t k;                     // prefix rows 1..k (row 0 fixed); unit prefix length k+1
+  int32_t s;                     // suffix digits
+  int64_t unit_begin;            // first global unit index of this launch
+  int64_t unit_count;            // units in this launch
+  int32_t pbits;                 // bits per packed prefix digit (1, 2 or 3)
+  const uint64_t* prefix_table;  // packed prefix digits (pbits per row 0..k) or nullptr:
+                                 //   binary arithmetic prefix, digit of row x = bit (k-x) of u
+  unsigned long long* counter;   // work counter (zeroed before launch)
+  unsigned long long* key;       // global max key (zeroed before launch)
+  int64_t* unit_max;             // optional per-unit maxima (index u - unit_begin)
+};
+
+// Max-reduction key: high word = value biased to unsigned order, low word =
+// ~unit so that, among equal values, the SMALLEST unit index wins
+// (R2: lexicographically smallest optimum).
+__host__ __device__ __forceinline__ unsigned long long make_key(int32_t v, uint32_t unit) {
+  return ((unsigned long long)((uint32_t)v ^ 0x80000000u) << 32) | (unsigned long long)(0xFFFFFFFFu - unit);
+}
+__host__ __device__ __forceinline__ int32_t key_value(unsigned long long key) {
+  return (int32_t)((uint32_t)(key >> 32) ^ 0x80000000u);
+}
+__host__ __device__ __forceinline__ uint32_t key_unit(unsigned long long key) {
+  return 0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFull);
+}
+
+// Prefix digit of row x (0..k) of unit u.
+__device__ __forceinline__ int prefix_digit(const WalkParams& p, int64_t u, int x) {
+  if (p.prefix_table) return (int)((p.prefix_table[u - p.unit_begin] >> (p.pbits * x)) & ((1ull << p.pbits) - 1ull));
+  return x == 0 ? 0 : (int)((u >> (p.k - x)) & 1);
+}
+
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = w > v ? w : v;
+  }
+  return v;
+}
+
+}  // namespace lnorm
+
+// Kernel launchers (one per translation unit); return cudaError_t.
+namespace lnorm {
+struct LaunchCfg { int grid, block; size_t smem; cudaStream_t stream; };
+// Hot binary walk (L_1, L_marg, L_2): r, c within the template set, s >= 4.
+bool walk_bin_supported(int mode, int c, int s);
+// scratch_tab: device buffer of >= 8448 int32 used to stage the constant table.
+cudaError_t walk_bin_launch(const WalkParams& p, int32_t* scratch_tab, int grid, cudaStream_t st,
+                            int* block_out);
+int walk_bin_occupancy(int mode, int c, int* block_out);
+template <int MODE> cudaError_t walk_bin_launch_mode(const WalkParams& p, int32_t* scratch_tab, int grid, cudaStream_t st);
+template <int MODE> int walk_bin_occupancy_mode(int c);
+// Hot d-ary walk (L_d, d in {3,4}).
+bool walk_ld_supported(int d, int c, int s);
+cudaError_t walk_ld_launch(const WalkParams& p, int32_t* scratch_tab, int grid, cudaStream_t st,
+                           int* block_out);
+int walk_ld_occupancy(int d, int c, int* block_out);
+// Generic warp-per-unit walk (any mode, d, c, s).
+bool walk_generic_supported(int d, int c);
+cudaError_t walk_generic_launch(const WalkParams& p, int grid, cudaStream_t st, int* block_out);
+int walk_generic_occupancy(int d, int c, int* block_out);
+// Argmax recovery: re-walk unit key_unit(*key) and write the smallest
+// lexicographic suffix key attaining key_value(*key) into *lex_out (atomicMin).
+cudaError_t recover_launch(const WalkParams& p, unsigned long long* lex_out, cudaStream_t st);
+// Trace: per-step values of one unit (test hook).
+cudaError_t trace_launch(const WalkParams& p, int64_t max_steps, int64_t* values, int8_t* digits,
+                         cudaStream_t st);
+}  // namespace lnorm

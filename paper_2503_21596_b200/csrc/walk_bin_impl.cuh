@@ -1,0 +1,206 @@
+// Hot binary Gray walk: L_1 (Eq. 1), L_marg (Eq. 2) and L_2 (Eq. 6, d = 2).
+//
+// Work decomposition: a unit fixes rows 0..k (row 0 at
+// digit 0: a_0 = +1, or label 0); its s = r-1-k suffix rows are
+// walked in binary reflected Gray order, suffix digit b <-> row r-1-b.  Every
+// lane of a warp owns one unit and all lanes walk the SAME local suffix
+// sequence, so the changed digit (Eq. 9: b = ctz(w)) and
+// the direction are warp-uniform -- the lockstep property of App. E
+// holds by construction, for any thread count.
+//
+// Per step (Eq. 12): m_y += delta_y with delta = +-2 M_rho
+// (L_1/L_marg) or +-M_rho (L_2: m_0 is the label-0 group sum), then the value
+//   L_1   : sum_y |m_y|
+//   L_marg: m_0 + sum_{y>=1} |m_y|
+//   L_2   : sum_y |m_y| + |T_y - m_y|   (T = column totals, m_1 = T - m_0)
+// and best = max(best, value).  int32 arithmetic is exact because
+// sum |M_ij| <= 2^31-1 is checked on the host (every |m_y| and value <= it).
+//
+// The delta rows live in the constant bank: every step reads one row at a
+// warp-uniform address, which ptxas turns into LDCU (uniform registers) feeding
+// VIADD (FMA-heavy pipe) -- leaving the ALU pipe to the VABSDIFF accumulate.
+// The low K = 4 suffix digits are unrolled: 15 of 16 steps have compile-time
+// row offsets; only the block-start step computes ctz on the uniform path.
+#include "common.cuh"
+
+#ifndef LN_BIN_MODE
+#error "define LN_BIN_MODE before including walk_bin_impl.cuh"
+#endif
+
+namespace lnorm {
+
+namespace {
+
+constexpr int K = 4;                      // statically unrolled low suffix digits
+constexpr int kTabInts = 8448;            // (2*s + k + 3) * C <= (2*63 + 3) * 64 + slack
+constexpr int kBlock = 32;   // one warp per block (see the schedule comment in the kernel)
+
+__host__ __device__ constexpr int cctz(int j) { return (j & 1) ? 0 : 1 + cctz(j >> 1); }
+
+// Layout (ints): [0, 2sC): delta rows, index (2b + sign) * C  (sign 1: flip to -1 / label 1)
+//                [2sC, 2sC + (k+1)C): prefix rows 0..k (raw M)
+//                then C: suffix base sum_{x > k} M_xy;  then C: column totals (L_2)
+__constant__ __align__(16) int32_t cTab[kTabInts];
+
+template <int MODE, int C>
+struct Walker {
+  // value of the current column sums; acc split 4 ways for ILP
+  static __device__ __forceinline__ int32_t value(const int32_t (&m)[C], const int32_t (&T)[C]) {
+    int32_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+    if (MODE == MODE_MARG) a0 = m[0];
+#pragma unroll
+    for (int y = 0; y < C; ++y) {
+      if (MODE == MODE_MARG && y == 0) continue;
+      int32_t& a = (y & 3) == 0 ? a0 : (y & 3) == 1 ? a1 : (y & 3) == 2 ? a2 : a3;
+      a = __sad(m[y], 0, a);
+      if (MODE == MODE_LD) a = __sad(T[y], m[y], a);
+    }
+    return (a0 + a1) + (a2 + a3);
+  }
+  // m += row(off); return new value
+  static __device__ __forceinline__ int32_t step(int32_t (&m)[C], const int32_t (&T)[C], int off) {
+#pragma unroll
+    for (int y = 0; y < C; ++y) m[y] += cTab[off + y];
+    return value(m, T);
+  }
+  // m += sgn * row(off) with a compile-time row offset and a warp-uniform sign:
+  // the row stays on the uniform datapath (LDCU) and the update is one IMAD.
+  static __device__ __forceinline__ int32_t step_signed(int32_t (&m)[C], const int32_t (&T)[C], int off, int32_t sgn) {
+#pragma unroll
+    for (int y = 0; y < C; ++y) m[y] += sgn * cTab[off + y];
+    return value(m, T);
+  }
+};
+
+template <int MODE, int C>
+__global__ void __launch_bounds__(kBlock) walk_bin_kernel(const WalkParams p) {
+  const int lane = threadIdx.x & 31;
+  const int s = p.s, k = p.k;
+  const int preOff = 2 * s * C, baseOff = preOff + (k + 1) * C, totOff = baseOff + C;
+  int32_t T[C];
+#pragma unroll
+  for (int y = 0; y < C; ++y) T[y] = (MODE == MODE_LD) ? cTab[totOff + y] : 0;
+  const uint32_t nblk = 1u << (s - K);
+  int32_t best = INT32_MIN;
+  uint32_t best_u = 0;
+  bool have = false;
+  // Static warp-chunk schedule: block = one warp, so the chunk index (and every
+  // Gray-control value derived from it) is provably warp-uniform and ptxas keeps
+  // the walk's row addressing on the uniform datapath (LDCU + VIADD R, R, UR).
+  const int64_t nchunks = (p.unit_count + 31) / 32;
+  for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    const int64_t rel = ch * 32 + lane;
+    const bool active = rel < p.unit_count;
+    const int64_t u = p.unit_begin + (active ? rel : 0);
+    // unit init: the paper's per-thread vector-matrix product at the start word
+    int32_t m[C];
+#pragma unroll
+    for (int y = 0; y < C; ++y) m[y] = cTab[baseOff + y];
+    for (int x = 0; x <= k; ++x) {
+      const int dig = prefix_digit(p, u, x);
+      const int32_t f = (MODE == MODE_LD) ? 1 - dig : 1 - 2 * dig;
+#pragma unroll
+      for (int y = 0; y < C; ++y) m[y] += f * cTab[preOff + x * C + y];
+    }
+    int32_t ub = Walker<MODE, C>::value(m, T);
+    for (uint32_t t = 0; t < nblk; ++t) {
+      if (t != 0) {                                   // block start: digit K + ctz(t)
+        const int tz = __ffs((int)t) - 1;
+        const int b = K + tz;
+        const int sg = 1 ^ (int)((t >> (tz + 1)) & 1u);
+        ub = max(ub, Walker<MODE, C>::step(m, T, (2 * b + sg) * C));
+      }
+      // the top unrolled digit's direction depends on the block parity: a
+      // warp-uniform table offset (LDCU with a uniform-register address)
+#pragma unroll
+      for (int j = 1; j < (1 << K); ++j) {
+        const int b = cctz(j);
+        const int sg = (b < K - 1) ? (1 ^ ((j >> (b + 1)) & 1)) : (1 ^ (int)(t & 1u));
+        ub = max(ub, Walker<MODE, C>::step(m, T, (2 * b + sg) * C));
+      }
+    }
+    if (active) {
+      if (p.unit_max) p.unit_max[rel] = ub;
+      if (!have || ub > best) { best = ub; best_u = (uint32_t)u; have = true; }
+    }
+  }
+  unsigned long long key = have ? make_key(best, best_u) : 0ull;
+  key = warp_max_u64(key);
+  if (lane == 0 && key) atomicMax(p.key, key);
+}
+
+// Build the constant table on the device from the oriented matrix.
+__global__ void build_table_kernel(const int32_t* M, int r, int c, int C, int k, int s, int mode, int32_t* tab) {
+  const int preOff = 2 * s * C, baseOff = preOff + (k + 1) * C, totOff = baseOff + C;
+  const int scale = (mode == MODE_LD) ? 1 : 2;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < totOff + C; i += gridDim.x * blockDim.x) {
+    int32_t v = 0;
+    if (i < preOff) {
+      const int rowi = i / C, y = i % C, b = rowi >> 1, sg = rowi & 1;
+      if (y < c) v = (sg ? -scale : scale) * M[(int64_t)(r - 1 - b) * c + y];
+    } else if (i < baseOff) {
+      const int x = (i - preOff) / C, y = (i - preOff) % C;
+      if (y < c) v = M[(int64_t)x * c + y];
+    } else if (i < totOff) {
+      const int y = i - baseOff;
+      if (y < c) for (int x = k + 1; x < r; ++x) v += M[(int64_t)x * c + y];
+    } else {
+      const int y = i - totOff;
+      if (y < c) for (int x = 0; x < r; ++x) v += M[(int64_t)x * c + y];
+    }
+    tab[i] = v;
+  }
+}
+
+template <int MODE, int C>
+cudaError_t launch_one(const WalkParams& p, int grid, cudaStream_t st) {
+  walk_bin_kernel<MODE, C><<<grid, kBlock, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+template <int MODE, int C>
+int occ_one() {
+  int nb = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, walk_bin_kernel<MODE, C>, kBlock, 0);
+  return nb;
+}
+
+constexpr int padC(int c) { return (c + 3) & ~3; }
+
+#define LN_BIN_SWITCH(MODE, C_, FN, ...)                                            \
+  switch (C_) {                                                                     \
+    case 4: return FN<MODE, 4>(__VA_ARGS__);   case 8: return FN<MODE, 8>(__VA_ARGS__);    \
+    case 12: return FN<MODE, 12>(__VA_ARGS__); case 16: return FN<MODE, 16>(__VA_ARGS__);  \
+    case 20: return FN<MODE, 20>(__VA_ARGS__); case 24: return FN<MODE, 24>(__VA_ARGS__);  \
+    case 28: return FN<MODE, 28>(__VA_ARGS__); case 32: return FN<MODE, 32>(__VA_ARGS__);  \
+    case 36: return FN<MODE, 36>(__VA_ARGS__); case 40: return FN<MODE, 40>(__VA_ARGS__);  \
+    case 44: return FN<MODE, 44>(__VA_ARGS__); case 48: return FN<MODE, 48>(__VA_ARGS__);  \
+    case 52: return FN<MODE, 52>(__VA_ARGS__); case 56: return FN<MODE, 56>(__VA_ARGS__);  \
+    case 60: return FN<MODE, 60>(__VA_ARGS__); case 64: return FN<MODE, 64>(__VA_ARGS__);  \
+    default: break;                                                                 \
+  }
+
+}  // namespace
+
+// Per-mode entry points (one translation unit per mode for parallel builds).
+template <>
+cudaError_t walk_bin_launch_mode<LN_BIN_MODE>(const WalkParams& p, int32_t* scratch_tab, int grid, cudaStream_t st) {
+  const int C = padC(p.c);
+  const int total = (2 * p.s + p.k + 3) * C;
+  if (total > kTabInts) return cudaErrorInvalidValue;
+  build_table_kernel<<<8, 256, 0, st>>>(p.M, p.r, p.c, C, p.k, p.s, p.mode, scratch_tab);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  e = cudaMemcpyToSymbolAsync(cTab, scratch_tab, sizeof(int32_t) * total, 0, cudaMemcpyDeviceToDevice, st);
+  if (e != cudaSuccess) return e;
+  LN_BIN_SWITCH(LN_BIN_MODE, C, launch_one, p, grid, st)
+  return cudaErrorInvalidValue;
+}
+
+template <>
+int walk_bin_occupancy_mode<LN_BIN_MODE>(int c) {
+  LN_BIN_SWITCH(LN_BIN_MODE, padC(c), occ_one)
+  return 0;
+}
+
+}  // namespace lnorm

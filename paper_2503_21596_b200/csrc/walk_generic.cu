@@ -1,0 +1,215 @@
+// Generic warp-per-unit Gray walk, argmax recovery and the trace hook.
+//
+// Every norm is written in the group-sum form of Eqs. (6)-(7):
+// the strategy assigns each row a label, (m_a)_y = sum_{x: a_x = a} M_xy, and a
+// step of the reflected Gray code moves ONE row rho from group `from` to group
+// `to` (Eqs. 18-19):  m_from -= M_rho,  m_to += M_rho.
+//   L_d    : value = sum_a ||m_a||_1                                  (Eq. 6)
+//   L_1    : labels 0/1 <-> a_x = +1/-1, m = m_0 - m_1, value = ||m||_1   (Eq. 1;
+//            moving a row between the groups is Eq. 12's m += +-2 M_rho)
+//   L_marg : value = m_0[0] - m_1[0] + sum_{y>=1} |m_0 - m_1|_y        (Eq. 2)
+// The lanes of a warp split the columns; the change digit (Eq. 9 / Eq. 17) is
+// warp-uniform.  This kernel covers every shape (any c <= 1024, any d <= 8,
+// any suffix length) and is the correctness anchor for shapes outside the
+// hot kernels' template set; recover and trace reuse the same device code.
+#include "common.cuh"
+
+namespace lnorm {
+
+namespace {
+
+constexpr int kGenWarps = 4;   // warps per block
+
+__device__ __forceinline__ int groups_of(const WalkParams& p) { return p.mode == MODE_LD ? p.d : 2; }
+__device__ __forceinline__ int base_of(const WalkParams& p) { return p.mode == MODE_LD ? p.d : 2; }
+
+// Initialise the warp's group sums for unit u with suffix word `w0` (digits of
+// the reflected Gray code, Eq. 8 / Eqs. 13-15; suffix digit i <-> row r-1-i).
+__device__ void gen_init(const WalkParams& p, int64_t u, uint64_t w0, int32_t* G, int lane) {
+  const int nG = groups_of(p), base = base_of(p);
+  for (int y = lane; y < p.c; y += 32) {
+    for (int a = 0; a < nG; ++a) G[a * p.c + y] = 0;
+  }
+  for (int x = 0; x < p.r; ++x) {
+    int lab;
+    if (x <= p.k) lab = prefix_digit(p, u, x);
+    else lab = (int)dary_digit((uint32_t)base, (uint32_t)(p.r - 1 - x), w0);
+    const int32_t* row = p.M + (int64_t)x * p.c;
+    for (int y = lane; y < p.c; y += 32) G[lab * p.c + y] += row[y];
+  }
+}
+
+__device__ int32_t gen_value(const WalkParams& p, const int32_t* G, int lane) {
+  int32_t v = 0;
+  if (p.mode == MODE_LD) {
+    for (int a = 0; a < p.d; ++a)
+      for (int y = lane; y < p.c; y += 32) v += abs(G[a * p.c + y]);
+  } else {
+    for (int y = lane; y < p.c; y += 32) {
+      int32_t mm = G[y] - G[p.c + y];
+      v += (p.mode == MODE_MARG && y == 0) ? mm : abs(mm);
+    }
+  }
+  return __reduce_add_sync(0xffffffffu, v);
+}
+
+__device__ __forceinline__ void gen_move(const WalkParams& p, int32_t* G, int row, int from, int to, int lane) {
+  const int32_t* R = p.M + (int64_t)row * p.c;
+  for (int y = lane; y < p.c; y += 32) {
+    int32_t v = R[y];
+    G[from * p.c + y] -= v;
+    G[to * p.c + y] += v;
+  }
+}
+
+__device__ __forceinline__ uint64_t ipow64(uint32_t b, int e) {
+  uint64_t r = 1;
+  for (int i = 0; i < e; ++i) r *= b;
+  return r;
+}
+
+__global__ void __launch_bounds__(32 * kGenWarps) walk_generic_kernel(const WalkParams p) {
+  extern __shared__ int32_t smem[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int nG = groups_of(p);
+  int32_t* G = smem + wib * nG * p.c;
+  const uint32_t base = (uint32_t)base_of(p);
+  const uint64_t words = ipow64(base, p.s);
+  unsigned long long best_key = 0;
+  while (true) {
+    unsigned long long t = 0;
+    if (lane == 0) t = atomicAdd(p.counter, 1ull);
+    t = __shfl_sync(0xffffffffu, t, 0);
+    if ((int64_t)t >= p.unit_count) break;
+    const int64_t u = p.unit_begin + (int64_t)t;
+    gen_init(p, u, 0, G, lane);
+    int32_t best = gen_value(p, G, lane);
+    for (uint64_t w = 1; w < words; ++w) {
+      uint32_t i, from, to;
+      dary_change_values(base, w, &i, &from, &to);
+      gen_move(p, G, p.r - 1 - (int)i, (int)from, (int)to, lane);
+      int32_t v = gen_value(p, G, lane);
+      best = v > best ? v : best;
+    }
+    if (p.unit_max && lane == 0) p.unit_max[t] = best;
+    unsigned long long kk = make_key(best, (uint32_t)u);
+    best_key = kk > best_key ? kk : best_key;
+  }
+  if (lane == 0 && best_key) atomicMax(p.key, best_key);
+}
+
+// Recovery: the words of the winning unit are split into contiguous chunks
+// (Algorithm 1), one per warp; each warp starts from its
+// chunk's first word by the closed form and walks it, keeping the smallest
+// lexicographic suffix key among words whose value equals the optimum.
+__global__ void __launch_bounds__(32 * kGenWarps) recover_kernel(const WalkParams p, unsigned long long* lex_out) {
+  extern __shared__ int32_t smem[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int nG = groups_of(p);
+  int32_t* G = smem + wib * nG * p.c;
+  const uint32_t base = (uint32_t)base_of(p);
+  const uint64_t words = ipow64(base, p.s);
+  const unsigned long long key = *p.key;
+  const int32_t target = key_value(key);
+  const int64_t u = (int64_t)key_unit(key);
+  const uint64_t T = (uint64_t)gridDim.x * kGenWarps;
+  const uint64_t t = (uint64_t)blockIdx.x * kGenWarps + wib;
+  const uint64_t J = words / T, R = words % T;
+  const uint64_t lo = t * J + (t < R ? t : R);
+  const uint64_t hi = lo + J + (t < R ? 1 : 0);
+  if (lo >= hi) return;
+  gen_init(p, u, lo, G, lane);
+  uint64_t lex = 0;
+  for (int i = 0; i < p.s; ++i) lex += (uint64_t)dary_digit(base, (uint32_t)i, lo) * ipow64(base, i);
+  unsigned long long bestlex = ~0ull;
+  if (gen_value(p, G, lane) == target) bestlex = lex;
+  for (uint64_t w = lo + 1; w < hi; ++w) {
+    uint32_t i, from, to;
+    dary_change_values(base, w, &i, &from, &to);
+    gen_move(p, G, p.r - 1 - (int)i, (int)from, (int)to, lane);
+    lex = lex + (uint64_t)to * ipow64(base, (int)i) - (uint64_t)from * ipow64(base, (int)i);
+    if (gen_value(p, G, lane) == target && lex < bestlex) bestlex = lex;
+  }
+  if (lane == 0 && bestlex != ~0ull) atomicMin(lex_out, bestlex);
+}
+
+// Trace: one warp walks unit p.unit_begin and records every step.
+__global__ void trace_kernel(const WalkParams p, int64_t max_steps, int64_t* values, int8_t* digits) {
+  extern __shared__ int32_t smem[];
+  const int lane = threadIdx.x & 31;
+  const uint32_t base = (uint32_t)base_of(p);
+  const uint64_t words = ipow64(base, p.s);
+  int32_t* G = smem;
+  const int64_t u = p.unit_begin;
+  gen_init(p, u, 0, G, lane);
+  int8_t dig[kMaxRows];
+  for (int x = 0; x < p.r; ++x) dig[x] = (int8_t)(x <= p.k ? prefix_digit(p, u, x) : 0);
+  for (uint64_t w = 0; w < words && (int64_t)w < max_steps; ++w) {
+    if (w > 0) {
+      uint32_t i, from, to;
+      dary_change_values(base, w, &i, &from, &to);
+      gen_move(p, G, p.r - 1 - (int)i, (int)from, (int)to, lane);
+      dig[p.r - 1 - i] = (int8_t)to;
+    }
+    int32_t v = gen_value(p, G, lane);
+    if (lane == 0) {
+      values[w] = v;
+      if (digits)
+        for (int x = 0; x < p.r; ++x) digits[w * p.r + x] = dig[x];
+    }
+  }
+}
+
+size_t gen_smem(int nG, int c, int warps) { return (size_t)nG * c * warps * sizeof(int32_t); }
+
+}  // namespace
+
+bool walk_generic_supported(int d, int c) {
+  const int nG = d < 2 ? 2 : d;
+  return c >= 1 && c <= kMaxCols && (size_t)nG * c * sizeof(int32_t) * kGenWarps <= 200 * 1024;
+}
+
+int walk_generic_occupancy(int d, int c, int* block_out) {
+  const int nG = d < 2 ? 2 : d;
+  size_t sm = gen_smem(nG, c, kGenWarps);
+  cudaFuncSetAttribute(walk_generic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  int nb = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, walk_generic_kernel, 32 * kGenWarps, sm);
+  *block_out = 32 * kGenWarps;
+  return nb;
+}
+
+cudaError_t walk_generic_launch(const WalkParams& p, int grid, cudaStream_t st, int* block_out) {
+  const int nG = p.mode == MODE_LD ? p.d : 2;
+  size_t sm = gen_smem(nG, p.c, kGenWarps);
+  cudaError_t e = cudaFuncSetAttribute(walk_generic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  walk_generic_kernel<<<grid, 32 * kGenWarps, sm, st>>>(p);
+  *block_out = 32 * kGenWarps;
+  return cudaGetLastError();
+}
+
+cudaError_t recover_launch(const WalkParams& p, unsigned long long* lex_out, cudaStream_t st) {
+  const int nG = p.mode == MODE_LD ? p.d : 2;
+  size_t sm = gen_smem(nG, p.c, kGenWarps);
+  cudaError_t e = cudaFuncSetAttribute(recover_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  // enough warps to split even a 2^20-word unit into ~1k-word chunks
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  recover_kernel<<<nsm * 2, 32 * kGenWarps, sm, st>>>(p, lex_out);
+  return cudaGetLastError();
+}
+
+cudaError_t trace_launch(const WalkParams& p, int64_t max_steps, int64_t* values, int8_t* digits,
+                         cudaStream_t st) {
+  const int nG = p.mode == MODE_LD ? p.d : 2;
+  size_t sm = gen_smem(nG, p.c, 1);
+  cudaError_t e = cudaFuncSetAttribute(trace_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  trace_kernel<<<1, 32, sm, st>>>(p, max_steps, values, digits);
+  return cudaGetLastError();
+}
+
+}  // namespace lnorm

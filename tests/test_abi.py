@@ -1,0 +1,140 @@
+"""C-ABI library: loads, exports every declared symbol, host-side helpers (-m "not gpu").
+
+The Gray-code helpers are the same __host__ __device__ code the kernels run
+(paper_2503_21596_b200/csrc/gray.cuh); they are pinned here to the paper's
+Tables 1 and 3 and to its appendix lemmas.
+"""
+import json
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2503_21596_b200 as L
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLD = os.path.join(ROOT, "tests", "golden")
+
+
+def header_functions():
+    txt = open(os.path.join(ROOT, "include", "lnorm.h")).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(lnorm_[a-z_]+)\s*\(", txt)))
+
+
+def test_library_exports_every_header_symbol():
+    lib = L.load()
+    funcs = header_functions()
+    assert len(funcs) >= 14
+    for f in funcs:
+        assert hasattr(lib, f), f
+    assert sorted(funcs) == sorted(L.SYMBOLS)
+    assert L.load().lnorm_version() >> 16 == 1
+
+
+def test_status_strings():
+    for s in range(8):
+        assert L.status_string(s)
+
+
+def gray_word(d, h, j):
+    return [L.gray_digit(d, i, j) for i in range(h)]
+
+
+def test_table1_brgc():
+    g = json.load(open(os.path.join(GOLD, "gray_tables.json")))
+    rows = g["brgc4_rows_i3_to_i0"]
+    for j in range(16):
+        for i in range(4):
+            assert L.gray_digit(2, i, j) == rows[3 - i][j]
+    # bottom row of Table 1: digit and direction of the change (word 0 compares with word 15)
+    for j in range(1, 16):
+        dig, frm, to = L.gray_change(2, j)
+        mark = g["brgc4_change"][j]
+        assert dig == int(mark[0]) and (to == 1) == (mark[1] == "+") and frm == 1 - to
+
+
+def test_table3_trgc():
+    g = json.load(open(os.path.join(GOLD, "gray_tables.json")))
+    rows = g["trgc3_rows_i2_to_i0"]
+    for j in range(27):
+        for i in range(3):
+            assert L.gray_digit(3, i, j) == rows[2 - i][j]
+    for j in range(1, 27):
+        assert L.gray_change(3, j)[0] == g["trgc3_change_from_word1"][j - 1]
+
+
+def reflect_construct(d, h):
+    """Recursive reflected construction (Table 4, d-ary analogue): words as digit tuples."""
+    if h == 0:
+        return [()]
+    prev = reflect_construct(d, h - 1)
+    out = []
+    for a in range(d):
+        seq = prev if a % 2 == 0 else prev[::-1]
+        out += [w + (a,) for w in seq]   # new most-significant digit
+    return out
+
+
+@pytest.mark.parametrize("d,h", [(2, 1), (2, 4), (2, 9), (3, 3), (3, 6), (4, 4), (5, 3)])
+def test_closed_form_equals_reflection_and_hamming(d, h):
+    words = reflect_construct(d, h)
+    assert len(set(words)) == d ** h
+    for j, w in enumerate(words):
+        assert tuple(gray_word(d, h, j)) == w
+        if j:
+            diff = [i for i in range(h) if w[i] != words[j - 1][i]]
+            assert len(diff) == 1
+            dig, frm, to = L.gray_change(d, j)
+            assert diff == [dig] and frm == words[j - 1][dig] and to == w[dig] and abs(to - frm) == 1
+
+
+@pytest.mark.parametrize("d,h,l", [(2, 6, 2), (2, 8, 3), (3, 5, 2), (4, 4, 1)])
+def test_appendix_e_group_alignment(d, h, l):
+    # for k > 0 the change digit of word g*d^(h-l)+k does not depend on g
+    for k in range(1, d ** (h - l)):
+        digs = {L.gray_change(d, g * d ** (h - l) + k)[0] for g in range(d ** l)}
+        assert len(digs) == 1
+
+
+def test_eq16_equals_eq17_and_ctz():
+    for d in (2, 3, 5):
+        for j in range(1, 2000):
+            i16 = max(i for i in range(40) if j % d ** i == 0)
+            assert L.gray_change(d, j)[0] == i16
+    for j in range(1, 4096):
+        assert L.gray_change(2, j)[0] == (j & -j).bit_length() - 1
+
+
+def test_change_probe_count_bound():
+    # expected number of probes of Eq. (9) is sum i/2^i -> 2 (<= 2 d^h total)
+    for d in (2, 3, 4):
+        h = 8 if d == 2 else 5
+        probes = 0
+        for j in range(1, d ** h):
+            probes += L.gray_change(d, j)[0] + 1
+        assert probes <= 2 * d ** h
+
+
+def test_algorithm1_partition():
+    # examples: SPEC.md:292-294 (hand trace of Algorithm 1)
+    assert [L.partition(8, 3, t) for t in range(3)] == [(0, 2), (3, 5), (6, 7)]
+    assert [L.partition(8, 4, t) for t in range(4)] == [(0, 1), (2, 3), (4, 5), (6, 7)]
+    assert [L.partition(2, 4, t) for t in range(4)] == [(0, 0), (1, 1), (2, 1), (2, 1)]
+    for C in range(1, 200):
+        for T in (1, 2, 3, 7, 16, 40):
+            rngs = [L.partition(C, T, t) for t in range(T)]
+            covered = [j for lo, hi in rngs for j in range(lo, hi + 1)]
+            assert covered == list(range(C))
+            sizes = [hi - lo + 1 for lo, hi in rngs]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def test_no_device_fails_loudly():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("device present")
+    with pytest.raises(L.LNormError) as e:
+        L.compute(np.eye(3, dtype=np.int32))
+    assert e.value.name == "ENODEV"
