@@ -67,7 +67,25 @@ struct Problem {
   int dl = 2;           // labels walked: 2 for +-1 strategies, else effective d
   bool transposed = false;
   int r = 0, c = 0;     // enumerated rows / columns
+  bool fits16 = false;  // packed 16-bit path is exact (DESIGN.md "Packed path" guard)
 };
+
+// Packed guard: for each parity class of the packed columns,
+// sum over its columns of sum_x |M_xy| <= 32767 bounds every 16-bit column sum and
+// every accumulator half.  M is the caller's n x m matrix; p gives the orientation.
+bool packed_guard(const int32_t* M, int m, const Problem& p) {
+  int64_t par[2] = {0, 0};
+  const int c0 = p.mode == MODE_MARG ? 1 : 0;
+  for (int y = c0; y < p.c; ++y) {
+    int64_t ca = 0;
+    for (int x = 0; x < p.r; ++x) {
+      int64_t v = p.transposed ? M[(int64_t)y * m + x] : M[(int64_t)x * m + y];
+      ca += v < 0 ? -v : v;
+    }
+    par[(y - c0) & 1] += ca;
+  }
+  return par[0] <= 32767 && par[1] <= 32767;
+}
 
 int validate(const int32_t* M, int n, int m, int d, int marg, Problem* pr) {
   if (!M || n < 1 || m < 1 || d < 1 || d > kMaxD || (marg != 0 && marg != 1)) return LNORM_EINVAL;
@@ -92,6 +110,7 @@ int validate(const int32_t* M, int n, int m, int d, int marg, Problem* pr) {
     p.r = n; p.c = m;                     // never transposed
   }
   if (p.r > kMaxRows - 1 || p.c > kMaxCols) return LNORM_ETOOLARGE;
+  p.fits16 = packed_guard(M, m, p);
   // search space d^(r-1) must fit a 63-bit word index
   long double space = 1;
   for (int i = 0; i < p.r - 1; ++i) space *= p.dl;
@@ -101,7 +120,16 @@ int validate(const int32_t* M, int n, int m, int d, int marg, Problem* pr) {
 }
 
 // ------------------------------------------------------------------ plan --
-enum Kernel { K_BIN = 0, K_LD = 1, K_GEN = 2 };
+enum Kernel { K_BIN = 0, K_LD = 1, K_GEN = 2, K_BIN16 = 3 };
+
+// LNORM_KERNEL=auto|int32|generic forces a kernel family (benchmarks and tests).
+int kernel_override() {
+  const char* e = getenv("LNORM_KERNEL");
+  if (!e || !*e || !strcmp(e, "auto")) return -1;
+  if (!strcmp(e, "int32")) return K_BIN;
+  if (!strcmp(e, "generic")) return K_GEN;
+  return -1;
+}
 
 struct Plan {
   int kernel = K_GEN;
@@ -158,6 +186,9 @@ int make_plan(const Problem& pr, int world, Plan* pl) {
     while (k < f - smin && k < 31 && (1LL << k) < target) ++k;
     p.k = k; p.s = f - k; p.units = 1LL << k;
     p.kernel = hot ? K_BIN : K_GEN;
+    if (hot && pr.fits16 && walk_bin16_supported(pr.mode, pr.c, p.s)) p.kernel = K_BIN16;
+    const int ov = kernel_override();
+    if (ov == K_GEN || (ov == K_BIN && hot)) p.kernel = ov;
   } else {
     const int d = pr.dl;
     const bool hot = walk_ld_supported(d, pr.c, 1) && f >= 1;
@@ -168,6 +199,7 @@ int make_plan(const Problem& pr, int world, Plan* pl) {
     rgs_enumerate(k + 1, d, p.table, kTableCap + 1);
     p.units = (int64_t)p.table.size();
     p.kernel = hot ? K_LD : K_GEN;
+    if (kernel_override() == K_GEN) p.kernel = K_GEN;
   }
   // per-unit word count must fit 32-bit block counters
   long double words = 1;
@@ -312,6 +344,7 @@ struct RunOut {
 int launch_walk(DevCtx& cx, const Problem& pr, const Plan& pl, WalkParams& wp, int* grid_out, int* block_out) {
   int block = 128, occ = 0;
   if (pl.kernel == K_BIN) occ = walk_bin_occupancy(pr.mode, pr.c, &block);
+  else if (pl.kernel == K_BIN16) occ = walk_bin16_occupancy(pr.mode, pr.c, pl.k, pl.s, &block);
   else if (pl.kernel == K_LD) occ = walk_ld_occupancy(pr.dl, pr.c, &block);
   else occ = walk_generic_occupancy(pr.dl, pr.c, &block);
   if (occ < 1) occ = 1;
@@ -320,6 +353,7 @@ int launch_walk(DevCtx& cx, const Problem& pr, const Plan& pl, WalkParams& wp, i
   int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)occ * cx.nsm, want));
   cudaError_t e;
   if (pl.kernel == K_BIN) e = walk_bin_launch(wp, cx.dTab, grid, cx.stream, &block);
+  else if (pl.kernel == K_BIN16) e = walk_bin16_launch(wp, cx.dTab, grid, cx.stream, &block);
   else if (pl.kernel == K_LD) e = walk_ld_launch(wp, cx.dTab, grid, cx.stream, &block);
   else e = walk_generic_launch(wp, grid, cx.stream, &block);
   if (e != cudaSuccess) { (void)cudaGetLastError(); return LNORM_ECUDA; }
@@ -601,6 +635,7 @@ int lnorm_prefix_maxima(const int32_t* M, int32_t n, int32_t m, int32_t d, int32
   // no orientation, no label reduction: the hook walks exactly the suffix of the given rows
   pr.transposed = false; pr.r = n; pr.c = m;
   pr.dl = d == 1 ? 2 : d;
+  pr.fits16 = packed_guard(M, m, pr);
   if (pr.r > kMaxRows - 1 || pr.c > kMaxCols) return LNORM_ETOOLARGE;
   const int base = pr.dl;
   Plan pl;
@@ -618,7 +653,12 @@ int lnorm_prefix_maxima(const int32_t* M, int32_t n, int32_t m, int32_t d, int32
     }
     pl.table[i] = w;
   }
-  if (base == 2) pl.kernel = walk_bin_supported(pr.mode, pr.c, pl.s) ? K_BIN : K_GEN;
+  if (base == 2) {
+    pl.kernel = walk_bin_supported(pr.mode, pr.c, pl.s) ? K_BIN : K_GEN;
+    if (pl.kernel == K_BIN && pr.fits16 && walk_bin16_supported(pr.mode, pr.c, pl.s)) pl.kernel = K_BIN16;
+    const int ov = kernel_override();
+    if (ov == K_GEN || (ov == K_BIN && pl.kernel != K_GEN)) pl.kernel = ov;
+  }
   else pl.kernel = walk_ld_supported(base, pr.c, pl.s) ? K_LD : K_GEN;
   long double words = 1;
   for (int i = 0; i < pl.s; ++i) words *= base;

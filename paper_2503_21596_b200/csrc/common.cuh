@@ -76,6 +76,13 @@ cudaError_t walk_bin_launch(const WalkParams& p, int32_t* scratch_tab, int grid,
 int walk_bin_occupancy(int mode, int c, int* block_out);
 template <int MODE> cudaError_t walk_bin_launch_mode(const WalkParams& p, int32_t* scratch_tab, int grid, cudaStream_t st);
 template <int MODE> int walk_bin_occupancy_mode(int c);
+// Packed 16-bit binary walk (exactness guard checked by the caller).
+bool walk_bin16_supported(int mode, int c, int s);
+cudaError_t walk_bin16_launch(const WalkParams& p, int32_t* scratch_tab, int grid, cudaStream_t st, int* block_out);
+int walk_bin16_occupancy(int mode, int c, int k, int s, int* block_out);
+template <int MODE> int walk_bin16_words(int c);
+template <int MODE> cudaError_t walk_bin16_launch_mode(const WalkParams& p, int32_t* scratch_tab, int grid, cudaStream_t st);
+template <int MODE> int walk_bin16_occupancy_mode(int c, int k, int s);
 // Hot d-ary walk (L_d, d in {3,4}).
 bool walk_ld_supported(int d, int c, int s);
 cudaError_t walk_ld_launch(const WalkParams& p, int32_t* scratch_tab, int grid, cudaStream_t st,

@@ -25,4 +25,26 @@ cudaError_t walk_bin_launch(const WalkParams& p, int32_t* scratch_tab, int grid,
   return walk_bin_launch_mode<MODE_LD>(p, scratch_tab, grid, st);
 }
 
+bool walk_bin16_supported(int mode, int c, int s) {
+  if (s < 4) return false;
+  if (mode == MODE_L1) return walk_bin16_words<MODE_L1>(c) > 0;
+  if (mode == MODE_MARG) return c >= 2 && walk_bin16_words<MODE_MARG>(c) > 0;
+  if (mode == MODE_LD) return walk_bin16_words<MODE_LD>(c) > 0;
+  return false;
+}
+
+int walk_bin16_occupancy(int mode, int c, int k, int s, int* block_out) {
+  *block_out = 32;
+  if (mode == MODE_L1) return walk_bin16_occupancy_mode<MODE_L1>(c, k, s);
+  if (mode == MODE_MARG) return walk_bin16_occupancy_mode<MODE_MARG>(c, k, s);
+  return walk_bin16_occupancy_mode<MODE_LD>(c, k, s);
+}
+
+cudaError_t walk_bin16_launch(const WalkParams& p, int32_t* scratch_tab, int grid, cudaStream_t st, int* block_out) {
+  *block_out = 32;
+  if (p.mode == MODE_L1) return walk_bin16_launch_mode<MODE_L1>(p, scratch_tab, grid, st);
+  if (p.mode == MODE_MARG) return walk_bin16_launch_mode<MODE_MARG>(p, scratch_tab, grid, st);
+  return walk_bin16_launch_mode<MODE_LD>(p, scratch_tab, grid, st);
+}
+
 }  // namespace lnorm

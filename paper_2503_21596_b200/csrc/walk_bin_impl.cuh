@@ -35,7 +35,8 @@ constexpr int K = 4;                      // statically unrolled low suffix digi
 constexpr int kTabInts = 8448;            // (2*s + k + 3) * C <= (2*63 + 3) * 64 + slack
 constexpr int kBlock = 32;   // one warp per block (see the schedule comment in the kernel)
 
-__host__ __device__ constexpr int cctz(int j) { return (j & 1) ? 0 : 1 + cctz(j >> 1); }
+// ctz for the unrolled step index j in [1, 16): a ternary chain that folds at compile time
+__host__ __device__ constexpr int cctz(int j) { return (j & 1) ? 0 : (j & 2) ? 1 : (j & 4) ? 2 : 3; }
 
 // Layout (ints): [0, 2sC): delta rows, index (2b + sign) * C  (sign 1: flip to -1 / label 1)
 //                [2sC, 2sC + (k+1)C): prefix rows 0..k (raw M)
