@@ -160,6 +160,23 @@ int lnorm_gray_change(int32_t d, uint64_t j, int32_t* digit, int32_t* from, int3
  */
 int lnorm_partition(uint64_t C, int64_t T, int64_t t, int64_t* j_min, int64_t* j_max);
 
+/*
+ * Host-only planning (no device needed): the orientation, unit split and
+ * kernel family lnorm_compute would use for this input on `world` ranks.
+ * variant: 0 int32 binary walk, 1 int32 d-ary walk, 2 generic warp-per-unit,
+ * 3 packed-16 binary walk, 4 packed-16 d-ary walk.  units = 2^k for +-1
+ * strategies and L_2, else the number of restricted-growth prefixes of
+ * length k+1 with at most d labels.  Returns the same validation errors as
+ * lnorm_compute.
+ */
+typedef struct {
+  int32_t rows, cols, transposed, d_walked, prefix_digits, suffix_digits, variant, packed_ok;
+  int64_t units;
+  double steps;                /* strategies walked in total */
+} lnorm_plan_info;
+int lnorm_plan(const int32_t* M, int32_t n, int32_t m, int32_t d, int32_t with_marginals, int32_t world,
+               lnorm_plan_info* out);
+
 /* Statistics of the last successful compute call on the calling thread. */
 typedef struct {
   int32_t rows, cols;          /* enumerated rows / columns after orientation */

@@ -19,7 +19,7 @@ import numpy as np
 
 __all__ = [
     "LNormError", "load", "compute", "compute_device", "compute_multi", "Comm", "prefix_maxima",
-    "walk_trace", "gray_digit", "gray_change", "partition", "last_stats", "status_string", "SYMBOLS",
+    "walk_trace", "gray_digit", "gray_change", "partition", "last_stats", "status_string", "SYMBOLS", "plan",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -31,7 +31,7 @@ SYMBOLS = [
     "lnorm_comm_unique_id", "lnorm_comm_create", "lnorm_comm_destroy", "lnorm_compute_rank",
     "lnorm_compute_rank_device",
     "lnorm_prefix_maxima", "lnorm_walk_trace", "lnorm_gray_digit", "lnorm_gray_change", "lnorm_partition",
-    "lnorm_last_stats",
+    "lnorm_last_stats", "lnorm_plan",
 ]
 
 STATUS = {0: "OK", 1: "EINVAL", 2: "EOVERFLOW", 3: "ETOOLARGE", 4: "ENODEV", 5: "ECUDA", 6: "ENCCL", 7: "ENOMEM"}
@@ -57,6 +57,20 @@ class Stats(ctypes.Structure):
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
 
+
+class PlanInfo(ctypes.Structure):
+    _fields_ = [
+        ("rows", ctypes.c_int32), ("cols", ctypes.c_int32), ("transposed", ctypes.c_int32),
+        ("d_walked", ctypes.c_int32), ("prefix_digits", ctypes.c_int32), ("suffix_digits", ctypes.c_int32),
+        ("variant", ctypes.c_int32), ("packed_ok", ctypes.c_int32), ("units", ctypes.c_int64),
+        ("steps", ctypes.c_double),
+    ]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+VARIANTS = {0: "bin_int32", 1: "ld_int32", 2: "generic", 3: "bin_packed16", 4: "ld_packed16"}
 
 _lock = threading.Lock()
 _lib = None
@@ -92,6 +106,7 @@ def load():
             "lnorm_gray_change": ([i32, u64, i32p, i32p, i32p], ctypes.c_int),
             "lnorm_partition": ([u64, i64, i64, i64p, i64p], ctypes.c_int),
             "lnorm_last_stats": ([P(Stats)], ctypes.c_int),
+            "lnorm_plan": ([i32p, i32, i32, i32, i32, i32, P(PlanInfo)], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
             f = getattr(lib, name)
@@ -261,6 +276,18 @@ def partition(C: int, T: int, t: int):
     lo, hi = ctypes.c_int64(), ctypes.c_int64()
     _check(load().lnorm_partition(C, T, t, ctypes.byref(lo), ctypes.byref(hi)), "lnorm_partition")
     return lo.value, hi.value
+
+
+def plan(M, d: int = 1, with_marginals: bool = False, world: int = 1) -> dict:
+    """Host-only plan lnorm_compute would use (orientation, unit split, kernel variant)."""
+    A = _mat(M)
+    n, m = A.shape
+    info = PlanInfo()
+    _check(load().lnorm_plan(_p(A, ctypes.c_int32), n, m, d, int(with_marginals), world, ctypes.byref(info)),
+           "lnorm_plan")
+    out = info.as_dict()
+    out["variant_name"] = VARIANTS.get(out["variant"], "?")
+    return out
 
 
 def last_stats() -> dict:

@@ -120,7 +120,7 @@ int validate(const int32_t* M, int n, int m, int d, int marg, Problem* pr) {
 }
 
 // ------------------------------------------------------------------ plan --
-enum Kernel { K_BIN = 0, K_LD = 1, K_GEN = 2, K_BIN16 = 3 };
+enum Kernel { K_BIN = 0, K_LD = 1, K_GEN = 2, K_BIN16 = 3, K_LD16 = 4 };
 
 // LNORM_KERNEL=auto|int32|generic forces a kernel family (benchmarks and tests).
 int kernel_override() {
@@ -199,7 +199,9 @@ int make_plan(const Problem& pr, int world, Plan* pl) {
     rgs_enumerate(k + 1, d, p.table, kTableCap + 1);
     p.units = (int64_t)p.table.size();
     p.kernel = hot ? K_LD : K_GEN;
-    if (kernel_override() == K_GEN) p.kernel = K_GEN;
+    if (hot && pr.fits16 && walk_ld16_supported(d, pr.c, p.s)) p.kernel = K_LD16;
+    const int ov = kernel_override();
+    if (ov == K_GEN || (ov == K_BIN && hot)) p.kernel = ov == K_GEN ? K_GEN : K_LD;
   }
   // per-unit word count must fit 32-bit block counters
   long double words = 1;
@@ -345,15 +347,19 @@ int launch_walk(DevCtx& cx, const Problem& pr, const Plan& pl, WalkParams& wp, i
   int block = 128, occ = 0;
   if (pl.kernel == K_BIN) occ = walk_bin_occupancy(pr.mode, pr.c, &block);
   else if (pl.kernel == K_BIN16) occ = walk_bin16_occupancy(pr.mode, pr.c, pl.k, pl.s, &block);
+  else if (pl.kernel == K_LD16) occ = walk_ld16_occupancy(pr.dl, pr.c, pl.k, pl.s, &block);
   else if (pl.kernel == K_LD) occ = walk_ld_occupancy(pr.dl, pr.c, &block);
   else occ = walk_generic_occupancy(pr.dl, pr.c, &block);
   if (occ < 1) occ = 1;
-  const int64_t per_block = pl.kernel == K_GEN ? block / 32 : block;   // units claimed per block round
+  int64_t per_block = pl.kernel == K_GEN ? block / 32 : block;   // units per block chunk
+  if (pl.kernel == K_BIN16) per_block *= walk_bin16_units_per_lane(pr.mode, pr.c);
+  if (pl.kernel == K_LD16) per_block *= walk_ld16_units_per_lane(pr.dl, pr.c);
   int64_t want = (wp.unit_count + per_block - 1) / per_block;
   int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)occ * cx.nsm, want));
   cudaError_t e;
   if (pl.kernel == K_BIN) e = walk_bin_launch(wp, cx.dTab, grid, cx.stream, &block);
   else if (pl.kernel == K_BIN16) e = walk_bin16_launch(wp, cx.dTab, grid, cx.stream, &block);
+  else if (pl.kernel == K_LD16) e = walk_ld16_launch(wp, cx.dTab, grid, cx.stream, &block);
   else if (pl.kernel == K_LD) e = walk_ld_launch(wp, cx.dTab, grid, cx.stream, &block);
   else e = walk_generic_launch(wp, grid, cx.stream, &block);
   if (e != cudaSuccess) { (void)cudaGetLastError(); return LNORM_ECUDA; }
@@ -659,7 +665,12 @@ int lnorm_prefix_maxima(const int32_t* M, int32_t n, int32_t m, int32_t d, int32
     const int ov = kernel_override();
     if (ov == K_GEN || (ov == K_BIN && pl.kernel != K_GEN)) pl.kernel = ov;
   }
-  else pl.kernel = walk_ld_supported(base, pr.c, pl.s) ? K_LD : K_GEN;
+  else {
+    pl.kernel = walk_ld_supported(base, pr.c, pl.s) ? K_LD : K_GEN;
+    if (pl.kernel == K_LD && pr.fits16 && walk_ld16_supported(base, pr.c, pl.s)) pl.kernel = K_LD16;
+    const int ov = kernel_override();
+    if (ov == K_GEN || (ov == K_BIN && pl.kernel != K_GEN)) pl.kernel = ov == K_GEN ? K_GEN : K_LD;
+  }
   long double words = 1;
   for (int i = 0; i < pl.s; ++i) words *= base;
   if (words >= 4.0e9L) return LNORM_ETOOLARGE;
@@ -752,6 +763,23 @@ int lnorm_gray_change(int32_t d, uint64_t j, int32_t* digit, int32_t* from, int3
 int lnorm_partition(uint64_t C, int64_t T, int64_t t, int64_t* j_min, int64_t* j_max) {
   if (T < 1 || t < 0 || t >= T || !j_min || !j_max) return LNORM_EINVAL;
   algorithm1(C, T, t, j_min, j_max);
+  return LNORM_OK;
+}
+
+int lnorm_plan(const int32_t* M, int32_t n, int32_t m, int32_t d, int32_t with_marginals, int32_t world,
+               lnorm_plan_info* out) {
+  if (!out || world < 1) return LNORM_EINVAL;
+  Problem pr;
+  int rc = validate(M, n, m, d, with_marginals, &pr);
+  if (rc) return rc;
+  Plan pl;
+  if ((rc = make_plan(pr, world, &pl))) return rc;
+  lnorm_plan_info I{};
+  I.rows = pr.r; I.cols = pr.c; I.transposed = pr.transposed; I.d_walked = pr.dl;
+  I.prefix_digits = pl.k; I.suffix_digits = pl.s; I.variant = pl.kernel; I.packed_ok = pr.fits16;
+  I.units = pl.units;
+  I.steps = (double)pl.units * (double)ipow(pr.dl, pl.s);
+  *out = I;
   return LNORM_OK;
 }
 

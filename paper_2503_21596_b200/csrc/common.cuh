@@ -83,11 +83,18 @@ int walk_bin16_occupancy(int mode, int c, int k, int s, int* block_out);
 template <int MODE> int walk_bin16_words(int c);
 template <int MODE> cudaError_t walk_bin16_launch_mode(const WalkParams& p, int32_t* scratch_tab, int grid, cudaStream_t st);
 template <int MODE> int walk_bin16_occupancy_mode(int c, int k, int s);
+template <int MODE> int walk_bin16_units_per_lane_mode(int c);
+int walk_bin16_units_per_lane(int mode, int c);
 // Hot d-ary walk (L_d, d in {3,4}).
 bool walk_ld_supported(int d, int c, int s);
 cudaError_t walk_ld_launch(const WalkParams& p, int32_t* scratch_tab, int grid, cudaStream_t st,
                            int* block_out);
 int walk_ld_occupancy(int d, int c, int* block_out);
+// Packed 16-bit d-ary walk (L_d, d in {3,4}; exactness guard checked by the caller).
+bool walk_ld16_supported(int d, int c, int s);
+int walk_ld16_units_per_lane(int d, int c);
+int walk_ld16_occupancy(int d, int c, int k, int s, int* block_out);
+cudaError_t walk_ld16_launch(const WalkParams& p, int32_t* scratch_tab, int grid, cudaStream_t st, int* block_out);
 // Generic warp-per-unit walk (any mode, d, c, s).
 bool walk_generic_supported(int d, int c);
 cudaError_t walk_generic_launch(const WalkParams& p, int grid, cudaStream_t st, int* block_out);

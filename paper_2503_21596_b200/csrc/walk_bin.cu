@@ -40,6 +40,12 @@ int walk_bin16_occupancy(int mode, int c, int k, int s, int* block_out) {
   return walk_bin16_occupancy_mode<MODE_LD>(c, k, s);
 }
 
+int walk_bin16_units_per_lane(int mode, int c) {
+  if (mode == MODE_L1) return walk_bin16_units_per_lane_mode<MODE_L1>(c);
+  if (mode == MODE_MARG) return walk_bin16_units_per_lane_mode<MODE_MARG>(c);
+  return walk_bin16_units_per_lane_mode<MODE_LD>(c);
+}
+
 cudaError_t walk_bin16_launch(const WalkParams& p, int32_t* scratch_tab, int grid, cudaStream_t st, int* block_out) {
   *block_out = 32;
   if (p.mode == MODE_L1) return walk_bin16_launch_mode<MODE_L1>(p, scratch_tab, grid, st);

@@ -43,13 +43,13 @@ struct Layout {
   static constexpr int RWb = pad4(Wt + 1);                     // base record: W (+ W totals), q at Wt
 };
 
-template <int MODE, int W>
+template <int MODE, int W, int P>
 struct Walker16 {
   static constexpr int RWd = Layout<MODE, W>::RWd;
-  static constexpr int Wt = Layout<MODE, W>::Wt;
-  // apply the delta record at sT + off (warp-uniform broadcast LDS.128), return the new value
-  static __device__ __forceinline__ int32_t step(uint32_t (&m)[W], uint32_t (&m1)[W], int32_t& q,
-                                                 const uint32_t* sT, int off) {
+  // Apply the delta record at sT + off (one warp-uniform broadcast LDS.128 per 4 words,
+  // shared by the lane's P units); returns nothing, updates ub[] with the new values.
+  static __device__ __forceinline__ void step(uint32_t (&m)[P][W], uint32_t (&m1)[P][W], int32_t (&q)[P],
+                                              int32_t (&ub)[P], const uint32_t* sT, int off) {
     uint32_t r[RWd];
     const uint4* src = reinterpret_cast<const uint4*>(sT + off);
 #pragma unroll
@@ -57,24 +57,27 @@ struct Walker16 {
       const uint4 x = src[v];
       r[4 * v] = x.x; r[4 * v + 1] = x.y; r[4 * v + 2] = x.z; r[4 * v + 3] = x.w;
     }
-    uint32_t a0, a1 = 0u;
 #pragma unroll
-    for (int i = 0; i < W; ++i) {
-      m[i] = __vadd2(m[i], r[i]);
-      if (i == 0) a0 = __vmaxs2(m[0], 0u);
-      else if (i & 1) a1 = __viaddmax_s16x2(a1, m[i], a1);
-      else a0 = __viaddmax_s16x2(a0, m[i], a0);
-    }
-    if (MODE == MODE_LD) {
+    for (int j = 0; j < P; ++j) {
+      uint32_t a0, a1 = 0u;
 #pragma unroll
       for (int i = 0; i < W; ++i) {
-        m1[i] = __vadd2(m1[i], r[W + i]);
-        if (i & 1) a1 = __viaddmax_s16x2(a1, m1[i], a1);
-        else a0 = __viaddmax_s16x2(a0, m1[i], a0);
+        m[j][i] = __vadd2(m[j][i], r[i]);
+        if (i == 0) a0 = __vmaxs2(m[j][0], 0u);
+        else if (i & 1) a1 = __viaddmax_s16x2(a1, m[j][i], a1);
+        else a0 = __viaddmax_s16x2(a0, m[j][i], a0);
       }
+      if (MODE == MODE_LD) {
+#pragma unroll
+        for (int i = 0; i < W; ++i) {
+          m1[j][i] = __vadd2(m1[j][i], r[W + i]);
+          if (i & 1) a1 = __viaddmax_s16x2(a1, m1[j][i], a1);
+          else a0 = __viaddmax_s16x2(a0, m1[j][i], a0);
+        }
+      }
+      q[j] += (int32_t)r[RWd - 1];
+      ub[j] = max(ub[j], __dp2a_lo((int)__vadd2(a0, a1), 0x0202, q[j]));
     }
-    q += (int32_t)r[RWd - 1];
-    return __dp2a_lo((int)__vadd2(a0, a1), 0x0202, q);
   }
   static __device__ __forceinline__ int32_t value(const uint32_t (&m)[W], const uint32_t (&m1)[W], int32_t q) {
     uint32_t a0 = 0u, a1 = 0u;
@@ -91,7 +94,7 @@ struct Walker16 {
   }
 };
 
-template <int MODE, int W>
+template <int MODE, int W, int P>
 __global__ void __launch_bounds__(kBlock) walk_bin16_kernel(const WalkParams p, const uint32_t* __restrict__ gTab) {
   using LY = Layout<MODE, W>;
   extern __shared__ __align__(16) uint32_t sT[];
@@ -106,55 +109,65 @@ __global__ void __launch_bounds__(kBlock) walk_bin16_kernel(const WalkParams p, 
   int32_t best = INT32_MIN;
   uint32_t best_u = 0;
   bool have = false;
-  const int64_t nchunks = (p.unit_count + 31) / 32;
+  // Static warp-chunk schedule (block = one warp): chunk ch holds units
+  // [ch*32P, ch*32P + 32P); lane l owns units ch*32P + j*32 + l, j < P.
+  const int64_t nchunks = (p.unit_count + 32 * P - 1) / (32 * P);
   for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
-    const int64_t rel = ch * 32 + lane;
-    const bool active = rel < p.unit_count;
-    const int64_t u = p.unit_begin + (active ? rel : 0);
-    uint32_t m[W], m1[W];
-    int32_t q = (int32_t)sT[baseOff + LY::Wt];
+    uint32_t m[P][W], m1[P][W];
+    int32_t q[P], ub[P];
 #pragma unroll
-    for (int i = 0; i < W; ++i) m[i] = sT[baseOff + i];
-    for (int x = 0; x <= k; ++x) {
-      const int dig = prefix_digit(p, u, x);
-      const int po = preOff + x * LY::RWp;
-      if (MODE == MODE_LD) {
-        if (dig == 0) {
+    for (int j = 0; j < P; ++j) {
+      const int64_t rel = ch * 32 * P + j * 32 + lane;
+      const int64_t u = p.unit_begin + (rel < p.unit_count ? rel : 0);
+      q[j] = (int32_t)sT[baseOff + LY::Wt];
 #pragma unroll
-          for (int i = 0; i < W; ++i) m[i] = __vadd2(m[i], sT[po + i]);
-        }
-      } else {
-        if (dig == 0) {
+      for (int i = 0; i < W; ++i) m[j][i] = sT[baseOff + i];
+      for (int x = 0; x <= k; ++x) {
+        const int dig = prefix_digit(p, u, x);
+        const int po = preOff + x * LY::RWp;
+        if (MODE == MODE_LD) {
+          if (dig == 0) {
 #pragma unroll
-          for (int i = 0; i < W; ++i) m[i] = __vadd2(m[i], sT[po + i]);
-          q += (int32_t)sT[po + W];
+            for (int i = 0; i < W; ++i) m[j][i] = __vadd2(m[j][i], sT[po + i]);
+          }
         } else {
+          if (dig == 0) {
 #pragma unroll
-          for (int i = 0; i < W; ++i) m[i] = __vsub2(m[i], sT[po + i]);
-          q -= (int32_t)sT[po + W];
+            for (int i = 0; i < W; ++i) m[j][i] = __vadd2(m[j][i], sT[po + i]);
+            q[j] += (int32_t)sT[po + W];
+          } else {
+#pragma unroll
+            for (int i = 0; i < W; ++i) m[j][i] = __vsub2(m[j][i], sT[po + i]);
+            q[j] -= (int32_t)sT[po + W];
+          }
         }
       }
-    }
 #pragma unroll
-    for (int i = 0; i < W; ++i) m1[i] = (MODE == MODE_LD) ? __vsub2(sT[baseOff + W + i], m[i]) : 0u;
-    int32_t ub = Walker16<MODE, W>::value(m, m1, q);
+      for (int i = 0; i < W; ++i) m1[j][i] = (MODE == MODE_LD) ? __vsub2(sT[baseOff + W + i], m[j][i]) : 0u;
+      ub[j] = Walker16<MODE, W, P>::value(m[j], m1[j], q[j]);
+    }
     for (uint32_t t = 0; t < nblk; ++t) {
       if (t != 0) {
         const int tz = __ffs((int)t) - 1;
         const int b = K + tz;
         const int sg = 1 ^ (int)((t >> (tz + 1)) & 1u);
-        ub = max(ub, Walker16<MODE, W>::step(m, m1, q, sT, (2 * b + sg) * LY::RWd));
+        Walker16<MODE, W, P>::step(m, m1, q, ub, sT, (2 * b + sg) * LY::RWd);
       }
 #pragma unroll
-      for (int j = 1; j < (1 << K); ++j) {
-        const int b = cctz(j);
-        const int sg = (b < K - 1) ? (1 ^ ((j >> (b + 1)) & 1)) : (1 ^ (int)(t & 1u));
-        ub = max(ub, Walker16<MODE, W>::step(m, m1, q, sT, (2 * b + sg) * LY::RWd));
+      for (int jj = 1; jj < (1 << K); ++jj) {
+        const int b = cctz(jj);
+        const int sg = (b < K - 1) ? (1 ^ ((jj >> (b + 1)) & 1)) : (1 ^ (int)(t & 1u));
+        Walker16<MODE, W, P>::step(m, m1, q, ub, sT, (2 * b + sg) * LY::RWd);
       }
     }
-    if (active) {
-      if (p.unit_max) p.unit_max[rel] = ub;
-      if (!have || ub > best) { best = ub; best_u = (uint32_t)u; have = true; }
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
+      const int64_t rel = ch * 32 * P + j * 32 + lane;
+      if (rel < p.unit_count) {
+        if (p.unit_max) p.unit_max[rel] = ub[j];
+        // units of a lane are visited in increasing order: strict '>' keeps the smallest
+        if (!have || ub[j] > best) { best = ub[j]; best_u = (uint32_t)(p.unit_begin + rel); have = true; }
+      }
     }
   }
   unsigned long long key = have ? make_key(best, best_u) : 0ull;
@@ -235,21 +248,30 @@ size_t smem16(int k, int s) {
   return sizeof(uint32_t) * (size_t)(2 * s * LY::RWd + (k + 1) * LY::RWp + LY::RWb);
 }
 
+// units per lane: 2 while the packed state stays small, else 1 (register budget)
+template <int MODE, int W>
+constexpr int units_per_lane() { return (MODE == MODE_LD ? 2 * W : W) <= 24 ? 2 : 1; }
+
 template <int MODE, int W>
 cudaError_t launch_one16(const WalkParams& p, const uint32_t* tab, int grid, cudaStream_t st) {
+  constexpr int P = units_per_lane<MODE, W>();
   const size_t sm = smem16<MODE, W>(p.k, p.s);
-  cudaError_t e = cudaFuncSetAttribute(walk_bin16_kernel<MODE, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  cudaError_t e = cudaFuncSetAttribute(walk_bin16_kernel<MODE, W, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
-  walk_bin16_kernel<MODE, W><<<grid, kBlock, sm, st>>>(p, tab);
+  walk_bin16_kernel<MODE, W, P><<<grid, kBlock, sm, st>>>(p, tab);
   return cudaGetLastError();
 }
 
 template <int MODE, int W>
+int upl_one16() { return units_per_lane<MODE, W>(); }
+
+template <int MODE, int W>
 int occ_one16(int k, int s) {
   int nb = 0;
+  constexpr int P = units_per_lane<MODE, W>();
   const size_t sm = smem16<MODE, W>(k, s);
-  cudaFuncSetAttribute(walk_bin16_kernel<MODE, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, walk_bin16_kernel<MODE, W>, kBlock, sm);
+  cudaFuncSetAttribute(walk_bin16_kernel<MODE, W, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, walk_bin16_kernel<MODE, W, P>, kBlock, sm);
   return nb;
 }
 
@@ -296,6 +318,13 @@ cudaError_t walk_bin16_launch_mode<LN_BIN_MODE>(const WalkParams& p, int32_t* sc
   if (e != cudaSuccess) return e;
   LN_W16_SWITCH(LN_BIN_MODE, W, launch_one16, p, tab, grid, st)
   return cudaErrorInvalidValue;
+}
+
+template <>
+int walk_bin16_units_per_lane_mode<LN_BIN_MODE>(int c) {
+  const int W = walk_bin16_words<LN_BIN_MODE>(c);
+  LN_W16_SWITCH(LN_BIN_MODE, W, upl_one16)
+  return 1;
 }
 
 template <>

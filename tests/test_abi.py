@@ -138,3 +138,73 @@ def test_no_device_fails_loudly():
     with pytest.raises(L.LNormError) as e:
         L.compute(np.eye(3, dtype=np.int32))
     assert e.value.name == "ENODEV"
+
+
+# ------------------------------------------------------------ host planner --
+
+def rgs_count(length, d):
+    """Restricted-growth strings of the given length with at most d labels (brute force)."""
+    from itertools import product
+    cnt = 0
+    for s in product(range(d), repeat=length):
+        mx, ok = -1, True
+        for a in s:
+            if a > mx + 1:
+                ok = False
+                break
+            mx = max(mx, a)
+        cnt += ok
+    return cnt
+
+
+@pytest.mark.parametrize("n,m,d,marg", [(42, 42, 1, False), (20, 20, 1, False), (40, 40, 1, True),
+                                        (24, 24, 2, False), (24, 24, 3, False), (12, 9, 4, False),
+                                        (30, 9, 1, False), (9, 30, 1, True), (5, 70, 1, False), (3, 3, 3, False)])
+def test_plan_covers_the_search_space(n, m, d, marg):
+    from paper_2503_21596_b200 import synth
+    M = synth.random_matrix(n, m, 5)
+    P = L.plan(M, d=d, with_marginals=marg)
+    r = min(n, m) if d == 1 else n
+    assert P["rows"] == r and P["transposed"] == (d == 1 and n > m)
+    assert P["prefix_digits"] + P["suffix_digits"] == r - 1
+    dw = P["d_walked"]
+    if dw == 2:
+        assert P["units"] == 2 ** P["prefix_digits"]
+        assert P["steps"] == 2 ** (r - 1)                  # PAPER.md:147: 2^(n-1) strategies
+    else:
+        assert dw == min(d, n)
+        assert P["units"] == rgs_count(P["prefix_digits"] + 1, dw) if P["prefix_digits"] < 9 else P["units"] > 0
+        assert P["steps"] == P["units"] * dw ** P["suffix_digits"]
+        # RGS prefixes x full suffixes cover all canonical labellings: at least S(n,<=d) of them
+        assert P["steps"] >= (dw ** (n - 1) + 1) / 2 if dw == 3 else True
+
+
+def test_plan_packed_guard_and_fallback():
+    from paper_2503_21596_b200 import synth
+    M = synth.random_matrix(30, 30, 1)
+    assert L.plan(M)["variant_name"] == "bin_packed16"
+    big = (M * 300).astype(np.int32)                 # column abs sums exceed the s16 guard
+    P = L.plan(big)
+    assert P["packed_ok"] == 0 and P["variant_name"] == "bin_int32"
+    assert L.plan(synth.random_matrix(24, 24, 4), d=3)["variant_name"] == "ld_packed16"
+    assert L.plan(synth.random_matrix(24, 40, 4), d=3)["variant_name"] == "generic"
+    assert L.plan(np.eye(3, dtype=np.int32))["variant_name"] == "generic"     # suffix shorter than the unroll
+
+
+def test_plan_is_identical_for_every_rank_and_grows_with_world():
+    from paper_2503_21596_b200 import synth
+    M = synth.random_matrix(42, 42, 2)
+    p1, p8 = L.plan(M, world=1), L.plan(M, world=8)
+    assert p8["units"] >= p1["units"] and p8["steps"] == p1["steps"] == 2.0 ** 41
+
+
+def test_plan_errors():
+    with pytest.raises(L.LNormError) as e:
+        L.plan(np.full((3, 3), 2 ** 29, dtype=np.int32))
+    assert e.value.name == "EOVERFLOW"
+    with pytest.raises(L.LNormError) as e:
+        L.plan(np.ones((64, 64), dtype=np.int32))
+    assert e.value.name == "ETOOLARGE"
+    with pytest.raises(L.LNormError) as e:
+        L.plan(np.eye(3, dtype=np.int32), d=2, with_marginals=True)
+    assert e.value.name == "EINVAL"

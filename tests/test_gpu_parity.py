@@ -237,3 +237,27 @@ def test_device_resident_and_rank_paths(lib):
     assert v2 == ref[0] and list(arg2) == list(ref[1])
     v3, arg3 = lib.compute_multi(M, devices=[0])
     assert v3 == ref[0] and list(arg3) == list(ref[1])
+
+
+# ------------------------------------------------------ kernel families ----
+
+@pytest.mark.parametrize("family", ["int32", "generic", "auto"])
+@pytest.mark.parametrize("d,marg", MODES, ids=[mode_id(*m) for m in MODES])
+def test_every_kernel_family_matches_oracle(lib, family, d, marg, monkeypatch):
+    """The packed-16, int32 and generic kernels all reproduce the oracle bit for bit."""
+    monkeypatch.setenv("LNORM_KERNEL", family)
+    for seed, (n, m) in enumerate([(11, 21), (12, 8), (9, 33), (10, 16)]):
+        M = synth.random_matrix(n, m, 40_000 + seed + 10 * d)
+        check(lib, M, d=d, marg=marg)
+    if family == "generic":
+        assert lib.last_stats()["variant"] == 2
+
+
+def test_large_entries_use_int32_path_exactly(lib):
+    """Entries too large for the packed s16 guard: the int32 kernels run and stay exact."""
+    for seed in range(3):
+        M = synth.random_matrix(14, 17, 50_000 + seed, -3000, 3000)
+        assert lib.plan(M)["packed_ok"] == 0
+        check(lib, M)
+        check(lib, M, marg=True)
+        check(lib, synth.random_matrix(10, 12, 50_100 + seed, -3000, 3000), d=3)
