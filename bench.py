@@ -39,6 +39,10 @@ CONFIGS = {
     "l3_24x24": (24, 24, 3, False, 4, "L_3 of a random 24x24 witness matrix, entries in [-10,10], seed 4"),
 }
 
+def metric_name(n, m, d, marg):
+    norm = "L_marg" if marg else ("L_1" if d == 1 else f"L_{d}")
+    return f"Gray-code steps/s (strategies evaluated per second), exact {norm} of the {n}x{m} matrix"
+
 SMI_FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -159,7 +163,7 @@ def main():
             times.append(time.perf_counter() - t0)
         T = sum(times)
         val = per_step * args.steps / T
-        line = {"metric": "Gray-code steps/s (strategies evaluated per second)", "impl": "reference",
+        line = {"metric": metric_name(n, m, d, marg), "impl": "reference",
                 "value": val, "unit": "steps/s", "n_gpus": args.gpus, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
@@ -256,7 +260,10 @@ def main():
         achieved_ops = 2.0 * col_updates / (walk_ms / 1e3) / 1e12     # Tops/s (add + |.|-accumulate)
         nsm = torch.cuda.get_device_properties(dev).multi_processor_count
         peak_mhz = load_peak_clock()
-        peak = 128.0 * nsm * peak_mhz * 1e6 * world / 1e12            # int32 lane-ops/clk/SM x SMs x f_max
+        packed = st["variant"] in (3, 4, 5, 6)                          # s16x2 kernels: 2 ops per lane-instruction
+        lanes = 128.0 * (2 if packed else 1)
+        peak = lanes * nsm * peak_mhz * 1e6 * world / 1e12             # integer lane-ops/clk/SM x SMs x f_max
+        dtype = "int16x2" if packed else "int32"
         traffic = None
         tf = os.path.join(ROOT, "profiles", "r01", "walk_traffic.json")
         if os.path.exists(tf):
@@ -265,10 +272,10 @@ def main():
             except Exception:
                 traffic = None
         line = {
-            "metric": "Gray-code steps/s (strategies evaluated per second) for the exact 42x42 L_1 search",
+            "metric": metric_name(n, m, d, marg),
             "value": val, "unit": "steps/s", "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup),
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "int32", "data": "synthetic",
+            "dtype": dtype, "data": "synthetic",
             "config": {"workload": desc, "n": n, "m": m, "d": d, "with_marginals": marg,
                        "strategies_per_step": total_steps, "parallelism": f"units split over {world} GPU(s) (Algorithm 1) + 1 NCCL all-reduce(max)",
                        "l2": "256 MiB buffer written between timed steps (flush); matrix 7 KB"},
@@ -278,10 +285,14 @@ def main():
             "e2e": {"value": e2e, "unit": "steps/s", "h2d_bytes_per_step": int(M.nbytes),
                     "d2h_bytes_per_step": 8 + n, "ms_per_step": TE / args.steps},
             "gpu_launches": int(launches),
-            "roofline": {"bound": "alu", "achieved": achieved_ops, "peak": peak, "unit": "Tops/s (int32)",
+            "roofline": {"bound": "alu", "achieved": achieved_ops, "peak": peak,
+                         "unit": "Tops/s (" + ("int16x2 SIMD lanes" if packed else "int32") + ")",
                          "frac": achieved_ops / peak, "traffic": traffic,
                          "kernel": "walk (dominant)", "walk_ms_per_launch": walk_ms,
-                         "peak_basis": f"128 int32 lane-ops/clk/SM (ALU + FMA-heavy pipes, measured 127 in profiles/r01/peaks_b4.jsonl) x {nsm} SMs x {peak_mhz:.0f} MHz",
+                         "peak_basis": (f"128 lane-instr/clk/SM (ALU + FMA-heavy integer pipes = issue limit; VIADD+VABSDIFF mix "
+                                        f"measured 127, profiles/r01/peaks_b4.jsonl) x {'2 s16 halves x ' if packed else ''}"
+                                        f"{nsm} SMs x {peak_mhz:.0f} MHz; algorithmic work = 2 ops per column update"),
+                         "kernel_variant": st["variant"],
                          "frac_at_measured_clock": (achieved_ops / (peak * (c["sm_mhz"] or peak_mhz) / peak_mhz)) if c["sm_mhz"] else None},
             "clocks": c,
             "stats": st,

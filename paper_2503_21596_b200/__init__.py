@@ -23,7 +23,7 @@ __all__ = [
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liblnorm.so")
+LIB_PATH = os.environ.get("LNORM_LIB") or os.path.join(_HERE, "liblnorm.so")   # LNORM_LIB: experiment builds
 
 # every function include/lnorm.h declares (checked by tests/test_abi.py)
 SYMBOLS = [
@@ -70,7 +70,7 @@ class PlanInfo(ctypes.Structure):
         return {f: getattr(self, f) for f, _ in self._fields_}
 
 
-VARIANTS = {0: "bin_int32", 1: "ld_int32", 2: "generic", 3: "bin_packed16", 4: "ld_packed16"}
+VARIANTS = {0: "bin_int32", 1: "ld_int32", 2: "generic", 3: "bin_packed16", 4: "ld_packed16", 5: "bin_pair16", 6: "ld_pair16"}
 
 _lock = threading.Lock()
 _lib = None

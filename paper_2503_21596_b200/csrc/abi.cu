@@ -67,7 +67,9 @@ struct Problem {
   int dl = 2;           // labels walked: 2 for +-1 strategies, else effective d
   bool transposed = false;
   int r = 0, c = 0;     // enumerated rows / columns
-  bool fits16 = false;  // packed 16-bit path is exact (DESIGN.md "Packed path" guard)
+  bool fits16 = false;  // packed 16-bit column-pair path is exact
+  bool fitsPair = false;  // strategy-paired path is exact: sum |M| <= 16383
+  bool fitsLdPair = false;  // last-row-paired d-ary path is exact: sum |M| <= 32767
 };
 
 // Packed guard: for each parity class of the packed columns,
@@ -111,6 +113,8 @@ int validate(const int32_t* M, int n, int m, int d, int marg, Problem* pr) {
   }
   if (p.r > kMaxRows - 1 || p.c > kMaxCols) return LNORM_ETOOLARGE;
   p.fits16 = packed_guard(M, m, p);
+  p.fitsPair = S <= 16383;
+  p.fitsLdPair = S <= 32767;
   // search space d^(r-1) must fit a 63-bit word index
   long double space = 1;
   for (int i = 0; i < p.r - 1; ++i) space *= p.dl;
@@ -120,14 +124,15 @@ int validate(const int32_t* M, int n, int m, int d, int marg, Problem* pr) {
 }
 
 // ------------------------------------------------------------------ plan --
-enum Kernel { K_BIN = 0, K_LD = 1, K_GEN = 2, K_BIN16 = 3, K_LD16 = 4 };
+enum Kernel { K_BIN = 0, K_LD = 1, K_GEN = 2, K_BIN16 = 3, K_LD16 = 4, K_PAIR16 = 5, K_LDPAIR16 = 6 };
 
-// LNORM_KERNEL=auto|int32|generic forces a kernel family (benchmarks and tests).
+// LNORM_KERNEL=auto|int32|packed|generic forces a kernel family (benchmarks and tests).
 int kernel_override() {
   const char* e = getenv("LNORM_KERNEL");
   if (!e || !*e || !strcmp(e, "auto")) return -1;
   if (!strcmp(e, "int32")) return K_BIN;
   if (!strcmp(e, "generic")) return K_GEN;
+  if (!strcmp(e, "packed")) return K_BIN16;
   return -1;
 }
 
@@ -180,28 +185,47 @@ int make_plan(const Problem& pr, int world, Plan* pl) {
   const int64_t target = kNominalLanes * 64 * std::max(1, world);
   Plan p;
   if (pr.dl == 2) {
+    // kernel family first (each has its own minimal suffix length), then the split
+    const int ov = kernel_override();
     const bool hot = walk_bin_supported(pr.mode, pr.c, std::min(f, 4)) && f >= 4;
-    const int smin = hot ? 4 : 0;
+    int kern = hot ? K_BIN : K_GEN;
+    int smin = hot ? 4 : 0;
+    auto min_s = [&](int kind) {
+      for (int s_ = 1; s_ <= f; ++s_) {
+        if (kind == K_PAIR16 && walk_pair16_supported(pr.mode, pr.c, s_)) return s_;
+        if (kind == K_BIN16 && walk_bin16_supported(pr.mode, pr.c, s_)) return s_;
+      }
+      return -1;
+    };
+    if (hot && ov != K_BIN && ov != K_GEN) {
+      int sp = pr.fitsPair && ov != K_BIN16 ? min_s(K_PAIR16) : -1;
+      int sb = pr.fits16 ? min_s(K_BIN16) : -1;
+      if (sp > 0) { kern = K_PAIR16; smin = sp; }
+      else if (sb > 0) { kern = K_BIN16; smin = sb; }
+    }
+    if (ov == K_GEN) { kern = K_GEN; smin = 0; }
     int k = 0;
     while (k < f - smin && k < 31 && (1LL << k) < target) ++k;
     p.k = k; p.s = f - k; p.units = 1LL << k;
-    p.kernel = hot ? K_BIN : K_GEN;
-    if (hot && pr.fits16 && walk_bin16_supported(pr.mode, pr.c, p.s)) p.kernel = K_BIN16;
-    const int ov = kernel_override();
-    if (ov == K_GEN || (ov == K_BIN && hot)) p.kernel = ov;
+    p.kernel = kern;
   } else {
     const int d = pr.dl;
+    const int ov = kernel_override();
     const bool hot = walk_ld_supported(d, pr.c, 1) && f >= 1;
-    const int smin = hot ? 1 : 0;
+    int kern = hot ? K_LD : K_GEN;
+    int smin = hot ? 1 : 0;
+    if (hot && ov != K_BIN && ov != K_GEN) {
+      if (pr.fitsLdPair && f >= 2 && walk_ldpair16_supported(d, pr.c, 2) && ov != K_BIN16) { kern = K_LDPAIR16; smin = 2; }
+      else if (pr.fits16 && walk_ld16_supported(d, pr.c, 1)) { kern = K_LD16; smin = 1; }
+    }
+    if (ov == K_GEN) { kern = K_GEN; smin = 0; }
     int k = 0;
     while (k < f - smin && (k + 2) * prefix_bits(d) <= 64 && rgs_count(k + 2, d) <= kTableCap && rgs_count(k + 1, d) < target) ++k;
     p.k = k; p.s = f - k;
     rgs_enumerate(k + 1, d, p.table, kTableCap + 1);
     p.units = (int64_t)p.table.size();
-    p.kernel = hot ? K_LD : K_GEN;
-    if (hot && pr.fits16 && walk_ld16_supported(d, pr.c, p.s)) p.kernel = K_LD16;
-    const int ov = kernel_override();
-    if (ov == K_GEN || (ov == K_BIN && hot)) p.kernel = ov == K_GEN ? K_GEN : K_LD;
+    p.kernel = kern;
+    if (kern == K_LDPAIR16 && !walk_ldpair16_supported(d, pr.c, p.s)) p.kernel = pr.fits16 && walk_ld16_supported(d, pr.c, p.s) ? K_LD16 : K_LD;
   }
   // per-unit word count must fit 32-bit block counters
   long double words = 1;
@@ -279,6 +303,7 @@ struct DevCtx {
   int32_t* dIn = nullptr; size_t capIn = 0;
   int32_t* dM = nullptr; size_t capM = 0;
   int32_t* dTab = nullptr;
+  int32_t* dInit = nullptr;
   unsigned long long* dCtl = nullptr;
   uint64_t* dPre = nullptr; size_t capPre = 0;
   int64_t* dRes = nullptr;          // [0] value, then int8 argmax[kMaxCols]
@@ -304,6 +329,7 @@ int ctx_get(int device, DevCtx** out) {
     for (auto& e : c.ev) CU(cudaEventCreate(&e));
     CU(cudaDeviceGetAttribute(&c.nsm, cudaDevAttrMultiProcessorCount, device));
     CU(cudaMalloc(&c.dTab, sizeof(int32_t) * 8448));
+    CU(cudaMalloc(&c.dInit, sizeof(int32_t) * 16384));
     CU(cudaMalloc(&c.dCtl, sizeof(unsigned long long) * 4));
     CU(cudaMalloc(&c.dRes, 8 + kMaxCols + 64));
     CU(cudaMallocHost(&c.hRes, 8 + kMaxCols + 64));
@@ -348,18 +374,24 @@ int launch_walk(DevCtx& cx, const Problem& pr, const Plan& pl, WalkParams& wp, i
   if (pl.kernel == K_BIN) occ = walk_bin_occupancy(pr.mode, pr.c, &block);
   else if (pl.kernel == K_BIN16) occ = walk_bin16_occupancy(pr.mode, pr.c, pl.k, pl.s, &block);
   else if (pl.kernel == K_LD16) occ = walk_ld16_occupancy(pr.dl, pr.c, pl.k, pl.s, &block);
+  else if (pl.kernel == K_PAIR16) occ = walk_pair16_occupancy(pr.mode, pr.c, pl.s, &block);
+  else if (pl.kernel == K_LDPAIR16) occ = walk_ldpair16_occupancy(pr.dl, pr.c, pl.s, &block);
   else if (pl.kernel == K_LD) occ = walk_ld_occupancy(pr.dl, pr.c, &block);
   else occ = walk_generic_occupancy(pr.dl, pr.c, &block);
   if (occ < 1) occ = 1;
   int64_t per_block = pl.kernel == K_GEN ? block / 32 : block;   // units per block chunk
   if (pl.kernel == K_BIN16) per_block *= walk_bin16_units_per_lane(pr.mode, pr.c);
   if (pl.kernel == K_LD16) per_block *= walk_ld16_units_per_lane(pr.dl, pr.c);
+  if (pl.kernel == K_PAIR16) per_block *= walk_pair16_units_per_lane(pr.mode, pr.c);
+  if (pl.kernel == K_LDPAIR16) per_block *= walk_ldpair16_units_per_lane(pr.dl, pr.c);
   int64_t want = (wp.unit_count + per_block - 1) / per_block;
   int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)occ * cx.nsm, want));
   cudaError_t e;
   if (pl.kernel == K_BIN) e = walk_bin_launch(wp, cx.dTab, grid, cx.stream, &block);
   else if (pl.kernel == K_BIN16) e = walk_bin16_launch(wp, cx.dTab, grid, cx.stream, &block);
   else if (pl.kernel == K_LD16) e = walk_ld16_launch(wp, cx.dTab, grid, cx.stream, &block);
+  else if (pl.kernel == K_PAIR16) e = walk_pair16_launch(wp, cx.dTab, cx.dInit, grid, cx.stream, &block);
+  else if (pl.kernel == K_LDPAIR16) e = walk_ldpair16_launch(wp, cx.dTab, cx.dInit, grid, cx.stream, &block);
   else if (pl.kernel == K_LD) e = walk_ld_launch(wp, cx.dTab, grid, cx.stream, &block);
   else e = walk_generic_launch(wp, grid, cx.stream, &block);
   if (e != cudaSuccess) { (void)cudaGetLastError(); return LNORM_ECUDA; }
@@ -661,13 +693,18 @@ int lnorm_prefix_maxima(const int32_t* M, int32_t n, int32_t m, int32_t d, int32
   }
   if (base == 2) {
     pl.kernel = walk_bin_supported(pr.mode, pr.c, pl.s) ? K_BIN : K_GEN;
-    if (pl.kernel == K_BIN && pr.fits16 && walk_bin16_supported(pr.mode, pr.c, pl.s)) pl.kernel = K_BIN16;
+    const bool hot = pl.kernel == K_BIN;
+    if (hot && pr.fits16 && walk_bin16_supported(pr.mode, pr.c, pl.s)) pl.kernel = K_BIN16;
+    if (hot && pr.fitsPair && walk_pair16_supported(pr.mode, pr.c, pl.s)) pl.kernel = K_PAIR16;
     const int ov = kernel_override();
-    if (ov == K_GEN || (ov == K_BIN && pl.kernel != K_GEN)) pl.kernel = ov;
+    if (ov == K_GEN || (ov == K_BIN && hot)) pl.kernel = ov;
+    if (ov == K_BIN16 && hot && pr.fits16 && walk_bin16_supported(pr.mode, pr.c, pl.s)) pl.kernel = K_BIN16;
   }
   else {
     pl.kernel = walk_ld_supported(base, pr.c, pl.s) ? K_LD : K_GEN;
     if (pl.kernel == K_LD && pr.fits16 && walk_ld16_supported(base, pr.c, pl.s)) pl.kernel = K_LD16;
+    if ((pl.kernel == K_LD || pl.kernel == K_LD16) && pr.fitsLdPair && walk_ldpair16_supported(base, pr.c, pl.s))
+      pl.kernel = K_LDPAIR16;
     const int ov = kernel_override();
     if (ov == K_GEN || (ov == K_BIN && pl.kernel != K_GEN)) pl.kernel = ov == K_GEN ? K_GEN : K_LD;
   }

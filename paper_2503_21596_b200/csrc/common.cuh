@@ -54,6 +54,17 @@ __device__ __forceinline__ int prefix_digit(const WalkParams& p, int64_t u, int 
   return x == 0 ? 0 : (int)((u >> (p.k - x)) & 1);
 }
 
+// Broadcast 16-byte shared-memory load issued as volatile PTX: every Gray step
+// re-reads its row (one LDS.128 per 4 words) instead of letting ptxas keep the
+// few distinct rows of an unrolled block resident in registers, which would
+// cost more registers (and occupancy) than the loads cost issue slots.
+__device__ __forceinline__ uint4 lds128(uint32_t saddr) {
+  uint4 v;
+  asm volatile("ld.volatile.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(saddr));
+  return v;
+}
+
 __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -84,17 +95,37 @@ template <int MODE> int walk_bin16_words(int c);
 template <int MODE> cudaError_t walk_bin16_launch_mode(const WalkParams& p, int32_t* scratch_tab, int grid, cudaStream_t st);
 template <int MODE> int walk_bin16_occupancy_mode(int c, int k, int s);
 template <int MODE> int walk_bin16_units_per_lane_mode(int c);
+template <int MODE> int walk_bin16_unroll_mode(int c);
 int walk_bin16_units_per_lane(int mode, int c);
 // Hot d-ary walk (L_d, d in {3,4}).
 bool walk_ld_supported(int d, int c, int s);
 cudaError_t walk_ld_launch(const WalkParams& p, int32_t* scratch_tab, int grid, cudaStream_t st,
                            int* block_out);
 int walk_ld_occupancy(int d, int c, int* block_out);
+// Strategy-paired packed 16-bit binary walk (guard: sum |M| <= 16383, checked by the caller).
+bool walk_pair16_supported(int mode, int c, int s);
+int walk_pair16_units_per_lane(int mode, int c);
+int walk_pair16_occupancy(int mode, int c, int s, int* block_out);
+// scratch_init: device buffer of >= 16384 int32 for the unit-init records.
+cudaError_t walk_pair16_launch(const WalkParams& p, int32_t* scratch_tab, int32_t* scratch_init, int grid,
+                               cudaStream_t st, int* block_out);
+template <int MODE> int walk_pair16_cols(int c);
+template <int MODE> cudaError_t walk_pair16_launch_mode(const WalkParams& p, int32_t* scratch_tab, int32_t* scratch_init,
+                                                        int grid, cudaStream_t st);
+template <int MODE> int walk_pair16_occupancy_mode(int c, int s);
+template <int MODE> int walk_pair16_units_per_lane_mode(int c);
+template <int MODE> int walk_pair16_unroll_mode(int c);
 // Packed 16-bit d-ary walk (L_d, d in {3,4}; exactness guard checked by the caller).
 bool walk_ld16_supported(int d, int c, int s);
 int walk_ld16_units_per_lane(int d, int c);
 int walk_ld16_occupancy(int d, int c, int k, int s, int* block_out);
 cudaError_t walk_ld16_launch(const WalkParams& p, int32_t* scratch_tab, int grid, cudaStream_t st, int* block_out);
+// d-ary walk with the last row evaluated for all d labels per word (guard: sum |M| <= 32767).
+bool walk_ldpair16_supported(int d, int c, int s);
+int walk_ldpair16_units_per_lane(int d, int c);
+int walk_ldpair16_occupancy(int d, int c, int s, int* block_out);
+cudaError_t walk_ldpair16_launch(const WalkParams& p, int32_t* scratch_tab, int32_t* scratch_init, int grid,
+                                 cudaStream_t st, int* block_out);
 // Generic warp-per-unit walk (any mode, d, c, s).
 bool walk_generic_supported(int d, int c);
 cudaError_t walk_generic_launch(const WalkParams& p, int grid, cudaStream_t st, int* block_out);

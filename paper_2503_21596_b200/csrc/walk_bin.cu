@@ -26,10 +26,10 @@ cudaError_t walk_bin_launch(const WalkParams& p, int32_t* scratch_tab, int grid,
 }
 
 bool walk_bin16_supported(int mode, int c, int s) {
-  if (s < 4) return false;
-  if (mode == MODE_L1) return walk_bin16_words<MODE_L1>(c) > 0;
-  if (mode == MODE_MARG) return c >= 2 && walk_bin16_words<MODE_MARG>(c) > 0;
-  if (mode == MODE_LD) return walk_bin16_words<MODE_LD>(c) > 0;
+  if (mode == MODE_L1) return walk_bin16_words<MODE_L1>(c) > 0 && s >= walk_bin16_unroll_mode<MODE_L1>(c);
+  if (mode == MODE_MARG)
+    return c >= 2 && walk_bin16_words<MODE_MARG>(c) > 0 && s >= walk_bin16_unroll_mode<MODE_MARG>(c);
+  if (mode == MODE_LD) return walk_bin16_words<MODE_LD>(c) > 0 && s >= walk_bin16_unroll_mode<MODE_LD>(c);
   return false;
 }
 
@@ -51,6 +51,38 @@ cudaError_t walk_bin16_launch(const WalkParams& p, int32_t* scratch_tab, int gri
   if (p.mode == MODE_L1) return walk_bin16_launch_mode<MODE_L1>(p, scratch_tab, grid, st);
   if (p.mode == MODE_MARG) return walk_bin16_launch_mode<MODE_MARG>(p, scratch_tab, grid, st);
   return walk_bin16_launch_mode<MODE_LD>(p, scratch_tab, grid, st);
+}
+
+bool walk_pair16_supported(int mode, int c, int s) {
+  int C = 0, K = 4;
+  if (mode == MODE_L1) { C = walk_pair16_cols<MODE_L1>(c); if (C) K = walk_pair16_unroll_mode<MODE_L1>(c); }
+  else if (mode == MODE_MARG) { C = c >= 2 ? walk_pair16_cols<MODE_MARG>(c) : 0; if (C) K = walk_pair16_unroll_mode<MODE_MARG>(c); }
+  else if (mode == MODE_LD) { C = walk_pair16_cols<MODE_LD>(c); if (C) K = walk_pair16_unroll_mode<MODE_LD>(c); }
+  if (C == 0 || s < 1 + K) return false;   // one paired digit + K unrolled walked digits
+  const int G = mode == MODE_LD ? 2 : 1;
+  const int RW = (G * C + 1 + 3) & ~3;
+  return 2 * (s - 1) * RW <= 8448;
+}
+
+int walk_pair16_units_per_lane(int mode, int c) {
+  if (mode == MODE_L1) return walk_pair16_units_per_lane_mode<MODE_L1>(c);
+  if (mode == MODE_MARG) return walk_pair16_units_per_lane_mode<MODE_MARG>(c);
+  return walk_pair16_units_per_lane_mode<MODE_LD>(c);
+}
+
+int walk_pair16_occupancy(int mode, int c, int s, int* block_out) {
+  *block_out = 32;
+  if (mode == MODE_L1) return walk_pair16_occupancy_mode<MODE_L1>(c, s);
+  if (mode == MODE_MARG) return walk_pair16_occupancy_mode<MODE_MARG>(c, s);
+  return walk_pair16_occupancy_mode<MODE_LD>(c, s);
+}
+
+cudaError_t walk_pair16_launch(const WalkParams& p, int32_t* scratch_tab, int32_t* scratch_init, int grid,
+                               cudaStream_t st, int* block_out) {
+  *block_out = 32;
+  if (p.mode == MODE_L1) return walk_pair16_launch_mode<MODE_L1>(p, scratch_tab, scratch_init, grid, st);
+  if (p.mode == MODE_MARG) return walk_pair16_launch_mode<MODE_MARG>(p, scratch_tab, scratch_init, grid, st);
+  return walk_pair16_launch_mode<MODE_LD>(p, scratch_tab, scratch_init, grid, st);
 }
 
 }  // namespace lnorm

@@ -25,12 +25,19 @@ namespace lnorm {
 
 namespace {
 
-constexpr int K = 4;
 constexpr int kTabWords = 8448;
 constexpr int kBlock = 32;
 
 // ctz for the unrolled step index j in [1, 16): a ternary chain that folds at compile time
 __host__ __device__ constexpr int cctz(int j) { return (j & 1) ? 0 : (j & 2) ? 1 : (j & 4) ? 2 : 3; }
+
+// Unrolled low suffix digits: as many as keep the unrolled block under ~800
+// instructions (instruction-cache footprint; see walk_pair16_impl.cuh).
+// (measured: with plain loads and K = 4 the 42x42 L_1 walk ran 3.80 s vs 4.18 s with
+// K = 3 and volatile loads, so the budget here is larger than the paired kernel's)
+__host__ __device__ constexpr int unroll_digits(int step_instr) {
+  return step_instr * 16 <= 1800 ? 4 : step_instr * 8 <= 1800 ? 3 : step_instr * 4 <= 1800 ? 2 : 1;
+}
 
 // Record strides are padded to 4 words so every row starts 16-byte aligned for LDS.128.
 __host__ __device__ constexpr int pad4(int x) { return (x + 3) & ~3; }
@@ -54,7 +61,7 @@ struct Walker16 {
     const uint4* src = reinterpret_cast<const uint4*>(sT + off);
 #pragma unroll
     for (int v = 0; v < RWd / 4; ++v) {
-      const uint4 x = src[v];
+      const uint4 x = src[v];   // plain loads: ptxas keeps the block's few distinct rows in registers
       r[4 * v] = x.x; r[4 * v + 1] = x.y; r[4 * v + 2] = x.z; r[4 * v + 3] = x.w;
     }
 #pragma unroll
@@ -95,8 +102,12 @@ struct Walker16 {
 };
 
 template <int MODE, int W, int P>
+__host__ __device__ constexpr int bin16_unroll() { return unroll_digits(P * (2 * Layout<MODE, W>::Wt + 5) + Layout<MODE, W>::RWd / 4); }
+
+template <int MODE, int W, int P>
 __global__ void __launch_bounds__(kBlock) walk_bin16_kernel(const WalkParams p, const uint32_t* __restrict__ gTab) {
   using LY = Layout<MODE, W>;
+  constexpr int K = bin16_unroll<MODE, W, P>();
   extern __shared__ __align__(16) uint32_t sT[];
   const int lane = threadIdx.x & 31;
   const int s = p.s, k = p.k;
@@ -250,7 +261,7 @@ size_t smem16(int k, int s) {
 
 // units per lane: 2 while the packed state stays small, else 1 (register budget)
 template <int MODE, int W>
-constexpr int units_per_lane() { return (MODE == MODE_LD ? 2 * W : W) <= 24 ? 2 : 1; }
+__host__ __device__ constexpr int units_per_lane() { return (MODE == MODE_LD ? 2 * W : W) <= 24 ? 2 : 1; }
 
 template <int MODE, int W>
 cudaError_t launch_one16(const WalkParams& p, const uint32_t* tab, int grid, cudaStream_t st) {
@@ -318,6 +329,16 @@ cudaError_t walk_bin16_launch_mode<LN_BIN_MODE>(const WalkParams& p, int32_t* sc
   if (e != cudaSuccess) return e;
   LN_W16_SWITCH(LN_BIN_MODE, W, launch_one16, p, tab, grid, st)
   return cudaErrorInvalidValue;
+}
+
+template <int MODE, int W>
+int unroll_one16() { return bin16_unroll<MODE, W, units_per_lane<MODE, W>()>(); }
+
+template <>
+int walk_bin16_unroll_mode<LN_BIN_MODE>(int c) {
+  const int W = walk_bin16_words<LN_BIN_MODE>(c);
+  LN_W16_SWITCH(LN_BIN_MODE, W, unroll_one16)
+  return 4;
 }
 
 template <>

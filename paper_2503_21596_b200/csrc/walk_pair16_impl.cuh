@@ -1,0 +1,388 @@
+// Hot binary Gray walk, "strategy-paired" 16-bit layout: L_1, L_marg, L_2.
+//
+// Same units and warp-uniform Gray control as walk_bin_impl.cuh, but the LAST
+// suffix row (row r-1, the digit that flips every other step of the binary
+// reflected code, Table 1) is not walked: every register holds ONE
+// column for the TWO strategies that differ only in that row,
+//     R_y = ( m_y(A) , m_y(B) )  as s16x2,  A: a_{r-1} = +1 (label 0), B: a_{r-1} = -1 (label 1).
+// A step of the walk flips a row rho among rows k+1..r-2 and changes both halves
+// by the same delta (Eq. 12), so one VIADD.16x2 updates column y of both
+// strategies and one VIADDMNMX.S16x2 accumulates max(m_y, 0) for both:
+//     |m| = 2 max(m, 0) - m,    value = 2 H + q,   H = sum_y max(m_y, 0)
+// with the linear part q carried per strategy (L_1: q = -sum m; L_marg: q =
+// m_0 - sum_{y>=1} m_y, column 0 kept out of the packed registers; L_2: m_1 =
+// T - m_0 is held too and q = -sum T).  The running maximum is kept packed:
+//     t = H + Q ;  best2 = max(H + t, best2)   (= max(2H + Q, best2), both halves)
+// where Q is the warp-uniform sum of q-deltas since the unit start, so the
+// epilogue costs two instructions per PAIR of strategies.  Per strategy
+// and column this is (1 + 1/c) instructions split over the FMA-heavy and ALU pipes.
+// Exactness guard: every 16-bit intermediate is bounded
+// by 2S with S = sum_ij |M_ij| (2H + Q = value - q(0), |value|, |q(0)| <= S), so
+// S <= 16383 is required and checked on the host.
+#include "common.cuh"
+
+#ifndef LN_BIN_MODE
+#error "define LN_BIN_MODE before including walk_pair16_impl.cuh"
+#endif
+
+namespace lnorm {
+
+namespace {
+
+constexpr int kBlock = 32;
+
+__host__ __device__ constexpr int cctz(int j) { return (j & 1) ? 0 : (j & 2) ? 1 : (j & 4) ? 2 : 3; }
+
+// Unrolled low walked digits: as many as keep the unrolled block under ~800
+// instructions (~13 KB): a larger body thrashes the instruction cache (ncu showed
+// 'no_instruction' as the dominant stall with 16 unrolled steps at C = 42, P = 2).
+#ifndef LN_PAIR_VOLATILE
+#define LN_PAIR_VOLATILE 0
+#endif
+#ifndef LN_PAIR_ACC
+#define LN_PAIR_ACC 2
+#endif
+#ifndef LN_PAIR_BUDGET
+#define LN_PAIR_BUDGET 1800
+#endif
+__host__ __device__ constexpr int unroll_digits(int step_instr) {
+  return step_instr * 16 <= LN_PAIR_BUDGET ? 4 : step_instr * 8 <= LN_PAIR_BUDGET ? 3 : step_instr * 4 <= LN_PAIR_BUDGET ? 2 : 1;
+}
+__host__ __device__ constexpr int pad4(int x) { return (x + 3) & ~3; }
+
+template <int MODE, int C>
+struct PairLayout {
+  static constexpr int G = (MODE == MODE_LD) ? 2 : 1;   // packed register groups (m_0, m_1 for L_2)
+  static constexpr int RW = pad4(G * C + 1);            // delta record: G*C duplicated words + q word
+};
+
+// Init data (global memory, int32), per record of IW = G*C + 2 ints:
+//   prefix rows x = 0..k : raw columns (C), then q contribution, unused
+//   base                 : suffix rows k+1..r-2 at digit 0 (C) [+ T (C) for L_2], q
+//   pair                 : row r-1 columns (C), q contribution of flipping it (A -> B)
+template <int MODE, int C>
+struct InitLayout {
+  static constexpr int IW = (MODE == MODE_LD ? 2 * C : C) + 2;
+};
+
+template <int MODE, int C, int P>
+struct PairStep {
+  static constexpr int G = PairLayout<MODE, C>::G, RW = PairLayout<MODE, C>::RW;
+  // One walked word: apply the delta record at sbase + off to both strategies of each
+  // unit.  Q is the warp-uniform running sum of the q deltas since the unit start
+  // (identical for every unit: the walk is lockstep), so per unit the epilogue is
+  //     t = H + Q ; best2 = max(H + t, best2)  =  max(2H + Q, best2)
+  // and the unit's own q at its start word is added once at the end.
+  static __device__ __forceinline__ void run(uint32_t (&R)[P][G * C], uint32_t& Q, uint32_t (&best2)[P],
+                                             uint32_t sbase, int off) {
+    uint32_t r[RW];
+#if LN_PAIR_VOLATILE
+#pragma unroll
+    for (int v = 0; v < RW / 4; ++v) {
+      const uint4 x4 = lds128(sbase + 4u * (uint32_t)(off + 4 * v));
+#else
+    const uint4* src = reinterpret_cast<const uint4*>(__cvta_shared_to_generic(sbase) ) + off / 4;
+#pragma unroll
+    for (int v = 0; v < RW / 4; ++v) {
+      const uint4 x4 = src[v];
+#endif
+      r[4 * v] = x4.x; r[4 * v + 1] = x4.y; r[4 * v + 2] = x4.z; r[4 * v + 3] = x4.w;
+    }
+    if (MODE != MODE_LD) Q = __vadd2(Q, r[RW - 1]);
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
+#if LN_PAIR_ACC == 2
+      uint32_t a0, a1 = 0u;
+#pragma unroll
+      for (int i = 0; i < G * C; ++i) {
+        R[j][i] = __vadd2(R[j][i], r[i]);
+        if (i == 0) a0 = __vmaxs2(R[j][0], 0u);
+        else if (i & 1) a1 = __viaddmax_s16x2(a1, R[j][i], a1);
+        else a0 = __viaddmax_s16x2(a0, R[j][i], a0);
+      }
+      const uint32_t a = __vadd2(a0, a1);
+#else
+      uint32_t a = 0u;
+#pragma unroll
+      for (int i = 0; i < G * C; ++i) {
+        R[j][i] = __vadd2(R[j][i], r[i]);
+        a = (i == 0) ? __vmaxs2(R[j][0], 0u) : __viaddmax_s16x2(a, R[j][i], a);
+      }
+#endif
+      best2[j] = __viaddmax_s16x2(a, __vadd2(a, Q), best2[j]);
+    }
+  }
+};
+
+template <int MODE, int C, int P>
+__host__ __device__ constexpr int pair_unroll() { return unroll_digits(P * (2 * PairLayout<MODE, C>::G * C + 4) + PairLayout<MODE, C>::RW / 4); }
+
+template <int MODE, int C, int P>
+__global__ void __launch_bounds__(kBlock) walk_pair16_kernel(const WalkParams p, const uint32_t* __restrict__ gTab,
+                                                             const int32_t* __restrict__ gInit) {
+  using LY = PairLayout<MODE, C>;
+  constexpr int G = LY::G, RW = LY::RW, IW = InitLayout<MODE, C>::IW;
+  constexpr int K = pair_unroll<MODE, C, P>();
+  extern __shared__ __align__(16) uint32_t sT[];
+  const int lane = threadIdx.x & 31;
+  const int sw = p.s - 1;                          // walked digits (rows k+1 .. r-2)
+  const int total = 2 * sw * RW;
+  for (int i = threadIdx.x; i < total; i += blockDim.x) sT[i] = gTab[i];
+  __syncthreads();
+  const int32_t* baseRec = gInit + (p.k + 1) * IW;
+  const int32_t* pairRec = baseRec + IW;
+  const uint32_t nblk = 1u << (sw - K);
+  int32_t best = INT32_MIN;
+  uint32_t best_u = 0;
+  bool have = false;
+  const int64_t nchunks = (p.unit_count + 32 * P - 1) / (32 * P);
+  for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    uint32_t R[P][G * C];
+    uint32_t q[P], best2[P];
+    uint32_t Q = 0u;                                   // uniform: q(t) - q(0), both halves
+    // ---- unit init: column sums of strategies A and B (the paper's per-thread product)
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
+      const int64_t rel = ch * 32 * P + j * 32 + lane;
+      const int64_t u = p.unit_begin + (rel < p.unit_count ? rel : 0);
+      int32_t mA[C];
+      int32_t qA = __ldg(baseRec + G * C);
+#pragma unroll
+      for (int y = 0; y < C; ++y) mA[y] = __ldg(baseRec + y);
+      for (int x = 0; x <= p.k; ++x) {
+        const int dig = prefix_digit(p, u, x);
+        const int32_t f = (MODE == MODE_LD) ? 1 - dig : 1 - 2 * dig;
+        const int32_t* rec = gInit + x * IW;
+#pragma unroll
+        for (int y = 0; y < C; ++y) mA[y] += f * __ldg(rec + y);
+        qA += f * __ldg(rec + C);
+      }
+      const int32_t qB = qA + __ldg(pairRec + C);
+      q[j] = (uint32_t)(qA & 0xFFFF) | ((uint32_t)(qB & 0xFFFF) << 16);
+#pragma unroll
+      for (int y = 0; y < C; ++y) {
+        const int32_t pr = __ldg(pairRec + y);
+        const int32_t mB = (MODE == MODE_LD) ? mA[y] - pr : mA[y] - 2 * pr;
+        R[j][y] = (uint32_t)(mA[y] & 0xFFFF) | ((uint32_t)(mB & 0xFFFF) << 16);
+        if (MODE == MODE_LD) {
+          const int32_t T = __ldg(baseRec + C + y);
+          const int32_t m1A = T - mA[y], m1B = T - mB;
+          R[j][C + y] = (uint32_t)(m1A & 0xFFFF) | ((uint32_t)(m1B & 0xFFFF) << 16);
+        }
+      }
+      // value of the starting pair
+      uint32_t a0 = __vmaxs2(R[j][0], 0u), a1 = 0u;
+#pragma unroll
+      for (int i = 1; i < G * C; ++i) {
+        if (i & 1) a1 = __viaddmax_s16x2(a1, R[j][i], a1);
+        else a0 = __viaddmax_s16x2(a0, R[j][i], a0);
+      }
+      const uint32_t h = __vadd2(a0, a1);
+      best2[j] = __vadd2(h, h);                         // 2H + Q at the start word (Q = 0); + q[j] at the end
+    }
+    // ---- the walk: 2^(s-1) words, each evaluating the pair (A, B)
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sT);
+    for (uint32_t t = 0; t < nblk; ++t) {
+      if (t != 0) {                                    // block start: walked digit K + ctz(t)
+        const int tz = __ffs((int)t) - 1;
+        const int b = K + tz;
+        const int sg = 1 ^ (int)((t >> (tz + 1)) & 1u);
+        PairStep<MODE, C, P>::run(R, Q, best2, sbase, (2 * b + sg) * RW);
+      }
+#pragma unroll
+      for (int jj = 1; jj < (1 << K); ++jj) {
+        const int b = cctz(jj);
+        const int sg = (b < K - 1) ? (1 ^ ((jj >> (b + 1)) & 1)) : (1 ^ (int)(t & 1u));
+        PairStep<MODE, C, P>::run(R, Q, best2, sbase, (2 * b + sg) * RW);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
+      const int64_t rel = ch * 32 * P + j * 32 + lane;
+      if (rel < p.unit_count) {
+        // add the unit's own start-word q (per strategy) back: value = 2H + Q + q(0)
+        const int32_t lo = (int32_t)(int16_t)(best2[j] & 0xFFFF) + (int32_t)(int16_t)(q[j] & 0xFFFF);
+        const int32_t hi = (int32_t)(int16_t)(best2[j] >> 16) + (int32_t)(int16_t)(q[j] >> 16);
+        const int32_t ub = max(lo, hi);
+        if (p.unit_max) p.unit_max[rel] = ub;
+        if (!have || ub > best) { best = ub; best_u = (uint32_t)(p.unit_begin + rel); have = true; }
+      }
+    }
+  }
+  unsigned long long key = have ? make_key(best, best_u) : 0ull;
+  key = warp_max_u64(key);
+  if (lane == 0 && key) atomicMax(p.key, key);
+}
+
+// Tables from the oriented matrix: packed duplicated delta records (walked digit b
+// <-> row r-2-b, sign 1 = flip to -1 / label 1) and the int32 init records.
+template <int MODE>
+__global__ void build_pair16_kernel(const int32_t* M, int r, int c, int C, int k, int s,
+                                    uint32_t* tab, int32_t* init) {
+  const int G = (MODE == MODE_LD) ? 2 : 1;
+  const int RW = pad4(G * C + 1), IW = G * C + 2;
+  const int c0 = (MODE == MODE_MARG) ? 1 : 0;
+  const int scale = (MODE == MODE_LD) ? 1 : 2;
+  const int sw = s - 1;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < 2 * sw * RW; i += blockDim.x) tab[i] = 0u;
+  for (int i = tid; i < (k + 3) * IW; i += blockDim.x) init[i] = 0;
+  __syncthreads();
+  for (int rec = tid; rec < 2 * sw; rec += blockDim.x) {
+    const int b = rec >> 1, sg = rec & 1;
+    const int32_t* row = M + (int64_t)(r - 2 - b) * c;
+    const int f = sg ? -scale : scale;
+    int32_t qd = 0;
+    for (int j = 0; j < C; ++j) {
+      const int y = c0 + j;
+      const int32_t v = y < c ? f * row[y] : 0;
+      tab[rec * RW + j] = (uint32_t)(v & 0xFFFF) * 0x10001u;
+      if (MODE == MODE_LD) tab[rec * RW + C + j] = (uint32_t)((-v) & 0xFFFF) * 0x10001u;
+      qd -= v;
+    }
+    if (MODE == MODE_MARG) qd += f * row[0];
+    tab[rec * RW + RW - 1] = MODE == MODE_LD ? 0u : (uint32_t)(qd & 0xFFFF) * 0x10001u;
+  }
+  // init records: prefix rows 0..k, base, pair
+  for (int rec = tid; rec < k + 3; rec += blockDim.x) {
+    int32_t* out = init + rec * IW;
+    if (rec <= k) {
+      const int32_t* row = M + (int64_t)rec * c;
+      int32_t qd = 0;
+      for (int j = 0; j < C; ++j) { const int y = c0 + j; const int32_t v = y < c ? row[y] : 0; out[j] = v; qd -= v; }
+      if (MODE == MODE_MARG) qd += row[0];
+      out[C] = MODE == MODE_LD ? 0 : qd;
+    } else if (rec == k + 1) {                     // base: suffix rows k+1..r-2 at digit 0
+      int32_t qd = 0, tsum = 0;
+      for (int j = 0; j < C; ++j) {
+        const int y = c0 + j;
+        int32_t bv = 0, tv = 0;
+        if (y < c)
+          for (int x = 0; x < r; ++x) {
+            const int32_t v = M[(int64_t)x * c + y];
+            tv += v;
+            if (x > k && x < r - 1) bv += v;
+          }
+        if (MODE == MODE_LD) {
+          // L_2: the walked base includes row r-1 in group 0 (strategy A)
+          if (y < c) bv += M[(int64_t)(r - 1) * c + y];
+          out[j] = bv;
+          out[C + j] = tv;
+        } else {
+          if (y < c) bv += M[(int64_t)(r - 1) * c + y];   // strategy A has a_{r-1} = +1
+          out[j] = bv;
+        }
+        qd -= bv;
+        tsum += tv;
+      }
+      if (MODE == MODE_MARG) {
+        int32_t b0 = 0;
+        for (int x = k + 1; x < r; ++x) b0 += M[(int64_t)x * c];
+        qd += b0;
+      }
+      out[G * C] = MODE == MODE_LD ? -tsum : qd;
+    } else {                                       // pair row r-1 and the q change A -> B
+      const int32_t* row = M + (int64_t)(r - 1) * c;
+      int32_t s1 = 0;
+      for (int j = 0; j < C; ++j) { const int y = c0 + j; const int32_t v = y < c ? row[y] : 0; out[j] = v; s1 += v; }
+      // L_1: m_B = m_A - 2 M_{r-1} => q_B - q_A = +2 sum;  L_marg: also the column-0 term -2 M_{r-1,0}
+      int32_t dq = 2 * s1;
+      if (MODE == MODE_MARG) dq -= 2 * row[0];
+      out[C] = MODE == MODE_LD ? 0 : dq;
+    }
+  }
+}
+
+template <int MODE, int C>
+__host__ __device__ constexpr int pair_units_per_lane() { return (MODE == MODE_LD ? 2 * C : C) <= 48 ? 2 : 1; }
+
+template <int MODE, int C>
+size_t pair_smem(int s) { return sizeof(uint32_t) * (size_t)(2 * (s - 1) * PairLayout<MODE, C>::RW); }
+
+template <int MODE, int C>
+cudaError_t launch_pair(const WalkParams& p, const uint32_t* tab, const int32_t* init, int grid, cudaStream_t st) {
+  constexpr int P = pair_units_per_lane<MODE, C>();
+  const size_t sm = pair_smem<MODE, C>(p.s);
+  cudaError_t e = cudaFuncSetAttribute(walk_pair16_kernel<MODE, C, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  walk_pair16_kernel<MODE, C, P><<<grid, kBlock, sm, st>>>(p, tab, init);
+  return cudaGetLastError();
+}
+
+template <int MODE, int C>
+int occ_pair(int s) {
+  constexpr int P = pair_units_per_lane<MODE, C>();
+  const size_t sm = pair_smem<MODE, C>(s);
+  cudaFuncSetAttribute(walk_pair16_kernel<MODE, C, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  int nb = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, walk_pair16_kernel<MODE, C, P>, kBlock, sm);
+  return nb;
+}
+
+template <int MODE, int C>
+int upl_pair() { return pair_units_per_lane<MODE, C>(); }
+
+#define LN_PAIR_SWITCH(MODE, C_, FN, ...)                                                            \
+  switch (C_) {                                                                                      \
+    case 2: return FN<MODE, 2>(__VA_ARGS__);   case 4: return FN<MODE, 4>(__VA_ARGS__);              \
+    case 6: return FN<MODE, 6>(__VA_ARGS__);   case 8: return FN<MODE, 8>(__VA_ARGS__);              \
+    case 10: return FN<MODE, 10>(__VA_ARGS__); case 12: return FN<MODE, 12>(__VA_ARGS__);            \
+    case 14: return FN<MODE, 14>(__VA_ARGS__); case 16: return FN<MODE, 16>(__VA_ARGS__);            \
+    case 18: return FN<MODE, 18>(__VA_ARGS__); case 20: return FN<MODE, 20>(__VA_ARGS__);            \
+    case 22: return FN<MODE, 22>(__VA_ARGS__); case 24: return FN<MODE, 24>(__VA_ARGS__);            \
+    case 26: return FN<MODE, 26>(__VA_ARGS__); case 28: return FN<MODE, 28>(__VA_ARGS__);            \
+    case 30: return FN<MODE, 30>(__VA_ARGS__); case 32: return FN<MODE, 32>(__VA_ARGS__);            \
+    case 34: return FN<MODE, 34>(__VA_ARGS__); case 36: return FN<MODE, 36>(__VA_ARGS__);            \
+    case 38: return FN<MODE, 38>(__VA_ARGS__); case 40: return FN<MODE, 40>(__VA_ARGS__);            \
+    case 42: return FN<MODE, 42>(__VA_ARGS__); case 44: return FN<MODE, 44>(__VA_ARGS__);            \
+    case 46: return FN<MODE, 46>(__VA_ARGS__); case 48: return FN<MODE, 48>(__VA_ARGS__);            \
+    case 52: return FN<MODE, 52>(__VA_ARGS__); case 56: return FN<MODE, 56>(__VA_ARGS__);            \
+    case 60: return FN<MODE, 60>(__VA_ARGS__); case 64: return FN<MODE, 64>(__VA_ARGS__);            \
+    default: break;                                                                                  \
+  }
+
+}  // namespace
+
+template <>
+int walk_pair16_cols<LN_BIN_MODE>(int c) {
+  const int cp = (LN_BIN_MODE == MODE_MARG) ? c - 1 : c;
+  int C = cp < 2 ? 2 : (cp + 1) & ~1;
+  if (C > 48) C = (C + 3) & ~3;
+  return C <= 64 ? C : 0;
+}
+
+template <>
+cudaError_t walk_pair16_launch_mode<LN_BIN_MODE>(const WalkParams& p, int32_t* scratch_tab, int32_t* scratch_init,
+                                                 int grid, cudaStream_t st) {
+  const int C = walk_pair16_cols<LN_BIN_MODE>(p.c);
+  if (C == 0) return cudaErrorInvalidValue;
+  uint32_t* tab = reinterpret_cast<uint32_t*>(scratch_tab);
+  build_pair16_kernel<LN_BIN_MODE><<<1, 128, 0, st>>>(p.M, p.r, p.c, C, p.k, p.s, tab, scratch_init);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  LN_PAIR_SWITCH(LN_BIN_MODE, C, launch_pair, p, tab, scratch_init, grid, st)
+  return cudaErrorInvalidValue;
+}
+
+template <>
+int walk_pair16_occupancy_mode<LN_BIN_MODE>(int c, int s) {
+  LN_PAIR_SWITCH(LN_BIN_MODE, walk_pair16_cols<LN_BIN_MODE>(c), occ_pair, s)
+  return 0;
+}
+
+template <int MODE, int C>
+int unroll_pair() { return pair_unroll<MODE, C, pair_units_per_lane<MODE, C>()>(); }
+
+template <>
+int walk_pair16_unroll_mode<LN_BIN_MODE>(int c) {
+  LN_PAIR_SWITCH(LN_BIN_MODE, walk_pair16_cols<LN_BIN_MODE>(c), unroll_pair)
+  return 4;
+}
+
+template <>
+int walk_pair16_units_per_lane_mode<LN_BIN_MODE>(int c) {
+  LN_PAIR_SWITCH(LN_BIN_MODE, walk_pair16_cols<LN_BIN_MODE>(c), upl_pair)
+  return 1;
+}
+
+}  // namespace lnorm

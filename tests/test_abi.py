@@ -182,11 +182,13 @@ def test_plan_covers_the_search_space(n, m, d, marg):
 def test_plan_packed_guard_and_fallback():
     from paper_2503_21596_b200 import synth
     M = synth.random_matrix(30, 30, 1)
-    assert L.plan(M)["variant_name"] == "bin_packed16"
+    assert L.plan(M)["variant_name"] == "bin_pair16"               # sum |M| <= 32767
+    mid = (M * 8).astype(np.int32)                   # sum |M| > 32767, per-parity column sums still fit
+    assert L.plan(mid)["packed_ok"] == 1 and L.plan(mid)["variant_name"] == "bin_packed16"
     big = (M * 300).astype(np.int32)                 # column abs sums exceed the s16 guard
     P = L.plan(big)
     assert P["packed_ok"] == 0 and P["variant_name"] == "bin_int32"
-    assert L.plan(synth.random_matrix(24, 24, 4), d=3)["variant_name"] == "ld_packed16"
+    assert L.plan(synth.random_matrix(24, 24, 4), d=3)["variant_name"] == "ld_pair16"
     assert L.plan(synth.random_matrix(24, 40, 4), d=3)["variant_name"] == "generic"
     assert L.plan(np.eye(3, dtype=np.int32))["variant_name"] == "generic"     # suffix shorter than the unroll
 

@@ -241,7 +241,7 @@ def test_device_resident_and_rank_paths(lib):
 
 # ------------------------------------------------------ kernel families ----
 
-@pytest.mark.parametrize("family", ["int32", "generic", "auto"])
+@pytest.mark.parametrize("family", ["int32", "packed", "generic", "auto"])
 @pytest.mark.parametrize("d,marg", MODES, ids=[mode_id(*m) for m in MODES])
 def test_every_kernel_family_matches_oracle(lib, family, d, marg, monkeypatch):
     """The packed-16, int32 and generic kernels all reproduce the oracle bit for bit."""
@@ -261,3 +261,43 @@ def test_large_entries_use_int32_path_exactly(lib):
         check(lib, M)
         check(lib, M, marg=True)
         check(lib, synth.random_matrix(10, 12, 50_100 + seed, -3000, 3000), d=3)
+
+
+def _with_abs_sums(col_sums, n, seed):
+    """n x len(col_sums) matrix with random signs whose column |.|-sums are exactly col_sums."""
+    g = synth.SplitMix64(seed)
+    M = np.zeros((n, len(col_sums)), dtype=np.int64)
+    for y, tot in enumerate(col_sums):
+        base, extra = divmod(tot, n)
+        for x in range(n):
+            v = base + (1 if x < extra else 0)
+            M[x, y] = v if g.next() & 1 else -v
+    return M.astype(np.int32)
+
+
+@pytest.mark.parametrize("S_pair", [16383, 16384])
+def test_pair_guard_boundary_exact(lib, S_pair):
+    """sum |M| at the strategy-paired path's guard (<= 16383) and one past it: both exact."""
+    n, m = 10, 12
+    cols = [S_pair // m + (1 if y < S_pair % m else 0) for y in range(m)]
+    M = _with_abs_sums(cols, n, 60_000 + S_pair)
+    assert int(np.abs(M.astype(np.int64)).sum()) == S_pair
+    P = lib.plan(M)
+    assert P["variant_name"] == ("bin_pair16" if S_pair <= 16383 else "bin_packed16")
+    check(lib, M)
+    # all-positive matrix: the optimum sits exactly at the bound (value = S)
+    A = np.abs(M)
+    v, _ = check(lib, A)
+    assert v == S_pair
+
+
+@pytest.mark.parametrize("par", [32767, 32768])
+def test_packed_guard_boundary_exact(lib, par):
+    """Per-parity column |.|-sums at the packed column-pair guard (<= 32767) and one past it."""
+    n = 6                                                             # n < m: no transposition
+    M = _with_abs_sums([par - 7, par - 10, 5, 7, 1, 1, 1, 1], n, 61_000 + par)   # parity sums: par, par - 1
+    P = lib.plan(M)
+    assert P["packed_ok"] == (1 if par <= 32767 else 0)
+    check(lib, M)
+    v, _ = check(lib, np.abs(M))
+    assert v == int(np.abs(M.astype(np.int64)).sum())
