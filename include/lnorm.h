@@ -120,6 +120,15 @@ int lnorm_compute_rank_device(lnorm_comm* comm, const int32_t* M_device, int32_t
                               int32_t with_marginals, int64_t* value, int8_t* argmax);
 
 /*
+ * Test hook for the multi-GPU decomposition on ONE device: plans for `slices`
+ * ranks, walks the Algorithm-1 slice of every virtual rank one after the other
+ * into the same 8-byte key (what ncclAllReduce(max) combines across GPUs) and
+ * recovers the argmax.  Results must be bit-identical to lnorm_compute.
+ */
+int lnorm_compute_sliced(const int32_t* M, int32_t n, int32_t m, int32_t d, int32_t with_marginals,
+                         int32_t slices, int64_t* value, int8_t* argmax);
+
+/*
  * Test hook for sampled parity at sizes the oracle cannot finish: for each of
  * `count` prefixes (int8[count][nfixed], row-major; digits 0/1 meaning +1/-1
  * for d = 1, labels 0..d-1 for d >= 2; for L_marg digit 0 of every prefix

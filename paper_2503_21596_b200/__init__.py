@@ -31,7 +31,7 @@ SYMBOLS = [
     "lnorm_comm_unique_id", "lnorm_comm_create", "lnorm_comm_destroy", "lnorm_compute_rank",
     "lnorm_compute_rank_device",
     "lnorm_prefix_maxima", "lnorm_walk_trace", "lnorm_gray_digit", "lnorm_gray_change", "lnorm_partition",
-    "lnorm_last_stats", "lnorm_plan",
+    "lnorm_last_stats", "lnorm_plan", "lnorm_compute_sliced",
 ]
 
 STATUS = {0: "OK", 1: "EINVAL", 2: "EOVERFLOW", 3: "ETOOLARGE", 4: "ENODEV", 5: "ECUDA", 6: "ENCCL", 7: "ENOMEM"}
@@ -106,6 +106,7 @@ def load():
             "lnorm_gray_change": ([i32, u64, i32p, i32p, i32p], ctypes.c_int),
             "lnorm_partition": ([u64, i64, i64, i64p, i64p], ctypes.c_int),
             "lnorm_last_stats": ([P(Stats)], ctypes.c_int),
+            "lnorm_compute_sliced": ([i32p, i32, i32, i32, i32, i32, i64p, i8p], ctypes.c_int),
             "lnorm_plan": ([i32p, i32, i32, i32, i32, i32, P(PlanInfo)], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
@@ -166,6 +167,17 @@ def compute_device(M_dev, d: int = 1, with_marginals: bool = False, stream=None)
     st = ctypes.c_void_p(stream) if stream else None
     _check(load().lnorm_compute_device(ctypes.c_void_p(M_dev.data_ptr()), n, m, d, int(with_marginals), st,
                                        ctypes.byref(v), _p(arg, ctypes.c_int8)), "lnorm_compute_device")
+    return int(v.value), arg
+
+
+def compute_sliced(M, slices: int, d: int = 1, with_marginals: bool = False):
+    """Test hook: the multi-rank unit split walked slice by slice on one GPU (bit-identical results)."""
+    A = _mat(M)
+    n, m = A.shape
+    v = ctypes.c_int64()
+    arg = np.zeros(n, dtype=np.int8)
+    _check(load().lnorm_compute_sliced(_p(A, ctypes.c_int32), n, m, d, int(with_marginals), slices,
+                                       ctypes.byref(v), _p(arg, ctypes.c_int8)), "lnorm_compute_sliced")
     return int(v.value), arg
 
 

@@ -401,10 +401,13 @@ int launch_walk(DevCtx& cx, const Problem& pr, const Plan& pl, WalkParams& wp, i
 
 // Full search on one device.  dIn: device copy of the caller's n x m matrix.
 // world > 1: this rank walks its Algorithm-1 slice and `comm` all-reduces the key.
+// vslices > 1 (test hook, world == 1): walk the Algorithm-1 slices of `vslices`
+// virtual ranks one after the other on this device; the shared key then holds
+// exactly what the multi-rank all-reduce(max) would.
 int run_device(DevCtx& cx, const int32_t* dIn, const Problem& pr, int rank, int world, ncclComm_t comm,
-               RunOut* out, lnorm_stats* st) {
+               RunOut* out, lnorm_stats* st, int vslices = 1) {
   Plan pl;
-  int rc = make_plan(pr, world, &pl);
+  int rc = make_plan(pr, std::max(world, vslices), &pl);
   if (rc) return rc;
   cudaStream_t s = cx.stream;
   if ((rc = grow(&cx.dM, &cx.capM, (size_t)pr.n * pr.m))) return rc;
@@ -421,24 +424,34 @@ int run_device(DevCtx& cx, const int32_t* dIn, const Problem& pr, int rank, int 
   init_ctl_kernel<<<1, 1, 0, s>>>(cx.dCtl);
   ++launches;
   // Algorithm 1 over the unit list: rank slice [lo, hi]
-  int64_t lo = 0, cnt = pl.units;
-  if (world > 1) {
-    int64_t jmin = 0, jmax = -1;
-    algorithm1((uint64_t)pl.units, world, rank, &jmin, &jmax);
-    lo = jmin;
-    cnt = jmax - jmin + 1;
-  }
+  int grid = 0, block = 0;
+  int64_t lo = 0, cnt = pl.units, walked = 0;
   WalkParams wp{};
   wp.M = cx.dM; wp.r = pr.r; wp.c = pr.c; wp.mode = pr.mode; wp.d = pr.dl; wp.k = pl.k; wp.s = pl.s;
-  wp.unit_begin = lo; wp.unit_count = cnt; wp.pbits = prefix_bits(pr.dl);
-  wp.prefix_table = pl.table.empty() ? nullptr : cx.dPre + lo;
+  wp.pbits = prefix_bits(pr.dl);
   wp.counter = cx.dCtl; wp.key = cx.dCtl + 1; wp.unit_max = nullptr;
-  int grid = 0, block = 0;
   CU(cudaEventRecord(cx.ev[1], s));
-  if (cnt > 0) {
-    if ((rc = launch_walk(cx, pr, pl, wp, &grid, &block))) return rc;
-    launches += pl.kernel == K_GEN ? 1 : 2;   // table build + walk
+  const int nslices = world > 1 ? 1 : std::max(1, vslices);
+  for (int sl = 0; sl < nslices; ++sl) {
+    const int T = world > 1 ? world : nslices, t = world > 1 ? rank : sl;
+    if (T > 1) {
+      int64_t jmin = 0, jmax = -1;
+      algorithm1((uint64_t)pl.units, T, t, &jmin, &jmax);
+      lo = jmin;
+      cnt = jmax - jmin + 1;
+    }
+    wp.unit_begin = lo; wp.unit_count = cnt;
+    wp.prefix_table = pl.table.empty() ? nullptr : cx.dPre + lo;
+    if (cnt > 0) {
+      if (sl > 0 && pl.kernel == K_GEN) {   // the generic kernel's work counter restarts per slice
+        CU(cudaMemsetAsync(cx.dCtl, 0, sizeof(unsigned long long), s));
+      }
+      if ((rc = launch_walk(cx, pr, pl, wp, &grid, &block))) return rc;
+      launches += pl.kernel == K_GEN ? 1 : 2;   // table build + walk
+      walked += cnt;
+    }
   }
+  cnt = walked;
   CU(cudaEventRecord(cx.ev[2], s));
   if (world > 1) {
     Nccl& nc = nccl();
@@ -490,7 +503,7 @@ void write_out(const RunOut& ro, int64_t* value, int8_t* argmax) {
 }
 
 int compute_on(int device, const int32_t* hostM, const int32_t* devM, int n, int m, int d, int marg,
-               int rank, int world, ncclComm_t comm, int64_t* value, int8_t* argmax) {
+               int rank, int world, ncclComm_t comm, int64_t* value, int8_t* argmax, int vslices = 1) {
   if (!value) return LNORM_EINVAL;
   Problem pr;
   std::vector<int32_t> hcopy;
@@ -514,7 +527,7 @@ int compute_on(int device, const int32_t* hostM, const int32_t* devM, int n, int
   }
   RunOut ro;
   lnorm_stats st{};
-  if ((rc = run_device(*cx, dIn, pr, rank, world, comm, &ro, &st))) return rc;
+  if ((rc = run_device(*cx, dIn, pr, rank, world, comm, &ro, &st, vslices))) return rc;
   g_stats = st;
   write_out(ro, value, argmax);
   return LNORM_OK;
@@ -661,6 +674,14 @@ int lnorm_compute_multi(const int32_t* M, int32_t n, int32_t m, int32_t d, int32
   }
   g_stats = S;
   return LNORM_OK;
+}
+
+int lnorm_compute_sliced(const int32_t* M, int32_t n, int32_t m, int32_t d, int32_t with_marginals,
+                         int32_t slices, int64_t* value, int8_t* argmax) {
+  if (!M || slices < 1 || slices > 4096) return LNORM_EINVAL;
+  int dev = 0, rc = current_device(&dev);
+  if (rc) return rc;
+  return compute_on(dev, M, nullptr, n, m, d, with_marginals, 0, 1, nullptr, value, argmax, slices);
 }
 
 int lnorm_prefix_maxima(const int32_t* M, int32_t n, int32_t m, int32_t d, int32_t with_marginals,

@@ -301,3 +301,25 @@ def test_packed_guard_boundary_exact(lib, par):
     check(lib, M)
     v, _ = check(lib, np.abs(M))
     assert v == int(np.abs(M.astype(np.int64)).sum())
+
+
+# ------------------------------------------------- multi-GPU decomposition --
+
+@pytest.mark.parametrize("d,marg", MODES, ids=[mode_id(*m) for m in MODES])
+def test_sliced_ranks_bit_identical(lib, d, marg):
+    """results for 1/2/3/4/8 ranks (Algorithm-1 slices, max-reduced key) are bit-identical."""
+    for seed, (n, m) in enumerate([(14, 20), (12, 12), (16, 9), (10, 31)]):
+        M = synth.random_matrix(n, m, 70_000 + seed + 7 * d, -4, 4)
+        ref = lib.compute(M, d=d, with_marginals=marg)
+        for slices in (2, 3, 4, 8):
+            got = lib.compute_sliced(M, slices, d=d, with_marginals=marg)
+            assert got[0] == ref[0] and list(got[1]) == list(ref[1]), (slices, seed)
+        check(lib, M, d=d, marg=marg)
+
+
+def test_sliced_ranks_42x42_planted(lib):
+    """The 42x42 planted twin split over 8 virtual ranks: same exact value as the direct sum of blocks."""
+    M, blocks = synth.planted_l1()
+    expect = sum(oracle.l1(B)[0] for B in blocks)
+    v, arg = lib.compute_sliced(M, 8)
+    assert v == expect and oracle.value(M, arg) == v
