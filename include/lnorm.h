@@ -120,6 +120,22 @@ int lnorm_compute_rank_device(lnorm_comm* comm, const int32_t* M_device, int32_t
                               int32_t with_marginals, int64_t* value, int8_t* argmax);
 
 /*
+ * Exact norm with the paper's norm-preserving reductions applied first
+ * (App. A/B): zero rows/columns removed,
+ * proportional rows (L_1, L_marg: any sign; L_d: positive factor only) and
+ * proportional columns merged, sign-uniform columns merged for L_d, row 0 and
+ * column 0 of L_marg exempt (both zero => L_1 of the rest).  The reduction runs
+ * in single-block kernels; the reduced matrix is searched as by lnorm_compute
+ * and the argmax is expanded back (merged row x'' = sgn(c) * its partner for
+ * L_1 / L_marg, same label for L_d; removed zero rows get +1 / label 0).  The
+ * value equals lnorm_compute's; the returned argmax attains it but need not be
+ * the lexicographically smallest optimum.  reduced_shape (may be NULL)
+ * receives {n', m'}.
+ */
+int lnorm_compute_reduced(const int32_t* M, int32_t n, int32_t m, int32_t d, int32_t with_marginals,
+                          int64_t* value, int8_t* argmax, int32_t* reduced_shape);
+
+/*
  * Test hook for the multi-GPU decomposition on ONE device: plans for `slices`
  * ranks, walks the Algorithm-1 slice of every virtual rank one after the other
  * into the same 8-byte key (what ncclAllReduce(max) combines across GPUs) and

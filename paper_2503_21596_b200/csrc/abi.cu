@@ -20,6 +20,14 @@
 
 using namespace lnorm;
 
+namespace lnorm {
+size_t reduce_scratch_ints(int n, int m);
+cudaError_t reduce_launch(const int32_t* M, int n, int m, int mode, int32_t* scratch, int32_t* R, int32_t* rowsel,
+                          int32_t* info_dev, cudaStream_t st);
+cudaError_t mapback_launch(int n, int m, int nred, int ld, int32_t* scratch, const int32_t* rowsel,
+                           const int8_t* argr, int8_t* out, int32_t* info_dev, cudaStream_t st);
+}  // namespace lnorm
+
 namespace {
 
 // ------------------------------------------------------------------ NCCL --
@@ -308,6 +316,7 @@ struct DevCtx {
   uint64_t* dPre = nullptr; size_t capPre = 0;
   int64_t* dRes = nullptr;          // [0] value, then int8 argmax[kMaxCols]
   int64_t* dUnit = nullptr; size_t capUnit = 0;
+  int32_t* dRed = nullptr; size_t capRed = 0;      // reduction scratch + reduced matrix + maps
   int64_t* hRes = nullptr;          // pinned mirror of dRes
   bool ready = false;
 };
@@ -673,6 +682,60 @@ int lnorm_compute_multi(const int32_t* M, int32_t n, int32_t m, int32_t d, int32
     S.launches += sts[g].launches;
   }
   g_stats = S;
+  return LNORM_OK;
+}
+
+int lnorm_compute_reduced(const int32_t* M, int32_t n, int32_t m, int32_t d, int32_t with_marginals,
+                          int64_t* value, int8_t* argmax, int32_t* reduced_shape) {
+  if (!M || !value) return LNORM_EINVAL;
+  int dev = 0, rc = current_device(&dev);
+  if (rc) return rc;
+  Problem pr0;
+  if ((rc = validate(M, n, m, d, with_marginals, &pr0))) return rc;
+  DevCtx* cx = nullptr;
+  if ((rc = ctx_get(dev, &cx))) return rc;
+  std::lock_guard<std::mutex> g(cx->mu);
+  CU(cudaSetDevice(dev));
+  cudaStream_t s = cx->stream;
+  const size_t nm = (size_t)n * m;
+  const size_t need = reduce_scratch_ints(n, m) + nm + (size_t)n + 8 + (size_t)n;   // scratch, R, rowsel, info, argr/out
+  if ((rc = grow(&cx->dRed, &cx->capRed, need))) return rc;
+  if ((rc = grow(&cx->dIn, &cx->capIn, nm))) return rc;
+  int32_t* scratch = cx->dRed;
+  int32_t* R = scratch + reduce_scratch_ints(n, m);
+  int32_t* rowsel = R + nm;
+  int32_t* info = rowsel + n;
+  int8_t* bytes = reinterpret_cast<int8_t*>(info + 8);        // argr (n) then out (n)
+  CU(cudaMemcpyAsync(cx->dIn, M, sizeof(int32_t) * nm, cudaMemcpyHostToDevice, s));
+  const int mode = with_marginals ? MODE_MARG : (d == 1 ? MODE_L1 : MODE_LD);
+  if (reduce_launch(cx->dIn, n, m, mode, scratch, R, rowsel, info, s) != cudaSuccess) { (void)cudaGetLastError(); return LNORM_ECUDA; }
+  int32_t hinfo[4] = {0, 0, 0, 0};
+  CU(cudaMemcpyAsync(hinfo, info, sizeof(hinfo), cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  const int nr = hinfo[0], mr = hinfo[1], mode2 = hinfo[2];
+  if (reduced_shape) { reduced_shape[0] = nr; reduced_shape[1] = mr; }
+  RunOut ro;
+  lnorm_stats st{};
+  if (nr > 0 && mr > 0) {
+    std::vector<int32_t> hR((size_t)nr * mr);
+    CU(cudaMemcpy(hR.data(), R, sizeof(int32_t) * hR.size(), cudaMemcpyDeviceToHost));
+    Problem pr;
+    const int marg2 = mode2 == MODE_MARG ? 1 : 0;
+    if ((rc = validate(hR.data(), nr, mr, d, marg2, &pr))) return rc;
+    if ((rc = run_device(*cx, R, pr, 0, 1, nullptr, &ro, &st))) return rc;
+    CU(cudaMemcpyAsync(bytes, ro.argmax.data(), (size_t)nr, cudaMemcpyHostToDevice, s));
+  } else {
+    ro.value = 0;   // everything reduced away: the zero matrix (norm 0)
+  }
+  if (mapback_launch(n, m, nr > 0 && mr > 0 ? nr : 0, mode == MODE_LD ? 1 : 0, scratch, rowsel, bytes, bytes + n,
+                     info, s) != cudaSuccess) { (void)cudaGetLastError(); return LNORM_ECUDA; }
+  std::vector<int8_t> out((size_t)n);
+  CU(cudaMemcpyAsync(out.data(), bytes + n, (size_t)n, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  st.launches += 3;
+  g_stats = st;
+  *value = ro.value;
+  if (argmax) std::memcpy(argmax, out.data(), (size_t)n);
   return LNORM_OK;
 }
 

@@ -36,6 +36,12 @@ __host__ __device__ constexpr int cctz(int j) { return (j & 1) ? 0 : (j & 2) ? 1
 // Unrolled low walked digits: as many as keep the unrolled block under ~800
 // instructions (~13 KB): a larger body thrashes the instruction cache (ncu showed
 // 'no_instruction' as the dominant stall with 16 unrolled steps at C = 42, P = 2).
+#ifndef LN_PAIR_PMAX
+#define LN_PAIR_PMAX 2
+#endif
+#ifndef LN_PAIR_MINB
+#define LN_PAIR_MINB 1
+#endif
 #ifndef LN_PAIR_VOLATILE
 #define LN_PAIR_VOLATILE 0
 #endif
@@ -118,7 +124,7 @@ template <int MODE, int C, int P>
 __host__ __device__ constexpr int pair_unroll() { return unroll_digits(P * (2 * PairLayout<MODE, C>::G * C + 4) + PairLayout<MODE, C>::RW / 4); }
 
 template <int MODE, int C, int P>
-__global__ void __launch_bounds__(kBlock) walk_pair16_kernel(const WalkParams p, const uint32_t* __restrict__ gTab,
+__global__ void __launch_bounds__(kBlock, LN_PAIR_MINB) walk_pair16_kernel(const WalkParams p, const uint32_t* __restrict__ gTab,
                                                              const int32_t* __restrict__ gInit) {
   using LY = PairLayout<MODE, C>;
   constexpr int G = LY::G, RW = LY::RW, IW = InitLayout<MODE, C>::IW;
@@ -294,7 +300,7 @@ __global__ void build_pair16_kernel(const int32_t* M, int r, int c, int C, int k
 }
 
 template <int MODE, int C>
-__host__ __device__ constexpr int pair_units_per_lane() { return (MODE == MODE_LD ? 2 * C : C) <= 48 ? 2 : 1; }
+__host__ __device__ constexpr int pair_units_per_lane() { return (MODE == MODE_LD ? 2 * C : C) <= 48 ? LN_PAIR_PMAX : 1; }
 
 template <int MODE, int C>
 size_t pair_smem(int s) { return sizeof(uint32_t) * (size_t)(2 * (s - 1) * PairLayout<MODE, C>::RW); }
