@@ -120,6 +120,18 @@ int lnorm_compute_rank_device(lnorm_comm* comm, const int32_t* M_device, int32_t
                               int32_t with_marginals, int64_t* value, int8_t* argmax);
 
 /*
+ * Batched search (the inner oracle of see-saw / branch-and-bound
+ * loops): `batch` matrices of the same shape, contiguous
+ * (batch x n x m int32, host).  values: int64[batch]; argmax: int8[batch][n]
+ * (may be NULL), same conventions as lnorm_compute.  When every matrix is within
+ * the strategy-paired packed path's guard (sum |M| <= 16383, d <= 2) one walk
+ * launch covers the whole batch (units of all matrices in one grid, per-matrix
+ * keys, batched recovery); otherwise the matrices are searched one after another.
+ */
+int lnorm_compute_batch(const int32_t* M, int32_t batch, int32_t n, int32_t m, int32_t d, int32_t with_marginals,
+                        int64_t* values, int8_t* argmax);
+
+/*
  * Exact norm with the paper's norm-preserving reductions applied first
  * (App. A/B): zero rows/columns removed,
  * proportional rows (L_1, L_marg: any sign; L_d: positive factor only) and

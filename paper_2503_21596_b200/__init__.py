@@ -18,7 +18,7 @@ import threading
 import numpy as np
 
 __all__ = [
-    "LNormError", "load", "compute", "compute_device", "compute_reduced", "compute_multi", "Comm", "prefix_maxima",
+    "LNormError", "load", "compute", "compute_device", "compute_reduced", "compute_batch", "compute_multi", "Comm", "prefix_maxima",
     "walk_trace", "gray_digit", "gray_change", "partition", "last_stats", "status_string", "SYMBOLS", "plan",
 ]
 
@@ -31,7 +31,7 @@ SYMBOLS = [
     "lnorm_comm_unique_id", "lnorm_comm_create", "lnorm_comm_destroy", "lnorm_compute_rank",
     "lnorm_compute_rank_device",
     "lnorm_prefix_maxima", "lnorm_walk_trace", "lnorm_gray_digit", "lnorm_gray_change", "lnorm_partition",
-    "lnorm_last_stats", "lnorm_plan", "lnorm_compute_sliced", "lnorm_compute_reduced",
+    "lnorm_last_stats", "lnorm_plan", "lnorm_compute_sliced", "lnorm_compute_reduced", "lnorm_compute_batch",
 ]
 
 STATUS = {0: "OK", 1: "EINVAL", 2: "EOVERFLOW", 3: "ETOOLARGE", 4: "ENODEV", 5: "ECUDA", 6: "ENCCL", 7: "ENOMEM"}
@@ -106,6 +106,7 @@ def load():
             "lnorm_gray_change": ([i32, u64, i32p, i32p, i32p], ctypes.c_int),
             "lnorm_partition": ([u64, i64, i64, i64p, i64p], ctypes.c_int),
             "lnorm_last_stats": ([P(Stats)], ctypes.c_int),
+            "lnorm_compute_batch": ([i32p, i32, i32, i32, i32, i32, i64p, i8p], ctypes.c_int),
             "lnorm_compute_reduced": ([i32p, i32, i32, i32, i32, i64p, i8p, i32p], ctypes.c_int),
             "lnorm_compute_sliced": ([i32p, i32, i32, i32, i32, i32, i64p, i8p], ctypes.c_int),
             "lnorm_plan": ([i32p, i32, i32, i32, i32, i32, P(PlanInfo)], ctypes.c_int),
@@ -169,6 +170,21 @@ def compute_device(M_dev, d: int = 1, with_marginals: bool = False, stream=None)
     _check(load().lnorm_compute_device(ctypes.c_void_p(M_dev.data_ptr()), n, m, d, int(with_marginals), st,
                                        ctypes.byref(v), _p(arg, ctypes.c_int8)), "lnorm_compute_device")
     return int(v.value), arg
+
+
+def compute_batch(Ms, d: int = 1, with_marginals: bool = False):
+    """Many same-shape matrices in one call (batched walk when the packed guard holds).
+
+    Ms: array-like (batch, n, m).  Returns (values int64[batch], argmax int8[batch, n])."""
+    A = np.ascontiguousarray(np.asarray(Ms), dtype=np.int32)
+    if A.ndim != 3:
+        raise ValueError("Ms must be (batch, n, m)")
+    b, n, m = A.shape
+    vals = np.zeros(b, dtype=np.int64)
+    args = np.zeros((b, n), dtype=np.int8)
+    _check(load().lnorm_compute_batch(_p(A, ctypes.c_int32), b, n, m, d, int(with_marginals), _p(vals, ctypes.c_int64),
+                                      _p(args, ctypes.c_int8)), "lnorm_compute_batch")
+    return vals, args
 
 
 def compute_reduced(M, d: int = 1, with_marginals: bool = False):

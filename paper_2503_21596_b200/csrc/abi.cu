@@ -188,9 +188,9 @@ int64_t rgs_count(int len, int d) {
   return t > 9e18L ? INT64_MAX : (int64_t)t;
 }
 
-int make_plan(const Problem& pr, int world, Plan* pl) {
+int make_plan(const Problem& pr, int world, Plan* pl, int64_t target_override = 0) {
   const int f = pr.r - 1;
-  const int64_t target = kNominalLanes * 64 * std::max(1, world);
+  const int64_t target = target_override > 0 ? target_override : kNominalLanes * 64 * std::max(1, world);
   Plan p;
   if (pr.dl == 2) {
     // kernel family first (each has its own minimal suffix length), then the split
@@ -246,6 +246,8 @@ int make_plan(const Problem& pr, int world, Plan* pl) {
 // --------------------------------------------------------------- kernels --
 __global__ void orient_kernel(const int32_t* in, int n, int m, int transpose, int32_t* out) {
   const int64_t total = (int64_t)n * m;
+  in += blockIdx.y * total;     // batched launches: blockIdx.y = matrix
+  out += blockIdx.y * total;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     if (!transpose) out[i] = in[i];
     else { const int64_t x = i / m, y = i % m; out[y * n + x] = in[i]; }
@@ -260,12 +262,13 @@ __global__ void init_ctl_kernel(unsigned long long* ctl) {
 }
 
 struct FinalizeArgs {
-  const unsigned long long* ctl;
+  const unsigned long long* key;   // [batch] max keys
+  const unsigned long long* lex;   // [batch] smallest optimal suffix keys
   const uint64_t* table;   // full prefix table or null (binary arithmetic)
   const int32_t* Min;      // original (un-oriented) input, n x m
   int n, m, r, k, s, base, mode, transposed, pbits;
-  int64_t* value_out;
-  int8_t* argmax_out;      // int8[n]
+  int64_t* value_out;      // [batch]
+  int8_t* argmax_out;      // int8[batch][n]
 };
 
 // Assemble the lexicographically smallest optimum from (unit, suffix key) and
@@ -273,10 +276,13 @@ struct FinalizeArgs {
 __global__ void finalize_kernel(FinalizeArgs a) {
   __shared__ int8_t dig[kMaxRows];
   __shared__ int flip;
-  const unsigned long long key = a.ctl[1], lex = a.ctl[2];
+  // batched launches: blockIdx.x = matrix
+  const unsigned long long key = a.key[blockIdx.x], lex = a.lex[blockIdx.x];
+  a.Min += (int64_t)blockIdx.x * a.n * a.m;
+  a.argmax_out += (int64_t)blockIdx.x * a.n;
   const int64_t u = (int64_t)key_unit(key);
   if (threadIdx.x == 0) {
-    *a.value_out = (int64_t)key_value(key);
+    a.value_out[blockIdx.x] = (int64_t)key_value(key);
     for (int x = 0; x <= a.k; ++x)
       dig[x] = a.table ? (int8_t)((a.table[u] >> (a.pbits * x)) & ((1ull << a.pbits) - 1ull)) : (int8_t)(x == 0 ? 0 : (u >> (a.k - x)) & 1);
     uint64_t q = lex;
@@ -317,6 +323,7 @@ struct DevCtx {
   int64_t* dRes = nullptr;          // [0] value, then int8 argmax[kMaxCols]
   int64_t* dUnit = nullptr; size_t capUnit = 0;
   int32_t* dRed = nullptr; size_t capRed = 0;      // reduction scratch + reduced matrix + maps
+  int64_t* dBatch = nullptr; size_t capBatch = 0;  // batched-call buffers
   int64_t* hRes = nullptr;          // pinned mirror of dRes
   bool ready = false;
 };
@@ -450,6 +457,7 @@ int run_device(DevCtx& cx, const int32_t* dIn, const Problem& pr, int rank, int 
       cnt = jmax - jmin + 1;
     }
     wp.unit_begin = lo; wp.unit_count = cnt;
+    walk_params_single(wp);
     wp.prefix_table = pl.table.empty() ? nullptr : cx.dPre + lo;
     if (cnt > 0) {
       if (sl > 0 && pl.kernel == K_GEN) {   // the generic kernel's work counter restarts per slice
@@ -470,11 +478,12 @@ int run_device(DevCtx& cx, const int32_t* dIn, const Problem& pr, int rank, int 
   // recovery over the full unit space (same winning unit on every rank)
   WalkParams rp = wp;
   rp.unit_begin = 0; rp.unit_count = pl.units;
+  walk_params_single(rp);
   rp.prefix_table = pl.table.empty() ? nullptr : cx.dPre;
   if (recover_launch(rp, cx.dCtl + 2, s) != cudaSuccess) { (void)cudaGetLastError(); return LNORM_ECUDA; }
   ++launches;
   FinalizeArgs fa;
-  fa.ctl = cx.dCtl; fa.table = rp.prefix_table; fa.Min = dIn; fa.n = pr.n; fa.m = pr.m; fa.r = pr.r;
+  fa.key = cx.dCtl + 1; fa.lex = cx.dCtl + 2; fa.table = rp.prefix_table; fa.Min = dIn; fa.n = pr.n; fa.m = pr.m; fa.r = pr.r;
   fa.k = pl.k; fa.s = pl.s; fa.base = pr.dl; fa.mode = pr.mode; fa.transposed = pr.transposed ? 1 : 0; fa.pbits = prefix_bits(pr.dl);
   fa.value_out = cx.dRes; fa.argmax_out = reinterpret_cast<int8_t*>(cx.dRes + 1);
   finalize_kernel<<<1, 256, 0, s>>>(fa);
@@ -739,6 +748,102 @@ int lnorm_compute_reduced(const int32_t* M, int32_t n, int32_t m, int32_t d, int
   return LNORM_OK;
 }
 
+int lnorm_compute_batch(const int32_t* M, int32_t batch, int32_t n, int32_t m, int32_t d, int32_t with_marginals,
+                        int64_t* values, int8_t* argmax) {
+  if (!M || !values || batch < 1) return LNORM_EINVAL;
+  int dev = 0, rc = current_device(&dev);
+  if (rc) return rc;
+  const size_t nm = (size_t)n * m;
+  // validate every matrix; the batched kernel needs the strategy-paired path for all of them
+  Problem pr;
+  bool all_pair = true;
+  for (int b = 0; b < batch; ++b) {
+    Problem q;
+    if ((rc = validate(M + b * nm, n, m, d, with_marginals, &q))) return rc;
+    if (b == 0) pr = q;
+    all_pair = all_pair && q.fitsPair;
+  }
+  Plan pl;
+  const int64_t target = std::max<int64_t>(1, kNominalLanes * 8 / batch);
+  if (all_pair && pr.dl == 2) {
+    if ((rc = make_plan(pr, 1, &pl, target))) return rc;
+  }
+  if (!all_pair || pr.dl != 2 || pl.kernel != K_PAIR16) {
+    // outside the batched kernel's reach (L_d, d >= 3, or a matrix beyond the packed
+    // guard): one search per matrix through the same device path
+    for (int b = 0; b < batch; ++b) {
+      if ((rc = compute_on(dev, M + b * nm, nullptr, n, m, d, with_marginals, 0, 1, nullptr, values + b,
+                           argmax ? argmax + (size_t)b * n : nullptr)))
+        return rc;
+    }
+    return LNORM_OK;
+  }
+  DevCtx* cx = nullptr;
+  if ((rc = ctx_get(dev, &cx))) return rc;
+  std::lock_guard<std::mutex> g(cx->mu);
+  CU(cudaSetDevice(dev));
+  cudaStream_t s = cx->stream;
+  int64_t tabw = 0, initw = 0;
+  walk_pair16_table_sizes(pr.mode, pr.c, pl.k, pl.s, &tabw, &initw);
+  auto up8 = [](size_t x) { return (x + 7) & ~(size_t)7; };
+  const size_t oIn = 0, oM = oIn + up8(batch * nm), oTab = oM + up8(batch * nm), oInit = oTab + up8(batch * (size_t)tabw);
+  const size_t oKey = oInit + up8(batch * (size_t)initw);                 // int32 units so far
+  const size_t words32 = oKey + 4 * (size_t)batch + 2 * (size_t)batch + up8((size_t)batch * n) / 4 + 8;
+  if ((rc = grow(&cx->dBatch, &cx->capBatch, words32 / 2 + 1))) return rc;
+  int32_t* base = reinterpret_cast<int32_t*>(cx->dBatch);
+  int32_t* dIn = base + oIn;
+  int32_t* dMo = base + oM;
+  uint32_t* dTab = reinterpret_cast<uint32_t*>(base + oTab);
+  int32_t* dInit = base + oInit;
+  unsigned long long* keys = reinterpret_cast<unsigned long long*>(base + oKey);
+  unsigned long long* lex = keys + batch;
+  int64_t* vals = reinterpret_cast<int64_t*>(lex + batch);
+  int8_t* args = reinterpret_cast<int8_t*>(vals + batch);
+  CU(cudaEventRecord(cx->ev[0], s));
+  CU(cudaMemcpyAsync(dIn, M, sizeof(int32_t) * batch * nm, cudaMemcpyHostToDevice, s));
+  orient_kernel<<<dim3(std::min(64, (int)((nm + 255) / 256)), batch), 256, 0, s>>>(dIn, n, m, pr.transposed ? 1 : 0, dMo);
+  CU(cudaGetLastError());
+  CU(cudaMemsetAsync(keys, 0, sizeof(unsigned long long) * batch, s));
+  CU(cudaMemsetAsync(lex, 0xFF, sizeof(unsigned long long) * batch, s));
+  WalkParams wp{};
+  wp.M = dMo; wp.r = pr.r; wp.c = pr.c; wp.mode = pr.mode; wp.d = pr.dl; wp.k = pl.k; wp.s = pl.s;
+  wp.pbits = prefix_bits(pr.dl); wp.prefix_table = nullptr; wp.counter = nullptr; wp.key = keys; wp.unit_max = nullptr;
+  wp.unit_begin = 0; wp.unit_count = pl.units * batch;
+  wp.batch = batch; wp.units_per = pl.units; wp.m_stride = (int64_t)nm; wp.tab_stride = tabw; wp.init_stride = initw;
+  int block = 32;
+  const int occ = std::max(1, walk_pair16_occupancy(pr.mode, pr.c, pl.s, &block));
+  const int64_t P = walk_pair16_units_per_lane(pr.mode, pr.c);
+  const int64_t chunks = (int64_t)batch * ((pl.units + 32 * P - 1) / (32 * P));
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)occ * cx->nsm, chunks));
+  CU(cudaEventRecord(cx->ev[1], s));
+  if (walk_pair16_launch(wp, reinterpret_cast<int32_t*>(dTab), dInit, grid, s, &block) != cudaSuccess) {
+    (void)cudaGetLastError(); return LNORM_ECUDA;
+  }
+  CU(cudaEventRecord(cx->ev[2], s));
+  if (recover_launch(wp, lex, s) != cudaSuccess) { (void)cudaGetLastError(); return LNORM_ECUDA; }
+  FinalizeArgs fa;
+  fa.key = keys; fa.lex = lex; fa.table = nullptr; fa.Min = dIn; fa.n = n; fa.m = m; fa.r = pr.r;
+  fa.k = pl.k; fa.s = pl.s; fa.base = 2; fa.mode = pr.mode; fa.transposed = pr.transposed ? 1 : 0; fa.pbits = 1;
+  fa.value_out = vals; fa.argmax_out = args;
+  finalize_kernel<<<batch, 128, 0, s>>>(fa);
+  CU(cudaGetLastError());
+  CU(cudaMemcpyAsync(values, vals, sizeof(int64_t) * batch, cudaMemcpyDeviceToHost, s));
+  if (argmax) CU(cudaMemcpyAsync(argmax, args, (size_t)batch * n, cudaMemcpyDeviceToHost, s));
+  CU(cudaEventRecord(cx->ev[3], s));
+  CU(cudaStreamSynchronize(s));
+  float wms = 0, tms = 0;
+  cudaEventElapsedTime(&wms, cx->ev[1], cx->ev[2]);
+  cudaEventElapsedTime(&tms, cx->ev[0], cx->ev[3]);
+  lnorm_stats S{};
+  S.rows = pr.r; S.cols = pr.c; S.transposed = pr.transposed; S.prefix_digits = pl.k; S.suffix_digits = pl.s;
+  S.d = 1; S.units = pl.units * batch; S.units_total = S.units;
+  S.steps = (double)S.units * (double)ipow(2, pl.s);
+  S.column_updates = S.steps * pr.c;
+  S.walk_ms = wms; S.total_ms = tms; S.launches = 5; S.variant = pl.kernel; S.block_threads = block; S.grid_blocks = grid;
+  g_stats = S;
+  return LNORM_OK;
+}
+
 int lnorm_compute_sliced(const int32_t* M, int32_t n, int32_t m, int32_t d, int32_t with_marginals,
                          int32_t slices, int64_t* value, int8_t* argmax) {
   if (!M || slices < 1 || slices > 4096) return LNORM_EINVAL;
@@ -810,6 +915,7 @@ int lnorm_prefix_maxima(const int32_t* M, int32_t n, int32_t m, int32_t d, int32
   WalkParams wp{};
   wp.M = cx->dM; wp.r = n; wp.c = m; wp.mode = pr.mode; wp.d = base; wp.k = pl.k; wp.s = pl.s;
   wp.unit_begin = 0; wp.unit_count = count; wp.prefix_table = cx->dPre; wp.pbits = pb;
+  walk_params_single(wp);
   wp.counter = cx->dCtl; wp.key = cx->dCtl + 1; wp.unit_max = cx->dUnit;
   int grid = 0, block = 0;
   if ((rc = launch_walk(*cx, pr, pl, wp, &grid, &block))) return rc;
@@ -852,6 +958,7 @@ int lnorm_walk_trace(const int32_t* M, int32_t n, int32_t m, int32_t d, int32_t 
   WalkParams wp{};
   wp.M = cx->dM; wp.r = n; wp.c = m; wp.mode = pr.mode; wp.d = base; wp.k = nfixed - 1; wp.s = s_;
   wp.unit_begin = 0; wp.unit_count = 1; wp.prefix_table = cx->dPre; wp.pbits = pb;
+  walk_params_single(wp);
   int8_t* ddig = reinterpret_cast<int8_t*>(cx->dUnit + nw);
   if (trace_launch(wp, nw, cx->dUnit, digits ? ddig : nullptr, s) != cudaSuccess) { (void)cudaGetLastError(); return LNORM_ECUDA; }
   CU(cudaMemcpyAsync(values, cx->dUnit, sizeof(int64_t) * nw, cudaMemcpyDeviceToHost, s));

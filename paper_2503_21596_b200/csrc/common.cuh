@@ -33,7 +33,21 @@ struct WalkParams {
   unsigned long long* counter;   // work counter (zeroed before launch)
   unsigned long long* key;       // global max key (zeroed before launch)
   int64_t* unit_max;             // optional per-unit maxima (index u - unit_begin)
+  // batched launches (walk_pair16 only; every other kernel uses batch == 1):
+  // matrix b has its oriented matrix at M + b*m_stride, its tables at
+  // table + b*tab_stride / init + b*init_stride and its key at key[b];
+  // each matrix has units_per units (unit_count = batch * units_per).
+  int32_t batch;
+  int64_t units_per;
+  int64_t m_stride, tab_stride, init_stride;
 };
+
+// Defaults for a single-matrix launch.
+inline void walk_params_single(WalkParams& p) {
+  p.batch = 1;
+  p.units_per = p.unit_count;
+  p.m_stride = p.tab_stride = p.init_stride = 0;
+}
 
 // Max-reduction key: high word = value biased to unsigned order, low word =
 // ~unit so that, among equal values, the SMALLEST unit index wins
@@ -115,6 +129,8 @@ template <int MODE> cudaError_t walk_pair16_launch_mode(const WalkParams& p, int
 template <int MODE> int walk_pair16_occupancy_mode(int c, int s);
 template <int MODE> int walk_pair16_units_per_lane_mode(int c);
 template <int MODE> int walk_pair16_unroll_mode(int c);
+template <int MODE> void walk_pair16_table_sizes_mode(int c, int k, int s, int64_t* tab_words, int64_t* init_ints);
+void walk_pair16_table_sizes(int mode, int c, int k, int s, int64_t* tab_words, int64_t* init_ints);
 // Packed 16-bit d-ary walk (L_d, d in {3,4}; exactness guard checked by the caller).
 bool walk_ld16_supported(int d, int c, int s);
 int walk_ld16_units_per_lane(int d, int c);

@@ -64,6 +64,12 @@ bool walk_pair16_supported(int mode, int c, int s) {
   return 2 * (s - 1) * RW <= 8448;
 }
 
+void walk_pair16_table_sizes(int mode, int c, int k, int s, int64_t* tab_words, int64_t* init_ints) {
+  if (mode == MODE_L1) walk_pair16_table_sizes_mode<MODE_L1>(c, k, s, tab_words, init_ints);
+  else if (mode == MODE_MARG) walk_pair16_table_sizes_mode<MODE_MARG>(c, k, s, tab_words, init_ints);
+  else walk_pair16_table_sizes_mode<MODE_LD>(c, k, s, tab_words, init_ints);
+}
+
 int walk_pair16_units_per_lane(int mode, int c) {
   if (mode == MODE_L1) return walk_pair16_units_per_lane_mode<MODE_L1>(c);
   if (mode == MODE_MARG) return walk_pair16_units_per_lane_mode<MODE_MARG>(c);

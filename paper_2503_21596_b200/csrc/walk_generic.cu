@@ -12,6 +12,8 @@
 // warp-uniform.  This kernel covers every shape (any c <= 1024, any d <= 8,
 // any suffix length) and is the correctness anchor for shapes outside the
 // hot kernels' template set; recover and trace reuse the same device code.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace lnorm {
@@ -102,9 +104,14 @@ __global__ void __launch_bounds__(32 * kGenWarps) walk_generic_kernel(const Walk
 // (Algorithm 1), one per warp; each warp starts from its
 // chunk's first word by the closed form and walks it, keeping the smallest
 // lexicographic suffix key among words whose value equals the optimum.
-__global__ void __launch_bounds__(32 * kGenWarps) recover_kernel(const WalkParams p, unsigned long long* lex_out) {
+__global__ void __launch_bounds__(32 * kGenWarps) recover_kernel(const WalkParams pin, unsigned long long* lex_out) {
   extern __shared__ int32_t smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  // batched launches: blockIdx.y = matrix
+  WalkParams p = pin;
+  p.M = pin.M + (int64_t)blockIdx.y * pin.m_stride;
+  p.key = pin.key + blockIdx.y;
+  lex_out += blockIdx.y;
   const int nG = groups_of(p);
   int32_t* G = smem + wib * nG * p.c;
   const uint32_t base = (uint32_t)base_of(p);
@@ -198,7 +205,12 @@ cudaError_t recover_launch(const WalkParams& p, unsigned long long* lex_out, cud
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  recover_kernel<<<nsm * 2, 32 * kGenWarps, sm, st>>>(p, lex_out);
+  // blocks per matrix: enough warps for ~1k-word chunks, at most 2 per SM
+  uint64_t words = 1;
+  for (int i = 0; i < p.s; ++i) words *= (uint64_t)(p.mode == MODE_LD ? p.d : 2);
+  int gx = (int)std::min<uint64_t>((uint64_t)nsm * 2, std::max<uint64_t>(1, words / (1024ull * kGenWarps)));
+  if (p.batch > 1) gx = std::max(1, std::min(gx, (nsm * 8 + p.batch - 1) / p.batch));
+  recover_kernel<<<dim3(gx, p.batch > 0 ? p.batch : 1), 32 * kGenWarps, sm, st>>>(p, lex_out);
   return cudaGetLastError();
 }
 

@@ -42,6 +42,9 @@ __host__ __device__ constexpr int cctz(int j) { return (j & 1) ? 0 : (j & 2) ? 1
 #ifndef LN_PAIR_MINB
 #define LN_PAIR_MINB 1
 #endif
+#ifndef LN_PAIR_CHUNKED
+#define LN_PAIR_CHUNKED 0
+#endif
 #ifndef LN_PAIR_VOLATILE
 #define LN_PAIR_VOLATILE 0
 #endif
@@ -81,6 +84,37 @@ struct PairStep {
   // and the unit's own q at its start word is added once at the end.
   static __device__ __forceinline__ void run(uint32_t (&R)[P][G * C], uint32_t& Q, uint32_t (&best2)[P],
                                              uint32_t sbase, int off) {
+#if LN_PAIR_CHUNKED
+    // row consumed 4 words at a time (one LDS.128 per quad, applied to every unit
+    // before the next quad is loaded): keeps only a quad of the row live
+    uint32_t a0[P], a1[P];
+#pragma unroll
+    for (int v = 0; v < RW / 4; ++v) {
+      const uint4 x4 = lds128(sbase + 4u * (uint32_t)(off + 4 * v));
+      const uint32_t rq[4] = {x4.x, x4.y, x4.z, x4.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int i = 4 * v + e;
+        if (i < G * C) {
+#pragma unroll
+          for (int j = 0; j < P; ++j) {
+            R[j][i] = __vadd2(R[j][i], rq[e]);
+            if (i == 0) a0[j] = __vmaxs2(R[j][0], 0u);
+            else if (i == 1) a1[j] = __vmaxs2(R[j][1], 0u);
+            else if (i & 1) a1[j] = __viaddmax_s16x2(a1[j], R[j][i], a1[j]);
+            else a0[j] = __viaddmax_s16x2(a0[j], R[j][i], a0[j]);
+          }
+        } else if (i == RW - 1 && MODE != MODE_LD) {
+          Q = __vadd2(Q, rq[e]);
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
+      const uint32_t a = (G * C > 1) ? __vadd2(a0[j], a1[j]) : a0[j];
+      best2[j] = __viaddmax_s16x2(a, __vadd2(a, Q), best2[j]);
+    }
+#else
     uint32_t r[RW];
 #if LN_PAIR_VOLATILE
 #pragma unroll
@@ -117,6 +151,7 @@ struct PairStep {
 #endif
       best2[j] = __viaddmax_s16x2(a, __vadd2(a, Q), best2[j]);
     }
+#endif
   }
 };
 
@@ -133,24 +168,42 @@ __global__ void __launch_bounds__(kBlock, LN_PAIR_MINB) walk_pair16_kernel(const
   const int lane = threadIdx.x & 31;
   const int sw = p.s - 1;                          // walked digits (rows k+1 .. r-2)
   const int total = 2 * sw * RW;
-  for (int i = threadIdx.x; i < total; i += blockDim.x) sT[i] = gTab[i];
-  __syncthreads();
-  const int32_t* baseRec = gInit + (p.k + 1) * IW;
-  const int32_t* pairRec = baseRec + IW;
   const uint32_t nblk = 1u << (sw - K);
   int32_t best = INT32_MIN;
   uint32_t best_u = 0;
   bool have = false;
-  const int64_t nchunks = (p.unit_count + 32 * P - 1) / (32 * P);
+  // Static warp-chunk schedule (block = one warp).  Chunks never straddle matrices
+  // (batched launches): chunk ch -> matrix b = ch / CPM, local chunk lc = ch % CPM.
+  const int64_t CPM = (p.units_per + 32 * P - 1) / (32 * P);
+  const int64_t nchunks = CPM * p.batch;
+  int64_t cur_b = -1;
+  const int32_t* gI = gInit;
   for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    const int64_t b = ch / CPM, lc = ch - b * CPM;
+    if (b != cur_b) {                              // (re)stage this matrix's delta table
+      if (cur_b >= 0) {
+        unsigned long long key = have ? make_key(best, best_u) : 0ull;
+        key = warp_max_u64(key);
+        if (lane == 0 && key) atomicMax(p.key + cur_b, key);
+        best = INT32_MIN; have = false;
+      }
+      __syncwarp();
+      const uint32_t* src = gTab + b * p.tab_stride;
+      for (int i = lane; i < total; i += 32) sT[i] = src[i];
+      __syncwarp();
+      gI = gInit + b * p.init_stride;
+      cur_b = b;
+    }
+    const int32_t* baseRec = gI + (p.k + 1) * IW;
+    const int32_t* pairRec = baseRec + IW;
     uint32_t R[P][G * C];
     uint32_t q[P], best2[P];
     uint32_t Q = 0u;                                   // uniform: q(t) - q(0), both halves
     // ---- unit init: column sums of strategies A and B (the paper's per-thread product)
 #pragma unroll
     for (int j = 0; j < P; ++j) {
-      const int64_t rel = ch * 32 * P + j * 32 + lane;
-      const int64_t u = p.unit_begin + (rel < p.unit_count ? rel : 0);
+      const int64_t rel = lc * 32 * P + j * 32 + lane;
+      const int64_t u = p.unit_begin + (rel < p.units_per ? rel : 0);
       int32_t mA[C];
       int32_t qA = __ldg(baseRec + G * C);
 #pragma unroll
@@ -158,7 +211,7 @@ __global__ void __launch_bounds__(kBlock, LN_PAIR_MINB) walk_pair16_kernel(const
       for (int x = 0; x <= p.k; ++x) {
         const int dig = prefix_digit(p, u, x);
         const int32_t f = (MODE == MODE_LD) ? 1 - dig : 1 - 2 * dig;
-        const int32_t* rec = gInit + x * IW;
+        const int32_t* rec = gI + x * IW;
 #pragma unroll
         for (int y = 0; y < C; ++y) mA[y] += f * __ldg(rec + y);
         qA += f * __ldg(rec + C);
@@ -204,8 +257,8 @@ __global__ void __launch_bounds__(kBlock, LN_PAIR_MINB) walk_pair16_kernel(const
     }
 #pragma unroll
     for (int j = 0; j < P; ++j) {
-      const int64_t rel = ch * 32 * P + j * 32 + lane;
-      if (rel < p.unit_count) {
+      const int64_t rel = lc * 32 * P + j * 32 + lane;
+      if (rel < p.units_per) {
         // add the unit's own start-word q (per strategy) back: value = 2H + Q + q(0)
         const int32_t lo = (int32_t)(int16_t)(best2[j] & 0xFFFF) + (int32_t)(int16_t)(q[j] & 0xFFFF);
         const int32_t hi = (int32_t)(int16_t)(best2[j] >> 16) + (int32_t)(int16_t)(q[j] >> 16);
@@ -217,14 +270,18 @@ __global__ void __launch_bounds__(kBlock, LN_PAIR_MINB) walk_pair16_kernel(const
   }
   unsigned long long key = have ? make_key(best, best_u) : 0ull;
   key = warp_max_u64(key);
-  if (lane == 0 && key) atomicMax(p.key, key);
+  if (lane == 0 && key && cur_b >= 0) atomicMax(p.key + cur_b, key);
 }
 
 // Tables from the oriented matrix: packed duplicated delta records (walked digit b
 // <-> row r-2-b, sign 1 = flip to -1 / label 1) and the int32 init records.
 template <int MODE>
 __global__ void build_pair16_kernel(const int32_t* M, int r, int c, int C, int k, int s,
-                                    uint32_t* tab, int32_t* init) {
+                                    uint32_t* tab, int32_t* init, int64_t m_stride, int64_t tab_stride,
+                                    int64_t init_stride) {
+  M += blockIdx.x * m_stride;            // one block per matrix of a batch
+  tab += blockIdx.x * tab_stride;
+  init += blockIdx.x * init_stride;
   const int G = (MODE == MODE_LD) ? 2 : 1;
   const int RW = pad4(G * C + 1), IW = G * C + 2;
   const int c0 = (MODE == MODE_MARG) ? 1 : 0;
@@ -363,7 +420,8 @@ cudaError_t walk_pair16_launch_mode<LN_BIN_MODE>(const WalkParams& p, int32_t* s
   const int C = walk_pair16_cols<LN_BIN_MODE>(p.c);
   if (C == 0) return cudaErrorInvalidValue;
   uint32_t* tab = reinterpret_cast<uint32_t*>(scratch_tab);
-  build_pair16_kernel<LN_BIN_MODE><<<1, 128, 0, st>>>(p.M, p.r, p.c, C, p.k, p.s, tab, scratch_init);
+  build_pair16_kernel<LN_BIN_MODE><<<p.batch, 128, 0, st>>>(p.M, p.r, p.c, C, p.k, p.s, tab, scratch_init,
+                                                             p.m_stride, p.tab_stride, p.init_stride);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   LN_PAIR_SWITCH(LN_BIN_MODE, C, launch_pair, p, tab, scratch_init, grid, st)
@@ -378,6 +436,19 @@ int walk_pair16_occupancy_mode<LN_BIN_MODE>(int c, int s) {
 
 template <int MODE, int C>
 int unroll_pair() { return pair_unroll<MODE, C, pair_units_per_lane<MODE, C>()>(); }
+
+template <int MODE, int C>
+int tabw_pair() { return PairLayout<MODE, C>::RW; }
+
+// words of the delta table / ints of the init records for one matrix
+template <>
+void walk_pair16_table_sizes_mode<LN_BIN_MODE>(int c, int k, int s, int64_t* tab_words, int64_t* init_ints) {
+  const int C = walk_pair16_cols<LN_BIN_MODE>(c);
+  const int G = (LN_BIN_MODE == MODE_LD) ? 2 : 1;
+  const int RW = (G * C + 1 + 3) & ~3, IW = G * C + 2;
+  *tab_words = (int64_t)2 * (s - 1) * RW;
+  *init_ints = (int64_t)(k + 3) * IW;
+}
 
 template <>
 int walk_pair16_unroll_mode<LN_BIN_MODE>(int c) {
