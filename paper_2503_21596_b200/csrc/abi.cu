@@ -195,27 +195,27 @@ int make_plan(const Problem& pr, int world, Plan* pl, int64_t target_override = 
   if (pr.dl == 2) {
     // kernel family first (each has its own minimal suffix length), then the split
     const int ov = kernel_override();
-    const bool hot = walk_bin_supported(pr.mode, pr.c, std::min(f, 4)) && f >= 4;
-    int kern = hot ? K_BIN : K_GEN;
-    int smin = hot ? 4 : 0;
     auto min_s = [&](int kind) {
       for (int s_ = 1; s_ <= f; ++s_) {
         if (kind == K_PAIR16 && walk_pair16_supported(pr.mode, pr.c, s_)) return s_;
         if (kind == K_BIN16 && walk_bin16_supported(pr.mode, pr.c, s_)) return s_;
+        if (kind == K_BIN && walk_bin_supported(pr.mode, pr.c, s_)) return s_;
       }
       return -1;
     };
-    if (hot && ov != K_BIN && ov != K_GEN) {
-      int sp = pr.fitsPair && ov != K_BIN16 ? min_s(K_PAIR16) : -1;
-      int sb = pr.fits16 ? min_s(K_BIN16) : -1;
-      if (sp > 0) { kern = K_PAIR16; smin = sp; }
-      else if (sb > 0) { kern = K_BIN16; smin = sb; }
-    }
-    if (ov == K_GEN) { kern = K_GEN; smin = 0; }
+    int kern = K_GEN, smin = 0;
+    const int sp = (pr.fitsPair && ov != K_BIN16 && ov != K_BIN && ov != K_GEN) ? min_s(K_PAIR16) : -1;
+    const int sb = (pr.fits16 && ov != K_BIN && ov != K_GEN) ? min_s(K_BIN16) : -1;
+    const int si = (ov != K_GEN) ? min_s(K_BIN) : -1;
+    if (sp > 0) { kern = K_PAIR16; smin = sp; }
+    else if (sb > 0) { kern = K_BIN16; smin = sb; }
+    else if (si > 0) { kern = K_BIN; smin = si; }
     int k = 0;
     while (k < f - smin && k < 31 && (1LL << k) < target) ++k;
     p.k = k; p.s = f - k; p.units = 1LL << k;
     p.kernel = kern;
+    if (kern == K_BIN16 && !walk_bin16_table_fits(pr.mode, pr.c, p.k, p.s))
+      p.kernel = walk_bin_supported(pr.mode, pr.c, p.s) ? K_BIN : K_GEN;
   } else {
     const int d = pr.dl;
     const int ov = kernel_override();
@@ -344,7 +344,7 @@ int ctx_get(int device, DevCtx** out) {
     CU(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
     for (auto& e : c.ev) CU(cudaEventCreate(&e));
     CU(cudaDeviceGetAttribute(&c.nsm, cudaDevAttrMultiProcessorCount, device));
-    CU(cudaMalloc(&c.dTab, sizeof(int32_t) * 8448));
+    CU(cudaMalloc(&c.dTab, sizeof(int32_t) * 32768));
     CU(cudaMalloc(&c.dInit, sizeof(int32_t) * 16384));
     CU(cudaMalloc(&c.dCtl, sizeof(unsigned long long) * 4));
     CU(cudaMalloc(&c.dRes, 8 + kMaxCols + 64));

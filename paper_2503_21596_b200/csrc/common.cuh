@@ -110,6 +110,8 @@ template <int MODE> cudaError_t walk_bin16_launch_mode(const WalkParams& p, int3
 template <int MODE> int walk_bin16_occupancy_mode(int c, int k, int s);
 template <int MODE> int walk_bin16_units_per_lane_mode(int c);
 template <int MODE> int walk_bin16_unroll_mode(int c);
+template <int MODE> int64_t walk_bin16_table_words_mode(int c, int k, int s);
+bool walk_bin16_table_fits(int mode, int c, int k, int s);
 int walk_bin16_units_per_lane(int mode, int c);
 // Hot d-ary walk (L_d, d in {3,4}).
 bool walk_ld_supported(int d, int c, int s);

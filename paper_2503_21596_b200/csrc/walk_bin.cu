@@ -33,6 +33,14 @@ bool walk_bin16_supported(int mode, int c, int s) {
   return false;
 }
 
+bool walk_bin16_table_fits(int mode, int c, int k, int s) {
+  int64_t w = 0;
+  if (mode == MODE_L1) w = walk_bin16_table_words_mode<MODE_L1>(c, k, s);
+  else if (mode == MODE_MARG) w = walk_bin16_table_words_mode<MODE_MARG>(c, k, s);
+  else w = walk_bin16_table_words_mode<MODE_LD>(c, k, s);
+  return w <= 16384;
+}
+
 int walk_bin16_occupancy(int mode, int c, int k, int s, int* block_out) {
   *block_out = 32;
   if (mode == MODE_L1) return walk_bin16_occupancy_mode<MODE_L1>(c, k, s);

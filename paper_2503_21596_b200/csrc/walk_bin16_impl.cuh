@@ -25,7 +25,7 @@ namespace lnorm {
 
 namespace {
 
-constexpr int kTabWords = 8448;
+constexpr int kTabWords = 16384;   // smem table limit (words); scratch buffer is 32768 ints
 constexpr int kBlock = 32;
 
 // ctz for the unrolled step index j in [1, 16): a ternary chain that folds at compile time
@@ -102,7 +102,11 @@ struct Walker16 {
 };
 
 template <int MODE, int W, int P>
-__host__ __device__ constexpr int bin16_unroll() { return unroll_digits(P * (2 * Layout<MODE, W>::Wt + 5) + Layout<MODE, W>::RWd / 4); }
+__host__ __device__ constexpr int bin16_unroll() {
+  // wide rows: keep the unrolled block near 1000 instructions (instruction cache)
+  return (Layout<MODE, W>::Wt > 40 && unroll_digits(P * (2 * Layout<MODE, W>::Wt + 5) + Layout<MODE, W>::RWd / 4) > 2)
+             ? 2 : unroll_digits(P * (2 * Layout<MODE, W>::Wt + 5) + Layout<MODE, W>::RWd / 4);
+}
 
 template <int MODE, int W, int P>
 __global__ void __launch_bounds__(kBlock) walk_bin16_kernel(const WalkParams p, const uint32_t* __restrict__ gTab) {
@@ -302,6 +306,10 @@ int occ_one16(int k, int s) {
     case 23: return FN<MODE, 23>(__VA_ARGS__); case 24: return FN<MODE, 24>(__VA_ARGS__);    \
     case 26: return FN<MODE, 26>(__VA_ARGS__); case 28: return FN<MODE, 28>(__VA_ARGS__);    \
     case 30: return FN<MODE, 30>(__VA_ARGS__); case 32: return FN<MODE, 32>(__VA_ARGS__);    \
+    case 40: return FN<MODE, 40>(__VA_ARGS__); case 48: return FN<MODE, 48>(__VA_ARGS__);    \
+    case 56: return FN<MODE, 56>(__VA_ARGS__); case 64: return FN<MODE, 64>(__VA_ARGS__);    \
+    case 72: return FN<MODE, 72>(__VA_ARGS__); case 80: return FN<MODE, 80>(__VA_ARGS__);    \
+    case 88: return FN<MODE, 88>(__VA_ARGS__); case 96: return FN<MODE, 96>(__VA_ARGS__);    \
     default: break;                                                                          \
   }
 
@@ -313,7 +321,8 @@ int walk_bin16_words<LN_BIN_MODE>(int c) {
   int W = (cp + 1) / 2;
   if (W < 1) W = 1;
   if (W > 24) W = (W + 1) & ~1;
-  return W <= 32 ? W : 0;
+  if (W > 32) W = (W + 7) & ~7;            // wide matrices (m up to 4n, SURVEY config 5a): W in 40..96
+  return W <= 96 ? W : 0;
 }
 
 template <>
@@ -339,6 +348,14 @@ int walk_bin16_unroll_mode<LN_BIN_MODE>(int c) {
   const int W = walk_bin16_words<LN_BIN_MODE>(c);
   LN_W16_SWITCH(LN_BIN_MODE, W, unroll_one16)
   return 4;
+}
+
+template <>
+int64_t walk_bin16_table_words_mode<LN_BIN_MODE>(int c, int k, int s) {
+  const int W = walk_bin16_words<LN_BIN_MODE>(c);
+  if (W == 0) return INT64_MAX;
+  const int Wt = (LN_BIN_MODE == MODE_LD ? 2 * W : W);
+  return (int64_t)2 * s * pad4(Wt + 1) + (int64_t)(k + 1) * pad4(W + 1) + pad4(Wt + 1);
 }
 
 template <>

@@ -40,10 +40,10 @@ __host__ __device__ constexpr int cctz(int j) { return (j & 1) ? 0 : (j & 2) ? 1
 #define LN_PAIR_PMAX 2
 #endif
 #ifndef LN_PAIR_MINB
-#define LN_PAIR_MINB 1
+#define LN_PAIR_MINB 12
 #endif
 #ifndef LN_PAIR_CHUNKED
-#define LN_PAIR_CHUNKED 0
+#define LN_PAIR_CHUNKED 1
 #endif
 #ifndef LN_PAIR_VOLATILE
 #define LN_PAIR_VOLATILE 0
@@ -159,7 +159,7 @@ template <int MODE, int C, int P>
 __host__ __device__ constexpr int pair_unroll() { return unroll_digits(P * (2 * PairLayout<MODE, C>::G * C + 4) + PairLayout<MODE, C>::RW / 4); }
 
 template <int MODE, int C, int P>
-__global__ void __launch_bounds__(kBlock, LN_PAIR_MINB) walk_pair16_kernel(const WalkParams p, const uint32_t* __restrict__ gTab,
+__global__ void __launch_bounds__(kBlock, (PairLayout<MODE, C>::G * C * P <= 96 ? LN_PAIR_MINB : 1)) walk_pair16_kernel(const WalkParams p, const uint32_t* __restrict__ gTab,
                                                              const int32_t* __restrict__ gInit) {
   using LY = PairLayout<MODE, C>;
   constexpr int G = LY::G, RW = LY::RW, IW = InitLayout<MODE, C>::IW;

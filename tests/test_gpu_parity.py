@@ -121,6 +121,7 @@ HOT_SHAPES = [
     (1, True, 11, 13), (1, True, 12, 41), (2, False, 11, 9), (2, False, 13, 30),
     (3, False, 9, 7), (3, False, 10, 32), (3, False, 8, 13), (4, False, 7, 5), (4, False, 8, 29),
     (5, False, 6, 4), (1, False, 9, 70), (2, False, 8, 100),
+    (1, True, 10, 97), (1, False, 11, 190), (1, False, 12, 128),      # wide rows (config 5a m = 4n)
 ]
 
 

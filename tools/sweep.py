@@ -1,0 +1,92 @@
+"""Scaling sweep (BASELINE.json config 5): L_1 for n = 32..48 (m = n and m = 4n) and L_3 for
+n = 16..26, reporting Gray steps/s and column updates/s against the integer roofline.
+
+Configurations whose full search fits the time budget run through lnorm_compute; larger ones
+are timed on a fixed seeded sample of prefixes through the same kernels (lnorm_prefix_maxima:
+2^s-strategy units exactly like the full search's), labelled "sampled".
+
+python tools/sweep.py [--budget-s 20] [--out profiles/r01/sweep.jsonl]
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import paper_2503_21596_b200 as L
+from paper_2503_21596_b200 import synth
+
+
+def roofline(col_updates_per_s, packed, nsm=148, mhz=1965.0):
+    peak_updates = 128.0 * nsm * mhz * 1e6 / (1 if packed else 2)   # 1 (packed) or 2 (int32) lane-instr per update
+    return col_updates_per_s / peak_updates
+
+
+def run(n, m, d, seed, budget_s):
+    import torch
+    M = synth.random_matrix(n, m, seed)
+    plan = L.plan(M, d=d)
+    r = plan["rows"]
+    updates_per_step = plan["cols"] * (2 if d >= 3 else 1)
+    est_rate = 5e11 if d == 1 else 4e11                      # strategies/s, rough, to size the run
+    full = plan["steps"] / est_rate <= budget_s
+    if full:
+        t0 = time.perf_counter()
+        v, _ = L.compute(M, d=d)
+        wall = time.perf_counter() - t0
+        st = L.last_stats()
+        steps, secs = st["steps"], st["walk_ms"] / 1e3
+        kind, variant = "full", st["variant"]
+    else:
+        base = 2 if d == 1 else d
+        # a seeded sample of prefixes of length nfixed, each walking base^(n - nfixed) strategies
+        nfixed = max(2, n - 24 if d == 1 else n - 14)
+        per = float(base) ** (n - nfixed)
+        count = int(max(2048, min(1 << 16, budget_s * est_rate / per)))
+        g = synth.SplitMix64(seed + 17)
+        P = np.zeros((count, nfixed), dtype=np.int8)
+        for i in range(count):
+            for x in range(1, nfixed):
+                P[i, x] = g.next() % base
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        L.prefix_maxima(M, P, d=d)
+        secs = time.perf_counter() - t0
+        steps = count * per
+        wall, v = secs, None
+        kind, variant = f"sampled ({count} prefixes of {nfixed} rows)", L.plan(M, d=d)["variant"]
+    rate = steps / secs
+    cu = rate * updates_per_step
+    packed = variant in (3, 4, 5, 6)
+    return {"config": f"L_{d} {n}x{m}", "n": n, "m": m, "d": d, "seed": seed, "kind": kind, "value": v,
+            "kernel_variant": L.VARIANTS.get(variant, variant), "strategies": plan["steps"],
+            "steps_per_s": rate, "column_updates_per_s": cu,
+            "roofline_frac": roofline(cu, packed),
+            "projected_full_search_s": plan["steps"] / rate, "measured_s": secs}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--budget-s", type=float, default=20.0)
+    ap.add_argument("--out", default=None)
+    a = ap.parse_args()
+    rows = []
+    for n in range(32, 49, 2):
+        for m in (n, 4 * n):
+            rows.append(run(n, m, 1, 100 + n, a.budget_s))
+            print(json.dumps(rows[-1]), flush=True)
+    for n in range(16, 27, 2):
+        rows.append(run(n, n, 3, 200 + n, a.budget_s))
+        print(json.dumps(rows[-1]), flush=True)
+    if a.out:
+        with open(a.out, "w") as f:
+            for r in rows:
+                f.write(json.dumps(r) + "\n")
+
+
+if __name__ == "__main__":
+    main()
