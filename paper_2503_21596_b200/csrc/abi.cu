@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <functional>
+#include <map>
+#include <memory>
 #include <nccl.h>
 
 #include <algorithm>
@@ -230,7 +232,25 @@ int make_plan(const Problem& pr, int world, Plan* pl, int64_t target_override = 
     int k = 0;
     while (k < f - smin && (k + 2) * prefix_bits(d) <= 64 && rgs_count(k + 2, d) <= kTableCap && rgs_count(k + 1, d) < target) ++k;
     p.k = k; p.s = f - k;
-    rgs_enumerate(k + 1, d, p.table, kTableCap + 1);
+    {
+      // the RGS prefix list depends only on (k, d): enumerate once per process
+      static std::mutex mu;
+      static std::map<std::pair<int, int>, std::shared_ptr<const std::vector<uint64_t>>> cache;
+      std::shared_ptr<const std::vector<uint64_t>> tab;
+      {
+        std::lock_guard<std::mutex> g(mu);
+        auto it = cache.find({k, d});
+        if (it != cache.end()) tab = it->second;
+      }
+      if (!tab) {
+        auto v = std::make_shared<std::vector<uint64_t>>();
+        rgs_enumerate(k + 1, d, *v, kTableCap + 1);
+        std::lock_guard<std::mutex> g(mu);
+        cache[{k, d}] = v;
+        tab = v;
+      }
+      p.table = *tab;
+    }
     p.units = (int64_t)p.table.size();
     p.kernel = kern;
     if (kern == K_LDPAIR16 && !walk_ldpair16_supported(d, pr.c, p.s)) p.kernel = pr.fits16 && walk_ld16_supported(d, pr.c, p.s) ? K_LD16 : K_LD;
@@ -881,13 +901,15 @@ int lnorm_prefix_maxima(const int32_t* M, int32_t n, int32_t m, int32_t d, int32
     pl.table[i] = w;
   }
   if (base == 2) {
-    pl.kernel = walk_bin_supported(pr.mode, pr.c, pl.s) ? K_BIN : K_GEN;
-    const bool hot = pl.kernel == K_BIN;
-    if (hot && pr.fits16 && walk_bin16_supported(pr.mode, pr.c, pl.s)) pl.kernel = K_BIN16;
-    if (hot && pr.fitsPair && walk_pair16_supported(pr.mode, pr.c, pl.s)) pl.kernel = K_PAIR16;
+    // same family preference as make_plan (paired > column-paired > int32 > generic)
     const int ov = kernel_override();
-    if (ov == K_GEN || (ov == K_BIN && hot)) pl.kernel = ov;
-    if (ov == K_BIN16 && hot && pr.fits16 && walk_bin16_supported(pr.mode, pr.c, pl.s)) pl.kernel = K_BIN16;
+    pl.kernel = K_GEN;
+    if (ov != K_GEN && walk_bin_supported(pr.mode, pr.c, pl.s)) pl.kernel = K_BIN;
+    if (ov != K_GEN && ov != K_BIN && pr.fits16 && walk_bin16_supported(pr.mode, pr.c, pl.s) &&
+        walk_bin16_table_fits(pr.mode, pr.c, pl.k, pl.s))
+      pl.kernel = K_BIN16;
+    if (ov != K_GEN && ov != K_BIN && ov != K_BIN16 && pr.fitsPair && walk_pair16_supported(pr.mode, pr.c, pl.s))
+      pl.kernel = K_PAIR16;
   }
   else {
     pl.kernel = walk_ld_supported(base, pr.c, pl.s) ? K_LD : K_GEN;

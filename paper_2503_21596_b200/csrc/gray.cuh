@@ -54,6 +54,20 @@ LN_HD void dary_change_values(uint32_t d, uint64_t j, uint32_t* i, uint32_t* fro
   *to = dary_digit(d, ci, j);
 }
 
+// Block-start step of a d-ary walk whose lowest digit is unrolled: word w = t*d
+// (t >= 1, 32-bit).  The changed digit is 1 + (number of trailing zero base-d digits
+// of t) (Eq. 17) and, with tt = t / d^ip, the old/new values are S[(tt-1) mod 2d] and
+// S[tt mod 2d] (Eqs. 13-15: floor((w-1)/d^i) = tt - 1 because w = tt d^i).
+template <int D>
+LN_HD void dary_block_start(uint32_t t, uint32_t* i, uint32_t* from, uint32_t* to) {
+  uint32_t tt = t, ip = 0;
+  while (tt % D == 0) { tt /= D; ++ip; }
+  const uint32_t a = (tt - 1) % (2 * D), b = tt % (2 * D);
+  *i = 1 + ip;
+  *from = a < D ? a : 2 * D - 1 - a;
+  *to = b < D ? b : 2 * D - 1 - b;
+}
+
 // Lexicographic key of a suffix word: digit i of the Gray word <-> row n-1-i,
 // so with the suffix's first row most significant the key is sum_i G_i d^i.
 // For d = 2 this is the Gray word itself: j ^ (j >> 1).

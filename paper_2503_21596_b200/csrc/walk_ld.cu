@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(kBlock) walk_ld_kernel(const WalkParams p) {
     for (uint32_t t = 0; t < nblk; ++t) {
       if (t != 0) {
         uint32_t i, from, to;
-        dary_change_values((uint32_t)D, (uint64_t)t * D, &i, &from, &to);
+        dary_block_start<D>(t, &i, &from, &to);
         v = LdWalker<D, C>::move_dyn(m, n, v, (int)i, (int)from, (int)to);
         ub = max(ub, v);
       }

@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(kBlock) walk_ldpair16_kernel(const WalkParams 
     for (uint32_t t = 0; t < nblk; ++t) {
       if (t != 0) {
         uint32_t i, from, to;
-        dary_change_values((uint32_t)D, (uint64_t)t * D, &i, &from, &to);
+        dary_block_start<D>(t, &i, &from, &to);
         WK::move_dyn(U, sbase, (int)i * RD, (int)from, (int)to);
       }
       if ((t & 1u) == 0) {

@@ -210,3 +210,19 @@ def test_plan_errors():
     with pytest.raises(L.LNormError) as e:
         L.plan(np.eye(3, dtype=np.int32), d=2, with_marginals=True)
     assert e.value.name == "EINVAL"
+
+
+def test_dary_block_start_matches_eq17():
+    """The unrolled d-ary walks' block-start shortcut equals Eqs. (13)-(17) at word t*d."""
+    import ctypes
+    for d in (3, 4):
+        for t in range(1, 3 ** 7):
+            dig, frm, to = L.gray_change(d, t * d)
+            # same quantities from the closed form of Eqs. (13)-(15)
+            assert frm == L.gray_digit(d, dig, t * d - 1) and to == L.gray_digit(d, dig, t * d)
+            tt, ip = t, 0
+            while tt % d == 0:
+                tt //= d
+                ip += 1
+            S = list(range(d)) + list(range(d - 1, -1, -1))
+            assert (dig, frm, to) == (1 + ip, S[(tt - 1) % (2 * d)], S[tt % (2 * d)])

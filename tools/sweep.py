@@ -43,15 +43,14 @@ def run(n, m, d, seed, budget_s):
         kind, variant = "full", st["variant"]
     else:
         base = 2 if d == 1 else d
-        # a seeded sample of prefixes of length nfixed, each walking base^(n - nfixed) strategies
-        nfixed = max(2, n - 24 if d == 1 else n - 14)
+        # a seeded sample of 2^19 prefixes (enough to fill every resident warp several
+        # times), each walking a full suffix of 18 binary / 11 ternary digits
+        nfixed = n - 18 if d == 1 else n - 11
         per = float(base) ** (n - nfixed)
-        count = int(max(2048, min(1 << 16, budget_s * est_rate / per)))
-        g = synth.SplitMix64(seed + 17)
+        count = 1 << 19
+        rng = np.random.default_rng(seed + 17)
         P = np.zeros((count, nfixed), dtype=np.int8)
-        for i in range(count):
-            for x in range(1, nfixed):
-                P[i, x] = g.next() % base
+        P[:, 1:] = rng.integers(0, base, size=(count, nfixed - 1), dtype=np.int8)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         L.prefix_maxima(M, P, d=d)
