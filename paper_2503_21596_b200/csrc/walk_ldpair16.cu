@@ -25,12 +25,19 @@ namespace {
 
 constexpr int kBlock = 32;
 constexpr int kTabWords = 8448;
+#ifndef LN_LDP_CHUNKED
+#define LN_LDP_CHUNKED 1
+#endif
+#ifndef LN_LDP_MINB
+#define LN_LDP_MINB 12
+#endif
 
 __host__ __device__ constexpr int pad4(int x) { return (x + 3) & ~3; }
 
 template <int D, int C, int P>
 struct LdPair {
-  static constexpr int RD = pad4(2 * C);   // delta record: +row (C dup words), -row (C dup words)
+  static constexpr int C4 = pad4(C);
+  static constexpr int RD = 2 * C4;        // delta record: +row at [0, C), -row at [C4, C4 + C) (16B aligned)
   static __device__ __forceinline__ uint32_t half_sums(const uint32_t (&v)[C]) {
     uint32_t a0 = __vmaxs2(v[0], 0u), a1 = 0u;
 #pragma unroll
@@ -58,6 +65,38 @@ struct LdPair {
   // move the walked row of record `off` from group PG to group QG in every unit
   template <int PG, int QG>
   static __device__ __forceinline__ void move(Unit (&U)[P], uint32_t sbase, int off) {
+#if LN_LDP_CHUNKED
+    // consume the +row / -row records a quad at a time (one LDS.128 each), updating and
+    // re-accumulating both groups column by column: only two quads of the row stay live
+    uint32_t ap0[P], ap1[P], aq0[P], aq1[P];
+#pragma unroll
+    for (int v = 0; v < (C + 3) / 4; ++v) {
+      const uint4 pq = lds128(sbase + 4u * (uint32_t)(off + 4 * v));        // +row quad
+      const uint4 nq = lds128(sbase + 4u * (uint32_t)(off + C4 + 4 * v));   // -row quad
+      const uint32_t pp[4] = {pq.x, pq.y, pq.z, pq.w}, nn[4] = {nq.x, nq.y, nq.z, nq.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int y = 4 * v + e;
+        if (y < C) {
+#pragma unroll
+          for (int j = 0; j < P; ++j) {
+            U[j].R[PG][y] = __vadd2(U[j].R[PG][y], nn[e]);
+            U[j].R[QG][y] = __vadd2(U[j].R[QG][y], pp[e]);
+            if (y == 0) { ap0[j] = __vmaxs2(U[j].R[PG][0], 0u); aq0[j] = __vmaxs2(U[j].R[QG][0], 0u); }
+            else if (y == 1) { ap1[j] = __vmaxs2(U[j].R[PG][1], 0u); aq1[j] = __vmaxs2(U[j].R[QG][1], 0u); }
+            else if (y & 1) { ap1[j] = __viaddmax_s16x2(ap1[j], U[j].R[PG][y], ap1[j]); aq1[j] = __viaddmax_s16x2(aq1[j], U[j].R[QG][y], aq1[j]); }
+            else { ap0[j] = __viaddmax_s16x2(ap0[j], U[j].R[PG][y], ap0[j]); aq0[j] = __viaddmax_s16x2(aq0[j], U[j].R[QG][y], aq0[j]); }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
+      refresh(U[j], PG, C > 1 ? __vadd2(ap0[j], ap1[j]) : ap0[j]);
+      refresh(U[j], QG, C > 1 ? __vadd2(aq0[j], aq1[j]) : aq0[j]);
+      U[j].best = max(U[j].best, U[j].lsum + maxd(U[j].dd));
+    }
+#else
     uint32_t r[RD];
 #pragma unroll
     for (int v = 0; v < RD / 4; ++v) {
@@ -68,13 +107,14 @@ struct LdPair {
     for (int j = 0; j < P; ++j) {
 #pragma unroll
       for (int y = 0; y < C; ++y) {
-        U[j].R[PG][y] = __vadd2(U[j].R[PG][y], r[C + y]);   // -row
+        U[j].R[PG][y] = __vadd2(U[j].R[PG][y], r[C4 + y]);  // -row
         U[j].R[QG][y] = __vadd2(U[j].R[QG][y], r[y]);       // +row
       }
       refresh(U[j], PG, half_sums(U[j].R[PG]));
       refresh(U[j], QG, half_sums(U[j].R[QG]));
       U[j].best = max(U[j].best, U[j].lsum + maxd(U[j].dd));
     }
+#endif
   }
   static __device__ __forceinline__ void move_dyn(Unit (&U)[P], uint32_t sbase, int off, int p, int q) {
     switch (p * D + q) {
@@ -97,7 +137,7 @@ struct LdPair {
 // Init records (global int32, stride IW = C + 1): prefix rows 0..k, the base
 // (walked rows k+1..r-2 at label 0), the paired row r-1, then [sum T].
 template <int D, int C, int P>
-__global__ void __launch_bounds__(kBlock) walk_ldpair16_kernel(const WalkParams p, const uint32_t* __restrict__ gTab,
+__global__ void __launch_bounds__(kBlock, (D * C * P <= 96 ? LN_LDP_MINB : 1)) walk_ldpair16_kernel(const WalkParams p, const uint32_t* __restrict__ gTab,
                                                                const int32_t* __restrict__ gInit) {
   using WK = LdPair<D, C, P>;
   constexpr int RD = WK::RD, IW = C + 1;
@@ -185,7 +225,7 @@ __global__ void __launch_bounds__(kBlock) walk_ldpair16_kernel(const WalkParams 
 
 __global__ void build_ldpair16_kernel(const int32_t* M, int r, int c, int C, int k, int s, uint32_t* tab,
                                       int32_t* init) {
-  const int RD = pad4(2 * C), IW = C + 1, sw = s - 1;
+  const int C4 = pad4(C), RD = 2 * C4, IW = C + 1, sw = s - 1;
   for (int i = threadIdx.x; i < sw * RD; i += blockDim.x) tab[i] = 0u;
   for (int i = threadIdx.x; i < (k + 3) * IW + 1; i += blockDim.x) init[i] = 0;
   __syncthreads();
@@ -194,7 +234,7 @@ __global__ void build_ldpair16_kernel(const int32_t* M, int r, int c, int C, int
     for (int y = 0; y < C; ++y) {
       const int32_t v = y < c ? row[y] : 0;
       tab[rec * RD + y] = (uint32_t)(v & 0xFFFF) * 0x10001u;
-      tab[rec * RD + C + y] = (uint32_t)((-v) & 0xFFFF) * 0x10001u;
+      tab[rec * RD + C4 + y] = (uint32_t)((-v) & 0xFFFF) * 0x10001u;
     }
   }
   for (int rec = threadIdx.x; rec < k + 3; rec += blockDim.x) {
@@ -219,7 +259,7 @@ __global__ void build_ldpair16_kernel(const int32_t* M, int r, int c, int C, int
 template <int D, int C>
 constexpr int ldpair_units_per_lane() { return D * C <= 40 ? 2 : 1; }
 
-size_t ldpair_smem(int C, int s) { return sizeof(uint32_t) * (size_t)((s - 1) * pad4(2 * C)); }
+size_t ldpair_smem(int C, int s) { return sizeof(uint32_t) * (size_t)((s - 1) * 2 * pad4(C)); }
 
 template <int D, int C>
 cudaError_t launch_one(const WalkParams& p, const uint32_t* tab, const int32_t* init, int grid, cudaStream_t st) {
@@ -265,7 +305,7 @@ bool walk_ldpair16_supported(int d, int c, int s) {
   if ((d != 3 && d != 4) || c < 1 || s < 2) return false;
   const int C = cols_of(c);
   if (C > 32) return false;
-  return (s - 1) * pad4(2 * C) <= kTabWords;
+  return (s - 1) * 2 * pad4(C) <= kTabWords;
 }
 
 int walk_ldpair16_units_per_lane(int d, int c) {
@@ -287,7 +327,7 @@ cudaError_t walk_ldpair16_launch(const WalkParams& p, int32_t* scratch_tab, int3
                                  cudaStream_t st, int* block_out) {
   *block_out = kBlock;
   const int C = cols_of(p.c);
-  if ((p.s - 1) * pad4(2 * C) > kTabWords || (p.k + 3) * (C + 1) + 1 > 16384) return cudaErrorInvalidValue;
+  if ((p.s - 1) * 2 * pad4(C) > kTabWords || (p.k + 3) * (C + 1) + 1 > 16384) return cudaErrorInvalidValue;
   uint32_t* tab = reinterpret_cast<uint32_t*>(scratch_tab);
   build_ldpair16_kernel<<<1, 128, 0, st>>>(p.M, p.r, p.c, C, p.k, p.s, tab, scratch_init);
   cudaError_t e = cudaGetLastError();

@@ -65,10 +65,10 @@ struct PairLayout {
   static constexpr int RW = pad4(G * C + 1);            // delta record: G*C duplicated words + q word
 };
 
-// Init data (global memory, int32), per record of IW = G*C + 2 ints:
-//   prefix rows x = 0..k : raw columns (C), then q contribution, unused
-//   base                 : suffix rows k+1..r-2 at digit 0 (C) [+ T (C) for L_2], q
-//   pair                 : row r-1 columns (C), q contribution of flipping it (A -> B)
+// Init data (global memory, packed s16x2 words), per record of IW = G*C + 2 words:
+//   prefix rows x = 0..k : row duplicated in both halves (+ its negation for L_2's m_1), q part
+//   base                 : suffix rows k+1..r-1 at digit 0 (strategy A) duplicated [+ T - base], q
+//   pair                 : the change A -> B (flip of row r-1) in the HIGH half only, and its q part
 template <int MODE, int C>
 struct InitLayout {
   static constexpr int IW = (MODE == MODE_LD ? 2 * C : C) + 2;
@@ -204,31 +204,29 @@ __global__ void __launch_bounds__(kBlock, (PairLayout<MODE, C>::G * C * P <= 96 
     for (int j = 0; j < P; ++j) {
       const int64_t rel = lc * 32 * P + j * 32 + lane;
       const int64_t u = p.unit_begin + (rel < p.units_per ? rel : 0);
-      int32_t mA[C];
-      int32_t qA = __ldg(baseRec + G * C);
+      // packed init (no int32 temporaries): base, +-prefix rows, then the pair row's
+      // contribution to the high (strategy B) half only
+      const uint32_t* bR = reinterpret_cast<const uint32_t*>(baseRec);
+      const uint32_t* pR = reinterpret_cast<const uint32_t*>(pairRec);
 #pragma unroll
-      for (int y = 0; y < C; ++y) mA[y] = __ldg(baseRec + y);
+      for (int i = 0; i < G * C; ++i) R[j][i] = __ldg(bR + i);
+      q[j] = __ldg(bR + G * C);
       for (int x = 0; x <= p.k; ++x) {
         const int dig = prefix_digit(p, u, x);
-        const int32_t f = (MODE == MODE_LD) ? 1 - dig : 1 - 2 * dig;
-        const int32_t* rec = gI + x * IW;
+        const uint32_t* rec = reinterpret_cast<const uint32_t*>(gI + x * IW);
+        if (dig == 0) {
 #pragma unroll
-        for (int y = 0; y < C; ++y) mA[y] += f * __ldg(rec + y);
-        qA += f * __ldg(rec + C);
-      }
-      const int32_t qB = qA + __ldg(pairRec + C);
-      q[j] = (uint32_t)(qA & 0xFFFF) | ((uint32_t)(qB & 0xFFFF) << 16);
+          for (int i = 0; i < G * C; ++i) R[j][i] = __vadd2(R[j][i], __ldg(rec + i));
+          q[j] = __vadd2(q[j], __ldg(rec + G * C));
+        } else if (MODE != MODE_LD) {
 #pragma unroll
-      for (int y = 0; y < C; ++y) {
-        const int32_t pr = __ldg(pairRec + y);
-        const int32_t mB = (MODE == MODE_LD) ? mA[y] - pr : mA[y] - 2 * pr;
-        R[j][y] = (uint32_t)(mA[y] & 0xFFFF) | ((uint32_t)(mB & 0xFFFF) << 16);
-        if (MODE == MODE_LD) {
-          const int32_t T = __ldg(baseRec + C + y);
-          const int32_t m1A = T - mA[y], m1B = T - mB;
-          R[j][C + y] = (uint32_t)(m1A & 0xFFFF) | ((uint32_t)(m1B & 0xFFFF) << 16);
+          for (int i = 0; i < G * C; ++i) R[j][i] = __vsub2(R[j][i], __ldg(rec + i));
+          q[j] = __vsub2(q[j], __ldg(rec + G * C));
         }
       }
+#pragma unroll
+      for (int i = 0; i < G * C; ++i) R[j][i] = __vadd2(R[j][i], __ldg(pR + i));
+      q[j] = __vadd2(q[j], __ldg(pR + G * C));
       // value of the starting pair
       uint32_t a0 = __vmaxs2(R[j][0], 0u), a1 = 0u;
 #pragma unroll
@@ -306,16 +304,25 @@ __global__ void build_pair16_kernel(const int32_t* M, int r, int c, int C, int k
     if (MODE == MODE_MARG) qd += f * row[0];
     tab[rec * RW + RW - 1] = MODE == MODE_LD ? 0u : (uint32_t)(qd & 0xFFFF) * 0x10001u;
   }
-  // init records: prefix rows 0..k, base, pair
+  // init records (packed s16x2): prefix rows 0..k, base, pair
+  auto dup = [](int32_t v) { return (uint32_t)(v & 0xFFFF) * 0x10001u; };
+  auto hi = [](int32_t v) { return (uint32_t)(v & 0xFFFF) << 16; };
+  uint32_t* initw = reinterpret_cast<uint32_t*>(init);
   for (int rec = tid; rec < k + 3; rec += blockDim.x) {
-    int32_t* out = init + rec * IW;
-    if (rec <= k) {
+    uint32_t* out = initw + rec * IW;
+    if (rec <= k) {                                // +row (m_0 part), -row (m_1 = T - m_0 part), q
       const int32_t* row = M + (int64_t)rec * c;
       int32_t qd = 0;
-      for (int j = 0; j < C; ++j) { const int y = c0 + j; const int32_t v = y < c ? row[y] : 0; out[j] = v; qd -= v; }
+      for (int j = 0; j < C; ++j) {
+        const int y = c0 + j;
+        const int32_t v = y < c ? row[y] : 0;
+        out[j] = dup(v);
+        if (MODE == MODE_LD) out[C + j] = dup(-v);
+        qd -= v;
+      }
       if (MODE == MODE_MARG) qd += row[0];
-      out[C] = MODE == MODE_LD ? 0 : qd;
-    } else if (rec == k + 1) {                     // base: suffix rows k+1..r-2 at digit 0
+      out[G * C] = MODE == MODE_LD ? 0u : dup(qd);
+    } else if (rec == k + 1) {                     // base: suffix rows k+1..r-1 at digit 0 (strategy A)
       int32_t qd = 0, tsum = 0;
       for (int j = 0; j < C; ++j) {
         const int y = c0 + j;
@@ -324,17 +331,10 @@ __global__ void build_pair16_kernel(const int32_t* M, int r, int c, int C, int k
           for (int x = 0; x < r; ++x) {
             const int32_t v = M[(int64_t)x * c + y];
             tv += v;
-            if (x > k && x < r - 1) bv += v;
+            if (x > k) bv += v;
           }
-        if (MODE == MODE_LD) {
-          // L_2: the walked base includes row r-1 in group 0 (strategy A)
-          if (y < c) bv += M[(int64_t)(r - 1) * c + y];
-          out[j] = bv;
-          out[C + j] = tv;
-        } else {
-          if (y < c) bv += M[(int64_t)(r - 1) * c + y];   // strategy A has a_{r-1} = +1
-          out[j] = bv;
-        }
+        out[j] = dup(bv);
+        if (MODE == MODE_LD) out[C + j] = dup(tv - bv);
         qd -= bv;
         tsum += tv;
       }
@@ -343,15 +343,20 @@ __global__ void build_pair16_kernel(const int32_t* M, int r, int c, int C, int k
         for (int x = k + 1; x < r; ++x) b0 += M[(int64_t)x * c];
         qd += b0;
       }
-      out[G * C] = MODE == MODE_LD ? -tsum : qd;
-    } else {                                       // pair row r-1 and the q change A -> B
+      out[G * C] = dup(MODE == MODE_LD ? -tsum : qd);
+    } else {                                       // pair row r-1: strategy B = A with a_{r-1} flipped
       const int32_t* row = M + (int64_t)(r - 1) * c;
       int32_t s1 = 0;
-      for (int j = 0; j < C; ++j) { const int y = c0 + j; const int32_t v = y < c ? row[y] : 0; out[j] = v; s1 += v; }
-      // L_1: m_B = m_A - 2 M_{r-1} => q_B - q_A = +2 sum;  L_marg: also the column-0 term -2 M_{r-1,0}
-      int32_t dq = 2 * s1;
+      for (int j = 0; j < C; ++j) {
+        const int y = c0 + j;
+        const int32_t v = y < c ? row[y] : 0;
+        out[j] = hi(MODE == MODE_LD ? -v : -2 * v);          // m_B = m_A - 2 M_{r-1} (L_2: - M_{r-1})
+        if (MODE == MODE_LD) out[C + j] = hi(v);             // m_1 = T - m_0
+        s1 += v;
+      }
+      int32_t dq = 2 * s1;                                   // L_1: q = -sum m
       if (MODE == MODE_MARG) dq -= 2 * row[0];
-      out[C] = MODE == MODE_LD ? 0 : dq;
+      out[G * C] = MODE == MODE_LD ? 0u : hi(dq);
     }
   }
 }
