@@ -137,7 +137,7 @@ struct LdPair {
 // Init records (global int32, stride IW = C + 1): prefix rows 0..k, the base
 // (walked rows k+1..r-2 at label 0), the paired row r-1, then [sum T].
 template <int D, int C, int P>
-__global__ void __launch_bounds__(kBlock, (D * C * P <= 96 ? LN_LDP_MINB : 1)) walk_ldpair16_kernel(const WalkParams p, const uint32_t* __restrict__ gTab,
+__global__ void __launch_bounds__(kBlock, (D * C * P <= 84 ? LN_LDP_MINB : 1)) walk_ldpair16_kernel(const WalkParams p, const uint32_t* __restrict__ gTab,
                                                                const int32_t* __restrict__ gInit) {
   using WK = LdPair<D, C, P>;
   constexpr int RD = WK::RD, IW = C + 1;
