@@ -120,6 +120,21 @@ int lnorm_compute_rank_device(lnorm_comm* comm, const int32_t* M_device, int32_t
                               int32_t with_marginals, int64_t* value, int8_t* argmax);
 
 /*
+ * Checkpoint / resume for long searches: the unit list is walked in
+ * chunks of chunk_units (<= 0: one chunk) and after every chunk the state
+ * (units done, best 8-byte key) is written atomically to `path` with a
+ * fingerprint of the matrix and plan.  A later call with the same matrix and
+ * path resumes from the saved state.  max_chunks (<= 0: unlimited) bounds the
+ * chunks walked by this call.  *done = 1 when the search finished: value and
+ * argmax are then final (bit-identical to lnorm_compute); otherwise value holds
+ * the best value found so far (INT64_MIN if none) and argmax is untouched.
+ * units_done (may be NULL) receives the number of units walked so far.
+ */
+int lnorm_compute_checkpointed(const int32_t* M, int32_t n, int32_t m, int32_t d, int32_t with_marginals,
+                               const char* path, int64_t chunk_units, int32_t max_chunks, int64_t* value,
+                               int8_t* argmax, int32_t* done, int64_t* units_done);
+
+/*
  * Batched search (the inner oracle of see-saw / branch-and-bound
  * loops): `batch` matrices of the same shape, contiguous
  * (batch x n x m int32, host).  values: int64[batch]; argmax: int8[batch][n]

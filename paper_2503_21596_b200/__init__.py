@@ -32,6 +32,7 @@ SYMBOLS = [
     "lnorm_compute_rank_device",
     "lnorm_prefix_maxima", "lnorm_walk_trace", "lnorm_gray_digit", "lnorm_gray_change", "lnorm_partition",
     "lnorm_last_stats", "lnorm_plan", "lnorm_compute_sliced", "lnorm_compute_reduced", "lnorm_compute_batch",
+    "lnorm_compute_checkpointed",
 ]
 
 STATUS = {0: "OK", 1: "EINVAL", 2: "EOVERFLOW", 3: "ETOOLARGE", 4: "ENODEV", 5: "ECUDA", 6: "ENCCL", 7: "ENOMEM"}
@@ -106,6 +107,8 @@ def load():
             "lnorm_gray_change": ([i32, u64, i32p, i32p, i32p], ctypes.c_int),
             "lnorm_partition": ([u64, i64, i64, i64p, i64p], ctypes.c_int),
             "lnorm_last_stats": ([P(Stats)], ctypes.c_int),
+            "lnorm_compute_checkpointed": ([i32p, i32, i32, i32, i32, ctypes.c_char_p, i64, i32, i64p, i8p, i32p, i64p],
+                                           ctypes.c_int),
             "lnorm_compute_batch": ([i32p, i32, i32, i32, i32, i32, i64p, i8p], ctypes.c_int),
             "lnorm_compute_reduced": ([i32p, i32, i32, i32, i32, i64p, i8p, i32p], ctypes.c_int),
             "lnorm_compute_sliced": ([i32p, i32, i32, i32, i32, i32, i64p, i8p], ctypes.c_int),
@@ -170,6 +173,22 @@ def compute_device(M_dev, d: int = 1, with_marginals: bool = False, stream=None)
     _check(load().lnorm_compute_device(ctypes.c_void_p(M_dev.data_ptr()), n, m, d, int(with_marginals), st,
                                        ctypes.byref(v), _p(arg, ctypes.c_int8)), "lnorm_compute_device")
     return int(v.value), arg
+
+
+def compute_checkpointed(M, path: str, d: int = 1, with_marginals: bool = False, chunk_units: int = 0,
+                         max_chunks: int = 0):
+    """Resumable search: returns (done, value, argmax or None, units_done); state persisted in `path`."""
+    A = _mat(M)
+    n, m = A.shape
+    v = ctypes.c_int64()
+    arg = np.zeros(n, dtype=np.int8)
+    done = ctypes.c_int32()
+    udone = ctypes.c_int64()
+    _check(load().lnorm_compute_checkpointed(_p(A, ctypes.c_int32), n, m, d, int(with_marginals),
+                                             os.fsencode(path), chunk_units, max_chunks, ctypes.byref(v),
+                                             _p(arg, ctypes.c_int8), ctypes.byref(done), ctypes.byref(udone)),
+           "lnorm_compute_checkpointed")
+    return bool(done.value), int(v.value), (arg if done.value else None), int(udone.value)
 
 
 def compute_batch(Ms, d: int = 1, with_marginals: bool = False):

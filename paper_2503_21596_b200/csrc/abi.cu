@@ -4,7 +4,9 @@
 // and plans; every step of the search runs in the kernels.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <cstdio>
 #include <functional>
+#include <string>
 #include <map>
 #include <memory>
 #include <nccl.h>
@@ -437,11 +439,52 @@ int launch_walk(DevCtx& cx, const Problem& pr, const Plan& pl, WalkParams& wp, i
 
 // Full search on one device.  dIn: device copy of the caller's n x m matrix.
 // world > 1: this rank walks its Algorithm-1 slice and `comm` all-reduces the key.
+// Checkpointed single-device search: the unit list is walked in chunks of
+// `chunk_units`; after every chunk (units done, best key) is written atomically
+// to `path` (tmp + rename) together with a fingerprint of the problem and plan,
+// so an interrupted run resumes exactly where it stopped.
+struct Checkpoint {
+  const char* path = nullptr;
+  int64_t chunk_units = 0;
+  int32_t max_chunks = 0;        // chunks to walk in this call (<= 0: all)
+  int32_t* done = nullptr;       // out: 1 when the search finished (value/argmax valid)
+  int64_t* units_done = nullptr; // out
+};
+
+uint64_t fnv1a(uint64_t h, const void* p, size_t n) {
+  const unsigned char* b = static_cast<const unsigned char*>(p);
+  for (size_t i = 0; i < n; ++i) { h ^= b[i]; h *= 1099511628211ull; }
+  return h;
+}
+
+struct CkState { uint64_t magic, fingerprint; int64_t next_unit; unsigned long long key; };
+
+bool ck_load(const char* path, uint64_t fp, CkState* st) {
+  FILE* f = fopen(path, "rb");
+  if (!f) return false;
+  CkState t{};
+  const bool ok = fread(&t, sizeof(t), 1, f) == 1;
+  fclose(f);
+  if (!ok || t.magic != 0x4c4e4f524d434b31ull || t.fingerprint != fp) return false;
+  *st = t;
+  return true;
+}
+
+bool ck_save(const char* path, const CkState& st) {
+  std::string tmp = std::string(path) + ".tmp";
+  FILE* f = fopen(tmp.c_str(), "wb");
+  if (!f) return false;
+  const bool ok = fwrite(&st, sizeof(st), 1, f) == 1;
+  fclose(f);
+  return ok && rename(tmp.c_str(), path) == 0;
+}
+
 // vslices > 1 (test hook, world == 1): walk the Algorithm-1 slices of `vslices`
 // virtual ranks one after the other on this device; the shared key then holds
 // exactly what the multi-rank all-reduce(max) would.
 int run_device(DevCtx& cx, const int32_t* dIn, const Problem& pr, int rank, int world, ncclComm_t comm,
-               RunOut* out, lnorm_stats* st, int vslices = 1) {
+               RunOut* out, lnorm_stats* st, int vslices = 1, const Checkpoint* ck = nullptr,
+               const int32_t* hostM = nullptr) {
   Plan pl;
   int rc = make_plan(pr, std::max(world, vslices), &pl);
   if (rc) return rc;
@@ -467,7 +510,46 @@ int run_device(DevCtx& cx, const int32_t* dIn, const Problem& pr, int rank, int 
   wp.pbits = prefix_bits(pr.dl);
   wp.counter = cx.dCtl; wp.key = cx.dCtl + 1; wp.unit_max = nullptr;
   CU(cudaEventRecord(cx.ev[1], s));
-  const int nslices = world > 1 ? 1 : std::max(1, vslices);
+  if (ck && ck->path && world == 1 && vslices <= 1) {
+    // ---- checkpointed walk: chunks of the unit list, state persisted after each
+    uint64_t fp = 1469598103934665603ull;
+    const int32_t hdr[8] = {pr.n, pr.m, pr.d, pr.marg, pl.k, pl.s, pl.kernel, (int32_t)pr.transposed};
+    fp = fnv1a(fp, hdr, sizeof(hdr));
+    if (hostM) fp = fnv1a(fp, hostM, sizeof(int32_t) * (size_t)pr.n * pr.m);
+    CkState cs{0x4c4e4f524d434b31ull, fp, 0, 0ull};
+    ck_load(ck->path, fp, &cs);
+    if (cs.key) CU(cudaMemcpyAsync(cx.dCtl + 1, &cs.key, sizeof(cs.key), cudaMemcpyHostToDevice, s));
+    const int64_t chunk = ck->chunk_units > 0 ? ck->chunk_units : pl.units;
+    int32_t chunks = 0;
+    while (cs.next_unit < pl.units && (ck->max_chunks <= 0 || chunks < ck->max_chunks)) {
+      const int64_t c0 = cs.next_unit, c1 = std::min<int64_t>(pl.units, c0 + chunk);
+      wp.unit_begin = c0; wp.unit_count = c1 - c0;
+      walk_params_single(wp);
+      wp.prefix_table = pl.table.empty() ? nullptr : cx.dPre + c0;
+      if (pl.kernel == K_GEN) CU(cudaMemsetAsync(cx.dCtl, 0, sizeof(unsigned long long), s));
+      if ((rc = launch_walk(cx, pr, pl, wp, &grid, &block))) return rc;
+      launches += pl.kernel == K_GEN ? 1 : 2;
+      walked += c1 - c0;
+      CU(cudaMemcpyAsync(&cs.key, cx.dCtl + 1, sizeof(cs.key), cudaMemcpyDeviceToHost, s));
+      CU(cudaStreamSynchronize(s));
+      cs.next_unit = c1;
+      if (!ck_save(ck->path, cs)) return LNORM_EINVAL;
+      ++chunks;
+    }
+    if (ck->units_done) *ck->units_done = cs.next_unit;
+    if (cs.next_unit < pl.units) {               // partial: report the best so far, no recovery yet
+      if (ck->done) *ck->done = 0;
+      out->value = cs.key ? (int64_t)key_value(cs.key) : INT64_MIN;
+      out->argmax.assign(pr.n, 0);
+      lnorm_stats S{};
+      S.rows = pr.r; S.cols = pr.c; S.units = walked; S.units_total = pl.units; S.launches = launches;
+      S.variant = pl.kernel;
+      *st = S;
+      return LNORM_OK;
+    }
+    if (ck->done) *ck->done = 1;
+  }
+  const int nslices = (ck && ck->path) ? 0 : (world > 1 ? 1 : std::max(1, vslices));
   for (int sl = 0; sl < nslices; ++sl) {
     const int T = world > 1 ? world : nslices, t = world > 1 ? rank : sl;
     if (T > 1) {
@@ -765,6 +847,31 @@ int lnorm_compute_reduced(const int32_t* M, int32_t n, int32_t m, int32_t d, int
   g_stats = st;
   *value = ro.value;
   if (argmax) std::memcpy(argmax, out.data(), (size_t)n);
+  return LNORM_OK;
+}
+
+int lnorm_compute_checkpointed(const int32_t* M, int32_t n, int32_t m, int32_t d, int32_t with_marginals,
+                               const char* path, int64_t chunk_units, int32_t max_chunks, int64_t* value,
+                               int8_t* argmax, int32_t* done, int64_t* units_done) {
+  if (!M || !value || !path || !done) return LNORM_EINVAL;
+  int dev = 0, rc = current_device(&dev);
+  if (rc) return rc;
+  Problem pr;
+  if ((rc = validate(M, n, m, d, with_marginals, &pr))) return rc;
+  DevCtx* cx = nullptr;
+  if ((rc = ctx_get(dev, &cx))) return rc;
+  std::lock_guard<std::mutex> g(cx->mu);
+  CU(cudaSetDevice(dev));
+  if ((rc = grow(&cx->dIn, &cx->capIn, (size_t)n * m))) return rc;
+  CU(cudaMemcpyAsync(cx->dIn, M, sizeof(int32_t) * n * m, cudaMemcpyHostToDevice, cx->stream));
+  Checkpoint ck;
+  ck.path = path; ck.chunk_units = chunk_units; ck.max_chunks = max_chunks; ck.done = done; ck.units_done = units_done;
+  RunOut ro;
+  lnorm_stats st{};
+  if ((rc = run_device(*cx, cx->dIn, pr, 0, 1, nullptr, &ro, &st, 1, &ck, M))) return rc;
+  g_stats = st;
+  *value = ro.value;
+  if (argmax && *done) std::memcpy(argmax, ro.argmax.data(), (size_t)n);
   return LNORM_OK;
 }
 
