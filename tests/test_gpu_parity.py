@@ -195,10 +195,12 @@ def test_planted_40x40_marg(lib):
 
 @pytest.mark.parametrize("d,marg,n,m,nfixed", [
     (1, False, 42, 42, 25), (1, True, 40, 40, 24), (2, False, 24, 24, 10), (3, False, 24, 24, 14),
+    (1, False, 48, 48, 33), (1, False, 48, 192, 35), (1, True, 40, 160, 28), (3, False, 26, 26, 16),
+    (4, False, 18, 18, 10),
 ])
 def test_sampled_prefixes_full_size(lib, d, marg, n, m, nfixed):
-    """Full-size configs: per-prefix maxima of the hot kernels vs the oracle, on sampled prefixes."""
-    M = synth.random_matrix(n, m, {(1, False): 2, (1, True): 3}.get((d, marg), 4))
+    """Full-size configs (BASELINE 2-5): per-prefix maxima of the hot kernels vs the oracle, on sampled prefixes."""
+    M = synth.random_matrix(n, m, {(1, False, 42): 2, (1, True, 40): 3}.get((d, marg, n), 100 + n if d == 1 else 200 + n))
     g = synth.SplitMix64(777 + d)
     base = 2 if d == 1 else d
     P = np.zeros((6, nfixed), dtype=np.int8)
