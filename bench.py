@@ -260,10 +260,11 @@ def main():
         achieved_ops = 2.0 * col_updates / (walk_ms / 1e3) / 1e12     # Tops/s (add + |.|-accumulate)
         nsm = torch.cuda.get_device_properties(dev).multi_processor_count
         peak_mhz = load_peak_clock()
-        packed = st["variant"] in (3, 4, 5, 6)                          # s16x2 kernels: 2 ops per lane-instruction
-        lanes = 128.0 * (2 if packed else 1)
+        simd = 4 if st["variant"] == 7 else (2 if st["variant"] in (3, 4, 5, 6) else 1)   # u8x4 / s16x2 / int32 lanes per register
+        packed = simd > 1
+        lanes = 128.0 * simd
         peak = lanes * nsm * peak_mhz * 1e6 * world / 1e12             # integer lane-ops/clk/SM x SMs x f_max
-        dtype = "int16x2" if packed else "int32"
+        dtype = {4: "u8x4", 2: "int16x2", 1: "int32"}[simd]
         traffic = None
         tf = os.path.join(ROOT, "profiles", "r01", "walk_traffic.json")
         if os.path.exists(tf):
@@ -286,11 +287,11 @@ def main():
                     "d2h_bytes_per_step": 8 + n, "ms_per_step": TE / args.steps},
             "gpu_launches": int(launches),
             "roofline": {"bound": "alu", "achieved": achieved_ops, "peak": peak,
-                         "unit": "Tops/s (" + ("int16x2 SIMD lanes" if packed else "int32") + ")",
+                         "unit": "Tops/s (" + ({4: "u8x4 SIMD lanes", 2: "int16x2 SIMD lanes", 1: "int32"}[simd]) + ")",
                          "frac": achieved_ops / peak, "traffic": traffic,
                          "kernel": "walk (dominant)", "walk_ms_per_launch": walk_ms,
                          "peak_basis": (f"128 lane-instr/clk/SM (ALU + FMA-heavy integer pipes = issue limit; VIADD+VABSDIFF mix "
-                                        f"measured 127, profiles/r01/peaks_b4.jsonl) x {'2 s16 halves x ' if packed else ''}"
+                                        f"measured 127, profiles/r01/peaks_b4.jsonl) x {({4: '4 u8 bytes x ', 2: '2 s16 halves x ', 1: ''})[simd]}"
                                         f"{nsm} SMs x {peak_mhz:.0f} MHz; algorithmic work = 2 ops per column update"),
                          "kernel_variant": st["variant"],
                          "frac_at_measured_clock": (achieved_ops / (peak * (c["sm_mhz"] or peak_mhz) / peak_mhz)) if c["sm_mhz"] else None},

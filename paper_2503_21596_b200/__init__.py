@@ -71,7 +71,8 @@ class PlanInfo(ctypes.Structure):
         return {f: getattr(self, f) for f, _ in self._fields_}
 
 
-VARIANTS = {0: "bin_int32", 1: "ld_int32", 2: "generic", 3: "bin_packed16", 4: "ld_packed16", 5: "bin_pair16", 6: "ld_pair16"}
+VARIANTS = {0: "bin_int32", 1: "ld_int32", 2: "generic", 3: "bin_packed16", 4: "ld_packed16", 5: "bin_pair16", 6: "ld_pair16",
+            7: "bin_u8"}
 
 _lock = threading.Lock()
 _lib = None

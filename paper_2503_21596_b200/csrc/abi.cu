@@ -82,7 +82,32 @@ struct Problem {
   bool fits16 = false;  // packed 16-bit column-pair path is exact
   bool fitsPair = false;  // strategy-paired path is exact: sum |M| <= 16383
   bool fitsLdPair = false;  // last-row-paired d-ary path is exact: sum |M| <= 32767
+  // u8 guard: sufW[s] = max over columns y of sum_{x = r-s}^{r-1} |M_xy| (the last s rows)
+  int64_t sufW[kMaxRows + 1] = {};
 };
+
+// Byte-packed path guard (walk_u8_impl.cuh): a unit's window of column y spans
+// 2 W_y (L_1, L_marg: +-1 on every suffix row) or W_y (L_2), W_y = sum over the s
+// suffix rows of |M_xy|; it must fit an unsigned byte.
+void suffix_guard(const int32_t* M, int m, Problem* p) {
+  std::vector<int64_t> colw(p->c, 0);
+  p->sufW[0] = 0;
+  for (int s = 1; s <= p->r && s <= kMaxRows; ++s) {
+    const int x = p->r - s;
+    int64_t mx = 0;
+    for (int y = 0; y < p->c; ++y) {
+      int64_t v = p->transposed ? M[(int64_t)y * m + x] : M[(int64_t)x * m + y];
+      colw[y] += v < 0 ? -v : v;
+      mx = std::max(mx, colw[y]);
+    }
+    p->sufW[s] = mx;
+  }
+}
+
+bool u8_fits(const Problem& p, int s) {
+  if (s < 1 || s > p.r) return false;
+  return p.mode == MODE_LD ? p.sufW[s] <= 255 : 2 * p.sufW[s] <= 255;
+}
 
 // Packed guard: for each parity class of the packed columns,
 // sum over its columns of sum_x |M_xy| <= 32767 bounds every 16-bit column sum and
@@ -125,6 +150,7 @@ int validate(const int32_t* M, int n, int m, int d, int marg, Problem* pr) {
   }
   if (p.r > kMaxRows - 1 || p.c > kMaxCols) return LNORM_ETOOLARGE;
   p.fits16 = packed_guard(M, m, p);
+  suffix_guard(M, m, &p);
   p.fitsPair = S <= 16383;
   p.fitsLdPair = S <= 32767;
   // search space d^(r-1) must fit a 63-bit word index
@@ -136,15 +162,18 @@ int validate(const int32_t* M, int n, int m, int d, int marg, Problem* pr) {
 }
 
 // ------------------------------------------------------------------ plan --
-enum Kernel { K_BIN = 0, K_LD = 1, K_GEN = 2, K_BIN16 = 3, K_LD16 = 4, K_PAIR16 = 5, K_LDPAIR16 = 6 };
+enum Kernel { K_BIN = 0, K_LD = 1, K_GEN = 2, K_BIN16 = 3, K_LD16 = 4, K_PAIR16 = 5, K_LDPAIR16 = 6, K_U8 = 7 };
 
-// LNORM_KERNEL=auto|int32|packed|generic forces a kernel family (benchmarks and tests).
+// LNORM_KERNEL=auto|u8|pair16|packed|int32|generic forces a kernel family (benchmarks
+// and tests): the named family or, where it cannot run, the next one down the
+// preference order u8 > pair16 > packed > int32 > generic.
 int kernel_override() {
   const char* e = getenv("LNORM_KERNEL");
-  if (!e || !*e || !strcmp(e, "auto")) return -1;
+  if (!e || !*e || !strcmp(e, "auto") || !strcmp(e, "u8")) return -1;
   if (!strcmp(e, "int32")) return K_BIN;
   if (!strcmp(e, "generic")) return K_GEN;
   if (!strcmp(e, "packed")) return K_BIN16;
+  if (!strcmp(e, "pair16")) return K_PAIR16;
   return -1;
 }
 
@@ -192,7 +221,7 @@ int64_t rgs_count(int len, int d) {
   return t > 9e18L ? INT64_MAX : (int64_t)t;
 }
 
-int make_plan(const Problem& pr, int world, Plan* pl, int64_t target_override = 0) {
+int make_plan(const Problem& pr, int world, Plan* pl, int64_t target_override = 0, bool allow_u8 = true) {
   const int f = pr.r - 1;
   const int64_t target = target_override > 0 ? target_override : kNominalLanes * 64 * std::max(1, world);
   Plan p;
@@ -208,6 +237,22 @@ int make_plan(const Problem& pr, int world, Plan* pl, int64_t target_override = 
       return -1;
     };
     int kern = K_GEN, smin = 0;
+    // byte-packed walk first: its guard bounds the suffix length from above, so the
+    // split takes at least f - su prefix digits (units must stay below 2^32)
+    if (ov < 0 && allow_u8) {
+      int su = 0;
+      for (int s_ = 1; s_ <= f && s_ <= 31; ++s_) if (u8_fits(pr, s_) && walk_u8_supported(pr.mode, pr.c, s_)) su = s_;
+      int s_lo = 0;
+      for (int s_ = 1; s_ <= su; ++s_) if (walk_u8_supported(pr.mode, pr.c, s_)) { s_lo = s_; break; }
+      if (su > 0 && s_lo > 0 && f - su <= 31) {
+        int k = std::max(0, f - su);
+        while (k < f - s_lo && k < 31 && (1LL << k) < target) ++k;
+        p.k = k; p.s = f - k; p.units = 1LL << k;
+        p.kernel = K_U8;
+        *pl = std::move(p);
+        return LNORM_OK;
+      }
+    }
     const int sp = (pr.fitsPair && ov != K_BIN16 && ov != K_BIN && ov != K_GEN) ? min_s(K_PAIR16) : -1;
     const int sb = (pr.fits16 && ov != K_BIN && ov != K_GEN) ? min_s(K_BIN16) : -1;
     const int si = (ov != K_GEN) ? min_s(K_BIN) : -1;
@@ -413,6 +458,7 @@ int launch_walk(DevCtx& cx, const Problem& pr, const Plan& pl, WalkParams& wp, i
   else if (pl.kernel == K_BIN16) occ = walk_bin16_occupancy(pr.mode, pr.c, pl.k, pl.s, &block);
   else if (pl.kernel == K_LD16) occ = walk_ld16_occupancy(pr.dl, pr.c, pl.k, pl.s, &block);
   else if (pl.kernel == K_PAIR16) occ = walk_pair16_occupancy(pr.mode, pr.c, pl.s, &block);
+  else if (pl.kernel == K_U8) occ = walk_u8_occupancy(pr.mode, pr.c, pl.s, &block);
   else if (pl.kernel == K_LDPAIR16) occ = walk_ldpair16_occupancy(pr.dl, pr.c, pl.s, &block);
   else if (pl.kernel == K_LD) occ = walk_ld_occupancy(pr.dl, pr.c, &block);
   else occ = walk_generic_occupancy(pr.dl, pr.c, &block);
@@ -421,6 +467,7 @@ int launch_walk(DevCtx& cx, const Problem& pr, const Plan& pl, WalkParams& wp, i
   if (pl.kernel == K_BIN16) per_block *= walk_bin16_units_per_lane(pr.mode, pr.c);
   if (pl.kernel == K_LD16) per_block *= walk_ld16_units_per_lane(pr.dl, pr.c);
   if (pl.kernel == K_PAIR16) per_block *= walk_pair16_units_per_lane(pr.mode, pr.c);
+  if (pl.kernel == K_U8) per_block *= walk_u8_units_per_lane(pr.mode, pr.c);
   if (pl.kernel == K_LDPAIR16) per_block *= walk_ldpair16_units_per_lane(pr.dl, pr.c);
   int64_t want = (wp.unit_count + per_block - 1) / per_block;
   int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)occ * cx.nsm, want));
@@ -429,6 +476,7 @@ int launch_walk(DevCtx& cx, const Problem& pr, const Plan& pl, WalkParams& wp, i
   else if (pl.kernel == K_BIN16) e = walk_bin16_launch(wp, cx.dTab, grid, cx.stream, &block);
   else if (pl.kernel == K_LD16) e = walk_ld16_launch(wp, cx.dTab, grid, cx.stream, &block);
   else if (pl.kernel == K_PAIR16) e = walk_pair16_launch(wp, cx.dTab, cx.dInit, grid, cx.stream, &block);
+  else if (pl.kernel == K_U8) e = walk_u8_launch(wp, cx.dTab, cx.dInit, grid, cx.stream, &block);
   else if (pl.kernel == K_LDPAIR16) e = walk_ldpair16_launch(wp, cx.dTab, cx.dInit, grid, cx.stream, &block);
   else if (pl.kernel == K_LD) e = walk_ld_launch(wp, cx.dTab, grid, cx.stream, &block);
   else e = walk_generic_launch(wp, grid, cx.stream, &block);
@@ -893,7 +941,7 @@ int lnorm_compute_batch(const int32_t* M, int32_t batch, int32_t n, int32_t m, i
   Plan pl;
   const int64_t target = std::max<int64_t>(1, kNominalLanes * 8 / batch);
   if (all_pair && pr.dl == 2) {
-    if ((rc = make_plan(pr, 1, &pl, target))) return rc;
+    if ((rc = make_plan(pr, 1, &pl, target, /*allow_u8=*/false))) return rc;
   }
   if (!all_pair || pr.dl != 2 || pl.kernel != K_PAIR16) {
     // outside the batched kernel's reach (L_d, d >= 3, or a matrix beyond the packed
@@ -991,6 +1039,7 @@ int lnorm_prefix_maxima(const int32_t* M, int32_t n, int32_t m, int32_t d, int32
   pr.dl = d == 1 ? 2 : d;
   pr.fits16 = packed_guard(M, m, pr);
   if (pr.r > kMaxRows - 1 || pr.c > kMaxCols) return LNORM_ETOOLARGE;
+  suffix_guard(M, m, &pr);
   const int base = pr.dl;
   Plan pl;
   pl.k = nfixed - 1; pl.s = n - nfixed; pl.units = count;
@@ -1017,6 +1066,7 @@ int lnorm_prefix_maxima(const int32_t* M, int32_t n, int32_t m, int32_t d, int32
       pl.kernel = K_BIN16;
     if (ov != K_GEN && ov != K_BIN && ov != K_BIN16 && pr.fitsPair && walk_pair16_supported(pr.mode, pr.c, pl.s))
       pl.kernel = K_PAIR16;
+    if (ov < 0 && u8_fits(pr, pl.s) && walk_u8_supported(pr.mode, pr.c, pl.s)) pl.kernel = K_U8;
   }
   else {
     pl.kernel = walk_ld_supported(base, pr.c, pl.s) ? K_LD : K_GEN;

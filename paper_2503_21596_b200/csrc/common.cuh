@@ -144,6 +144,19 @@ int walk_ldpair16_units_per_lane(int d, int c);
 int walk_ldpair16_occupancy(int d, int c, int s, int* block_out);
 cudaError_t walk_ldpair16_launch(const WalkParams& p, int32_t* scratch_tab, int32_t* scratch_init, int grid,
                                  cudaStream_t st, int* block_out);
+// Byte-packed binary walk (L_1, L_marg, L_2): four column sums per register as offset
+// bytes; exact when every column's suffix window fits a byte (guard checked by the caller).
+bool walk_u8_supported(int mode, int c, int s);
+int walk_u8_units_per_lane(int mode, int c);
+int walk_u8_occupancy(int mode, int c, int s, int* block_out);
+cudaError_t walk_u8_launch(const WalkParams& p, int32_t* scratch_tab, int32_t* scratch_init, int grid,
+                           cudaStream_t st, int* block_out);
+template <int MODE> int walk_u8_words_mode(int c);
+template <int MODE> cudaError_t walk_u8_launch_mode(const WalkParams& p, int32_t* scratch_tab, int32_t* scratch_init,
+                                                    int grid, cudaStream_t st);
+template <int MODE> int walk_u8_occupancy_mode(int c, int s);
+template <int MODE> int walk_u8_units_per_lane_mode(int c);
+template <int MODE> int walk_u8_unroll_mode(int c);
 // Generic warp-per-unit walk (any mode, d, c, s).
 bool walk_generic_supported(int d, int c);
 cudaError_t walk_generic_launch(const WalkParams& p, int grid, cudaStream_t st, int* block_out);

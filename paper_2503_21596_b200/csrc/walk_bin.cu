@@ -99,4 +99,35 @@ cudaError_t walk_pair16_launch(const WalkParams& p, int32_t* scratch_tab, int32_
   return walk_pair16_launch_mode<MODE_LD>(p, scratch_tab, scratch_init, grid, st);
 }
 
+bool walk_u8_supported(int mode, int c, int s) {
+  int NW = 0, K = 4;
+  if (mode == MODE_L1) { NW = walk_u8_words_mode<MODE_L1>(c); if (NW) K = walk_u8_unroll_mode<MODE_L1>(c); }
+  else if (mode == MODE_MARG) { NW = walk_u8_words_mode<MODE_MARG>(c); if (NW) K = walk_u8_unroll_mode<MODE_MARG>(c); }
+  else if (mode == MODE_LD) { NW = walk_u8_words_mode<MODE_LD>(c); if (NW) K = walk_u8_unroll_mode<MODE_LD>(c); }
+  if (NW == 0 || s < K || s > 31) return false;
+  const int RW = (NW + 3) & ~3;
+  return 2 * s * RW <= 16384;     // delta table staged in shared memory (dTab holds 32768 words)
+}
+
+int walk_u8_units_per_lane(int mode, int c) {
+  if (mode == MODE_L1) return walk_u8_units_per_lane_mode<MODE_L1>(c);
+  if (mode == MODE_MARG) return walk_u8_units_per_lane_mode<MODE_MARG>(c);
+  return walk_u8_units_per_lane_mode<MODE_LD>(c);
+}
+
+int walk_u8_occupancy(int mode, int c, int s, int* block_out) {
+  *block_out = 32;
+  if (mode == MODE_L1) return walk_u8_occupancy_mode<MODE_L1>(c, s);
+  if (mode == MODE_MARG) return walk_u8_occupancy_mode<MODE_MARG>(c, s);
+  return walk_u8_occupancy_mode<MODE_LD>(c, s);
+}
+
+cudaError_t walk_u8_launch(const WalkParams& p, int32_t* scratch_tab, int32_t* scratch_init, int grid,
+                           cudaStream_t st, int* block_out) {
+  *block_out = 32;
+  if (p.mode == MODE_L1) return walk_u8_launch_mode<MODE_L1>(p, scratch_tab, scratch_init, grid, st);
+  if (p.mode == MODE_MARG) return walk_u8_launch_mode<MODE_MARG>(p, scratch_tab, scratch_init, grid, st);
+  return walk_u8_launch_mode<MODE_LD>(p, scratch_tab, scratch_init, grid, st);
+}
+
 }  // namespace lnorm

@@ -1,0 +1,379 @@
+// Hot binary Gray walk with the column sums packed FOUR per register as offset
+// bytes: L_1, L_marg, L_2.
+//
+// Same units, warp-uniform Gray control and lexicographic reduction key as the
+// other binary walks (walk_pair16_impl.cuh): a unit fixes rows 0..k and walks its
+// s suffix rows (digit b <-> row r-1-b) in reflected Gray order (Eq. 9,
+// Table 1), each step adding ONE row of M to the column sums (Eq. 12: +-2 M_rho
+// for L_1 / L_marg; Eqs. 18-19 with d = 2: m_0 -/+= M_rho for L_2).
+//
+// Byte encoding.  Within one unit column y only moves inside a window fixed by
+// the unit's prefix part P_y (rows 0..k) and the suffix rows' W_y = sum_{suffix x}
+// |M_xy|:  L_1: m_y in [P_y - W_y, P_y + W_y];  L_2: m_0y in [P_y + N_y, P_y + N_y + W_y]
+// with N_y = sum_{suffix x} min(M_xy, 0).  With Lo_y the window's low end, the lane
+// keeps a_y = m_y - Lo_y in [0, 2 W_y] (L_1) or [0, W_y] (L_2): one unsigned byte as
+// long as the window is at most 255 wide (the exactness guard, checked on the host).
+// Four bytes share a 32-bit register and ONE 32-bit add of the packed step delta
+// sum_e 256^e delta_e updates all four exactly (no byte ever leaves [0, 255], so no
+// carry or borrow crosses a byte).  Every |.| is then one byte of
+//     |m_y| = |a_y - B_y| + kappa_y,   B_y = clamp(c_y, 0, 255),  kappa_y = |c_y - B_y|,
+// with c_y = -Lo_y (for |m_y|) or T_y - Lo_y (for |m_1y| = |T_y - m_0y|, L_2), because a_y
+// stays on one side of c_y whenever c_y is outside [0, 255].  VABSDIFF4.U8.ACC adds the
+// four |a - B| of a register to a 32-bit accumulator in one instruction, so a Gray
+// step costs one IADD (FMA-heavy pipe) + one VABSDIFF4 (ALU pipe) per FOUR columns
+// (L_2: + one more VABSDIFF4 for m_1), and the unit's value is acc + K, K = sum kappa.
+// L_marg's column 0 is linear (Eq. 2): it is kept as a byte too with B_0 = 0 and
+// kappa_0 = Lo_0, so that |a_0 - 0| + Lo_0 = m_0.  Per unit, B and K are computed once
+// (the paper's per-thread initial product) and the start bytes a_y are
+// the same for every unit (a uniform table).
+#include "common.cuh"
+
+#ifndef LN_BIN_MODE
+#error "define LN_BIN_MODE before including walk_u8_impl.cuh"
+#endif
+
+namespace lnorm {
+
+namespace {
+
+constexpr int kBlockU8 = 32;
+
+#ifndef LN_U8_BUDGET
+#define LN_U8_BUDGET 1800
+#endif
+#ifndef LN_U8_MINB
+#define LN_U8_MINB 12
+#endif
+
+__host__ __device__ constexpr int u8_cctz(int j) { return (j & 1) ? 0 : (j & 2) ? 1 : (j & 4) ? 2 : 3; }
+__host__ __device__ constexpr int u8_pad4(int x) { return (x + 3) & ~3; }
+
+// d = acc + sum over the 4 bytes of |a_b - b_b| (unsigned bytes): VABSDIFF4.U8.ACC
+__device__ __forceinline__ uint32_t sad4(uint32_t a, uint32_t b, uint32_t acc) {
+  uint32_t d;
+  asm("vabsdiff4.u32.u32.u32.add %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(acc));
+  return d;
+}
+
+template <int MODE, int NW>
+struct U8Layout {
+  static constexpr int G = (MODE == MODE_LD) ? 2 : 1;   // bias sets: |m_0| (and |m_1| for L_2)
+  static constexpr int RW = u8_pad4(NW);                // words per packed delta record
+  static constexpr int CW = 4 * NW;                     // int32 columns per init row
+};
+
+// units per lane: the row quad loaded once per step is shared by P units
+template <int MODE, int NW>
+__host__ __device__ constexpr int u8_units_per_lane() { return U8Layout<MODE, NW>::G * NW <= 16 ? 2 : 1; }
+
+template <int MODE, int NW, int P>
+__host__ __device__ constexpr int u8_step_instr() { return P * (U8Layout<MODE, NW>::G + 1) * NW + P + U8Layout<MODE, NW>::RW / 4; }
+
+template <int MODE, int NW, int P>
+__host__ __device__ constexpr int u8_unroll() {
+  return u8_step_instr<MODE, NW, P>() * 16 <= LN_U8_BUDGET ? 4
+       : u8_step_instr<MODE, NW, P>() * 8 <= LN_U8_BUDGET ? 3
+       : u8_step_instr<MODE, NW, P>() * 4 <= LN_U8_BUDGET ? 2 : 1;
+}
+
+template <int MODE, int NW, int P>
+struct U8Step {
+  static constexpr int G = U8Layout<MODE, NW>::G, RW = U8Layout<MODE, NW>::RW;
+  // One Gray step: add the packed delta record at sbase + off to every unit's bytes,
+  // re-accumulate sum |a - B| (two chains), best = max(acc0 + acc1, best).
+  static __device__ __forceinline__ void run(uint32_t (&A)[P][NW], const uint32_t (&B)[P][G * NW],
+                                             const uint32_t (&K)[P], int32_t (&best)[P], uint32_t sbase, int off) {
+    uint32_t a0[P], a1[P];
+#pragma unroll
+    for (int v = 0; v < RW / 4; ++v) {
+      const uint4 x4 = lds128(sbase + 4u * (uint32_t)(off + 4 * v));
+      const uint32_t rq[4] = {x4.x, x4.y, x4.z, x4.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int i = 4 * v + e;
+        if (i < NW) {
+#pragma unroll
+          for (int j = 0; j < P; ++j) {
+            A[j][i] += rq[e];
+            if (G == 2) {
+              a0[j] = sad4(A[j][i], B[j][i], i == 0 ? K[j] : a0[j]);
+              a1[j] = sad4(A[j][i], B[j][NW + i], i == 0 ? 0u : a1[j]);
+            } else if (i == 0) {
+              a0[j] = sad4(A[j][0], B[j][0], K[j]);
+            } else if (i == 1) {
+              a1[j] = sad4(A[j][1], B[j][1], 0u);
+            } else if (i & 1) {
+              a1[j] = sad4(A[j][i], B[j][i], a1[j]);
+            } else {
+              a0[j] = sad4(A[j][i], B[j][i], a0[j]);
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < P; ++j)
+      best[j] = (G == 1 && NW == 1) ? max(best[j], (int32_t)a0[j]) : __viaddmax_s32((int32_t)a0[j], (int32_t)a1[j], best[j]);
+  }
+};
+
+// Init records (global, int32), per matrix:
+//   [0, (k+1)*CW)          prefix rows 0..k, columns padded to CW with zeros
+//   [(k+1)*CW, +CW)        Lo_y - P_y: -W_y (L_1, L_marg) or N_y (L_2)
+//   [(k+2)*CW, +CW)        T_y = sum_x M_xy (L_2 only)
+//   [(k+3)*CW, +NW)        start bytes a_y (packed, identical for every unit)
+template <int MODE, int NW, int P>
+__global__ void __launch_bounds__(kBlockU8, (U8Layout<MODE, NW>::G * NW * P <= 24 ? LN_U8_MINB : 1))
+walk_u8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int32_t* __restrict__ gInit) {
+  using LY = U8Layout<MODE, NW>;
+  constexpr int G = LY::G, RW = LY::RW, CW = LY::CW;
+  constexpr int K = u8_unroll<MODE, NW, P>();
+  extern __shared__ __align__(16) uint32_t sT[];
+  const int lane = threadIdx.x & 31;
+  const int total = 2 * p.s * RW;
+  for (int i = lane; i < total; i += 32) sT[i] = gTab[i];
+  __syncwarp();
+  const uint32_t nblk = 1u << (p.s - K);
+  const int32_t* loRec = gInit + (p.k + 1) * CW;
+  const int32_t* tRec = loRec + CW;
+  const uint32_t* a0Rec = reinterpret_cast<const uint32_t*>(tRec + CW);
+  int32_t best_all = INT32_MIN;
+  uint32_t best_u = 0;
+  bool have = false;
+  const int64_t nchunks = (p.unit_count + 32 * P - 1) / (32 * P);
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sT);
+  for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    uint32_t A[P][NW];
+    uint32_t B[P][G * NW];
+    uint32_t Kc[P];
+    int32_t best[P];
+    // ---- unit init: prefix part P_y, window, biases B and constant K
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
+      const int64_t rel = ch * 32 * P + j * 32 + lane;
+      const int64_t u = p.unit_begin + (rel < p.unit_count ? rel : 0);
+      uint64_t neg = 0;                          // bit x: prefix digit of row x is 1
+      for (int x = 0; x <= p.k; ++x) neg |= (uint64_t)(prefix_digit(p, u, x) != 0) << x;
+      int32_t kap = 0;
+#pragma unroll
+      for (int q = 0; q < NW; ++q) {
+        int32_t Pv[4] = {0, 0, 0, 0};            // prefix part of columns 4q..4q+3
+        for (int x = 0; x <= p.k; ++x) {
+          // L_1 / L_marg: a_x = +1 (digit 0) or -1; L_2: only rows in group 0 count
+          const int dig = (int)((neg >> x) & 1ull);
+          const int32_t f = (MODE == MODE_LD) ? 1 - dig : 1 - 2 * dig;
+          const int4 v = __ldg(reinterpret_cast<const int4*>(gInit + x * CW) + q);
+          Pv[0] += f * v.x; Pv[1] += f * v.y; Pv[2] += f * v.z; Pv[3] += f * v.w;
+        }
+        uint32_t w0 = 0, w1 = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int y = 4 * q + e;
+          const int32_t lo = Pv[e] + __ldg(loRec + y);
+          const int32_t c0 = -lo;
+          int32_t b0;
+          if (MODE == MODE_MARG && y == 0) {     // linear column: m_0 = a_0 + Lo_0
+            b0 = 0;
+            kap += lo;
+          } else {
+            b0 = min(max(c0, 0), 255);
+            kap += abs(c0 - b0);
+          }
+          w0 |= (uint32_t)b0 << (8 * e);
+          if (G == 2) {
+            const int32_t c1 = __ldg(tRec + y) - lo;
+            const int32_t b1 = min(max(c1, 0), 255);
+            kap += abs(c1 - b1);
+            w1 |= (uint32_t)b1 << (8 * e);
+          }
+        }
+        B[j][q] = w0;
+        if (G == 2) B[j][NW + q] = w1;
+      }
+      Kc[j] = (uint32_t)kap;
+#pragma unroll
+      for (int q = 0; q < NW; ++q) A[j][q] = __ldg(a0Rec + q);
+      // value of the unit's start strategy
+      uint32_t acc = Kc[j];
+#pragma unroll
+      for (int q = 0; q < NW; ++q) {
+        acc = sad4(A[j][q], B[j][q], acc);
+        if (G == 2) acc = sad4(A[j][q], B[j][NW + q], acc);
+      }
+      best[j] = (int32_t)acc;
+    }
+    // ---- the walk: 2^s - 1 Gray steps (low K digits unrolled, Table 1's ruler pattern)
+    for (uint32_t t = 0; t < nblk; ++t) {
+      if (t != 0) {                                    // block start: digit K + ctz(t)
+        const int tz = __ffs((int)t) - 1;
+        const int b = K + tz;
+        const int sg = 1 ^ (int)((t >> (tz + 1)) & 1u);
+        U8Step<MODE, NW, P>::run(A, B, Kc, best, sbase, (2 * b + sg) * RW);
+      }
+#pragma unroll
+      for (int jj = 1; jj < (1 << K); ++jj) {
+        const int b = u8_cctz(jj);
+        const int sg = (b < K - 1) ? (1 ^ ((jj >> (b + 1)) & 1)) : (1 ^ (int)(t & 1u));
+        U8Step<MODE, NW, P>::run(A, B, Kc, best, sbase, (2 * b + sg) * RW);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
+      const int64_t rel = ch * 32 * P + j * 32 + lane;
+      if (rel < p.unit_count) {
+        if (p.unit_max) p.unit_max[rel] = best[j];
+        if (!have || best[j] > best_all) { best_all = best[j]; best_u = (uint32_t)(p.unit_begin + rel); have = true; }
+      }
+    }
+  }
+  unsigned long long key = have ? make_key(best_all, best_u) : 0ull;
+  key = warp_max_u64(key);
+  if (lane == 0 && key) atomicMax(p.key, key);
+}
+
+// Delta table (walked digit b <-> row r-1-b, sign sg = new digit value) and init records.
+template <int MODE>
+__global__ void build_u8_kernel(const int32_t* M, int r, int c, int NW, int k, int s, uint32_t* tab, int32_t* init) {
+  const int RW = u8_pad4(NW), CW = 4 * NW;
+  const int scale = (MODE == MODE_LD) ? 1 : 2;
+  const int tid = threadIdx.x;
+  for (int rec = tid; rec < 2 * s; rec += blockDim.x) {
+    const int b = rec >> 1, sg = rec & 1;
+    const int32_t* row = M + (int64_t)(r - 1 - b) * c;
+    const int f = sg ? -scale : scale;     // digit -> 1: a_x = -1 (m -= 2M) or group 1 (m_0 -= M)
+    for (int i = 0; i < RW; ++i) {
+      uint32_t w = 0;
+      for (int e = 0; e < 4; ++e) {
+        const int y = 4 * i + e;
+        const int32_t v = (i < NW && y < c) ? f * row[y] : 0;
+        w += (uint32_t)v << (8 * e);       // packed signed delta sum_e 256^e delta_e (mod 2^32)
+      }
+      tab[rec * RW + i] = w;
+    }
+  }
+  for (int i = tid; i < (k + 1) * CW; i += blockDim.x) {
+    const int x = i / CW, y = i % CW;
+    init[i] = y < c ? M[(int64_t)x * c + y] : 0;
+  }
+  for (int y = tid; y < CW; y += blockDim.x) {
+    int32_t W = 0, N = 0, T = 0;
+    if (y < c)
+      for (int x = 0; x < r; ++x) {
+        const int32_t v = M[(int64_t)x * c + y];
+        T += v;
+        if (x >= r - s) { W += abs(v); N += min(v, 0); }
+      }
+    init[(k + 1) * CW + y] = (MODE == MODE_LD) ? N : -W;
+    init[(k + 2) * CW + y] = (MODE == MODE_LD) ? T : 0;
+  }
+  __syncthreads();
+  uint32_t* a0 = reinterpret_cast<uint32_t*>(init + (k + 3) * CW);
+  for (int i = tid; i < NW; i += blockDim.x) {
+    uint32_t w = 0;
+    for (int e = 0; e < 4; ++e) {
+      const int y = 4 * i + e;
+      int32_t a = 0;
+      if (y < c) {
+        int32_t W = 0, Sm = 0, Sp = 0;
+        for (int x = r - s; x < r; ++x) {
+          const int32_t v = M[(int64_t)x * c + y];
+          W += abs(v); Sm += v; Sp += max(v, 0);
+        }
+        // start strategy: every suffix digit 0 (a_x = +1 / group 0)
+        a = (MODE == MODE_LD) ? Sp : Sm + W;
+      }
+      w |= (uint32_t)(a & 0xFF) << (8 * e);
+    }
+    a0[i] = w;
+  }
+}
+
+template <int MODE, int NW>
+size_t u8_smem(int s) { return sizeof(uint32_t) * (size_t)(2 * s * U8Layout<MODE, NW>::RW); }
+
+template <int MODE, int NW>
+cudaError_t launch_u8(const WalkParams& p, const uint32_t* tab, const int32_t* init, int grid, cudaStream_t st) {
+  constexpr int P = u8_units_per_lane<MODE, NW>();
+  const size_t sm = u8_smem<MODE, NW>(p.s);
+  cudaError_t e = cudaFuncSetAttribute(walk_u8_kernel<MODE, NW, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  walk_u8_kernel<MODE, NW, P><<<grid, kBlockU8, sm, st>>>(p, tab, init);
+  return cudaGetLastError();
+}
+
+template <int MODE, int NW>
+int occ_u8(int s) {
+  constexpr int P = u8_units_per_lane<MODE, NW>();
+  const size_t sm = u8_smem<MODE, NW>(s);
+  cudaFuncSetAttribute(walk_u8_kernel<MODE, NW, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  int nb = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, walk_u8_kernel<MODE, NW, P>, kBlockU8, sm);
+  return nb;
+}
+
+template <int MODE, int NW>
+int upl_u8() { return u8_units_per_lane<MODE, NW>(); }
+
+template <int MODE, int NW>
+int unroll_u8() { return u8_unroll<MODE, NW, u8_units_per_lane<MODE, NW>()>(); }
+
+#define LN_U8_SWITCH(MODE, NW_, FN, ...)                                                             \
+  switch (NW_) {                                                                                     \
+    case 1: return FN<MODE, 1>(__VA_ARGS__);   case 2: return FN<MODE, 2>(__VA_ARGS__);              \
+    case 3: return FN<MODE, 3>(__VA_ARGS__);   case 4: return FN<MODE, 4>(__VA_ARGS__);              \
+    case 5: return FN<MODE, 5>(__VA_ARGS__);   case 6: return FN<MODE, 6>(__VA_ARGS__);              \
+    case 7: return FN<MODE, 7>(__VA_ARGS__);   case 8: return FN<MODE, 8>(__VA_ARGS__);              \
+    case 9: return FN<MODE, 9>(__VA_ARGS__);   case 10: return FN<MODE, 10>(__VA_ARGS__);            \
+    case 11: return FN<MODE, 11>(__VA_ARGS__); case 12: return FN<MODE, 12>(__VA_ARGS__);            \
+    case 13: return FN<MODE, 13>(__VA_ARGS__); case 14: return FN<MODE, 14>(__VA_ARGS__);            \
+    case 15: return FN<MODE, 15>(__VA_ARGS__); case 16: return FN<MODE, 16>(__VA_ARGS__);            \
+    case 20: return FN<MODE, 20>(__VA_ARGS__); case 24: return FN<MODE, 24>(__VA_ARGS__);            \
+    case 28: return FN<MODE, 28>(__VA_ARGS__); case 32: return FN<MODE, 32>(__VA_ARGS__);            \
+    case 40: return FN<MODE, 40>(__VA_ARGS__); case 48: return FN<MODE, 48>(__VA_ARGS__);            \
+    default: break;                                                                                  \
+  }
+
+}  // namespace
+
+// packed words for c columns (0 = unsupported)
+template <>
+int walk_u8_words_mode<LN_BIN_MODE>(int c) {
+  int nw = (c + 3) / 4;
+  if (nw < 1) return 0;
+  if (nw > 16) nw = (nw + 3) & ~3;
+  if (nw > 32) nw = (nw + 7) & ~7;
+  return nw <= 48 ? nw : 0;
+}
+
+template <>
+cudaError_t walk_u8_launch_mode<LN_BIN_MODE>(const WalkParams& p, int32_t* scratch_tab, int32_t* scratch_init,
+                                             int grid, cudaStream_t st) {
+  const int NW = walk_u8_words_mode<LN_BIN_MODE>(p.c);
+  if (NW == 0) return cudaErrorInvalidValue;
+  uint32_t* tab = reinterpret_cast<uint32_t*>(scratch_tab);
+  build_u8_kernel<LN_BIN_MODE><<<1, 256, 0, st>>>(p.M, p.r, p.c, NW, p.k, p.s, tab, scratch_init);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  LN_U8_SWITCH(LN_BIN_MODE, NW, launch_u8, p, tab, scratch_init, grid, st)
+  return cudaErrorInvalidValue;
+}
+
+template <>
+int walk_u8_occupancy_mode<LN_BIN_MODE>(int c, int s) {
+  LN_U8_SWITCH(LN_BIN_MODE, walk_u8_words_mode<LN_BIN_MODE>(c), occ_u8, s)
+  return 0;
+}
+
+template <>
+int walk_u8_units_per_lane_mode<LN_BIN_MODE>(int c) {
+  LN_U8_SWITCH(LN_BIN_MODE, walk_u8_words_mode<LN_BIN_MODE>(c), upl_u8)
+  return 1;
+}
+
+template <>
+int walk_u8_unroll_mode<LN_BIN_MODE>(int c) {
+  LN_U8_SWITCH(LN_BIN_MODE, walk_u8_words_mode<LN_BIN_MODE>(c), unroll_u8)
+  return 4;
+}
+
+}  // namespace lnorm

@@ -244,10 +244,10 @@ def test_device_resident_and_rank_paths(lib):
 
 # ------------------------------------------------------ kernel families ----
 
-@pytest.mark.parametrize("family", ["int32", "packed", "generic", "auto"])
+@pytest.mark.parametrize("family", ["int32", "packed", "pair16", "generic", "u8", "auto"])
 @pytest.mark.parametrize("d,marg", MODES, ids=[mode_id(*m) for m in MODES])
 def test_every_kernel_family_matches_oracle(lib, family, d, marg, monkeypatch):
-    """The packed-16, int32 and generic kernels all reproduce the oracle bit for bit."""
+    """The byte-packed, paired-16, packed-16, int32 and generic kernels all reproduce the oracle bit for bit."""
     monkeypatch.setenv("LNORM_KERNEL", family)
     for seed, (n, m) in enumerate([(11, 21), (12, 8), (9, 33), (10, 16)]):
         M = synth.random_matrix(n, m, 40_000 + seed + 10 * d)
@@ -279,8 +279,9 @@ def _with_abs_sums(col_sums, n, seed):
 
 
 @pytest.mark.parametrize("S_pair", [16383, 16384])
-def test_pair_guard_boundary_exact(lib, S_pair):
+def test_pair_guard_boundary_exact(lib, S_pair, monkeypatch):
     """sum |M| at the strategy-paired path's guard (<= 16383) and one past it: both exact."""
+    monkeypatch.setenv("LNORM_KERNEL", "pair16")
     n, m = 10, 12
     cols = [S_pair // m + (1 if y < S_pair % m else 0) for y in range(m)]
     M = _with_abs_sums(cols, n, 60_000 + S_pair)
@@ -304,6 +305,37 @@ def test_packed_guard_boundary_exact(lib, par):
     check(lib, M)
     v, _ = check(lib, np.abs(M))
     assert v == int(np.abs(M.astype(np.int64)).sum())
+
+
+def _u8_boundary_matrix(W, d, seed, s=4, n=9, m=12):
+    """n x m matrix whose last s rows give column 0 the suffix |.|-sum W (column 3 too,
+    all positive), every other column less, and row n-s-1 non-zero in column 0 so that a
+    longer suffix breaks the byte guard."""
+    g = synth.SplitMix64(seed)
+    M = np.array(synth.random_matrix(n, m, seed, -6, 6), dtype=np.int64)
+    for y, sign in ((0, None), (3, 1)):
+        base, extra = divmod(W, s)
+        for i in range(s):
+            v = base + (1 if i < extra else 0)
+            M[n - s + i, y] = v if (sign == 1 or g.next() & 1) else -v
+    M[n - s - 1, 0] = 5
+    return M.astype(np.int32)
+
+
+@pytest.mark.parametrize("d,marg,W", [(1, False, 127), (1, False, 128), (1, True, 127), (1, True, 128),
+                                      (2, False, 255), (2, False, 256)])
+def test_u8_guard_boundary_exact(lib, d, marg, W):
+    """Byte-packed walk: a suffix window exactly at the byte guard (2W <= 255 for L_1/L_marg,
+    W <= 255 for L_2) runs the u8 kernel and is exact; one past it falls back, also exact."""
+    M = _u8_boundary_matrix(W, d, 62_000 + W + 10 * d + (5 if marg else 0))
+    P = lib.plan(M, d=d, with_marginals=marg)
+    fits = (W <= 127) if d == 1 else (W <= 255)
+    assert (P["variant_name"] == "bin_u8") == fits, P
+    if fits:
+        assert P["suffix_digits"] == 4
+    check(lib, M, d=d, marg=marg)
+    check(lib, np.abs(M), d=d, marg=marg)
+    check(lib, -np.abs(M), d=d, marg=marg)
 
 
 # ------------------------------------------------- multi-GPU decomposition --

@@ -46,15 +46,20 @@ enum {
   OP_IADD3,          // 3-input add a+b+c -> IADD3
   OP_VIADDMAX32,     // __viaddmax_s32     -> VIADDMNMX
   OP_MAD_VIADDMAX2,  // mad (packed biased update) + viaddmax s16x2
+  OP_SAD4,           // vabsdiff4.add (u8x4 sum of |a_b - b_b| + acc) -> VABSDIFF4.U8.ACC
+  OP_MAD_SAD4,       // 1:1 mad (packed u8x4 update) + vabsdiff4.add
+  OP_ADD_SAD4,       // 1:1 add (uniform operand) + vabsdiff4.add
+  OP_MAD_SAD4V,      // 1:1 mad + vabsdiff4.add with a DISTINCT bias register per chain (3 live sources)
   OP_N
 };
 static const char* kNames[OP_N] = {
   "add.s32(uniform operand)", "mad.lo.s32", "sad.s32", "add+sad", "mad+sad", "vadd2", "viaddmax_s16x2",
   "vadd2+viaddmax_s16x2", "vmaxu2", "mad+vmaxu2+mad", "hadd2", "hfma2_abs", "hadd2+hfma2_abs",
-  "add_constbank+sad", "lds128_bcast", "iadd3", "viaddmax_s32", "mad+viaddmax_s16x2"};
+  "add_constbank+sad", "lds128_bcast", "iadd3", "viaddmax_s32", "mad+viaddmax_s16x2", "vabsdiff4_acc",
+  "mad+vabsdiff4_acc", "add+vabsdiff4_acc", "mad+vabsdiff4_acc(per-chain bias)"};
 // SASS instructions per chain per unrolled iteration, read off `cuobjdump -sass`
 // (ptxas fuses two u16x2 maxes into one VIMNMX3; the constant-bank probe adds one LDCU.128 per 4 adds)
-static const double kInstr[OP_N] = {1,1,1,2,2,1,1,2,0.5,3,1,1,2,2.25,1,1,1,2};
+static const double kInstr[OP_N] = {1,1,1,2,2,1,1,2,0.5,3,1,1,2,2.25,1,1,1,2,1,2,2,2};
 
 template <int OP>
 __global__ void __launch_bounds__(256) probe(int32_t* out, Rec* rec, int trips, int32_t a_in, int32_t one_in, int32_t zero_in) {
@@ -68,6 +73,10 @@ __global__ void __launch_bounds__(256) probe(int32_t* out, Rec* rec, int trips, 
   const int32_t tz = (int32_t)(threadIdx.x >> 10);
   const int32_t a = a_in ^ tz, one = one_in ^ tz, zero = zero_in ^ tz;
   const unsigned au = ((unsigned)a_in * 0x00010001u) ^ (unsigned)tz;
+  const unsigned bias = 0x80808080u ^ (unsigned)tz;
+  unsigned bv[CH];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) bv[c] = (0x80808080u + 0x01010101u * c) ^ (unsigned)(threadIdx.x >> (10 + c));
   long long t0 = clock64();
   for (int t = 0; t < trips; ++t) {
 #pragma unroll
@@ -136,6 +145,17 @@ __global__ void __launch_bounds__(256) probe(int32_t* out, Rec* rec, int trips, 
         } else if constexpr (OP == OP_MAD_VIADDMAX2) {
           asm volatile("mad.lo.s32 %0, %1, %2, %0;" : "+r"(y[c]) : "r"(a), "r"(one));
           x[c] = __viaddmax_s16x2(x[c], y[c], x[c]); asm volatile("" : "+r"(x[c]));
+        } else if constexpr (OP == OP_SAD4) {
+          asm volatile("vabsdiff4.u32.u32.u32.add %0, %1, %2, %0;" : "+r"(x[c]) : "r"(y[c]), "r"(bias));
+        } else if constexpr (OP == OP_MAD_SAD4) {
+          asm volatile("mad.lo.s32 %0, %1, %2, %0;" : "+r"(y[c]) : "r"(a), "r"(one));
+          asm volatile("vabsdiff4.u32.u32.u32.add %0, %1, %2, %0;" : "+r"(x[c]) : "r"(y[c]), "r"(bias));
+        } else if constexpr (OP == OP_MAD_SAD4V) {
+          asm volatile("mad.lo.s32 %0, %1, %2, %0;" : "+r"(y[c]) : "r"(a), "r"(one));
+          asm volatile("vabsdiff4.u32.u32.u32.add %0, %1, %2, %0;" : "+r"(x[c]) : "r"(y[c]), "r"(bv[c]));
+        } else if constexpr (OP == OP_ADD_SAD4) {
+          asm volatile("add.s32 %0, %0, %1;" : "+r"(y[c]) : "r"(a));
+          asm volatile("vabsdiff4.u32.u32.u32.add %0, %1, %2, %0;" : "+r"(x[c]) : "r"(y[c]), "r"(bias));
         }
       }
     }
@@ -196,6 +216,6 @@ int main(int argc, char** argv) {
   std::vector<Rec> h;
   All<OP_ADD, OP_MAD, OP_SAD, OP_ADD_SAD, OP_MAD_SAD, OP_VADD2, OP_VIADDMAX2, OP_VADD2_VIADDMAX2, OP_VMAXU2,
       OP_MAD_VMAXU2_MAD, OP_HADD2, OP_HFMA2ABS, OP_HADD2_HFMA2ABS, OP_ADDC_SAD, OP_LDS128, OP_IADD3,
-      OP_VIADDMAX32, OP_MAD_VIADDMAX2>::go(nsm, bps, threads, trips, dout, drec, h);
+      OP_VIADDMAX32, OP_MAD_VIADDMAX2, OP_SAD4, OP_MAD_SAD4, OP_ADD_SAD4, OP_MAD_SAD4V>::go(nsm, bps, threads, trips, dout, drec, h);
   return 0;
 }

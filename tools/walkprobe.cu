@@ -7,6 +7,7 @@
 //   V_I32_CST   int32 sums, row from the constant bank at a uniform index
 //   V_S16_LDS   s16x2 packed sums: VIADD.16x2 update + VIADDMNMX.S16x2 max-accumulate
 //   V_B16_LDS   biased packed sums: 32-bit IADD update + LOP3 fix + VIADDMNMX.S16x2
+//   V_U8_LDS    u8x4 offset sums: 32-bit IADD update + VABSDIFF4.U8.ACC against a per-unit bias word
 //
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 tools/walkprobe.cu -o tools/walkprobe
 #include <cuda_runtime.h>
@@ -20,8 +21,8 @@
 #define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { \
   fprintf(stderr, "CUDA %s at %s:%d\n", cudaGetErrorString(e_), __FILE__, __LINE__); exit(1);} } while (0)
 
-enum { V_I32_LDS = 0, V_I32_CST, V_S16_LDS, V_B16_LDS, V_N };
-static const char* kNames[V_N] = {"i32_lds", "i32_const", "s16x2_lds", "biased16_lds"};
+enum { V_I32_LDS = 0, V_I32_CST, V_S16_LDS, V_B16_LDS, V_U8_LDS, V_N };
+static const char* kNames[V_N] = {"i32_lds", "i32_const", "s16x2_lds", "biased16_lds", "u8x4_lds"};
 
 constexpr int NROWS = 64;
 __constant__ int32_t cRows[NROWS * 64];
@@ -31,19 +32,21 @@ __device__ __forceinline__ unsigned smid() { unsigned r; asm volatile("mov.u32 %
 
 template <int V, int C, int P>
 __global__ void __launch_bounds__(128) walk(int32_t* out, Rec* rec, int steps, const int32_t* rows) {
-  constexpr int W = (V == V_S16_LDS || V == V_B16_LDS) ? C / 2 : C;   // 32-bit words per unit
+  constexpr int W = (V == V_U8_LDS) ? C / 4 : (V == V_S16_LDS || V == V_B16_LDS) ? C / 2 : C;   // 32-bit words per unit
   __shared__ __align__(16) int32_t srow[NROWS * W];
   __shared__ int32_t srsum[NROWS];
   for (int i = threadIdx.x; i < NROWS * W; i += blockDim.x) srow[i] = rows[i];
   for (int i = threadIdx.x; i < NROWS; i += blockDim.x) srsum[i] = rows[NROWS * W + i];
   __syncthreads();
   int32_t m[P][W];
+  uint32_t bb[P][W];
   int32_t best[P], S[P];
 #pragma unroll
   for (int p = 0; p < P; ++p) {
     best[p] = INT_MIN; S[p] = 0;
 #pragma unroll
-    for (int y = 0; y < W; ++y) m[p][y] = (int32_t)((threadIdx.x * 13 + y * 7 + p) & 15) - 8;
+    for (int y = 0; y < W; ++y) { m[p][y] = (int32_t)((threadIdx.x * 13 + y * 7 + p) & 15) - 8;
+                                  bb[p][y] = 0x40404040u * (uint32_t)((threadIdx.x * 5 + y + p) & 3); }
   }
   long long t0 = clock64();
   for (int s = 0; s < steps; ++s) {
@@ -79,6 +82,18 @@ __global__ void __launch_bounds__(128) walk(int32_t* out, Rec* rec, int steps, c
         uint32_t a = __vadd2(a0, a1);
         int32_t h = __dp2a_lo((int)a, 0x00010001, 0);   // lo16 + hi16 (signed)
         best[p] = max(best[p], 2 * h - S[p]);
+      } else if constexpr (V == V_U8_LDS) {
+        uint32_t a0 = (uint32_t)S[p], a1 = 0;
+#pragma unroll
+        for (int y = 0; y < W; y += 2) {
+          m[p][y] += r[y];
+          asm("vabsdiff4.u32.u32.u32.add %0, %1, %2, %0;" : "+r"(a0) : "r"(m[p][y]), "r"(bb[p][y]));
+          if (y + 1 < W) {
+            m[p][y+1] += r[y+1];
+            asm("vabsdiff4.u32.u32.u32.add %0, %1, %2, %0;" : "+r"(a1) : "r"(m[p][y+1]), "r"(bb[p][y+1]));
+          }
+        }
+        best[p] = __viaddmax_s32((int)a0, (int)a1, best[p]);
       } else {  // V_B16_LDS: low half biased by 0x8000 so a plain 32-bit add is carry-free
         uint32_t a0 = 0, a1 = 0;
 #pragma unroll
@@ -149,6 +164,10 @@ int main(int argc, char** argv) {
     run<V_S16_LDS, 64, 2>(nsm, bps, steps, dout, drec, drows);
     run<V_B16_LDS, 32, 2>(nsm, bps, steps, dout, drec, drows);
     run<V_B16_LDS, 48, 2>(nsm, bps, steps, dout, drec, drows);
+    run<V_U8_LDS, 48, 2>(nsm, bps, steps, dout, drec, drows);
+    run<V_U8_LDS, 32, 4>(nsm, bps, steps, dout, drec, drows);
+    run<V_U8_LDS, 48, 4>(nsm, bps, steps, dout, drec, drows);
+    run<V_U8_LDS, 64, 4>(nsm, bps, steps, dout, drec, drows);
   }
   return 0;
 }
