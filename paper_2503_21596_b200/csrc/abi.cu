@@ -104,6 +104,13 @@ void suffix_guard(const int32_t* M, int m, Problem* p) {
   }
 }
 
+// log2 of the u8 kernel's lane group: its units differ in the last lane_bits prefix
+// rows, which join the byte window (walk_u8_impl.cuh "Lane groups")
+int u8_lane_bits(const Problem& p) {
+  const int P = walk_u8_units_per_lane(p.mode, p.c);
+  return P >= 4 ? 2 : (P == 2 ? 1 : 0);
+}
+
 bool u8_fits(const Problem& p, int s) {
   if (s < 1 || s > p.r) return false;
   return p.mode == MODE_LD ? p.sufW[s] <= 255 : 2 * p.sufW[s] <= 255;
@@ -240,12 +247,14 @@ int make_plan(const Problem& pr, int world, Plan* pl, int64_t target_override = 
     // byte-packed walk first: its guard bounds the suffix length from above, so the
     // split takes at least f - su prefix digits (units must stay below 2^32)
     if (ov < 0 && allow_u8) {
+      const int lg = u8_lane_bits(pr);
       int su = 0;
-      for (int s_ = 1; s_ <= f && s_ <= 31; ++s_) if (u8_fits(pr, s_) && walk_u8_supported(pr.mode, pr.c, s_)) su = s_;
+      for (int s_ = 1; s_ <= f - lg && s_ <= 31; ++s_)
+        if (u8_fits(pr, s_ + lg) && walk_u8_supported(pr.mode, pr.c, s_)) su = s_;
       int s_lo = 0;
       for (int s_ = 1; s_ <= su; ++s_) if (walk_u8_supported(pr.mode, pr.c, s_)) { s_lo = s_; break; }
       if (su > 0 && s_lo > 0 && f - su <= 31) {
-        int k = std::max(0, f - su);
+        int k = std::max(lg, f - su);
         while (k < f - s_lo && k < 31 && (1LL << k) < target) ++k;
         p.k = k; p.s = f - k; p.units = 1LL << k;
         p.kernel = K_U8;
@@ -984,7 +993,7 @@ int lnorm_compute_batch(const int32_t* M, int32_t batch, int32_t n, int32_t m, i
   wp.M = dMo; wp.r = pr.r; wp.c = pr.c; wp.mode = pr.mode; wp.d = pr.dl; wp.k = pl.k; wp.s = pl.s;
   wp.pbits = prefix_bits(pr.dl); wp.prefix_table = nullptr; wp.counter = nullptr; wp.key = keys; wp.unit_max = nullptr;
   wp.unit_begin = 0; wp.unit_count = pl.units * batch;
-  wp.batch = batch; wp.units_per = pl.units; wp.m_stride = (int64_t)nm; wp.tab_stride = tabw; wp.init_stride = initw;
+  wp.batch = batch; wp.units_per = pl.units; wp.m_stride = (int64_t)nm; wp.tab_stride = tabw; wp.init_stride = initw; wp.one = 1;
   int block = 32;
   const int occ = std::max(1, walk_pair16_occupancy(pr.mode, pr.c, pl.s, &block));
   const int64_t P = walk_pair16_units_per_lane(pr.mode, pr.c);
@@ -1066,7 +1075,20 @@ int lnorm_prefix_maxima(const int32_t* M, int32_t n, int32_t m, int32_t d, int32
       pl.kernel = K_BIN16;
     if (ov != K_GEN && ov != K_BIN && ov != K_BIN16 && pr.fitsPair && walk_pair16_supported(pr.mode, pr.c, pl.s))
       pl.kernel = K_PAIR16;
-    if (ov < 0 && u8_fits(pr, pl.s) && walk_u8_supported(pr.mode, pr.c, pl.s)) pl.kernel = K_U8;
+    // the u8 kernel needs aligned lane groups: prefix i*P + j equals prefix i*P on rows
+    // 0..k-lg and carries the bits of j on the last lg prefix rows (row k = bit 0)
+    const int lg = u8_lane_bits(pr), P = 1 << lg;
+    bool grouped = ov < 0 && pl.k >= lg && count % P == 0 && u8_fits(pr, pl.s + lg) &&
+                   walk_u8_supported(pr.mode, pr.c, pl.s);
+    for (int64_t i = 0; grouped && i < count; ++i) {
+      const int64_t h = i - i % P;
+      for (int x = 0; x <= pl.k && grouped; ++x) {
+        const int v = prefixes[i * nfixed + x];
+        if (x <= pl.k - lg) grouped = v == prefixes[h * nfixed + x];
+        else grouped = v == (int)(((i % P) >> (pl.k - x)) & 1);
+      }
+    }
+    if (grouped) pl.kernel = K_U8;
   }
   else {
     pl.kernel = walk_ld_supported(base, pr.c, pl.s) ? K_LD : K_GEN;

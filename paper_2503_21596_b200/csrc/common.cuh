@@ -40,10 +40,12 @@ struct WalkParams {
   int32_t batch;
   int64_t units_per;
   int64_t m_stride, tab_stride, init_stride;
+  uint32_t one;                  // = 1 (a uniform operand the compiler cannot fold)
 };
 
 // Defaults for a single-matrix launch.
 inline void walk_params_single(WalkParams& p) {
+  p.one = 1;
   p.batch = 1;
   p.units_per = p.unit_count;
   p.m_stride = p.tab_stride = p.init_stride = 0;

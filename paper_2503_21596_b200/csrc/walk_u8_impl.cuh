@@ -62,9 +62,34 @@ struct U8Layout {
   static constexpr int CW = 4 * NW;                     // int32 columns per init row
 };
 
+#ifndef LN_U8_P
+#define LN_U8_P 4
+#endif
+#ifndef LN_U8_MAD
+#define LN_U8_MAD 0
+#endif
+#ifndef LN_U8_CHAINS
+#define LN_U8_CHAINS 2
+#endif
+
 // units per lane: the row quad loaded once per step is shared by P units
 template <int MODE, int NW>
-__host__ __device__ constexpr int u8_units_per_lane() { return U8Layout<MODE, NW>::G * NW <= 16 ? 2 : 1; }
+__host__ __device__ constexpr int u8_units_per_lane() {
+  return U8Layout<MODE, NW>::G * NW <= 16 ? LN_U8_P : (U8Layout<MODE, NW>::G * NW <= 32 ? 2 : 1);
+}
+
+// packed byte update A + D; LN_U8_MAD: as IMAD D * one + A with `one` a kernel
+// parameter (uniform register operand), pinning the add to the FMA-heavy pipe
+__device__ __forceinline__ uint32_t u8_add(uint32_t a, uint32_t d, uint32_t one) {
+#if LN_U8_MAD
+  uint32_t r;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(d), "r"(one), "r"(a));
+  return r;
+#else
+  (void)one;
+  return a + d;
+#endif
+}
 
 template <int MODE, int NW, int P>
 __host__ __device__ constexpr int u8_step_instr() { return P * (U8Layout<MODE, NW>::G + 1) * NW + P + U8Layout<MODE, NW>::RW / 4; }
@@ -81,8 +106,9 @@ struct U8Step {
   static constexpr int G = U8Layout<MODE, NW>::G, RW = U8Layout<MODE, NW>::RW;
   // One Gray step: add the packed delta record at sbase + off to every unit's bytes,
   // re-accumulate sum |a - B| (two chains), best = max(acc0 + acc1, best).
-  static __device__ __forceinline__ void run(uint32_t (&A)[P][NW], const uint32_t (&B)[P][G * NW],
-                                             const uint32_t (&K)[P], int32_t (&best)[P], uint32_t sbase, int off) {
+  static __device__ __forceinline__ void run(uint32_t (&A)[P][NW], const uint32_t (&B)[G * NW],
+                                             const uint32_t K, int32_t (&best)[P], uint32_t sbase, int off,
+                                             uint32_t one) {
     uint32_t a0[P], a1[P];
 #pragma unroll
     for (int v = 0; v < RW / 4; ++v) {
@@ -94,39 +120,57 @@ struct U8Step {
         if (i < NW) {
 #pragma unroll
           for (int j = 0; j < P; ++j) {
-            A[j][i] += rq[e];
+            A[j][i] = u8_add(A[j][i], rq[e], one);
             if (G == 2) {
-              a0[j] = sad4(A[j][i], B[j][i], i == 0 ? K[j] : a0[j]);
-              a1[j] = sad4(A[j][i], B[j][NW + i], i == 0 ? 0u : a1[j]);
+              a0[j] = sad4(A[j][i], B[i], i == 0 ? K : a0[j]);
+              a1[j] = sad4(A[j][i], B[NW + i], i == 0 ? 0u : a1[j]);
             } else if (i == 0) {
-              a0[j] = sad4(A[j][0], B[j][0], K[j]);
+              a0[j] = sad4(A[j][0], B[0], K);
+            } else if (LN_U8_CHAINS == 1) {
+              a0[j] = sad4(A[j][i], B[i], a0[j]);
             } else if (i == 1) {
-              a1[j] = sad4(A[j][1], B[j][1], 0u);
+              a1[j] = sad4(A[j][1], B[1], 0u);
             } else if (i & 1) {
-              a1[j] = sad4(A[j][i], B[j][i], a1[j]);
+              a1[j] = sad4(A[j][i], B[i], a1[j]);
             } else {
-              a0[j] = sad4(A[j][i], B[j][i], a0[j]);
+              a0[j] = sad4(A[j][i], B[i], a0[j]);
             }
           }
         }
       }
     }
+    if (G == 1 && (NW == 1 || LN_U8_CHAINS == 1)) {
 #pragma unroll
-    for (int j = 0; j < P; ++j)
-      best[j] = (G == 1 && NW == 1) ? max(best[j], (int32_t)a0[j]) : __viaddmax_s32((int32_t)a0[j], (int32_t)a1[j], best[j]);
+      for (int j = 0; j < P; ++j) best[j] = max(best[j], (int32_t)a0[j]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < P; ++j) best[j] = __viaddmax_s32((int32_t)a0[j], (int32_t)a1[j], best[j]);
+    }
   }
 };
 
+// Lane groups.  The P units of a lane are the P consecutive units of one aligned
+// group g (units gP .. gP+P-1), which differ only in the last L = log2 P prefix rows
+// k-L+1 .. k.  Those rows are counted in the byte window together with the suffix
+// (window rows = the last s + L rows), so the P units share ONE set of bias words B
+// and one K: consecutive VABSDIFF4 of the P units then read B from the operand
+// reuse cache (two register-file reads per VABSDIFF4 instead of three, the
+// register-bank limit measured in profiles/r01), and B costs NW registers per lane,
+// not P*NW.  Slices that do not start or end on a group boundary (Algorithm 1 ranks,
+// checkpoint chunks) mask the units outside [unit_begin, unit_begin + unit_count).
+//
 // Init records (global, int32), per matrix:
 //   [0, (k+1)*CW)          prefix rows 0..k, columns padded to CW with zeros
-//   [(k+1)*CW, +CW)        Lo_y - P_y: -W_y (L_1, L_marg) or N_y (L_2)
+//   [(k+1)*CW, +CW)        Lo_y - Ph_y over the window rows: -W_y (L_1, L_marg) or N_y (L_2)
 //   [(k+2)*CW, +CW)        T_y = sum_x M_xy (L_2 only)
-//   [(k+3)*CW, +NW)        start bytes a_y (packed, identical for every unit)
+//   [(k+3)*CW, +CW)        a_y - delta_y at the start word: sum_suffix M_xy + W_y (L_1, L_marg)
+//                          or sum_suffix M_xy - N_y (L_2); delta = the unit's low prefix rows
 template <int MODE, int NW, int P>
-__global__ void __launch_bounds__(kBlockU8, (U8Layout<MODE, NW>::G * NW * P <= 24 ? LN_U8_MINB : 1))
+__global__ void __launch_bounds__(kBlockU8, (U8Layout<MODE, NW>::G * NW * P <= 64 ? LN_U8_MINB : 1))
 walk_u8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int32_t* __restrict__ gInit) {
   using LY = U8Layout<MODE, NW>;
   constexpr int G = LY::G, RW = LY::RW, CW = LY::CW;
+  constexpr int LG = (P >= 4) ? 2 : (P == 2 ? 1 : 0);
   constexpr int K = u8_unroll<MODE, NW, P>();
   extern __shared__ __align__(16) uint32_t sT[];
   const int lane = threadIdx.x & 31;
@@ -136,29 +180,32 @@ walk_u8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int3
   const uint32_t nblk = 1u << (p.s - K);
   const int32_t* loRec = gInit + (p.k + 1) * CW;
   const int32_t* tRec = loRec + CW;
-  const uint32_t* a0Rec = reinterpret_cast<const uint32_t*>(tRec + CW);
+  const int32_t* abRec = tRec + CW;
+  const int kh = p.k - LG;                         // last row of the shared (high) prefix part
   int32_t best_all = INT32_MIN;
   uint32_t best_u = 0;
   bool have = false;
-  const int64_t nchunks = (p.unit_count + 32 * P - 1) / (32 * P);
+  const int64_t u_end = p.unit_begin + p.unit_count;
+  const int64_t g0 = p.unit_begin / P, g_end = (u_end + P - 1) / P;
+  const int64_t nchunks = (g_end - g0 + 31) / 32;
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sT);
   for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    const int64_t g = g0 + ch * 32 + lane;
+    const int64_t uh = min(max(g * P, p.unit_begin), u_end - 1);   // a valid unit of the group
     uint32_t A[P][NW];
-    uint32_t B[P][G * NW];
-    uint32_t Kc[P];
+    uint32_t B[G * NW];
+    uint32_t Kc;
     int32_t best[P];
-    // ---- unit init: prefix part P_y, window, biases B and constant K
-#pragma unroll
-    for (int j = 0; j < P; ++j) {
-      const int64_t rel = ch * 32 * P + j * 32 + lane;
-      const int64_t u = p.unit_begin + (rel < p.unit_count ? rel : 0);
-      uint64_t neg = 0;                          // bit x: prefix digit of row x is 1
-      for (int x = 0; x <= p.k; ++x) neg |= (uint64_t)(prefix_digit(p, u, x) != 0) << x;
+    // ---- lane init (PAPER.md:253's per-thread product): shared high part -> B, K;
+    //      per unit: its low prefix rows -> start bytes
+    {
+      uint64_t neg = 0;                            // bit x: digit of row x (0..kh) is 1
+      for (int x = 0; x <= kh; ++x) neg |= (uint64_t)(prefix_digit(p, uh, x) != 0) << x;
       int32_t kap = 0;
 #pragma unroll
       for (int q = 0; q < NW; ++q) {
-        int32_t Pv[4] = {0, 0, 0, 0};            // prefix part of columns 4q..4q+3
-        for (int x = 0; x <= p.k; ++x) {
+        int32_t Pv[4] = {0, 0, 0, 0};              // high prefix part of columns 4q..4q+3
+        for (int x = 0; x <= kh; ++x) {
           // L_1 / L_marg: a_x = +1 (digit 0) or -1; L_2: only rows in group 0 count
           const int dig = (int)((neg >> x) & 1ull);
           const int32_t f = (MODE == MODE_LD) ? 1 - dig : 1 - 2 * dig;
@@ -172,7 +219,7 @@ walk_u8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int3
           const int32_t lo = Pv[e] + __ldg(loRec + y);
           const int32_t c0 = -lo;
           int32_t b0;
-          if (MODE == MODE_MARG && y == 0) {     // linear column: m_0 = a_0 + Lo_0
+          if (MODE == MODE_MARG && y == 0) {       // linear column: m_0 = a_0 + Lo_0
             b0 = 0;
             kap += lo;
           } else {
@@ -187,18 +234,39 @@ walk_u8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int3
             w1 |= (uint32_t)b1 << (8 * e);
           }
         }
-        B[j][q] = w0;
-        if (G == 2) B[j][NW + q] = w1;
+        B[q] = w0;
+        if (G == 2) B[NW + q] = w1;
       }
-      Kc[j] = (uint32_t)kap;
+      Kc = (uint32_t)kap;
+    }
 #pragma unroll
-      for (int q = 0; q < NW; ++q) A[j][q] = __ldg(a0Rec + q);
-      // value of the unit's start strategy
-      uint32_t acc = Kc[j];
+    for (int j = 0; j < P; ++j) {
+      int64_t u = g * P + j;
+      if (u < p.unit_begin || u >= u_end) u = uh; // masked unit: walk a valid copy
+      int lowdig[LG > 0 ? LG : 1];
+#pragma unroll
+      for (int b = 0; b < LG; ++b) lowdig[b] = prefix_digit(p, u, kh + 1 + b);
 #pragma unroll
       for (int q = 0; q < NW; ++q) {
-        acc = sad4(A[j][q], B[j][q], acc);
-        if (G == 2) acc = sad4(A[j][q], B[j][NW + q], acc);
+        int32_t a[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) a[e] = __ldg(abRec + 4 * q + e);
+#pragma unroll
+        for (int b = 0; b < LG; ++b) {
+          const int dig = lowdig[b];
+          const int32_t f = (MODE == MODE_LD) ? 1 - dig : 1 - 2 * dig;
+          const int4 v = __ldg(reinterpret_cast<const int4*>(gInit + (kh + 1 + b) * CW) + q);
+          a[0] += f * v.x; a[1] += f * v.y; a[2] += f * v.z; a[3] += f * v.w;
+        }
+        A[j][q] = (uint32_t)(a[0] & 0xFF) | ((uint32_t)(a[1] & 0xFF) << 8) | ((uint32_t)(a[2] & 0xFF) << 16) |
+                  ((uint32_t)(a[3] & 0xFF) << 24);
+      }
+      // value of the unit's start strategy
+      uint32_t acc = Kc;
+#pragma unroll
+      for (int q = 0; q < NW; ++q) {
+        acc = sad4(A[j][q], B[q], acc);
+        if (G == 2) acc = sad4(A[j][q], B[NW + q], acc);
       }
       best[j] = (int32_t)acc;
     }
@@ -208,21 +276,21 @@ walk_u8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int3
         const int tz = __ffs((int)t) - 1;
         const int b = K + tz;
         const int sg = 1 ^ (int)((t >> (tz + 1)) & 1u);
-        U8Step<MODE, NW, P>::run(A, B, Kc, best, sbase, (2 * b + sg) * RW);
+        U8Step<MODE, NW, P>::run(A, B, Kc, best, sbase, (2 * b + sg) * RW, p.one);
       }
 #pragma unroll
       for (int jj = 1; jj < (1 << K); ++jj) {
         const int b = u8_cctz(jj);
         const int sg = (b < K - 1) ? (1 ^ ((jj >> (b + 1)) & 1)) : (1 ^ (int)(t & 1u));
-        U8Step<MODE, NW, P>::run(A, B, Kc, best, sbase, (2 * b + sg) * RW);
+        U8Step<MODE, NW, P>::run(A, B, Kc, best, sbase, (2 * b + sg) * RW, p.one);
       }
     }
 #pragma unroll
     for (int j = 0; j < P; ++j) {
-      const int64_t rel = ch * 32 * P + j * 32 + lane;
-      if (rel < p.unit_count) {
-        if (p.unit_max) p.unit_max[rel] = best[j];
-        if (!have || best[j] > best_all) { best_all = best[j]; best_u = (uint32_t)(p.unit_begin + rel); have = true; }
+      const int64_t u = g * P + j;
+      if (u >= p.unit_begin && u < u_end) {
+        if (p.unit_max) p.unit_max[u - p.unit_begin] = best[j];
+        if (!have || best[j] > best_all) { best_all = best[j]; best_u = (uint32_t)u; have = true; }
       }
     }
   }
@@ -231,9 +299,11 @@ walk_u8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int3
   if (lane == 0 && key) atomicMax(p.key, key);
 }
 
-// Delta table (walked digit b <-> row r-1-b, sign sg = new digit value) and init records.
+// Delta table (walked digit b <-> row r-1-b, sign sg = new digit value) and init
+// records; the byte window covers the last s + lg rows (lg = log2 of the lane group).
 template <int MODE>
-__global__ void build_u8_kernel(const int32_t* M, int r, int c, int NW, int k, int s, uint32_t* tab, int32_t* init) {
+__global__ void build_u8_kernel(const int32_t* M, int r, int c, int NW, int k, int s, int lg, uint32_t* tab,
+                                int32_t* init) {
   const int RW = u8_pad4(NW), CW = 4 * NW;
   const int scale = (MODE == MODE_LD) ? 1 : 2;
   const int tid = threadIdx.x;
@@ -256,35 +326,17 @@ __global__ void build_u8_kernel(const int32_t* M, int r, int c, int NW, int k, i
     init[i] = y < c ? M[(int64_t)x * c + y] : 0;
   }
   for (int y = tid; y < CW; y += blockDim.x) {
-    int32_t W = 0, N = 0, T = 0;
+    int32_t W = 0, N = 0, T = 0, Ssuf = 0;
     if (y < c)
       for (int x = 0; x < r; ++x) {
         const int32_t v = M[(int64_t)x * c + y];
         T += v;
-        if (x >= r - s) { W += abs(v); N += min(v, 0); }
+        if (x >= r - s - lg) { W += abs(v); N += min(v, 0); }   // window rows
+        if (x >= r - s) Ssuf += v;                             // suffix rows (all digit 0 at the start)
       }
     init[(k + 1) * CW + y] = (MODE == MODE_LD) ? N : -W;
     init[(k + 2) * CW + y] = (MODE == MODE_LD) ? T : 0;
-  }
-  __syncthreads();
-  uint32_t* a0 = reinterpret_cast<uint32_t*>(init + (k + 3) * CW);
-  for (int i = tid; i < NW; i += blockDim.x) {
-    uint32_t w = 0;
-    for (int e = 0; e < 4; ++e) {
-      const int y = 4 * i + e;
-      int32_t a = 0;
-      if (y < c) {
-        int32_t W = 0, Sm = 0, Sp = 0;
-        for (int x = r - s; x < r; ++x) {
-          const int32_t v = M[(int64_t)x * c + y];
-          W += abs(v); Sm += v; Sp += max(v, 0);
-        }
-        // start strategy: every suffix digit 0 (a_x = +1 / group 0)
-        a = (MODE == MODE_LD) ? Sp : Sm + W;
-      }
-      w |= (uint32_t)(a & 0xFF) << (8 * e);
-    }
-    a0[i] = w;
+    init[(k + 3) * CW + y] = (MODE == MODE_LD) ? Ssuf - N : Ssuf + W;
   }
 }
 
@@ -351,7 +403,9 @@ cudaError_t walk_u8_launch_mode<LN_BIN_MODE>(const WalkParams& p, int32_t* scrat
   const int NW = walk_u8_words_mode<LN_BIN_MODE>(p.c);
   if (NW == 0) return cudaErrorInvalidValue;
   uint32_t* tab = reinterpret_cast<uint32_t*>(scratch_tab);
-  build_u8_kernel<LN_BIN_MODE><<<1, 256, 0, st>>>(p.M, p.r, p.c, NW, p.k, p.s, tab, scratch_init);
+  const int P = [&]() -> int { LN_U8_SWITCH(LN_BIN_MODE, NW, upl_u8) return 1; }();
+  build_u8_kernel<LN_BIN_MODE><<<1, 256, 0, st>>>(p.M, p.r, p.c, NW, p.k, p.s, P >= 4 ? 2 : (P == 2 ? 1 : 0), tab,
+                                                  scratch_init);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   LN_U8_SWITCH(LN_BIN_MODE, NW, launch_u8, p, tab, scratch_init, grid, st)

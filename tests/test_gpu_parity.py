@@ -199,17 +199,45 @@ def test_planted_40x40_marg(lib):
     (4, False, 18, 18, 10),
 ])
 def test_sampled_prefixes_full_size(lib, d, marg, n, m, nfixed):
-    """Full-size configs (BASELINE 2-5): per-prefix maxima of the hot kernels vs the oracle, on sampled prefixes."""
+    """Full-size configs (BASELINE 2-5): per-prefix maxima of the hot kernels vs the oracle, on sampled prefixes.
+
+    Binary modes sample aligned groups of four prefixes that share rows 0..k-2 and run
+    through the last two prefix rows, exactly the lane groups of the byte-packed kernel
+    the full search launches (walk_u8_impl.cuh)."""
     M = synth.random_matrix(n, m, {(1, False, 42): 2, (1, True, 40): 3}.get((d, marg, n), 100 + n if d == 1 else 200 + n))
     g = synth.SplitMix64(777 + d)
     base = 2 if d == 1 else d
-    P = np.zeros((6, nfixed), dtype=np.int8)
-    for i in range(6):
+    P = np.zeros((8, nfixed), dtype=np.int8)
+    for i in range(8):
         for x in range(1, nfixed):
             P[i, x] = g.next() % base
+        if base == 2:
+            P[i, :nfixed - 2] = P[i - i % 4, :nfixed - 2]
+            P[i, nfixed - 2], P[i, nfixed - 1] = (i % 4) >> 1, (i % 4) & 1
     got = lib.prefix_maxima(M, P, d=d, with_marginals=marg)
-    for i in range(6):
+    for i in range(8):
         assert got[i] == oracle.prefix_max(M, P[i], d=d, with_marginals=marg)[0]
+
+
+@pytest.mark.parametrize("d,marg", [(1, False), (1, True), (2, False)], ids=["L1", "marg", "L2"])
+def test_sampled_prefixes_ungrouped(lib, d, marg):
+    """Prefixes that do not form aligned lane groups (arbitrary order and count) take the
+    per-unit kernels and still match the oracle."""
+    M = synth.random_matrix(30, 33, 880 + d + marg)
+    g = synth.SplitMix64(881)
+    P = np.zeros((7, 16), dtype=np.int8)
+    for i in range(7):
+        for x in range(1, 16):
+            P[i, x] = g.next() % 2
+    got = lib.prefix_maxima(M, P, d=d, with_marginals=marg)
+    for i in range(7):
+        assert got[i] == oracle.prefix_max(M, P[i], d=d, with_marginals=marg)[0]
+
+
+def test_bench_configs_plan_the_byte_kernel(lib):
+    """The 42x42 L_1 and 40x40 L_marg bench workloads run the byte-packed kernel."""
+    assert lib.plan(synth.random_matrix(42, 42, 2))["variant_name"] == "bin_u8"
+    assert lib.plan(synth.random_matrix(40, 40, 3), with_marginals=True)["variant_name"] == "bin_u8"
 
 
 # ------------------------------------------------------------- errors ----
@@ -307,10 +335,11 @@ def test_packed_guard_boundary_exact(lib, par):
     assert v == int(np.abs(M.astype(np.int64)).sum())
 
 
-def _u8_boundary_matrix(W, d, seed, s=4, n=9, m=12):
-    """n x m matrix whose last s rows give column 0 the suffix |.|-sum W (column 3 too,
+def _u8_boundary_matrix(W, d, seed, s=6, n=9, m=12):
+    """n x m matrix whose last s rows give column 0 the window |.|-sum W (column 3 too,
     all positive), every other column less, and row n-s-1 non-zero in column 0 so that a
-    longer suffix breaks the byte guard."""
+    longer window breaks the byte guard.  The u8 kernel's window is the 4-row suffix plus
+    the 2 prefix rows of its lane group (walk_u8_impl.cuh)."""
     g = synth.SplitMix64(seed)
     M = np.array(synth.random_matrix(n, m, seed, -6, 6), dtype=np.int64)
     for y, sign in ((0, None), (3, 1)):
@@ -332,7 +361,7 @@ def test_u8_guard_boundary_exact(lib, d, marg, W):
     fits = (W <= 127) if d == 1 else (W <= 255)
     assert (P["variant_name"] == "bin_u8") == fits, P
     if fits:
-        assert P["suffix_digits"] == 4
+        assert P["suffix_digits"] == 4 and P["prefix_digits"] == 4
     check(lib, M, d=d, marg=marg)
     check(lib, np.abs(M), d=d, marg=marg)
     check(lib, -np.abs(M), d=d, marg=marg)

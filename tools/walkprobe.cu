@@ -8,6 +8,8 @@
 //   V_S16_LDS   s16x2 packed sums: VIADD.16x2 update + VIADDMNMX.S16x2 max-accumulate
 //   V_B16_LDS   biased packed sums: 32-bit IADD update + LOP3 fix + VIADDMNMX.S16x2
 //   V_U8_LDS    u8x4 offset sums: 32-bit IADD update + VABSDIFF4.U8.ACC against a per-unit bias word
+//   V_U8S_LDS   same, the P units of a lane share their bias words (operand reuse)
+//   V_U8SE_LDS  shared bias, evaluate-then-update order (A in the reuse slot of the add)
 //
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 tools/walkprobe.cu -o tools/walkprobe
 #include <cuda_runtime.h>
@@ -21,8 +23,8 @@
 #define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { \
   fprintf(stderr, "CUDA %s at %s:%d\n", cudaGetErrorString(e_), __FILE__, __LINE__); exit(1);} } while (0)
 
-enum { V_I32_LDS = 0, V_I32_CST, V_S16_LDS, V_B16_LDS, V_U8_LDS, V_N };
-static const char* kNames[V_N] = {"i32_lds", "i32_const", "s16x2_lds", "biased16_lds", "u8x4_lds"};
+enum { V_I32_LDS = 0, V_I32_CST, V_S16_LDS, V_B16_LDS, V_U8_LDS, V_U8S_LDS, V_U8SE_LDS, V_N };
+static const char* kNames[V_N] = {"i32_lds", "i32_const", "s16x2_lds", "biased16_lds", "u8x4_lds", "u8x4_sharedB_lds", "u8x4_sharedB_evalfirst_lds"};
 
 constexpr int NROWS = 64;
 __constant__ int32_t cRows[NROWS * 64];
@@ -32,7 +34,7 @@ __device__ __forceinline__ unsigned smid() { unsigned r; asm volatile("mov.u32 %
 
 template <int V, int C, int P>
 __global__ void __launch_bounds__(128) walk(int32_t* out, Rec* rec, int steps, const int32_t* rows) {
-  constexpr int W = (V == V_U8_LDS) ? C / 4 : (V == V_S16_LDS || V == V_B16_LDS) ? C / 2 : C;   // 32-bit words per unit
+  constexpr int W = (V == V_U8_LDS || V == V_U8S_LDS || V == V_U8SE_LDS) ? C / 4 : (V == V_S16_LDS || V == V_B16_LDS) ? C / 2 : C;   // 32-bit words per unit
   __shared__ __align__(16) int32_t srow[NROWS * W];
   __shared__ int32_t srsum[NROWS];
   for (int i = threadIdx.x; i < NROWS * W; i += blockDim.x) srow[i] = rows[i];
@@ -91,6 +93,30 @@ __global__ void __launch_bounds__(128) walk(int32_t* out, Rec* rec, int steps, c
           if (y + 1 < W) {
             m[p][y+1] += r[y+1];
             asm("vabsdiff4.u32.u32.u32.add %0, %1, %2, %0;" : "+r"(a1) : "r"(m[p][y+1]), "r"(bb[p][y+1]));
+          }
+        }
+        best[p] = __viaddmax_s32((int)a0, (int)a1, best[p]);
+      } else if constexpr (V == V_U8S_LDS) {
+        uint32_t a0 = (uint32_t)S[p], a1 = 0;
+#pragma unroll
+        for (int y = 0; y < W; y += 2) {
+          m[p][y] += r[y];
+          asm("vabsdiff4.u32.u32.u32.add %0, %1, %2, %0;" : "+r"(a0) : "r"(m[p][y]), "r"(bb[0][y]));
+          if (y + 1 < W) {
+            m[p][y+1] += r[y+1];
+            asm("vabsdiff4.u32.u32.u32.add %0, %1, %2, %0;" : "+r"(a1) : "r"(m[p][y+1]), "r"(bb[0][y+1]));
+          }
+        }
+        best[p] = __viaddmax_s32((int)a0, (int)a1, best[p]);
+      } else if constexpr (V == V_U8SE_LDS) {
+        uint32_t a0 = (uint32_t)S[p], a1 = 0;
+#pragma unroll
+        for (int y = 0; y < W; y += 2) {
+          asm("vabsdiff4.u32.u32.u32.add %0, %1, %2, %0;" : "+r"(a0) : "r"(m[p][y]), "r"(bb[0][y]));
+          m[p][y] += r[y];
+          if (y + 1 < W) {
+            asm("vabsdiff4.u32.u32.u32.add %0, %1, %2, %0;" : "+r"(a1) : "r"(m[p][y+1]), "r"(bb[0][y+1]));
+            m[p][y+1] += r[y+1];
           }
         }
         best[p] = __viaddmax_s32((int)a0, (int)a1, best[p]);
@@ -168,6 +194,10 @@ int main(int argc, char** argv) {
     run<V_U8_LDS, 32, 4>(nsm, bps, steps, dout, drec, drows);
     run<V_U8_LDS, 48, 4>(nsm, bps, steps, dout, drec, drows);
     run<V_U8_LDS, 64, 4>(nsm, bps, steps, dout, drec, drows);
+    run<V_U8S_LDS, 48, 2>(nsm, bps, steps, dout, drec, drows);
+    run<V_U8S_LDS, 48, 4>(nsm, bps, steps, dout, drec, drows);
+    run<V_U8SE_LDS, 48, 2>(nsm, bps, steps, dout, drec, drows);
+    run<V_U8SE_LDS, 48, 4>(nsm, bps, steps, dout, drec, drows);
   }
   return 0;
 }
