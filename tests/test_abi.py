@@ -182,7 +182,9 @@ def test_plan_covers_the_search_space(n, m, d, marg):
 def test_plan_packed_guard_and_fallback():
     from paper_2503_21596_b200 import synth
     M = synth.random_matrix(30, 30, 1)
-    assert L.plan(M)["variant_name"] == "bin_pair16"               # sum |M| <= 32767
+    assert L.plan(M)["variant_name"] == "bin_u8"                   # suffix window fits a byte
+    assert L.plan((M * 2).astype(np.int32))["variant_name"] == "bin_u8"
+    assert L.plan((M * 3).astype(np.int32))["variant_name"] == "bin_pair16"    # sum |M| <= 16383, windows too wide
     mid = (M * 8).astype(np.int32)                   # sum |M| > 32767, per-parity column sums still fit
     assert L.plan(mid)["packed_ok"] == 1 and L.plan(mid)["variant_name"] == "bin_packed16"
     big = (M * 300).astype(np.int32)                 # column abs sums exceed the s16 guard
