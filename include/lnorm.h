@@ -177,7 +177,11 @@ int lnorm_compute_sliced(const int32_t* M, int32_t n, int32_t m, int32_t d, int3
  * for d = 1, labels 0..d-1 for d >= 2; for L_marg digit 0 of every prefix
  * must be 0) return in out[i] the maximum value over all strategies whose
  * rows 0..nfixed-1 equal prefix i and whose remaining rows are free.  No
- * orientation is applied.  Runs the same walk kernels as lnorm_compute.
+ * orientation is applied.  Runs the same walk kernels as lnorm_compute: the
+ * byte-packed kernel when the prefixes come in aligned groups of its lane group
+ * (P = 4 consecutive prefixes equal on rows 0..nfixed-3 and running through the
+ * four values of the last two rows, row nfixed-1 least significant), else a
+ * per-unit kernel.  lnorm_last_stats then reports the kernel variant and walk time.
  * Requires 1 <= nfixed <= n.
  */
 int lnorm_prefix_maxima(const int32_t* M, int32_t n, int32_t m, int32_t d, int32_t with_marginals,

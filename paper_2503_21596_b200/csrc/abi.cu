@@ -108,7 +108,7 @@ void suffix_guard(const int32_t* M, int m, Problem* p) {
 // rows, which join the byte window (walk_u8_impl.cuh "Lane groups")
 int u8_lane_bits(const Problem& p) {
   const int P = walk_u8_units_per_lane(p.mode, p.c);
-  return P >= 4 ? 2 : (P == 2 ? 1 : 0);
+  return P >= 8 ? 3 : P >= 4 ? 2 : (P == 2 ? 1 : 0);
 }
 
 bool u8_fits(const Problem& p, int s) {
@@ -1119,9 +1119,21 @@ int lnorm_prefix_maxima(const int32_t* M, int32_t n, int32_t m, int32_t d, int32
   walk_params_single(wp);
   wp.counter = cx->dCtl; wp.key = cx->dCtl + 1; wp.unit_max = cx->dUnit;
   int grid = 0, block = 0;
+  CU(cudaEventRecord(cx->ev[1], s));
   if ((rc = launch_walk(*cx, pr, pl, wp, &grid, &block))) return rc;
+  CU(cudaEventRecord(cx->ev[2], s));
   CU(cudaMemcpyAsync(out, cx->dUnit, sizeof(int64_t) * count, cudaMemcpyDeviceToHost, s));
   CU(cudaStreamSynchronize(s));
+  float wms = 0;
+  cudaEventElapsedTime(&wms, cx->ev[1], cx->ev[2]);
+  lnorm_stats S{};
+  S.rows = pr.r; S.cols = pr.c; S.prefix_digits = pl.k; S.suffix_digits = pl.s; S.d = pr.d == 1 ? 1 : base;
+  S.units = count; S.units_total = count;
+  S.steps = (double)count * (double)ipow(base, pl.s);
+  S.column_updates = S.steps * pr.c * (pr.mode == MODE_LD && base >= 3 ? 2 : 1);
+  S.walk_ms = wms; S.total_ms = wms; S.launches = pl.kernel == K_GEN ? 1 : 2; S.variant = pl.kernel;
+  S.block_threads = block; S.grid_blocks = grid;
+  g_stats = S;
   return LNORM_OK;
 }
 

@@ -42,7 +42,7 @@ constexpr int kBlockU8 = 32;
 #define LN_U8_BUDGET 1800
 #endif
 #ifndef LN_U8_MINB
-#define LN_U8_MINB 12
+#define LN_U8_MINB 16
 #endif
 
 __host__ __device__ constexpr int u8_cctz(int j) { return (j & 1) ? 0 : (j & 2) ? 1 : (j & 4) ? 2 : 3; }
@@ -165,12 +165,19 @@ struct U8Step {
 //   [(k+2)*CW, +CW)        T_y = sum_x M_xy (L_2 only)
 //   [(k+3)*CW, +CW)        a_y - delta_y at the start word: sum_suffix M_xy + W_y (L_1, L_marg)
 //                          or sum_suffix M_xy - N_y (L_2); delta = the unit's low prefix rows
+// resident warps per SM asked of ptxas: 16 (128 registers) where the lane's bytes and
+// biases leave room for it without spilling, else 12 (168 registers), else no bound
 template <int MODE, int NW, int P>
-__global__ void __launch_bounds__(kBlockU8, (U8Layout<MODE, NW>::G * NW * P <= 64 ? LN_U8_MINB : 1))
+__host__ __device__ constexpr int u8_min_blocks() {
+  return (U8Layout<MODE, NW>::G == 1 && NW * P + NW <= 56) ? LN_U8_MINB : ((U8Layout<MODE, NW>::G * NW * (P + 1) <= 80 && P >= 4) || U8Layout<MODE, NW>::G * NW * (P + 1) <= 54 ? 12 : 1);
+}
+
+template <int MODE, int NW, int P>
+__global__ void __launch_bounds__(kBlockU8, u8_min_blocks<MODE, NW, P>())
 walk_u8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int32_t* __restrict__ gInit) {
   using LY = U8Layout<MODE, NW>;
   constexpr int G = LY::G, RW = LY::RW, CW = LY::CW;
-  constexpr int LG = (P >= 4) ? 2 : (P == 2 ? 1 : 0);
+  constexpr int LG = (P >= 8) ? 3 : (P >= 4) ? 2 : (P == 2 ? 1 : 0);
   constexpr int K = u8_unroll<MODE, NW, P>();
   extern __shared__ __align__(16) uint32_t sT[];
   const int lane = threadIdx.x & 31;
@@ -369,6 +376,10 @@ int upl_u8() { return u8_units_per_lane<MODE, NW>(); }
 template <int MODE, int NW>
 int unroll_u8() { return u8_unroll<MODE, NW, u8_units_per_lane<MODE, NW>()>(); }
 
+#ifdef LN_U8_ONLY_NW   // experiment builds (tools/build_variant.py): one instance only
+#define LN_U8_SWITCH(MODE, NW_, FN, ...)                                                             \
+  if ((NW_) == LN_U8_ONLY_NW) return FN<MODE, LN_U8_ONLY_NW>(__VA_ARGS__);
+#else
 #define LN_U8_SWITCH(MODE, NW_, FN, ...)                                                             \
   switch (NW_) {                                                                                     \
     case 1: return FN<MODE, 1>(__VA_ARGS__);   case 2: return FN<MODE, 2>(__VA_ARGS__);              \
@@ -384,6 +395,7 @@ int unroll_u8() { return u8_unroll<MODE, NW, u8_units_per_lane<MODE, NW>()>(); }
     case 40: return FN<MODE, 40>(__VA_ARGS__); case 48: return FN<MODE, 48>(__VA_ARGS__);            \
     default: break;                                                                                  \
   }
+#endif
 
 }  // namespace
 
@@ -391,6 +403,9 @@ int unroll_u8() { return u8_unroll<MODE, NW, u8_units_per_lane<MODE, NW>()>(); }
 template <>
 int walk_u8_words_mode<LN_BIN_MODE>(int c) {
   int nw = (c + 3) / 4;
+#ifdef LN_U8_ONLY_NW
+  if (nw != LN_U8_ONLY_NW) return 0;
+#endif
   if (nw < 1) return 0;
   if (nw > 16) nw = (nw + 3) & ~3;
   if (nw > 32) nw = (nw + 7) & ~7;
@@ -404,7 +419,7 @@ cudaError_t walk_u8_launch_mode<LN_BIN_MODE>(const WalkParams& p, int32_t* scrat
   if (NW == 0) return cudaErrorInvalidValue;
   uint32_t* tab = reinterpret_cast<uint32_t*>(scratch_tab);
   const int P = [&]() -> int { LN_U8_SWITCH(LN_BIN_MODE, NW, upl_u8) return 1; }();
-  build_u8_kernel<LN_BIN_MODE><<<1, 256, 0, st>>>(p.M, p.r, p.c, NW, p.k, p.s, P >= 4 ? 2 : (P == 2 ? 1 : 0), tab,
+  build_u8_kernel<LN_BIN_MODE><<<1, 256, 0, st>>>(p.M, p.r, p.c, NW, p.k, p.s, P >= 8 ? 3 : P >= 4 ? 2 : (P == 2 ? 1 : 0), tab,
                                                   scratch_init);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;

@@ -13,6 +13,8 @@ sys.path.insert(0, ROOT)
 from paper_2503_21596_b200 import build as B  # noqa: E402
 
 name, flags = sys.argv[1], sys.argv[2:]
+if not any(f.startswith("-DLN_U8_ONLY_NW") for f in flags):
+    flags.append("-DLN_U8_ONLY_NW=11")   # the 42-column instance only (keeps the .so small)
 B.build()
 out_dir = os.path.join(ROOT, "paper_2503_21596_b200", "_exp", name)
 os.makedirs(out_dir, exist_ok=True)

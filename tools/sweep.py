@@ -21,8 +21,10 @@ import paper_2503_21596_b200 as L
 from paper_2503_21596_b200 import synth
 
 
-def roofline(col_updates_per_s, packed, nsm=148, mhz=1965.0):
-    peak_updates = 128.0 * nsm * mhz * 1e6 / (1 if packed else 2)   # 1 (packed) or 2 (int32) lane-instr per update
+def roofline(col_updates_per_s, variant, nsm=148, mhz=1965.0):
+    # lane-instructions per column update: 2 (int32 add + |.|-accumulate), 1 (s16x2), 1/2 (u8x4)
+    simd = 4 if variant == 7 else (2 if variant in (3, 4, 5, 6) else 1)
+    peak_updates = 128.0 * nsm * mhz * 1e6 * simd / 2
     return col_updates_per_s / peak_updates
 
 
@@ -44,27 +46,29 @@ def run(n, m, d, seed, budget_s):
     else:
         base = 2 if d == 1 else d
         # a seeded sample of 2^19 prefixes (enough to fill every resident warp several
-        # times), each walking a full suffix of 18 binary / 11 ternary digits
-        nfixed = n - 18 if d == 1 else n - 11
+        # times) with the full search's split: each walks the planned suffix of s digits
+        nfixed = n - plan["suffix_digits"]
         per = float(base) ** (n - nfixed)
         count = 1 << 19
         rng = np.random.default_rng(seed + 17)
         P = np.zeros((count, nfixed), dtype=np.int8)
         P[:, 1:] = rng.integers(0, base, size=(count, nfixed - 1), dtype=np.int8)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
+        if base == 2:   # aligned lane groups of 4 (the byte kernel's units, walk_u8_impl.cuh)
+            P[:, :nfixed - 2] = P[::4, :nfixed - 2].repeat(4, axis=0)
+            j = np.arange(count) % 4
+            P[:, nfixed - 2], P[:, nfixed - 1] = j >> 1, j & 1
+        L.prefix_maxima(M, P[:4096], d=d)                 # warm-up
         L.prefix_maxima(M, P, d=d)
-        secs = time.perf_counter() - t0
+        secs = L.last_stats()["walk_ms"] / 1e3            # the walk launch (CUDA events), as for "full"
         steps = count * per
         wall, v = secs, None
-        kind, variant = f"sampled ({count} prefixes of {nfixed} rows)", L.plan(M, d=d)["variant"]
+        kind, variant = f"sampled ({count} prefixes of {nfixed} rows)", L.last_stats()["variant"]
     rate = steps / secs
     cu = rate * updates_per_step
-    packed = variant in (3, 4, 5, 6)
     return {"config": f"L_{d} {n}x{m}", "n": n, "m": m, "d": d, "seed": seed, "kind": kind, "value": v,
             "kernel_variant": L.VARIANTS.get(variant, variant), "strategies": plan["steps"],
             "steps_per_s": rate, "column_updates_per_s": cu,
-            "roofline_frac": roofline(cu, packed),
+            "roofline_frac": roofline(cu, variant),
             "projected_full_search_s": plan["steps"] / rate, "measured_s": secs}
 
 
