@@ -260,7 +260,7 @@ def main():
         achieved_ops = 2.0 * col_updates / (walk_ms / 1e3) / 1e12     # Tops/s (add + |.|-accumulate)
         nsm = torch.cuda.get_device_properties(dev).multi_processor_count
         peak_mhz = load_peak_clock()
-        simd = 4 if st["variant"] == 7 else (2 if st["variant"] in (3, 4, 5, 6) else 1)   # u8x4 / s16x2 / int32 lanes per register
+        simd = 4 if st["variant"] in (7, 8) else (2 if st["variant"] in (3, 4, 5, 6) else 1)   # u8x4 / s16x2 / int32 lanes per register
         packed = simd > 1
         lanes = 128.0 * simd
         peak = lanes * nsm * peak_mhz * 1e6 * world / 1e12             # integer lane-ops/clk/SM x SMs x f_max

@@ -72,7 +72,7 @@ class PlanInfo(ctypes.Structure):
 
 
 VARIANTS = {0: "bin_int32", 1: "ld_int32", 2: "generic", 3: "bin_packed16", 4: "ld_packed16", 5: "bin_pair16", 6: "ld_pair16",
-            7: "bin_u8"}
+            7: "bin_u8", 8: "ld_u8"}
 
 _lock = threading.Lock()
 _lib = None

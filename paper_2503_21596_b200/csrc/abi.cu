@@ -169,7 +169,7 @@ int validate(const int32_t* M, int n, int m, int d, int marg, Problem* pr) {
 }
 
 // ------------------------------------------------------------------ plan --
-enum Kernel { K_BIN = 0, K_LD = 1, K_GEN = 2, K_BIN16 = 3, K_LD16 = 4, K_PAIR16 = 5, K_LDPAIR16 = 6, K_U8 = 7 };
+enum Kernel { K_BIN = 0, K_LD = 1, K_GEN = 2, K_BIN16 = 3, K_LD16 = 4, K_PAIR16 = 5, K_LDPAIR16 = 6, K_U8 = 7, K_LDU8 = 8 };
 
 // LNORM_KERNEL=auto|u8|pair16|packed|int32|generic forces a kernel family (benchmarks
 // and tests): the named family or, where it cannot run, the next one down the
@@ -281,7 +281,8 @@ int make_plan(const Problem& pr, int world, Plan* pl, int64_t target_override = 
     int kern = hot ? K_LD : K_GEN;
     int smin = hot ? 1 : 0;
     if (hot && ov != K_BIN && ov != K_GEN) {
-      if (pr.fitsLdPair && f >= 2 && walk_ldpair16_supported(d, pr.c, 2) && ov != K_BIN16) { kern = K_LDPAIR16; smin = 2; }
+      if (ov < 0 && pr.mode == MODE_LD && pr.sufW[pr.r] <= 255 && f >= 2 && walk_ldu8_supported(d, pr.c, 2)) { kern = K_LDU8; smin = 2; }
+      else if (pr.fitsLdPair && f >= 2 && walk_ldpair16_supported(d, pr.c, 2) && ov != K_BIN16) { kern = K_LDPAIR16; smin = 2; }
       else if (pr.fits16 && walk_ld16_supported(d, pr.c, 1)) { kern = K_LD16; smin = 1; }
     }
     if (ov == K_GEN) { kern = K_GEN; smin = 0; }
@@ -309,6 +310,7 @@ int make_plan(const Problem& pr, int world, Plan* pl, int64_t target_override = 
     }
     p.units = (int64_t)p.table.size();
     p.kernel = kern;
+    if (kern == K_LDU8 && !walk_ldu8_supported(d, pr.c, p.s)) kern = p.kernel = K_LDPAIR16;
     if (kern == K_LDPAIR16 && !walk_ldpair16_supported(d, pr.c, p.s)) p.kernel = pr.fits16 && walk_ld16_supported(d, pr.c, p.s) ? K_LD16 : K_LD;
   }
   // per-unit word count must fit 32-bit block counters
@@ -469,6 +471,7 @@ int launch_walk(DevCtx& cx, const Problem& pr, const Plan& pl, WalkParams& wp, i
   else if (pl.kernel == K_PAIR16) occ = walk_pair16_occupancy(pr.mode, pr.c, pl.s, &block);
   else if (pl.kernel == K_U8) occ = walk_u8_occupancy(pr.mode, pr.c, pl.s, &block);
   else if (pl.kernel == K_LDPAIR16) occ = walk_ldpair16_occupancy(pr.dl, pr.c, pl.s, &block);
+  else if (pl.kernel == K_LDU8) occ = walk_ldu8_occupancy(pr.dl, pr.c, pl.s, &block);
   else if (pl.kernel == K_LD) occ = walk_ld_occupancy(pr.dl, pr.c, &block);
   else occ = walk_generic_occupancy(pr.dl, pr.c, &block);
   if (occ < 1) occ = 1;
@@ -478,6 +481,7 @@ int launch_walk(DevCtx& cx, const Problem& pr, const Plan& pl, WalkParams& wp, i
   if (pl.kernel == K_PAIR16) per_block *= walk_pair16_units_per_lane(pr.mode, pr.c);
   if (pl.kernel == K_U8) per_block *= walk_u8_units_per_lane(pr.mode, pr.c);
   if (pl.kernel == K_LDPAIR16) per_block *= walk_ldpair16_units_per_lane(pr.dl, pr.c);
+  if (pl.kernel == K_LDU8) per_block *= walk_ldu8_units_per_lane(pr.dl, pr.c);
   int64_t want = (wp.unit_count + per_block - 1) / per_block;
   int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)occ * cx.nsm, want));
   cudaError_t e;
@@ -487,6 +491,7 @@ int launch_walk(DevCtx& cx, const Problem& pr, const Plan& pl, WalkParams& wp, i
   else if (pl.kernel == K_PAIR16) e = walk_pair16_launch(wp, cx.dTab, cx.dInit, grid, cx.stream, &block);
   else if (pl.kernel == K_U8) e = walk_u8_launch(wp, cx.dTab, cx.dInit, grid, cx.stream, &block);
   else if (pl.kernel == K_LDPAIR16) e = walk_ldpair16_launch(wp, cx.dTab, cx.dInit, grid, cx.stream, &block);
+  else if (pl.kernel == K_LDU8) e = walk_ldu8_launch(wp, cx.dTab, cx.dInit, grid, cx.stream, &block);
   else if (pl.kernel == K_LD) e = walk_ld_launch(wp, cx.dTab, grid, cx.stream, &block);
   else e = walk_generic_launch(wp, grid, cx.stream, &block);
   if (e != cudaSuccess) { (void)cudaGetLastError(); return LNORM_ECUDA; }
@@ -1096,6 +1101,8 @@ int lnorm_prefix_maxima(const int32_t* M, int32_t n, int32_t m, int32_t d, int32
     if ((pl.kernel == K_LD || pl.kernel == K_LD16) && pr.fitsLdPair && walk_ldpair16_supported(base, pr.c, pl.s))
       pl.kernel = K_LDPAIR16;
     const int ov = kernel_override();
+    if (ov < 0 && pl.kernel == K_LDPAIR16 && pr.sufW[pr.r] <= 255 && walk_ldu8_supported(base, pr.c, pl.s))
+      pl.kernel = K_LDU8;
     if (ov == K_GEN || (ov == K_BIN && pl.kernel != K_GEN)) pl.kernel = ov == K_GEN ? K_GEN : K_LD;
   }
   long double words = 1;

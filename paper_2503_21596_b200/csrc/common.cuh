@@ -159,6 +159,13 @@ template <int MODE> cudaError_t walk_u8_launch_mode(const WalkParams& p, int32_t
 template <int MODE> int walk_u8_occupancy_mode(int c, int s);
 template <int MODE> int walk_u8_units_per_lane_mode(int c);
 template <int MODE> int walk_u8_unroll_mode(int c);
+// Byte-packed d-ary walk, last row paired (L_d, d in {3,4}; guard: every column's
+// sum_x |M_xy| <= 255, checked by the caller).
+bool walk_ldu8_supported(int d, int c, int s);
+int walk_ldu8_units_per_lane(int d, int c);
+int walk_ldu8_occupancy(int d, int c, int s, int* block_out);
+cudaError_t walk_ldu8_launch(const WalkParams& p, int32_t* scratch_tab, int32_t* scratch_init, int grid,
+                             cudaStream_t st, int* block_out);
 // Generic warp-per-unit walk (any mode, d, c, s).
 bool walk_generic_supported(int d, int c);
 cudaError_t walk_generic_launch(const WalkParams& p, int grid, cudaStream_t st, int* block_out);

@@ -1,0 +1,353 @@
+// Hot d-ary Gray walk for L_d, d in {3, 4}, column sums packed four per register
+// as offset bytes, the LAST row evaluated for all d labels at every walked word.
+//
+// Units and control as in walk_ldpair16.cu (restricted-growth prefixes, warp-uniform
+// d-ary reflected walk, Eqs. 13-17; walked rows k+1..r-2, row r-1 paired).
+// Group g's column sum m_g,y = sum_{x labelled g} M_xy is a subset sum of column y,
+// so it always lies in [N_y, N_y + W_y] with N_y = sum_x min(M_xy, 0) and
+// W_y = sum_x |M_xy|.  When every W_y <= 255 (the exactness guard, checked on the
+// host) the lane keeps a_g,y = m_g,y - N_y as one unsigned byte, four columns per
+// register, and one 32-bit add of the packed row moves a row between groups exactly
+// (Eqs. 18-19: m_p -= M_rho, m_q += M_rho; no byte leaves [0, 255]).  The window is
+// the same for every unit, so the biases are global constants:
+//     |m_g,y|          = |a_g,y - B_y|,            B_y  = -N_y            (in [0, 255])
+//     |m_g,y + rho_y|  = |a_g,y - B'_y| + kappa'_y, B'_y = clamp(c_y, 0, 255),
+//                                                   c_y = -N_y - rho_y, kappa'_y = |c_y - B'_y|
+// and VABSDIFF4.U8.ACC accumulates four |.| per instruction.  With H_g = sum_y |m_g,y|
+// and H'_g = sum_y |m_g,y + rho_y| the value of the strategy that puts row r-1 in
+// group a is (Eq. 6)  L*(a) = sum_g H_g + (H'_a - H_a),  so a walked word evaluates
+// all d labels of the last row: best = max(best, lsum + max_a dd_a).  A move p -> q
+// costs 2 IADD + 4 VABSDIFF4 per four columns for d strategies.
+#include "common.cuh"
+
+namespace lnorm {
+
+namespace {
+
+constexpr int kBlockLU = 32;
+constexpr int kTabWordsLU = 16384;
+#ifndef LN_LDU8_MINB
+#define LN_LDU8_MINB 12
+#endif
+
+__host__ __device__ constexpr int lu_pad4(int x) { return (x + 3) & ~3; }
+
+__device__ __forceinline__ uint32_t lu_sad4(uint32_t a, uint32_t b, uint32_t acc) {
+  uint32_t d;
+  asm("vabsdiff4.u32.u32.u32.add %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(acc));
+  return d;
+}
+
+template <int D, int NW, int P>
+struct LdU8 {
+  static constexpr int RW = lu_pad4(NW);
+  static constexpr int RD = 2 * RW;        // delta record: +row at [0, NW), -row at [RW, RW + NW)
+  struct Unit {
+    uint32_t A[D][NW];
+    int32_t lo[D], dd[D];
+    int32_t lsum, best;
+  };
+  static __device__ __forceinline__ int32_t maxd(const int32_t (&dd)[D]) {
+    if constexpr (D == 3) return __vimax3_s32(dd[0], dd[1], dd[2]);
+    else return max(__vimax3_s32(dd[0], dd[1], dd[2]), dd[3]);
+  }
+  static __device__ __forceinline__ void refresh(Unit& U, int g, uint32_t h, uint32_t hp) {
+    const int32_t l = (int32_t)h;
+    U.lsum += l - U.lo[g];
+    U.lo[g] = l;
+    U.dd[g] = (int32_t)hp - l;
+  }
+  // move the walked row of record `off` from group PG to group QG in every unit
+  template <int PG, int QG>
+  static __device__ __forceinline__ void move(Unit (&U)[P], const uint32_t (&Bb)[NW], const uint32_t (&Bp)[NW],
+                                              uint32_t Kp, uint32_t sbase, int off) {
+    uint32_t hp[P], hpp[P], hq[P], hqp[P];
+#pragma unroll
+    for (int v = 0; v < RW / 4; ++v) {
+      const uint4 pq = lds128(sbase + 4u * (uint32_t)(off + 4 * v));        // +row quad
+      const uint4 nq = lds128(sbase + 4u * (uint32_t)(off + RW + 4 * v));   // -row quad
+      const uint32_t pp[4] = {pq.x, pq.y, pq.z, pq.w}, nn[4] = {nq.x, nq.y, nq.z, nq.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int i = 4 * v + e;
+        if (i < NW) {
+#pragma unroll
+          for (int j = 0; j < P; ++j) {
+            U[j].A[PG][i] += nn[e];
+            U[j].A[QG][i] += pp[e];
+            hp[j] = lu_sad4(U[j].A[PG][i], Bb[i], i == 0 ? 0u : hp[j]);
+            hpp[j] = lu_sad4(U[j].A[PG][i], Bp[i], i == 0 ? Kp : hpp[j]);
+            hq[j] = lu_sad4(U[j].A[QG][i], Bb[i], i == 0 ? 0u : hq[j]);
+            hqp[j] = lu_sad4(U[j].A[QG][i], Bp[i], i == 0 ? Kp : hqp[j]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
+      refresh(U[j], PG, hp[j], hpp[j]);
+      refresh(U[j], QG, hq[j], hqp[j]);
+      U[j].best = max(U[j].best, U[j].lsum + maxd(U[j].dd));
+    }
+  }
+  static __device__ __forceinline__ void move_dyn(Unit (&U)[P], const uint32_t (&Bb)[NW], const uint32_t (&Bp)[NW],
+                                                  uint32_t Kp, uint32_t sbase, int off, int p, int q) {
+    switch (p * D + q) {
+      case 0 * D + 1: move<0, 1>(U, Bb, Bp, Kp, sbase, off); return;
+      case 1 * D + 0: move<1, 0>(U, Bb, Bp, Kp, sbase, off); return;
+      case 1 * D + 2: move<1, 2>(U, Bb, Bp, Kp, sbase, off); return;
+      case 2 * D + 1: move<2, 1>(U, Bb, Bp, Kp, sbase, off); return;
+      default: break;
+    }
+    if constexpr (D >= 4) {
+      switch (p * D + q) {
+        case 2 * D + 3: move<2, 3>(U, Bb, Bp, Kp, sbase, off); return;
+        case 3 * D + 2: move<3, 2>(U, Bb, Bp, Kp, sbase, off); return;
+        default: break;
+      }
+    }
+  }
+};
+
+// Init records (global int32, stride CW = 4 NW): prefix rows 0..k, the base (walked
+// rows k+1..r-2 at label 0), then -N_y, then the packed bias words B (NW), B' (NW), K'.
+template <int D, int NW, int P>
+__global__ void __launch_bounds__(kBlockLU, (D * NW * P <= 72 ? LN_LDU8_MINB : 1))
+walk_ldu8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int32_t* __restrict__ gInit) {
+  using WK = LdU8<D, NW, P>;
+  constexpr int RD = WK::RD, CW = 4 * NW;
+  extern __shared__ __align__(16) uint32_t sT[];
+  const int lane = threadIdx.x & 31;
+  const int sw = p.s - 1;
+  for (int i = lane; i < sw * RD; i += 32) sT[i] = gTab[i];
+  __syncwarp();
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sT);
+  const int32_t* baseRec = gInit + (p.k + 1) * CW;
+  const int32_t* negRec = baseRec + CW;
+  const uint32_t* biasRec = reinterpret_cast<const uint32_t*>(negRec + CW);
+  uint32_t Bb[NW], Bp[NW];
+#pragma unroll
+  for (int i = 0; i < NW; ++i) { Bb[i] = __ldg(biasRec + i); Bp[i] = __ldg(biasRec + NW + i); }
+  const uint32_t Kp = __ldg(biasRec + 2 * NW);
+  uint32_t nblk = 1;
+  for (int i = 1; i < sw; ++i) nblk *= D;
+  int32_t best = INT32_MIN;
+  uint32_t best_u = 0;
+  bool have = false;
+  const int64_t nchunks = (p.unit_count + 32 * P - 1) / (32 * P);
+  for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    typename WK::Unit U[P];
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
+      const int64_t rel = ch * 32 * P + j * 32 + lane;
+      const int64_t u = p.unit_begin + (rel < p.unit_count ? rel : 0);
+      // prefix labels, pbits per row (the RGS table word; arithmetic prefixes repacked)
+      uint64_t lab = 0;
+      if (p.prefix_table) lab = p.prefix_table[u - p.unit_begin];
+      else for (int x = 0; x <= p.k; ++x) lab |= (uint64_t)prefix_digit(p, u, x) << (p.pbits * x);
+      const uint64_t lmask = (1ull << p.pbits) - 1ull;
+      U[j].lsum = 0;
+#pragma unroll
+      for (int q = 0; q < NW; ++q) {
+        int32_t a[D][4];
+#pragma unroll
+        for (int g = 0; g < D; ++g)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) a[g][e] = __ldg(negRec + 4 * q + e) + (g == 0 ? __ldg(baseRec + 4 * q + e) : 0);
+        for (int x = 0; x <= p.k; ++x) {
+          const int dig = (int)((lab >> (p.pbits * x)) & lmask);
+          const int4 v = __ldg(reinterpret_cast<const int4*>(gInit + x * CW) + q);
+#pragma unroll
+          for (int g = 0; g < D; ++g) {
+            const int32_t f = dig == g ? 1 : 0;
+            a[g][0] += f * v.x; a[g][1] += f * v.y; a[g][2] += f * v.z; a[g][3] += f * v.w;
+          }
+        }
+#pragma unroll
+        for (int g = 0; g < D; ++g)
+          U[j].A[g][q] = (uint32_t)(a[g][0] & 0xFF) | ((uint32_t)(a[g][1] & 0xFF) << 8) |
+                         ((uint32_t)(a[g][2] & 0xFF) << 16) | ((uint32_t)(a[g][3] & 0xFF) << 24);
+      }
+#pragma unroll
+      for (int g = 0; g < D; ++g) {
+        uint32_t h = 0u, hp = Kp;
+#pragma unroll
+        for (int q = 0; q < NW; ++q) { h = lu_sad4(U[j].A[g][q], Bb[q], h); hp = lu_sad4(U[j].A[g][q], Bp[q], hp); }
+        U[j].lo[g] = (int32_t)h;
+        U[j].dd[g] = (int32_t)hp - (int32_t)h;
+        U[j].lsum += (int32_t)h;
+      }
+      U[j].best = U[j].lsum + WK::maxd(U[j].dd);
+    }
+    for (uint32_t t = 0; t < nblk; ++t) {
+      if (t != 0) {
+        uint32_t i, from, to;
+        dary_block_start<D>(t, &i, &from, &to);
+        WK::move_dyn(U, Bb, Bp, Kp, sbase, (int)i * RD, (int)from, (int)to);
+      }
+      if ((t & 1u) == 0) {
+        WK::template move<0, 1>(U, Bb, Bp, Kp, sbase, 0);
+        WK::template move<1, 2>(U, Bb, Bp, Kp, sbase, 0);
+        if constexpr (D >= 4) WK::template move<2, 3>(U, Bb, Bp, Kp, sbase, 0);
+      } else {
+        if constexpr (D >= 4) WK::template move<3, 2>(U, Bb, Bp, Kp, sbase, 0);
+        WK::template move<2, 1>(U, Bb, Bp, Kp, sbase, 0);
+        WK::template move<1, 0>(U, Bb, Bp, Kp, sbase, 0);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
+      const int64_t rel = ch * 32 * P + j * 32 + lane;
+      if (rel < p.unit_count) {
+        const int32_t ub = U[j].best;
+        if (p.unit_max) p.unit_max[rel] = ub;
+        if (!have || ub > best) { best = ub; best_u = (uint32_t)(p.unit_begin + rel); have = true; }
+      }
+    }
+  }
+  unsigned long long key = have ? make_key(best, best_u) : 0ull;
+  key = warp_max_u64(key);
+  if (lane == 0 && key) atomicMax(p.key, key);
+}
+
+__global__ void build_ldu8_kernel(const int32_t* M, int r, int c, int NW, int k, int s, uint32_t* tab,
+                                  int32_t* init) {
+  const int RW = lu_pad4(NW), RD = 2 * RW, CW = 4 * NW, sw = s - 1;
+  auto pack = [](const int32_t* v) {
+    uint32_t w = 0;
+    for (int e = 0; e < 4; ++e) w += (uint32_t)v[e] << (8 * e);   // sum_e 256^e v_e (mod 2^32)
+    return w;
+  };
+  for (int rec = threadIdx.x; rec < sw; rec += blockDim.x) {      // walked digit rec <-> row r-2-rec
+    const int32_t* row = M + (int64_t)(r - 2 - rec) * c;
+    for (int i = 0; i < RW; ++i) {
+      int32_t vp[4], vn[4];
+      for (int e = 0; e < 4; ++e) {
+        const int y = 4 * i + e;
+        vp[e] = (i < NW && y < c) ? row[y] : 0;
+        vn[e] = -vp[e];
+      }
+      tab[rec * RD + i] = pack(vp);
+      tab[rec * RD + RW + i] = pack(vn);
+    }
+  }
+  for (int i = threadIdx.x; i < (k + 1) * CW; i += blockDim.x) {
+    const int x = i / CW, y = i % CW;
+    init[i] = y < c ? M[(int64_t)x * c + y] : 0;
+  }
+  for (int y = threadIdx.x; y < CW; y += blockDim.x) {
+    int32_t b = 0, N = 0;
+    if (y < c)
+      for (int x = 0; x < r; ++x) {
+        const int32_t v = M[(int64_t)x * c + y];
+        N += min(v, 0);
+        if (x > k && x < r - 1) b += v;
+      }
+    init[(k + 1) * CW + y] = b;
+    init[(k + 2) * CW + y] = -N;
+  }
+  if (threadIdx.x == 0) {
+    uint32_t* bias = reinterpret_cast<uint32_t*>(init + (k + 3) * CW);
+    int32_t kap = 0;
+    for (int i = 0; i < NW; ++i) {
+      uint32_t wb = 0, wp = 0;
+      for (int e = 0; e < 4; ++e) {
+        const int y = 4 * i + e;
+        int32_t N = 0, rho = 0;
+        if (y < c) {
+          for (int x = 0; x < r; ++x) N += min(M[(int64_t)x * c + y], 0);
+          rho = M[(int64_t)(r - 1) * c + y];
+        }
+        const int32_t cb = -N, cp = -N - rho;
+        const int32_t bp = min(max(cp, 0), 255);
+        kap += abs(cp - bp);
+        wb |= (uint32_t)(cb & 0xFF) << (8 * e);
+        wp |= (uint32_t)bp << (8 * e);
+      }
+      bias[i] = wb;
+      bias[NW + i] = wp;
+    }
+    bias[2 * NW] = (uint32_t)kap;
+  }
+}
+
+template <int D, int NW>
+constexpr int ldu8_units_per_lane() { return D * NW <= 24 ? 4 : (D * NW <= 48 ? 2 : 1); }
+
+size_t ldu8_smem(int NW, int s) { return sizeof(uint32_t) * (size_t)((s - 1) * 2 * lu_pad4(NW)); }
+
+template <int D, int NW>
+cudaError_t launch_lu(const WalkParams& p, const uint32_t* tab, const int32_t* init, int grid, cudaStream_t st) {
+  constexpr int P = ldu8_units_per_lane<D, NW>();
+  const size_t sm = ldu8_smem(NW, p.s);
+  cudaError_t e = cudaFuncSetAttribute(walk_ldu8_kernel<D, NW, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  walk_ldu8_kernel<D, NW, P><<<grid, kBlockLU, sm, st>>>(p, tab, init);
+  return cudaGetLastError();
+}
+
+template <int D, int NW>
+int occ_lu(int s) {
+  constexpr int P = ldu8_units_per_lane<D, NW>();
+  const size_t sm = ldu8_smem(NW, s);
+  cudaFuncSetAttribute(walk_ldu8_kernel<D, NW, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  int nb = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, walk_ldu8_kernel<D, NW, P>, kBlockLU, sm);
+  return nb;
+}
+
+template <int D, int NW>
+int upl_lu() { return ldu8_units_per_lane<D, NW>(); }
+
+#define LN_LDU8_SWITCH(D, NW_, FN, ...)                                                      \
+  switch (NW_) {                                                                             \
+    case 1: return FN<D, 1>(__VA_ARGS__);   case 2: return FN<D, 2>(__VA_ARGS__);            \
+    case 3: return FN<D, 3>(__VA_ARGS__);   case 4: return FN<D, 4>(__VA_ARGS__);            \
+    case 5: return FN<D, 5>(__VA_ARGS__);   case 6: return FN<D, 6>(__VA_ARGS__);            \
+    case 7: return FN<D, 7>(__VA_ARGS__);   case 8: return FN<D, 8>(__VA_ARGS__);            \
+    case 9: return FN<D, 9>(__VA_ARGS__);   case 10: return FN<D, 10>(__VA_ARGS__);          \
+    case 11: return FN<D, 11>(__VA_ARGS__); case 12: return FN<D, 12>(__VA_ARGS__);          \
+    default: break;                                                                          \
+  }
+
+int words_of(int c) { return (c + 3) / 4; }
+
+}  // namespace
+
+bool walk_ldu8_supported(int d, int c, int s) {
+  if ((d != 3 && d != 4) || c < 1 || s < 2) return false;
+  const int NW = words_of(c);
+  if (NW > 12) return false;
+  return (s - 1) * 2 * lu_pad4(NW) <= kTabWordsLU;
+}
+
+int walk_ldu8_units_per_lane(int d, int c) {
+  const int NW = words_of(c);
+  if (d == 3) { LN_LDU8_SWITCH(3, NW, upl_lu) }
+  if (d == 4) { LN_LDU8_SWITCH(4, NW, upl_lu) }
+  return 1;
+}
+
+int walk_ldu8_occupancy(int d, int c, int s, int* block_out) {
+  *block_out = kBlockLU;
+  const int NW = words_of(c);
+  if (d == 3) { LN_LDU8_SWITCH(3, NW, occ_lu, s) }
+  if (d == 4) { LN_LDU8_SWITCH(4, NW, occ_lu, s) }
+  return 0;
+}
+
+cudaError_t walk_ldu8_launch(const WalkParams& p, int32_t* scratch_tab, int32_t* scratch_init, int grid,
+                             cudaStream_t st, int* block_out) {
+  *block_out = kBlockLU;
+  const int NW = words_of(p.c);
+  if ((p.s - 1) * 2 * lu_pad4(NW) > kTabWordsLU || (p.k + 3) * 4 * NW + 2 * NW + 1 > 16384) return cudaErrorInvalidValue;
+  uint32_t* tab = reinterpret_cast<uint32_t*>(scratch_tab);
+  build_ldu8_kernel<<<1, 128, 0, st>>>(p.M, p.r, p.c, NW, p.k, p.s, tab, scratch_init);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  if (p.d == 3) { LN_LDU8_SWITCH(3, NW, launch_lu, p, tab, scratch_init, grid, st) }
+  if (p.d == 4) { LN_LDU8_SWITCH(4, NW, launch_lu, p, tab, scratch_init, grid, st) }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace lnorm

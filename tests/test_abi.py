@@ -190,7 +190,8 @@ def test_plan_packed_guard_and_fallback():
     big = (M * 300).astype(np.int32)                 # column abs sums exceed the s16 guard
     P = L.plan(big)
     assert P["packed_ok"] == 0 and P["variant_name"] == "bin_int32"
-    assert L.plan(synth.random_matrix(24, 24, 4), d=3)["variant_name"] == "ld_pair16"
+    assert L.plan(synth.random_matrix(24, 24, 4), d=3)["variant_name"] == "ld_u8"       # column |.|-sums <= 255
+    assert L.plan(synth.random_matrix(24, 24, 4) * 3, d=3)["variant_name"] == "ld_pair16"
     assert L.plan(synth.random_matrix(24, 40, 4), d=3)["variant_name"] == "generic"
     assert L.plan(np.eye(3, dtype=np.int32))["variant_name"] == "generic"     # suffix shorter than the unroll
 

@@ -367,6 +367,20 @@ def test_u8_guard_boundary_exact(lib, d, marg, W):
     check(lib, -np.abs(M), d=d, marg=marg)
 
 
+@pytest.mark.parametrize("d", [3, 4])
+@pytest.mark.parametrize("W", [255, 256])
+def test_ldu8_guard_boundary_exact(lib, d, W):
+    """Byte-packed d-ary walk: a column |.|-sum exactly at the byte guard (255) runs the
+    ld_u8 kernel and is exact (subset sums span the whole byte); 256 falls back, exact too."""
+    n, m = 9, 12
+    M = _with_abs_sums([W, W - 40, 7, 90, 31, 5, 60, 12, W - 1, 3, 44, 18], n, 63_000 + W + d)
+    P = lib.plan(M, d=d)
+    assert (P["variant_name"] == "ld_u8") == (W <= 255), P
+    check(lib, M, d=d)
+    check(lib, np.abs(M), d=d)
+    check(lib, -np.abs(M), d=d)
+
+
 # ------------------------------------------------- multi-GPU decomposition --
 
 @pytest.mark.parametrize("d,marg", MODES, ids=[mode_id(*m) for m in MODES])

@@ -23,7 +23,7 @@ from paper_2503_21596_b200 import synth
 
 def roofline(col_updates_per_s, variant, nsm=148, mhz=1965.0):
     # lane-instructions per column update: 2 (int32 add + |.|-accumulate), 1 (s16x2), 1/2 (u8x4)
-    simd = 4 if variant == 7 else (2 if variant in (3, 4, 5, 6) else 1)
+    simd = 4 if variant in (7, 8) else (2 if variant in (3, 4, 5, 6) else 1)
     peak_updates = 128.0 * nsm * mhz * 1e6 * simd / 2
     return col_updates_per_s / peak_updates
 
@@ -45,11 +45,11 @@ def run(n, m, d, seed, budget_s):
         kind, variant = "full", st["variant"]
     else:
         base = 2 if d == 1 else d
-        # a seeded sample of 2^19 prefixes (enough to fill every resident warp several
+        # a seeded sample of 2^21 prefixes (enough to fill every resident warp many
         # times) with the full search's split: each walks the planned suffix of s digits
         nfixed = n - plan["suffix_digits"]
         per = float(base) ** (n - nfixed)
-        count = 1 << 19
+        count = 1 << 21
         rng = np.random.default_rng(seed + 17)
         P = np.zeros((count, nfixed), dtype=np.int8)
         P[:, 1:] = rng.integers(0, base, size=(count, nfixed - 1), dtype=np.int8)
