@@ -104,7 +104,7 @@ bool walk_u8_supported(int mode, int c, int s) {
   if (mode == MODE_L1) { NW = walk_u8_words_mode<MODE_L1>(c); if (NW) K = walk_u8_unroll_mode<MODE_L1>(c); }
   else if (mode == MODE_MARG) { NW = walk_u8_words_mode<MODE_MARG>(c); if (NW) K = walk_u8_unroll_mode<MODE_MARG>(c); }
   else if (mode == MODE_LD) { NW = walk_u8_words_mode<MODE_LD>(c); if (NW) K = walk_u8_unroll_mode<MODE_LD>(c); }
-  if (NW == 0 || s < K || s > 31) return false;
+  if (NW == 0 || s < K + 1 || s > 31) return false;    // K unrolled digits + the paired last row
   const int RW = (NW + 3) & ~3;
   return 2 * s * RW <= 16384;     // delta table staged in shared memory (dTab holds 32768 words)
 }

@@ -71,6 +71,13 @@ struct U8Layout {
 #ifndef LN_U8_CHAINS
 #define LN_U8_CHAINS 2
 #endif
+// LN_U8_PAIR: the last row r-1 is not walked; every walked word evaluates both of its
+// signs (strategies A: a_{r-1} = +1 / group 0, B: -1 / group 1) against a second set
+// of bias words, B'_y = clamp(c_y + scale rho_y): one IADD per four columns serves two
+// strategies (walk_ldu8.cu applies the same pairing to the d-ary walk).
+#ifndef LN_U8_PAIR
+#define LN_U8_PAIR 1
+#endif
 
 // units per lane: the row quad loaded once per step is shared by P units
 template <int MODE, int NW>
@@ -92,7 +99,9 @@ __device__ __forceinline__ uint32_t u8_add(uint32_t a, uint32_t d, uint32_t one)
 }
 
 template <int MODE, int NW, int P>
-__host__ __device__ constexpr int u8_step_instr() { return P * (U8Layout<MODE, NW>::G + 1) * NW + P + U8Layout<MODE, NW>::RW / 4; }
+__host__ __device__ constexpr int u8_step_instr() {
+  return P * ((1 + LN_U8_PAIR) * U8Layout<MODE, NW>::G + 1) * NW + P + U8Layout<MODE, NW>::RW / 4;
+}
 
 template <int MODE, int NW, int P>
 __host__ __device__ constexpr int u8_unroll() {
@@ -104,12 +113,13 @@ __host__ __device__ constexpr int u8_unroll() {
 template <int MODE, int NW, int P>
 struct U8Step {
   static constexpr int G = U8Layout<MODE, NW>::G, RW = U8Layout<MODE, NW>::RW;
+  static constexpr int NB = (1 + LN_U8_PAIR) * G * NW;   // bias words: B (G*NW) [, B' (G*NW)]
   // One Gray step: add the packed delta record at sbase + off to every unit's bytes,
-  // re-accumulate sum |a - B| (two chains), best = max(acc0 + acc1, best).
-  static __device__ __forceinline__ void run(uint32_t (&A)[P][NW], const uint32_t (&B)[G * NW],
-                                             const uint32_t K, int32_t (&best)[P], uint32_t sbase, int off,
+  // re-accumulate sum |a - B| (and sum |a - B'| for the paired strategy), keep the max.
+  static __device__ __forceinline__ void run(uint32_t (&A)[P][NW], const uint32_t (&B)[NB],
+                                             const uint32_t (&K)[2], int32_t (&best)[P], uint32_t sbase, int off,
                                              uint32_t one) {
-    uint32_t a0[P], a1[P];
+    uint32_t a0[P], a1[P], b0[P], b1[P];
 #pragma unroll
     for (int v = 0; v < RW / 4; ++v) {
       const uint4 x4 = lds128(sbase + 4u * (uint32_t)(off + 4 * v));
@@ -121,11 +131,18 @@ struct U8Step {
 #pragma unroll
           for (int j = 0; j < P; ++j) {
             A[j][i] = u8_add(A[j][i], rq[e], one);
-            if (G == 2) {
-              a0[j] = sad4(A[j][i], B[i], i == 0 ? K : a0[j]);
+            if (LN_U8_PAIR) {
+              a0[j] = sad4(A[j][i], B[i], i == 0 ? K[0] : a0[j]);
+              b0[j] = sad4(A[j][i], B[G * NW + i], i == 0 ? K[1] : b0[j]);
+              if (G == 2) {
+                a1[j] = sad4(A[j][i], B[NW + i], i == 0 ? 0u : a1[j]);
+                b1[j] = sad4(A[j][i], B[G * NW + NW + i], i == 0 ? 0u : b1[j]);
+              }
+            } else if (G == 2) {
+              a0[j] = sad4(A[j][i], B[i], i == 0 ? K[0] : a0[j]);
               a1[j] = sad4(A[j][i], B[NW + i], i == 0 ? 0u : a1[j]);
             } else if (i == 0) {
-              a0[j] = sad4(A[j][0], B[0], K);
+              a0[j] = sad4(A[j][0], B[0], K[0]);
             } else if (LN_U8_CHAINS == 1) {
               a0[j] = sad4(A[j][i], B[i], a0[j]);
             } else if (i == 1) {
@@ -139,7 +156,14 @@ struct U8Step {
         }
       }
     }
-    if (G == 1 && (NW == 1 || LN_U8_CHAINS == 1)) {
+    if (LN_U8_PAIR) {
+#pragma unroll
+      for (int j = 0; j < P; ++j) {
+        const int32_t va = (G == 2) ? (int32_t)(a0[j] + a1[j]) : (int32_t)a0[j];
+        const int32_t vb = (G == 2) ? (int32_t)(b0[j] + b1[j]) : (int32_t)b0[j];
+        best[j] = __vimax3_s32(best[j], va, vb);
+      }
+    } else if (G == 1 && (NW == 1 || LN_U8_CHAINS == 1)) {
 #pragma unroll
       for (int j = 0; j < P; ++j) best[j] = max(best[j], (int32_t)a0[j]);
     } else {
@@ -165,11 +189,19 @@ struct U8Step {
 //   [(k+2)*CW, +CW)        T_y = sum_x M_xy (L_2 only)
 //   [(k+3)*CW, +CW)        a_y - delta_y at the start word: sum_suffix M_xy + W_y (L_1, L_marg)
 //                          or sum_suffix M_xy - N_y (L_2); delta = the unit's low prefix rows
+//   [(k+4)*CW, +CW)        scale * rho_y, rho = row r-1 (the paired row; scale 2 for L_1 / L_marg)
 // resident warps per SM asked of ptxas: 16 (128 registers) where the lane's bytes and
-// biases leave room for it without spilling, else 12 (168 registers), else no bound
+// biases leave room for it without spilling, else 14 or 12, else no bound
+#ifndef LN_U8_MINB_MID
+#define LN_U8_MINB_MID 14
+#endif
+template <int MODE, int NW, int P>
+__host__ __device__ constexpr int u8_foot() { return U8Layout<MODE, NW>::G * NW * (P + 1 + LN_U8_PAIR); }
 template <int MODE, int NW, int P>
 __host__ __device__ constexpr int u8_min_blocks() {
-  return (U8Layout<MODE, NW>::G == 1 && NW * P + NW <= 56) ? LN_U8_MINB : ((U8Layout<MODE, NW>::G * NW * (P + 1) <= 80 && P >= 4) || U8Layout<MODE, NW>::G * NW * (P + 1) <= 54 ? 12 : 1);
+  return (U8Layout<MODE, NW>::G == 1 && u8_foot<MODE, NW, P>() <= 56) ? LN_U8_MINB
+       : (U8Layout<MODE, NW>::G == 1 && u8_foot<MODE, NW, P>() <= 70) ? LN_U8_MINB_MID
+       : ((u8_foot<MODE, NW, P>() <= 96 && P >= 4) || u8_foot<MODE, NW, P>() <= 54) ? 12 : 1;
 }
 
 template <int MODE, int NW, int P>
@@ -179,15 +211,18 @@ walk_u8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int3
   constexpr int G = LY::G, RW = LY::RW, CW = LY::CW;
   constexpr int LG = (P >= 8) ? 3 : (P >= 4) ? 2 : (P == 2 ? 1 : 0);
   constexpr int K = u8_unroll<MODE, NW, P>();
+  constexpr int NB = U8Step<MODE, NW, P>::NB;
   extern __shared__ __align__(16) uint32_t sT[];
   const int lane = threadIdx.x & 31;
-  const int total = 2 * p.s * RW;
+  const int sw = p.s - LN_U8_PAIR;                 // walked digits (row r-1 paired, not walked)
+  const int total = 2 * sw * RW;
   for (int i = lane; i < total; i += 32) sT[i] = gTab[i];
   __syncwarp();
-  const uint32_t nblk = 1u << (p.s - K);
+  const uint32_t nblk = 1u << (sw - K);
   const int32_t* loRec = gInit + (p.k + 1) * CW;
   const int32_t* tRec = loRec + CW;
   const int32_t* abRec = tRec + CW;
+  const int32_t* rhoRec = abRec + CW;
   const int kh = p.k - LG;                         // last row of the shared (high) prefix part
   int32_t best_all = INT32_MIN;
   uint32_t best_u = 0;
@@ -200,15 +235,15 @@ walk_u8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int3
     const int64_t g = g0 + ch * 32 + lane;
     const int64_t uh = min(max(g * P, p.unit_begin), u_end - 1);   // a valid unit of the group
     uint32_t A[P][NW];
-    uint32_t B[G * NW];
-    uint32_t Kc;
+    uint32_t B[NB];
+    uint32_t Kc[2];
     int32_t best[P];
     // ---- lane init (PAPER.md:253's per-thread product): shared high part -> B, K;
     //      per unit: its low prefix rows -> start bytes
     {
       uint64_t neg = 0;                            // bit x: digit of row x (0..kh) is 1
       for (int x = 0; x <= kh; ++x) neg |= (uint64_t)(prefix_digit(p, uh, x) != 0) << x;
-      int32_t kap = 0;
+      int32_t kap = 0, kapb = 0;
 #pragma unroll
       for (int q = 0; q < NW; ++q) {
         int32_t Pv[4] = {0, 0, 0, 0};              // high prefix part of columns 4q..4q+3
@@ -219,32 +254,42 @@ walk_u8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int3
           const int4 v = __ldg(reinterpret_cast<const int4*>(gInit + x * CW) + q);
           Pv[0] += f * v.x; Pv[1] += f * v.y; Pv[2] += f * v.z; Pv[3] += f * v.w;
         }
-        uint32_t w0 = 0, w1 = 0;
+        uint32_t w[2][2] = {{0u, 0u}, {0u, 0u}};   // [paired][bias set]
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int y = 4 * q + e;
           const int32_t lo = Pv[e] + __ldg(loRec + y);
-          const int32_t c0 = -lo;
-          int32_t b0;
-          if (MODE == MODE_MARG && y == 0) {       // linear column: m_0 = a_0 + Lo_0
-            b0 = 0;
-            kap += lo;
-          } else {
-            b0 = min(max(c0, 0), 255);
-            kap += abs(c0 - b0);
-          }
-          w0 |= (uint32_t)b0 << (8 * e);
-          if (G == 2) {
-            const int32_t c1 = __ldg(tRec + y) - lo;
-            const int32_t b1 = min(max(c1, 0), 255);
-            kap += abs(c1 - b1);
-            w1 |= (uint32_t)b1 << (8 * e);
+          const int32_t srho = LN_U8_PAIR ? __ldg(rhoRec + y) : 0;
+#pragma unroll
+          for (int h = 0; h <= LN_U8_PAIR; ++h) {  // h = 1: strategy B, row r-1 flipped (m -= scale rho)
+            const int32_t sh = h ? srho : 0;
+            int32_t& kk = h ? kapb : kap;
+            const int32_t c0 = -lo + sh;
+            int32_t b0;
+            if (MODE == MODE_MARG && y == 0) {     // linear column: m_0 = a_0 + Lo_0 (- 2 rho_0)
+              b0 = 0;
+              kk += lo - sh;
+            } else {
+              b0 = min(max(c0, 0), 255);
+              kk += abs(c0 - b0);
+            }
+            w[h][0] |= (uint32_t)b0 << (8 * e);
+            if (G == 2) {
+              const int32_t c1 = __ldg(tRec + y) - lo + sh;
+              const int32_t b1 = min(max(c1, 0), 255);
+              kk += abs(c1 - b1);
+              w[h][1] |= (uint32_t)b1 << (8 * e);
+            }
           }
         }
-        B[q] = w0;
-        if (G == 2) B[NW + q] = w1;
+#pragma unroll
+        for (int h = 0; h <= LN_U8_PAIR; ++h) {
+          B[h * G * NW + q] = w[h][0];
+          if (G == 2) B[h * G * NW + NW + q] = w[h][1];
+        }
       }
-      Kc = (uint32_t)kap;
+      Kc[0] = (uint32_t)kap;
+      Kc[1] = (uint32_t)kapb;
     }
 #pragma unroll
     for (int j = 0; j < P; ++j) {
@@ -268,14 +313,19 @@ walk_u8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int3
         A[j][q] = (uint32_t)(a[0] & 0xFF) | ((uint32_t)(a[1] & 0xFF) << 8) | ((uint32_t)(a[2] & 0xFF) << 16) |
                   ((uint32_t)(a[3] & 0xFF) << 24);
       }
-      // value of the unit's start strategy
-      uint32_t acc = Kc;
+      // value of the unit's start word (strategy A, and B when paired)
+      int32_t v0 = 0;
 #pragma unroll
-      for (int q = 0; q < NW; ++q) {
-        acc = sad4(A[j][q], B[q], acc);
-        if (G == 2) acc = sad4(A[j][q], B[NW + q], acc);
+      for (int h = 0; h <= LN_U8_PAIR; ++h) {
+        uint32_t acc = Kc[h];
+#pragma unroll
+        for (int q = 0; q < NW; ++q) {
+          acc = sad4(A[j][q], B[h * G * NW + q], acc);
+          if (G == 2) acc = sad4(A[j][q], B[h * G * NW + NW + q], acc);
+        }
+        v0 = h == 0 ? (int32_t)acc : max(v0, (int32_t)acc);
       }
-      best[j] = (int32_t)acc;
+      best[j] = v0;
     }
     // ---- the walk: 2^s - 1 Gray steps (low K digits unrolled, Table 1's ruler pattern)
     for (uint32_t t = 0; t < nblk; ++t) {
@@ -314,9 +364,10 @@ __global__ void build_u8_kernel(const int32_t* M, int r, int c, int NW, int k, i
   const int RW = u8_pad4(NW), CW = 4 * NW;
   const int scale = (MODE == MODE_LD) ? 1 : 2;
   const int tid = threadIdx.x;
-  for (int rec = tid; rec < 2 * s; rec += blockDim.x) {
+  const int sw = s - LN_U8_PAIR;
+  for (int rec = tid; rec < 2 * sw; rec += blockDim.x) {
     const int b = rec >> 1, sg = rec & 1;
-    const int32_t* row = M + (int64_t)(r - 1 - b) * c;
+    const int32_t* row = M + (int64_t)(r - 1 - LN_U8_PAIR - b) * c;   // walked digit b
     const int f = sg ? -scale : scale;     // digit -> 1: a_x = -1 (m -= 2M) or group 1 (m_0 -= M)
     for (int i = 0; i < RW; ++i) {
       uint32_t w = 0;
@@ -344,11 +395,12 @@ __global__ void build_u8_kernel(const int32_t* M, int r, int c, int NW, int k, i
     init[(k + 1) * CW + y] = (MODE == MODE_LD) ? N : -W;
     init[(k + 2) * CW + y] = (MODE == MODE_LD) ? T : 0;
     init[(k + 3) * CW + y] = (MODE == MODE_LD) ? Ssuf - N : Ssuf + W;
+    init[(k + 4) * CW + y] = y < c ? scale * M[(int64_t)(r - 1) * c + y] : 0;
   }
 }
 
 template <int MODE, int NW>
-size_t u8_smem(int s) { return sizeof(uint32_t) * (size_t)(2 * s * U8Layout<MODE, NW>::RW); }
+size_t u8_smem(int s) { return sizeof(uint32_t) * (size_t)(2 * (s - LN_U8_PAIR) * U8Layout<MODE, NW>::RW); }
 
 template <int MODE, int NW>
 cudaError_t launch_u8(const WalkParams& p, const uint32_t* tab, const int32_t* init, int grid, cudaStream_t st) {

@@ -335,11 +335,12 @@ def test_packed_guard_boundary_exact(lib, par):
     assert v == int(np.abs(M.astype(np.int64)).sum())
 
 
-def _u8_boundary_matrix(W, d, seed, s=6, n=9, m=12):
+def _u8_boundary_matrix(W, d, seed, s=7, n=9, m=12):
     """n x m matrix whose last s rows give column 0 the window |.|-sum W (column 3 too,
     all positive), every other column less, and row n-s-1 non-zero in column 0 so that a
-    longer window breaks the byte guard.  The u8 kernel's window is the 4-row suffix plus
-    the 2 prefix rows of its lane group (walk_u8_impl.cuh)."""
+    longer window breaks the byte guard.  The u8 kernel's window is its 5-row suffix (4
+    unrolled digits + the paired last row) plus the 2 prefix rows of its lane group
+    (walk_u8_impl.cuh)."""
     g = synth.SplitMix64(seed)
     M = np.array(synth.random_matrix(n, m, seed, -6, 6), dtype=np.int64)
     for y, sign in ((0, None), (3, 1)):
@@ -361,7 +362,7 @@ def test_u8_guard_boundary_exact(lib, d, marg, W):
     fits = (W <= 127) if d == 1 else (W <= 255)
     assert (P["variant_name"] == "bin_u8") == fits, P
     if fits:
-        assert P["suffix_digits"] == 4 and P["prefix_digits"] == 4
+        assert P["suffix_digits"] == 5 and P["prefix_digits"] == 3
     check(lib, M, d=d, marg=marg)
     check(lib, np.abs(M), d=d, marg=marg)
     check(lib, -np.abs(M), d=d, marg=marg)
