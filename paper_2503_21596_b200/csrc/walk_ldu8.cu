@@ -271,8 +271,11 @@ __global__ void build_ldu8_kernel(const int32_t* M, int r, int c, int NW, int k,
   }
 }
 
+#ifndef LN_LDU8_PMAX
+#define LN_LDU8_PMAX 4
+#endif
 template <int D, int NW>
-constexpr int ldu8_units_per_lane() { return D * NW <= 24 ? 4 : (D * NW <= 48 ? 2 : 1); }
+constexpr int ldu8_units_per_lane() { return D * NW <= 24 ? LN_LDU8_PMAX : (D * NW <= 48 ? (LN_LDU8_PMAX < 2 ? LN_LDU8_PMAX : 2) : 1); }
 
 size_t ldu8_smem(int NW, int s) { return sizeof(uint32_t) * (size_t)((s - 1) * 2 * lu_pad4(NW)); }
 

@@ -13,6 +13,7 @@ sys.path.insert(0, ROOT)
 from paper_2503_21596_b200 import build as B  # noqa: E402
 
 name, flags = sys.argv[1], sys.argv[2:]
+tus = os.environ.get("VARIANT_TUS", "walk_u8_")      # prefix of the translation units rebuilt with the flags
 if not any(f.startswith("-DLN_U8_ONLY_NW") for f in flags):
     flags.append("-DLN_U8_ONLY_NW=11")   # the 42-column instance only (keeps the .so small)
 B.build()
@@ -21,7 +22,7 @@ os.makedirs(out_dir, exist_ok=True)
 objs = []
 for src in sorted(glob.glob(os.path.join(B.CSRC, "*.cu"))):
     base = os.path.basename(src)[:-3]
-    if base.startswith("walk_u8_"):
+    if base.startswith(tus):
         obj = os.path.join(out_dir, base + ".o")
         r = subprocess.run([B.NVCC] + B.ARCH + B.FLAGS + flags + ["-c", src, "-o", obj], capture_output=True, text=True)
         if r.returncode:
