@@ -81,8 +81,12 @@ struct U8Layout {
 
 // units per lane: the row quad loaded once per step is shared by P units
 template <int MODE, int NW>
+#ifndef LN_U8_PWIDE
+#define LN_U8_PWIDE 1
+#endif
 __host__ __device__ constexpr int u8_units_per_lane() {
-  return U8Layout<MODE, NW>::G * NW <= 16 ? LN_U8_P : (U8Layout<MODE, NW>::G * NW <= 32 ? 2 : 1);
+  return U8Layout<MODE, NW>::G * NW <= 16 ? LN_U8_P
+       : (U8Layout<MODE, NW>::G * NW <= 32 ? 2 : (U8Layout<MODE, NW>::G == 1 ? LN_U8_PWIDE : 1));
 }
 
 // packed byte update A + D; LN_U8_MAD: as IMAD D * one + A with `one` a kernel
