@@ -221,7 +221,11 @@ int lnorm_partition(uint64_t C, int64_t T, int64_t t, int64_t* j_min, int64_t* j
  * kernel family lnorm_compute would use for this input on `world` ranks.
  * variant: 0 int32 binary walk, 1 int32 d-ary walk, 2 generic warp-per-unit,
  * 3 packed-16 binary walk, 4 packed-16 d-ary walk, 5 strategy-paired packed-16
- * binary walk, 6 last-row-paired packed-16 d-ary walk.  units = 2^k for +-1
+ * binary walk, 6 last-row-paired packed-16 d-ary walk, 7 byte-packed binary walk
+ * (L_1, L_marg, L_2), 8 byte-packed d-ary walk (L_3, L_4).  The planner takes the
+ * first exact family in the order 7/8 > 5/6 > 3/4 > 0/1 > 2; the environment
+ * variable LNORM_KERNEL=auto|u8|pair16|packed|int32|generic starts that order at
+ * the named family (tests, A/B timing).  units = 2^k for +-1
  * strategies and L_2, else the number of restricted-growth prefixes of
  * length k+1 with at most d labels.  Returns the same validation errors as
  * lnorm_compute.
