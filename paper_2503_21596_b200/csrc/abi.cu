@@ -481,7 +481,7 @@ int launch_walk(DevCtx& cx, const Problem& pr, const Plan& pl, WalkParams& wp, i
   if (pl.kernel == K_PAIR16) per_block *= walk_pair16_units_per_lane(pr.mode, pr.c);
   if (pl.kernel == K_U8) per_block *= walk_u8_units_per_lane(pr.mode, pr.c);
   if (pl.kernel == K_LDPAIR16) per_block *= walk_ldpair16_units_per_lane(pr.dl, pr.c);
-  if (pl.kernel == K_LDU8) per_block *= walk_ldu8_units_per_lane(pr.dl, pr.c);
+  if (pl.kernel == K_LDU8) per_block *= walk_ldu8_units_per_lane(pr.dl, pr.c, pl.s);
   int64_t want = (wp.unit_count + per_block - 1) / per_block;
   int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)occ * cx.nsm, want));
   cudaError_t e;

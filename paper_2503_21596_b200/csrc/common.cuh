@@ -162,7 +162,7 @@ template <int MODE> int walk_u8_unroll_mode(int c);
 // Byte-packed d-ary walk, last row paired (L_d, d in {3,4}; guard: every column's
 // sum_x |M_xy| <= 255, checked by the caller).
 bool walk_ldu8_supported(int d, int c, int s);
-int walk_ldu8_units_per_lane(int d, int c);
+int walk_ldu8_units_per_lane(int d, int c, int s);
 int walk_ldu8_occupancy(int d, int c, int s, int* block_out);
 cudaError_t walk_ldu8_launch(const WalkParams& p, int32_t* scratch_tab, int32_t* scratch_init, int grid,
                              cudaStream_t st, int* block_out);

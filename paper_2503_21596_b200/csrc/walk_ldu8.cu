@@ -1,8 +1,10 @@
 // Hot d-ary Gray walk for L_d, d in {3, 4}, column sums packed four per register
-// as offset bytes, the LAST row evaluated for all d labels at every walked word.
+// as offset bytes, the LAST TWO rows evaluated for all d^2 labellings at every walked
+// word (LN_LDU8_ROWS = 2; 1 = last row only, used when the suffix is too short).
 //
 // Units and control as in walk_ldpair16.cu (restricted-growth prefixes, warp-uniform
-// d-ary reflected walk, Eqs. 13-17; walked rows k+1..r-2, row r-1 paired).
+// d-ary reflected walk, Eqs. 13-17; walked rows k+1..r-1-PR, rows r-PR..r-1
+// paired).
 // Group g's column sum m_g,y = sum_{x labelled g} M_xy is a subset sum of column y,
 // so it always lies in [N_y, N_y + W_y] with N_y = sum_x min(M_xy, 0) and
 // W_y = sum_x |M_xy|.  When every W_y <= 255 (the exactness guard, checked on the
@@ -16,8 +18,7 @@
 // and VABSDIFF4.U8.ACC accumulates four |.| per instruction.  With H_g = sum_y |m_g,y|
 // and H'_g = sum_y |m_g,y + rho_y| the value of the strategy that puts row r-1 in
 // group a is (Eq. 6)  L*(a) = sum_g H_g + (H'_a - H_a),  so a walked word evaluates
-// all d labels of the last row: best = max(best, lsum + max_a dd_a).  A move p -> q
-// costs 2 IADD + 4 VABSDIFF4 per four columns for d strategies.
+// all d labels of the last row; with two paired rows (below) all d^2 labellings.
 #include "common.cuh"
 
 namespace lnorm {
@@ -38,30 +39,53 @@ __device__ __forceinline__ uint32_t lu_sad4(uint32_t a, uint32_t b, uint32_t acc
   return d;
 }
 
-template <int D, int NW, int P>
+// PR = number of paired last rows (1: row r-1; 2: rows r-1 and r-2).  Bias set m
+// (bitmask over the paired rows) serves |m_g,y + sum_{i in m} rho_i,y|; with
+// E_m,g = H_m,g - H_g the value for paired-row labels (a_1 for row r-1, a_2 for r-2) is
+//   PR = 1:  S + E_1,a1;     PR = 2:  S + E_1,a1 + E_2,a2 (a1 != a2),  S + E_3,a1 (a1 == a2)
+// with S = sum_g H_g.  PR = 2 evaluates d^2 strategies per walked word from 8 sums of the
+// two groups a move changes: 2 IADD + 8 VABSDIFF4 per four columns for d^2 strategies.
+template <int D, int NW, int P, int PR>
 struct LdU8 {
   static constexpr int RW = lu_pad4(NW);
   static constexpr int RD = 2 * RW;        // delta record: +row at [0, NW), -row at [RW, RW + NW)
+  static constexpr int NS = 1 << PR;       // bias sets
   struct Unit {
     uint32_t A[D][NW];
-    int32_t lo[D], dd[D];
-    int32_t lsum, best;
+    int32_t H[D], E[NS - 1][D];
+    int32_t S, best;
   };
-  static __device__ __forceinline__ int32_t maxd(const int32_t (&dd)[D]) {
-    if constexpr (D == 3) return __vimax3_s32(dd[0], dd[1], dd[2]);
-    else return max(__vimax3_s32(dd[0], dd[1], dd[2]), dd[3]);
+  static __device__ __forceinline__ int32_t max_of(const int32_t (&v)[D]) {
+    if constexpr (D == 3) return __vimax3_s32(v[0], v[1], v[2]);
+    else return max(__vimax3_s32(v[0], v[1], v[2]), v[3]);
   }
-  static __device__ __forceinline__ void refresh(Unit& U, int g, uint32_t h, uint32_t hp) {
-    const int32_t l = (int32_t)h;
-    U.lsum += l - U.lo[g];
-    U.lo[g] = l;
-    U.dd[g] = (int32_t)hp - l;
+  // best paired-row extension of the current word, relative to S
+  static __device__ __forceinline__ int32_t ext(const Unit& U) {
+    if constexpr (PR == 1) {
+      return max_of(U.E[0]);
+    } else {
+      int32_t m[D];
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        int32_t o = INT32_MIN;
+        if constexpr (D == 3) o = max(U.E[1][(a + 1) % 3], U.E[1][(a + 2) % 3]);
+        else o = __vimax3_s32(U.E[1][(a + 1) % 4], U.E[1][(a + 2) % 4], U.E[1][(a + 3) % 4]);
+        m[a] = U.E[0][a] + o;
+      }
+      return max(max_of(m), max_of(U.E[2]));
+    }
+  }
+  static __device__ __forceinline__ void refresh(Unit& U, int g, const uint32_t (&h)[NS]) {
+    U.S += (int32_t)h[0] - U.H[g];
+    U.H[g] = (int32_t)h[0];
+#pragma unroll
+    for (int m = 1; m < NS; ++m) U.E[m - 1][g] = (int32_t)h[m] - (int32_t)h[0];
   }
   // move the walked row of record `off` from group PG to group QG in every unit
   template <int PG, int QG>
-  static __device__ __forceinline__ void move(Unit (&U)[P], const uint32_t (&Bb)[NW], const uint32_t (&Bp)[NW],
-                                              uint32_t Kp, uint32_t sbase, int off) {
-    uint32_t hp[P], hpp[P], hq[P], hqp[P];
+  static __device__ __forceinline__ void move(Unit (&U)[P], const uint32_t (&Bs)[NS * NW], const uint32_t (&Ks)[NS],
+                                              uint32_t sbase, int off) {
+    uint32_t hp[P][NS], hq[P][NS];
 #pragma unroll
     for (int v = 0; v < RW / 4; ++v) {
       const uint4 pq = lds128(sbase + 4u * (uint32_t)(off + 4 * v));        // +row quad
@@ -75,60 +99,66 @@ struct LdU8 {
           for (int j = 0; j < P; ++j) {
             U[j].A[PG][i] += nn[e];
             U[j].A[QG][i] += pp[e];
-            hp[j] = lu_sad4(U[j].A[PG][i], Bb[i], i == 0 ? 0u : hp[j]);
-            hpp[j] = lu_sad4(U[j].A[PG][i], Bp[i], i == 0 ? Kp : hpp[j]);
-            hq[j] = lu_sad4(U[j].A[QG][i], Bb[i], i == 0 ? 0u : hq[j]);
-            hqp[j] = lu_sad4(U[j].A[QG][i], Bp[i], i == 0 ? Kp : hqp[j]);
+#pragma unroll
+            for (int m = 0; m < NS; ++m) {
+              hp[j][m] = lu_sad4(U[j].A[PG][i], Bs[m * NW + i], i == 0 ? Ks[m] : hp[j][m]);
+              hq[j][m] = lu_sad4(U[j].A[QG][i], Bs[m * NW + i], i == 0 ? Ks[m] : hq[j][m]);
+            }
           }
         }
       }
     }
 #pragma unroll
     for (int j = 0; j < P; ++j) {
-      refresh(U[j], PG, hp[j], hpp[j]);
-      refresh(U[j], QG, hq[j], hqp[j]);
-      U[j].best = max(U[j].best, U[j].lsum + maxd(U[j].dd));
+      refresh(U[j], PG, hp[j]);
+      refresh(U[j], QG, hq[j]);
+      U[j].best = max(U[j].best, U[j].S + ext(U[j]));
     }
   }
-  static __device__ __forceinline__ void move_dyn(Unit (&U)[P], const uint32_t (&Bb)[NW], const uint32_t (&Bp)[NW],
-                                                  uint32_t Kp, uint32_t sbase, int off, int p, int q) {
+  static __device__ __forceinline__ void move_dyn(Unit (&U)[P], const uint32_t (&Bs)[NS * NW], const uint32_t (&Ks)[NS],
+                                                  uint32_t sbase, int off, int p, int q) {
     switch (p * D + q) {
-      case 0 * D + 1: move<0, 1>(U, Bb, Bp, Kp, sbase, off); return;
-      case 1 * D + 0: move<1, 0>(U, Bb, Bp, Kp, sbase, off); return;
-      case 1 * D + 2: move<1, 2>(U, Bb, Bp, Kp, sbase, off); return;
-      case 2 * D + 1: move<2, 1>(U, Bb, Bp, Kp, sbase, off); return;
+      case 0 * D + 1: move<0, 1>(U, Bs, Ks, sbase, off); return;
+      case 1 * D + 0: move<1, 0>(U, Bs, Ks, sbase, off); return;
+      case 1 * D + 2: move<1, 2>(U, Bs, Ks, sbase, off); return;
+      case 2 * D + 1: move<2, 1>(U, Bs, Ks, sbase, off); return;
       default: break;
     }
     if constexpr (D >= 4) {
       switch (p * D + q) {
-        case 2 * D + 3: move<2, 3>(U, Bb, Bp, Kp, sbase, off); return;
-        case 3 * D + 2: move<3, 2>(U, Bb, Bp, Kp, sbase, off); return;
+        case 2 * D + 3: move<2, 3>(U, Bs, Ks, sbase, off); return;
+        case 3 * D + 2: move<3, 2>(U, Bs, Ks, sbase, off); return;
         default: break;
       }
     }
   }
 };
 
+#ifndef LN_LDU8_ROWS
+#define LN_LDU8_ROWS 2
+#endif
+
 // Init records (global int32, stride CW = 4 NW): prefix rows 0..k, the base (walked
-// rows k+1..r-2 at label 0), then -N_y, then the packed bias words B (NW), B' (NW), K'.
-template <int D, int NW, int P>
-__global__ void __launch_bounds__(kBlockLU, (D * NW * P <= 72 ? LN_LDU8_MINB : 1))
+// rows at label 0), -N_y, then the packed bias words of the NS sets and their K_m.
+template <int D, int NW, int P, int PR>
+__global__ void __launch_bounds__(kBlockLU, (D * NW * P * (PR == 2 ? 2 : 1) <= 72 ? LN_LDU8_MINB : 1))
 walk_ldu8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int32_t* __restrict__ gInit) {
-  using WK = LdU8<D, NW, P>;
-  constexpr int RD = WK::RD, CW = 4 * NW;
+  using WK = LdU8<D, NW, P, PR>;
+  constexpr int RD = WK::RD, CW = 4 * NW, NS = WK::NS;
   extern __shared__ __align__(16) uint32_t sT[];
   const int lane = threadIdx.x & 31;
-  const int sw = p.s - 1;
+  const int sw = p.s - PR;                         // walked digits
   for (int i = lane; i < sw * RD; i += 32) sT[i] = gTab[i];
   __syncwarp();
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sT);
   const int32_t* baseRec = gInit + (p.k + 1) * CW;
   const int32_t* negRec = baseRec + CW;
   const uint32_t* biasRec = reinterpret_cast<const uint32_t*>(negRec + CW);
-  uint32_t Bb[NW], Bp[NW];
+  uint32_t Bs[NS * NW], Ks[NS];
 #pragma unroll
-  for (int i = 0; i < NW; ++i) { Bb[i] = __ldg(biasRec + i); Bp[i] = __ldg(biasRec + NW + i); }
-  const uint32_t Kp = __ldg(biasRec + 2 * NW);
+  for (int i = 0; i < NS * NW; ++i) Bs[i] = __ldg(biasRec + i);
+#pragma unroll
+  for (int m = 0; m < NS; ++m) Ks[m] = __ldg(biasRec + NS * NW + m);
   uint32_t nblk = 1;
   for (int i = 1; i < sw; ++i) nblk *= D;
   int32_t best = INT32_MIN;
@@ -146,7 +176,6 @@ walk_ldu8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const in
       if (p.prefix_table) lab = p.prefix_table[u - p.unit_begin];
       else for (int x = 0; x <= p.k; ++x) lab |= (uint64_t)prefix_digit(p, u, x) << (p.pbits * x);
       const uint64_t lmask = (1ull << p.pbits) - 1ull;
-      U[j].lsum = 0;
 #pragma unroll
       for (int q = 0; q < NW; ++q) {
         int32_t a[D][4];
@@ -168,31 +197,37 @@ walk_ldu8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const in
           U[j].A[g][q] = (uint32_t)(a[g][0] & 0xFF) | ((uint32_t)(a[g][1] & 0xFF) << 8) |
                          ((uint32_t)(a[g][2] & 0xFF) << 16) | ((uint32_t)(a[g][3] & 0xFF) << 24);
       }
+      U[j].S = 0;
 #pragma unroll
       for (int g = 0; g < D; ++g) {
-        uint32_t h = 0u, hp = Kp;
+        uint32_t h[NS];
 #pragma unroll
-        for (int q = 0; q < NW; ++q) { h = lu_sad4(U[j].A[g][q], Bb[q], h); hp = lu_sad4(U[j].A[g][q], Bp[q], hp); }
-        U[j].lo[g] = (int32_t)h;
-        U[j].dd[g] = (int32_t)hp - (int32_t)h;
-        U[j].lsum += (int32_t)h;
+        for (int m = 0; m < NS; ++m) {
+          h[m] = Ks[m];
+#pragma unroll
+          for (int q = 0; q < NW; ++q) h[m] = lu_sad4(U[j].A[g][q], Bs[m * NW + q], h[m]);
+        }
+        U[j].H[g] = (int32_t)h[0];
+        U[j].S += (int32_t)h[0];
+#pragma unroll
+        for (int m = 1; m < NS; ++m) U[j].E[m - 1][g] = (int32_t)h[m] - (int32_t)h[0];
       }
-      U[j].best = U[j].lsum + WK::maxd(U[j].dd);
+      U[j].best = U[j].S + WK::ext(U[j]);
     }
     for (uint32_t t = 0; t < nblk; ++t) {
       if (t != 0) {
         uint32_t i, from, to;
         dary_block_start<D>(t, &i, &from, &to);
-        WK::move_dyn(U, Bb, Bp, Kp, sbase, (int)i * RD, (int)from, (int)to);
+        WK::move_dyn(U, Bs, Ks, sbase, (int)i * RD, (int)from, (int)to);
       }
       if ((t & 1u) == 0) {
-        WK::template move<0, 1>(U, Bb, Bp, Kp, sbase, 0);
-        WK::template move<1, 2>(U, Bb, Bp, Kp, sbase, 0);
-        if constexpr (D >= 4) WK::template move<2, 3>(U, Bb, Bp, Kp, sbase, 0);
+        WK::template move<0, 1>(U, Bs, Ks, sbase, 0);
+        WK::template move<1, 2>(U, Bs, Ks, sbase, 0);
+        if constexpr (D >= 4) WK::template move<2, 3>(U, Bs, Ks, sbase, 0);
       } else {
-        if constexpr (D >= 4) WK::template move<3, 2>(U, Bb, Bp, Kp, sbase, 0);
-        WK::template move<2, 1>(U, Bb, Bp, Kp, sbase, 0);
-        WK::template move<1, 0>(U, Bb, Bp, Kp, sbase, 0);
+        if constexpr (D >= 4) WK::template move<3, 2>(U, Bs, Ks, sbase, 0);
+        WK::template move<2, 1>(U, Bs, Ks, sbase, 0);
+        WK::template move<1, 0>(U, Bs, Ks, sbase, 0);
       }
     }
 #pragma unroll
@@ -210,16 +245,16 @@ walk_ldu8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const in
   if (lane == 0 && key) atomicMax(p.key, key);
 }
 
-__global__ void build_ldu8_kernel(const int32_t* M, int r, int c, int NW, int k, int s, uint32_t* tab,
+__global__ void build_ldu8_kernel(const int32_t* M, int r, int c, int NW, int k, int s, int pr, uint32_t* tab,
                                   int32_t* init) {
-  const int RW = lu_pad4(NW), RD = 2 * RW, CW = 4 * NW, sw = s - 1;
+  const int RW = lu_pad4(NW), RD = 2 * RW, CW = 4 * NW, sw = s - pr, NS = 1 << pr;
   auto pack = [](const int32_t* v) {
     uint32_t w = 0;
     for (int e = 0; e < 4; ++e) w += (uint32_t)v[e] << (8 * e);   // sum_e 256^e v_e (mod 2^32)
     return w;
   };
-  for (int rec = threadIdx.x; rec < sw; rec += blockDim.x) {      // walked digit rec <-> row r-2-rec
-    const int32_t* row = M + (int64_t)(r - 2 - rec) * c;
+  for (int rec = threadIdx.x; rec < sw; rec += blockDim.x) {      // walked digit rec <-> row r-1-pr-rec
+    const int32_t* row = M + (int64_t)(r - 1 - pr - rec) * c;
     for (int i = 0; i < RW; ++i) {
       int32_t vp[4], vn[4];
       for (int e = 0; e < 4; ++e) {
@@ -241,66 +276,82 @@ __global__ void build_ldu8_kernel(const int32_t* M, int r, int c, int NW, int k,
       for (int x = 0; x < r; ++x) {
         const int32_t v = M[(int64_t)x * c + y];
         N += min(v, 0);
-        if (x > k && x < r - 1) b += v;
+        if (x > k && x < r - pr) b += v;
       }
     init[(k + 1) * CW + y] = b;
     init[(k + 2) * CW + y] = -N;
   }
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < NS) {
+    const int m = threadIdx.x;                   // bias set: paired rows in bitmask m
     uint32_t* bias = reinterpret_cast<uint32_t*>(init + (k + 3) * CW);
     int32_t kap = 0;
     for (int i = 0; i < NW; ++i) {
-      uint32_t wb = 0, wp = 0;
+      uint32_t w = 0;
       for (int e = 0; e < 4; ++e) {
         const int y = 4 * i + e;
-        int32_t N = 0, rho = 0;
+        int32_t cb = 0;
         if (y < c) {
+          int32_t N = 0, add = 0;
           for (int x = 0; x < r; ++x) N += min(M[(int64_t)x * c + y], 0);
-          rho = M[(int64_t)(r - 1) * c + y];
+          for (int b = 0; b < pr; ++b)
+            if ((m >> b) & 1) add += M[(int64_t)(r - 1 - b) * c + y];
+          cb = -N - add;
         }
-        const int32_t cb = -N, cp = -N - rho;
-        const int32_t bp = min(max(cp, 0), 255);
-        kap += abs(cp - bp);
-        wb |= (uint32_t)(cb & 0xFF) << (8 * e);
-        wp |= (uint32_t)bp << (8 * e);
+        const int32_t bb = min(max(cb, 0), 255);
+        kap += abs(cb - bb);
+        w |= (uint32_t)bb << (8 * e);
       }
-      bias[i] = wb;
-      bias[NW + i] = wp;
+      bias[m * NW + i] = w;
     }
-    bias[2 * NW] = (uint32_t)kap;
+    bias[NS * NW + m] = (uint32_t)kap;
   }
 }
 
 #ifndef LN_LDU8_PMAX
 #define LN_LDU8_PMAX 4
 #endif
-template <int D, int NW>
-constexpr int ldu8_units_per_lane() { return D * NW <= 24 ? LN_LDU8_PMAX : (D * NW <= 48 ? (LN_LDU8_PMAX < 2 ? LN_LDU8_PMAX : 2) : 1); }
+// units per lane: the row quad loaded once per move is shared by P units (fewer when the
+// per-unit bytes and the 2^PR bias sets would not fit the register budget)
+template <int D, int NW, int PR>
+constexpr int ldu8_units_per_lane() {
+  return D * NW * (PR == 2 ? 2 : 1) <= 24 ? LN_LDU8_PMAX : (D * NW <= 48 ? (LN_LDU8_PMAX < 2 ? LN_LDU8_PMAX : 2) : 1);
+}
 
-size_t ldu8_smem(int NW, int s) { return sizeof(uint32_t) * (size_t)((s - 1) * 2 * lu_pad4(NW)); }
+// paired rows for a unit of s suffix digits (at least one walked digit stays)
+int ldu8_rows(int s) { return s >= LN_LDU8_ROWS + 1 ? LN_LDU8_ROWS : 1; }
 
-template <int D, int NW>
-cudaError_t launch_lu(const WalkParams& p, const uint32_t* tab, const int32_t* init, int grid, cudaStream_t st) {
-  constexpr int P = ldu8_units_per_lane<D, NW>();
+size_t ldu8_smem(int NW, int s) { return sizeof(uint32_t) * (size_t)((s - ldu8_rows(s)) * 2 * lu_pad4(NW)); }
+
+template <int D, int NW, int PR>
+cudaError_t launch_lu_pr(const WalkParams& p, const uint32_t* tab, const int32_t* init, int grid, cudaStream_t st) {
+  constexpr int P = ldu8_units_per_lane<D, NW, PR>();
   const size_t sm = ldu8_smem(NW, p.s);
-  cudaError_t e = cudaFuncSetAttribute(walk_ldu8_kernel<D, NW, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  cudaError_t e = cudaFuncSetAttribute(walk_ldu8_kernel<D, NW, P, PR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
-  walk_ldu8_kernel<D, NW, P><<<grid, kBlockLU, sm, st>>>(p, tab, init);
+  walk_ldu8_kernel<D, NW, P, PR><<<grid, kBlockLU, sm, st>>>(p, tab, init);
   return cudaGetLastError();
 }
 
 template <int D, int NW>
-int occ_lu(int s) {
-  constexpr int P = ldu8_units_per_lane<D, NW>();
+cudaError_t launch_lu(const WalkParams& p, const uint32_t* tab, const int32_t* init, int grid, cudaStream_t st) {
+  return ldu8_rows(p.s) == 2 ? launch_lu_pr<D, NW, 2>(p, tab, init, grid, st) : launch_lu_pr<D, NW, 1>(p, tab, init, grid, st);
+}
+
+template <int D, int NW, int PR>
+int occ_lu_pr(int s) {
+  constexpr int P = ldu8_units_per_lane<D, NW, PR>();
   const size_t sm = ldu8_smem(NW, s);
-  cudaFuncSetAttribute(walk_ldu8_kernel<D, NW, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   int nb = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, walk_ldu8_kernel<D, NW, P>, kBlockLU, sm);
+  cudaFuncSetAttribute(walk_ldu8_kernel<D, NW, P, PR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, walk_ldu8_kernel<D, NW, P, PR>, kBlockLU, sm);
   return nb;
 }
 
 template <int D, int NW>
-int upl_lu() { return ldu8_units_per_lane<D, NW>(); }
+int occ_lu(int s) { return ldu8_rows(s) == 2 ? occ_lu_pr<D, NW, 2>(s) : occ_lu_pr<D, NW, 1>(s); }
+
+template <int D, int NW>
+int upl_lu(int s) { return ldu8_rows(s) == 2 ? ldu8_units_per_lane<D, NW, 2>() : ldu8_units_per_lane<D, NW, 1>(); }
 
 #define LN_LDU8_SWITCH(D, NW_, FN, ...)                                                      \
   switch (NW_) {                                                                             \
@@ -324,10 +375,10 @@ bool walk_ldu8_supported(int d, int c, int s) {
   return (s - 1) * 2 * lu_pad4(NW) <= kTabWordsLU;
 }
 
-int walk_ldu8_units_per_lane(int d, int c) {
+int walk_ldu8_units_per_lane(int d, int c, int s) {
   const int NW = words_of(c);
-  if (d == 3) { LN_LDU8_SWITCH(3, NW, upl_lu) }
-  if (d == 4) { LN_LDU8_SWITCH(4, NW, upl_lu) }
+  if (d == 3) { LN_LDU8_SWITCH(3, NW, upl_lu, s) }
+  if (d == 4) { LN_LDU8_SWITCH(4, NW, upl_lu, s) }
   return 1;
 }
 
@@ -343,9 +394,10 @@ cudaError_t walk_ldu8_launch(const WalkParams& p, int32_t* scratch_tab, int32_t*
                              cudaStream_t st, int* block_out) {
   *block_out = kBlockLU;
   const int NW = words_of(p.c);
-  if ((p.s - 1) * 2 * lu_pad4(NW) > kTabWordsLU || (p.k + 3) * 4 * NW + 2 * NW + 1 > 16384) return cudaErrorInvalidValue;
+  const int pr = ldu8_rows(p.s);
+  if ((p.s - pr) * 2 * lu_pad4(NW) > kTabWordsLU || (p.k + 3) * 4 * NW + (NW + 1) * (1 << pr) > 16384) return cudaErrorInvalidValue;
   uint32_t* tab = reinterpret_cast<uint32_t*>(scratch_tab);
-  build_ldu8_kernel<<<1, 128, 0, st>>>(p.M, p.r, p.c, NW, p.k, p.s, tab, scratch_init);
+  build_ldu8_kernel<<<1, 128, 0, st>>>(p.M, p.r, p.c, NW, p.k, p.s, pr, tab, scratch_init);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   if (p.d == 3) { LN_LDU8_SWITCH(3, NW, launch_lu, p, tab, scratch_init, grid, st) }
