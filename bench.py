@@ -294,7 +294,12 @@ def main():
                                         f"measured 127, profiles/r01/peaks_b4.jsonl) x {({4: '4 u8 bytes x ', 2: '2 s16 halves x ', 1: ''})[simd]}"
                                         f"{nsm} SMs x {peak_mhz:.0f} MHz; algorithmic work = 2 ops per column update"),
                          "kernel_variant": st["variant"],
-                         "frac_at_measured_clock": (achieved_ops / (peak * (c["sm_mhz"] or peak_mhz) / peak_mhz)) if c["sm_mhz"] else None},
+                         "frac_at_measured_clock": (achieved_ops / (peak * (c["sm_mhz"] or peak_mhz) / peak_mhz)) if c["sm_mhz"] else None,
+                         "note": ("algorithmic work counts 2 ops per column update of a plain walk (SURVEY 8(d)); "
+                                  "frac > 1 means the kernel's row pairing (last rows evaluated for all labels per "
+                                  "walked word) needs fewer instructions per strategy than that count"
+                                  if achieved_ops > peak else
+                                  "algorithmic work counts 2 ops per column update of a plain walk (SURVEY 8(d))")},
             "clocks": c,
             "stats": st,
         }

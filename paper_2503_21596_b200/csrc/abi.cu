@@ -189,6 +189,9 @@ struct Plan {
   int k = 0, s = 0;
   int64_t units = 1;
   std::vector<uint64_t> table;   // packed prefixes (RGS for d >= 3, explicit for hooks); empty = arithmetic
+  // RGS plans: the process-wide immutable prefix list for (k, d), shared instead of copied
+  std::shared_ptr<const std::vector<uint64_t>> shared;
+  const std::vector<uint64_t>& prefixes() const { return shared ? *shared : table; }
 };
 
 constexpr int64_t kNominalLanes = 148LL * 1024;   // plan is hardware-independent => identical on every rank
@@ -306,9 +309,9 @@ int make_plan(const Problem& pr, int world, Plan* pl, int64_t target_override = 
         cache[{k, d}] = v;
         tab = v;
       }
-      p.table = *tab;
+      p.shared = tab;
     }
-    p.units = (int64_t)p.table.size();
+    p.units = (int64_t)p.shared->size();
     p.kernel = kern;
     if (kern == K_LDU8 && !walk_ldu8_supported(d, pr.c, p.s)) kern = p.kernel = K_LDPAIR16;
     if (kern == K_LDPAIR16 && !walk_ldpair16_supported(d, pr.c, p.s)) p.kernel = pr.fits16 && walk_ld16_supported(d, pr.c, p.s) ? K_LD16 : K_LD;
@@ -398,6 +401,7 @@ struct DevCtx {
   int32_t* dInit = nullptr;
   unsigned long long* dCtl = nullptr;
   uint64_t* dPre = nullptr; size_t capPre = 0;
+  const void* preSrc = nullptr;     // host list dPre currently mirrors (immutable RGS lists only)
   int64_t* dRes = nullptr;          // [0] value, then int8 argmax[kMaxCols]
   int64_t* dUnit = nullptr; size_t capUnit = 0;
   int32_t* dRed = nullptr; size_t capRed = 0;      // reduction scratch + reduced matrix + maps
@@ -552,16 +556,21 @@ int run_device(DevCtx& cx, const int32_t* dIn, const Problem& pr, int rank, int 
   if (rc) return rc;
   cudaStream_t s = cx.stream;
   if ((rc = grow(&cx.dM, &cx.capM, (size_t)pr.n * pr.m))) return rc;
-  if (!pl.table.empty()) {
-    if ((rc = grow(&cx.dPre, &cx.capPre, pl.table.size()))) return rc;
+  const std::vector<uint64_t>& ptab = pl.prefixes();
+  if (!ptab.empty() && cx.preSrc != (const void*)&ptab) {
+    cx.preSrc = nullptr;
+    if ((rc = grow(&cx.dPre, &cx.capPre, ptab.size()))) return rc;
   }
   CU(cudaEventRecord(cx.ev[0], s));
   int launches = 0;
   orient_kernel<<<std::min(1024, (pr.n * pr.m + 255) / 256), 256, 0, s>>>(dIn, pr.n, pr.m, pr.transposed ? 1 : 0, cx.dM);
   ++launches;
   CU(cudaGetLastError());
-  if (!pl.table.empty())
-    CU(cudaMemcpyAsync(cx.dPre, pl.table.data(), sizeof(uint64_t) * pl.table.size(), cudaMemcpyHostToDevice, s));
+  if (!ptab.empty() && cx.preSrc != (const void*)&ptab) {
+    // the RGS list for (k, d) is immutable and lives for the process: upload it once per device
+    CU(cudaMemcpyAsync(cx.dPre, ptab.data(), sizeof(uint64_t) * ptab.size(), cudaMemcpyHostToDevice, s));
+    if (pl.shared) cx.preSrc = (const void*)&ptab;
+  }
   init_ctl_kernel<<<1, 1, 0, s>>>(cx.dCtl);
   ++launches;
   // Algorithm 1 over the unit list: rank slice [lo, hi]
@@ -587,7 +596,7 @@ int run_device(DevCtx& cx, const int32_t* dIn, const Problem& pr, int rank, int 
       const int64_t c0 = cs.next_unit, c1 = std::min<int64_t>(pl.units, c0 + chunk);
       wp.unit_begin = c0; wp.unit_count = c1 - c0;
       walk_params_single(wp);
-      wp.prefix_table = pl.table.empty() ? nullptr : cx.dPre + c0;
+      wp.prefix_table = ptab.empty() ? nullptr : cx.dPre + c0;
       if (pl.kernel == K_GEN) CU(cudaMemsetAsync(cx.dCtl, 0, sizeof(unsigned long long), s));
       if ((rc = launch_walk(cx, pr, pl, wp, &grid, &block))) return rc;
       launches += pl.kernel == K_GEN ? 1 : 2;
@@ -622,7 +631,7 @@ int run_device(DevCtx& cx, const int32_t* dIn, const Problem& pr, int rank, int 
     }
     wp.unit_begin = lo; wp.unit_count = cnt;
     walk_params_single(wp);
-    wp.prefix_table = pl.table.empty() ? nullptr : cx.dPre + lo;
+    wp.prefix_table = ptab.empty() ? nullptr : cx.dPre + lo;
     if (cnt > 0) {
       if (sl > 0 && pl.kernel == K_GEN) {   // the generic kernel's work counter restarts per slice
         CU(cudaMemsetAsync(cx.dCtl, 0, sizeof(unsigned long long), s));
@@ -643,7 +652,7 @@ int run_device(DevCtx& cx, const int32_t* dIn, const Problem& pr, int rank, int 
   WalkParams rp = wp;
   rp.unit_begin = 0; rp.unit_count = pl.units;
   walk_params_single(rp);
-  rp.prefix_table = pl.table.empty() ? nullptr : cx.dPre;
+  rp.prefix_table = ptab.empty() ? nullptr : cx.dPre;
   if (recover_launch(rp, cx.dCtl + 2, s) != cudaSuccess) { (void)cudaGetLastError(); return LNORM_ECUDA; }
   ++launches;
   FinalizeArgs fa;
@@ -1118,6 +1127,7 @@ int lnorm_prefix_maxima(const int32_t* M, int32_t n, int32_t m, int32_t d, int32
   if ((rc = grow(&cx->dUnit, &cx->capUnit, (size_t)count))) return rc;
   cudaStream_t s = cx->stream;
   CU(cudaMemcpyAsync(cx->dM, M, sizeof(int32_t) * n * m, cudaMemcpyHostToDevice, s));
+  cx->preSrc = nullptr;
   CU(cudaMemcpyAsync(cx->dPre, pl.table.data(), sizeof(uint64_t) * count, cudaMemcpyHostToDevice, s));
   init_ctl_kernel<<<1, 1, 0, s>>>(cx->dCtl);
   WalkParams wp{};
@@ -1174,6 +1184,7 @@ int lnorm_walk_trace(const int32_t* M, int32_t n, int32_t m, int32_t d, int32_t 
   if ((rc = grow(&cx->dUnit, &cx->capUnit, (size_t)nw + (size_t)(nw * n + 7) / 8))) return rc;
   cudaStream_t s = cx->stream;
   CU(cudaMemcpyAsync(cx->dM, M, sizeof(int32_t) * n * m, cudaMemcpyHostToDevice, s));
+  cx->preSrc = nullptr;
   CU(cudaMemcpyAsync(cx->dPre, &w, sizeof(uint64_t), cudaMemcpyHostToDevice, s));
   WalkParams wp{};
   wp.M = cx->dM; wp.r = n; wp.c = m; wp.mode = pr.mode; wp.d = base; wp.k = nfixed - 1; wp.s = s_;
