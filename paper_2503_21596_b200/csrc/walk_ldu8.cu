@@ -60,19 +60,49 @@ struct LdU8 {
     else return max(__vimax3_s32(v[0], v[1], v[2]), v[3]);
   }
   // best paired-row extension of the current word, relative to S
+  // max over a != b of X[a] + Y[b]
+  static __device__ __forceinline__ int32_t pairmax(const int32_t (&X)[D], const int32_t (&Y)[D]) {
+    int32_t m[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      int32_t o;
+      if constexpr (D == 3) o = max(Y[(a + 1) % 3], Y[(a + 2) % 3]);
+      else o = __vimax3_s32(Y[(a + 1) % 4], Y[(a + 2) % 4], Y[(a + 3) % 4]);
+      m[a] = X[a] + o;
+    }
+    return max_of(m);
+  }
+  // max over pairwise distinct a, b, c of X[a] + Y[b] + Z[c]
+  static __device__ __forceinline__ int32_t triplemax(const int32_t (&X)[D], const int32_t (&Y)[D], const int32_t (&Z)[D]) {
+    int32_t m[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      int32_t o;
+      if constexpr (D == 3) {
+        const int b = (a + 1) % 3, c = (a + 2) % 3;
+        o = max(Y[b] + Z[c], Y[c] + Z[b]);
+      } else {
+        const int b = (a + 1) % 4, c = (a + 2) % 4, e = (a + 3) % 4;
+        o = __vimax3_s32(Y[b] + max(Z[c], Z[e]), Y[c] + max(Z[b], Z[e]), Y[e] + max(Z[b], Z[c]));
+      }
+      m[a] = X[a] + o;
+    }
+    return max_of(m);
+  }
+  // best paired-row extension of the current word, relative to S.  E[m - 1] serves the
+  // subset m of paired rows (bit 0 = row r-1, bit 1 = row r-2, bit 2 = row r-3); the
+  // labellings of the paired rows are the set partitions of them into distinct groups.
   static __device__ __forceinline__ int32_t ext(const Unit& U) {
     if constexpr (PR == 1) {
       return max_of(U.E[0]);
+    } else if constexpr (PR == 2) {
+      return max(pairmax(U.E[0], U.E[1]), max_of(U.E[2]));
     } else {
-      int32_t m[D];
-#pragma unroll
-      for (int a = 0; a < D; ++a) {
-        int32_t o = INT32_MIN;
-        if constexpr (D == 3) o = max(U.E[1][(a + 1) % 3], U.E[1][(a + 2) % 3]);
-        else o = __vimax3_s32(U.E[1][(a + 1) % 4], U.E[1][(a + 2) % 4], U.E[1][(a + 3) % 4]);
-        m[a] = U.E[0][a] + o;
-      }
-      return max(max_of(m), max_of(U.E[2]));
+      const int32_t t1 = triplemax(U.E[0], U.E[1], U.E[3]);          // {1}{2}{3}
+      const int32_t t2 = __vimax3_s32(pairmax(U.E[2], U.E[3]),       // {12}{3}
+                                      pairmax(U.E[4], U.E[1]),       // {13}{2}
+                                      pairmax(U.E[5], U.E[0]));      // {23}{1}
+      return __vimax3_s32(t1, t2, max_of(U.E[6]));                  // {123}
     }
   }
   static __device__ __forceinline__ void refresh(Unit& U, int g, const uint32_t (&h)[NS]) {
@@ -135,13 +165,13 @@ struct LdU8 {
 };
 
 #ifndef LN_LDU8_ROWS
-#define LN_LDU8_ROWS 2
+#define LN_LDU8_ROWS 3
 #endif
 
 // Init records (global int32, stride CW = 4 NW): prefix rows 0..k, the base (walked
 // rows at label 0), -N_y, then the packed bias words of the NS sets and their K_m.
 template <int D, int NW, int P, int PR>
-__global__ void __launch_bounds__(kBlockLU, (D * NW * P * (PR == 2 ? 2 : 1) <= 72 ? LN_LDU8_MINB : 1))
+__global__ void __launch_bounds__(kBlockLU, (D * NW * P * (PR >= 2 ? PR : 1) <= 72 ? LN_LDU8_MINB : 1))
 walk_ldu8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int32_t* __restrict__ gInit) {
   using WK = LdU8<D, NW, P, PR>;
   constexpr int RD = WK::RD, CW = 4 * NW, NS = WK::NS;
@@ -314,11 +344,12 @@ __global__ void build_ldu8_kernel(const int32_t* M, int r, int c, int NW, int k,
 // per-unit bytes and the 2^PR bias sets would not fit the register budget)
 template <int D, int NW, int PR>
 constexpr int ldu8_units_per_lane() {
-  return D * NW * (PR == 2 ? 2 : 1) <= 24 ? LN_LDU8_PMAX : (D * NW <= 48 ? (LN_LDU8_PMAX < 2 ? LN_LDU8_PMAX : 2) : 1);
+  return PR == 3 ? (D * NW <= 12 ? 2 : 1)
+       : D * NW * (PR == 2 ? 2 : 1) <= 24 ? LN_LDU8_PMAX : (D * NW <= 48 ? (LN_LDU8_PMAX < 2 ? LN_LDU8_PMAX : 2) : 1);
 }
 
 // paired rows for a unit of s suffix digits (at least one walked digit stays)
-int ldu8_rows(int s) { return s >= LN_LDU8_ROWS + 1 ? LN_LDU8_ROWS : 1; }
+int ldu8_rows(int s) { return s >= LN_LDU8_ROWS + 1 ? LN_LDU8_ROWS : (s >= 3 ? 2 : 1); }
 
 size_t ldu8_smem(int NW, int s) { return sizeof(uint32_t) * (size_t)((s - ldu8_rows(s)) * 2 * lu_pad4(NW)); }
 
@@ -334,7 +365,13 @@ cudaError_t launch_lu_pr(const WalkParams& p, const uint32_t* tab, const int32_t
 
 template <int D, int NW>
 cudaError_t launch_lu(const WalkParams& p, const uint32_t* tab, const int32_t* init, int grid, cudaStream_t st) {
-  return ldu8_rows(p.s) == 2 ? launch_lu_pr<D, NW, 2>(p, tab, init, grid, st) : launch_lu_pr<D, NW, 1>(p, tab, init, grid, st);
+  switch (ldu8_rows(p.s)) {
+#if LN_LDU8_ROWS >= 3
+    case 3: return launch_lu_pr<D, NW, 3>(p, tab, init, grid, st);
+#endif
+    case 2: return launch_lu_pr<D, NW, 2>(p, tab, init, grid, st);
+    default: return launch_lu_pr<D, NW, 1>(p, tab, init, grid, st);
+  }
 }
 
 template <int D, int NW, int PR>
@@ -348,10 +385,26 @@ int occ_lu_pr(int s) {
 }
 
 template <int D, int NW>
-int occ_lu(int s) { return ldu8_rows(s) == 2 ? occ_lu_pr<D, NW, 2>(s) : occ_lu_pr<D, NW, 1>(s); }
+int occ_lu(int s) {
+  switch (ldu8_rows(s)) {
+#if LN_LDU8_ROWS >= 3
+    case 3: return occ_lu_pr<D, NW, 3>(s);
+#endif
+    case 2: return occ_lu_pr<D, NW, 2>(s);
+    default: return occ_lu_pr<D, NW, 1>(s);
+  }
+}
 
 template <int D, int NW>
-int upl_lu(int s) { return ldu8_rows(s) == 2 ? ldu8_units_per_lane<D, NW, 2>() : ldu8_units_per_lane<D, NW, 1>(); }
+int upl_lu(int s) {
+  switch (ldu8_rows(s)) {
+#if LN_LDU8_ROWS >= 3
+    case 3: return ldu8_units_per_lane<D, NW, 3>();
+#endif
+    case 2: return ldu8_units_per_lane<D, NW, 2>();
+    default: return ldu8_units_per_lane<D, NW, 1>();
+  }
+}
 
 #define LN_LDU8_SWITCH(D, NW_, FN, ...)                                                      \
   switch (NW_) {                                                                             \
