@@ -201,14 +201,14 @@ cudaError_t recover_launch(const WalkParams& p, unsigned long long* lex_out, cud
   size_t sm = gen_smem(nG, p.c, kGenWarps);
   cudaError_t e = cudaFuncSetAttribute(recover_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
-  // enough warps to split even a 2^20-word unit into ~1k-word chunks
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  // blocks per matrix: enough warps for ~1k-word chunks, at most 2 per SM
+  // blocks per matrix: enough warps for ~64-word chunks (a d-ary step of this generic
+  // walk costs ~1k cycles: runtime-d digit arithmetic + a full re-evaluation), at most 4 per SM
   uint64_t words = 1;
   for (int i = 0; i < p.s; ++i) words *= (uint64_t)(p.mode == MODE_LD ? p.d : 2);
-  int gx = (int)std::min<uint64_t>((uint64_t)nsm * 2, std::max<uint64_t>(1, words / (1024ull * kGenWarps)));
+  int gx = (int)std::min<uint64_t>((uint64_t)nsm * 4, std::max<uint64_t>(1, words / (64ull * kGenWarps)));
   if (p.batch > 1) gx = std::max(1, std::min(gx, (nsm * 8 + p.batch - 1) / p.batch));
   recover_kernel<<<dim3(gx, p.batch > 0 ? p.batch : 1), 32 * kGenWarps, sm, st>>>(p, lex_out);
   return cudaGetLastError();
