@@ -234,6 +234,27 @@ def test_sampled_prefixes_ungrouped(lib, d, marg):
         assert got[i] == oracle.prefix_max(M, P[i], d=d, with_marginals=marg)[0]
 
 
+@pytest.mark.parametrize("d", [3, 4])
+@pytest.mark.parametrize("s", [2, 3, 4, 6])
+def test_ldu8_paired_rows_every_suffix_length(lib, d, s):
+    """The byte d-ary walk pairs the last 1, 2 or 3 rows depending on the suffix length
+    (s = 2, 3, >= 4): per-prefix maxima for every case against the oracle, and the value
+    of the full search (whose planner picks its own split)."""
+    n, m = 11, 13
+    M = synth.random_matrix(n, m, 64_000 + 10 * d + s)
+    nfixed = n - s
+    g = synth.SplitMix64(640 + s)
+    P = np.zeros((40, nfixed), dtype=np.int8)
+    for i in range(40):
+        for x in range(1, nfixed):
+            P[i, x] = g.next() % d
+    got = lib.prefix_maxima(M, P, d=d)
+    assert lib.last_stats()["variant"] == 8
+    for i in range(40):
+        assert got[i] == oracle.prefix_max(M, P[i], d=d)[0], (i, list(P[i]))
+    check(lib, M, d=d)
+
+
 def test_bench_configs_plan_the_byte_kernel(lib):
     """The 42x42 L_1 and 40x40 L_marg bench workloads run the byte-packed kernel."""
     assert lib.plan(synth.random_matrix(42, 42, 2))["variant_name"] == "bin_u8"
