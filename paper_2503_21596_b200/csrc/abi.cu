@@ -483,7 +483,7 @@ int launch_walk(DevCtx& cx, const Problem& pr, const Plan& pl, WalkParams& wp, i
   if (pl.kernel == K_BIN16) per_block *= walk_bin16_units_per_lane(pr.mode, pr.c);
   if (pl.kernel == K_LD16) per_block *= walk_ld16_units_per_lane(pr.dl, pr.c);
   if (pl.kernel == K_PAIR16) per_block *= walk_pair16_units_per_lane(pr.mode, pr.c);
-  if (pl.kernel == K_U8) per_block *= walk_u8_units_per_lane(pr.mode, pr.c);
+  if (pl.kernel == K_U8) per_block = per_block * walk_u8_units_per_lane(pr.mode, pr.c) / walk_u8_lanes_per_unit(pr.mode, pr.c);
   if (pl.kernel == K_LDPAIR16) per_block *= walk_ldpair16_units_per_lane(pr.dl, pr.c);
   if (pl.kernel == K_LDU8) per_block *= walk_ldu8_units_per_lane(pr.dl, pr.c, pl.s);
   int64_t want = (wp.unit_count + per_block - 1) / per_block;

@@ -158,6 +158,8 @@ template <int MODE> cudaError_t walk_u8_launch_mode(const WalkParams& p, int32_t
                                                     int grid, cudaStream_t st);
 template <int MODE> int walk_u8_occupancy_mode(int c, int s);
 template <int MODE> int walk_u8_units_per_lane_mode(int c);
+template <int MODE> int walk_u8_lanes_per_unit_mode(int c);
+int walk_u8_lanes_per_unit(int mode, int c);
 template <int MODE> int walk_u8_unroll_mode(int c);
 // Byte-packed d-ary walk, last row paired (L_d, d in {3,4}; guard: every column's
 // sum_x |M_xy| <= 255, checked by the caller).

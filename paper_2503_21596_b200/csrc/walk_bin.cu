@@ -105,8 +105,14 @@ bool walk_u8_supported(int mode, int c, int s) {
   else if (mode == MODE_MARG) { NW = walk_u8_words_mode<MODE_MARG>(c); if (NW) K = walk_u8_unroll_mode<MODE_MARG>(c); }
   else if (mode == MODE_LD) { NW = walk_u8_words_mode<MODE_LD>(c); if (NW) K = walk_u8_unroll_mode<MODE_LD>(c); }
   if (NW == 0 || s < K + 1 || s > 31) return false;    // K unrolled digits + the paired last row
-  const int RW = (NW + 3) & ~3;
+  const int RW = 2 * (((NW + 1) / 2 + 3) & ~3);         // record words incl. lane-pair slice padding
   return 2 * s * RW <= 16384;     // delta table staged in shared memory (dTab holds 32768 words)
+}
+
+int walk_u8_lanes_per_unit(int mode, int c) {
+  if (mode == MODE_L1) return walk_u8_lanes_per_unit_mode<MODE_L1>(c);
+  if (mode == MODE_MARG) return walk_u8_lanes_per_unit_mode<MODE_MARG>(c);
+  return walk_u8_lanes_per_unit_mode<MODE_LD>(c);
 }
 
 int walk_u8_units_per_lane(int mode, int c) {

@@ -80,12 +80,25 @@ struct U8Layout {
 #endif
 
 // units per lane: the row quad loaded once per step is shared by P units
-template <int MODE, int NW>
 #ifndef LN_U8_PWIDE
 #define LN_U8_PWIDE 1
 #endif
+// Lanes per unit (experiment knob, off by default): wide L_1 / L_marg rows (more than 128
+// columns) split over a lane PAIR (each lane holds half of the words of the same units; the
+// two partial sums of a strategy are combined with one SHFL), so a lane keeps two units
+// sharing one bias set instead of one unit with its own.  Measured +7-9 % on 144-190 columns,
+// but the second unit adds a prefix row to the byte window, which pushed the 48x192 config
+// past the guard (k > 31) onto the 16-bit kernel; a planner choice between both instances
+// would be needed to enable it.
+#ifndef LN_U8_LPU2
+#define LN_U8_LPU2 0
+#endif
+template <int MODE, int NW>
+__host__ __device__ constexpr int u8_lpu() { return (U8Layout<MODE, NW>::G == 1 && NW > 32 && LN_U8_LPU2 && LN_U8_PAIR) ? 2 : 1; }
+template <int MODE, int NW>
 __host__ __device__ constexpr int u8_units_per_lane() {
-  return U8Layout<MODE, NW>::G * NW <= 16 ? LN_U8_P
+  return u8_lpu<MODE, NW>() == 2 ? (NW / 2 <= 8 ? 4 : 2)
+       : U8Layout<MODE, NW>::G * NW <= 16 ? LN_U8_P
        : (U8Layout<MODE, NW>::G * NW <= 32 ? 2 : (U8Layout<MODE, NW>::G == 1 ? LN_U8_PWIDE : 1));
 }
 
@@ -114,8 +127,10 @@ __host__ __device__ constexpr int u8_unroll() {
        : u8_step_instr<MODE, NW, P>() * 4 <= LN_U8_BUDGET ? 2 : 1;
 }
 
-template <int MODE, int NW, int P>
+template <int MODE, int NW, int P, int LPU = 1>
 struct U8Step {
+  // NW here = the words THIS lane holds (half of the unit's words when LPU = 2)
+  static_assert(LPU == 1 || LN_U8_PAIR, "lane pairs need the paired epilogue");
   static constexpr int G = U8Layout<MODE, NW>::G, RW = U8Layout<MODE, NW>::RW;
   static constexpr int NB = (1 + LN_U8_PAIR) * G * NW;   // bias words: B (G*NW) [, B' (G*NW)]
   // One Gray step: add the packed delta record at sbase + off to every unit's bytes,
@@ -163,8 +178,12 @@ struct U8Step {
     if (LN_U8_PAIR) {
 #pragma unroll
       for (int j = 0; j < P; ++j) {
-        const int32_t va = (G == 2) ? (int32_t)(a0[j] + a1[j]) : (int32_t)a0[j];
-        const int32_t vb = (G == 2) ? (int32_t)(b0[j] + b1[j]) : (int32_t)b0[j];
+        int32_t va = (G == 2) ? (int32_t)(a0[j] + a1[j]) : (int32_t)a0[j];
+        int32_t vb = (G == 2) ? (int32_t)(b0[j] + b1[j]) : (int32_t)b0[j];
+        if (LPU == 2) {                          // the partner lane holds the other half of the words
+          va += __shfl_xor_sync(0xffffffffu, va, 1);
+          vb += __shfl_xor_sync(0xffffffffu, vb, 1);
+        }
         best[j] = __vimax3_s32(best[j], va, vb);
       }
     } else if (G == 1 && (NW == 1 || LN_U8_CHAINS == 1)) {
@@ -200,10 +219,11 @@ struct U8Step {
 #define LN_U8_MINB_MID 14
 #endif
 template <int MODE, int NW, int P>
-__host__ __device__ constexpr int u8_foot() { return U8Layout<MODE, NW>::G * NW * (P + 1 + LN_U8_PAIR); }
+__host__ __device__ constexpr int u8_foot() { return U8Layout<MODE, NW>::G * (NW / u8_lpu<MODE, NW>()) * (P + 1 + LN_U8_PAIR); }
 template <int MODE, int NW, int P>
 __host__ __device__ constexpr int u8_min_blocks() {
-  return (U8Layout<MODE, NW>::G == 1 && u8_foot<MODE, NW, P>() <= 56) ? LN_U8_MINB
+  return u8_lpu<MODE, NW>() == 2 ? (u8_foot<MODE, NW, P>() <= 40 ? 12 : 1)
+       : (U8Layout<MODE, NW>::G == 1 && u8_foot<MODE, NW, P>() <= 56) ? LN_U8_MINB
        : (U8Layout<MODE, NW>::G == 1 && u8_foot<MODE, NW, P>() <= 70) ? LN_U8_MINB_MID
        : ((u8_foot<MODE, NW, P>() <= 96 && P >= 4) || u8_foot<MODE, NW, P>() <= 54) ? 12 : 1;
 }
@@ -212,14 +232,21 @@ template <int MODE, int NW, int P>
 __global__ void __launch_bounds__(kBlockU8, u8_min_blocks<MODE, NW, P>())
 walk_u8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int32_t* __restrict__ gInit) {
   using LY = U8Layout<MODE, NW>;
-  constexpr int G = LY::G, RW = LY::RW, CW = LY::CW;
+  constexpr int G = LY::G, CW = LY::CW;
   constexpr int LG = (P >= 8) ? 3 : (P >= 4) ? 2 : (P == 2 ? 1 : 0);
-  constexpr int K = u8_unroll<MODE, NW, P>();
-  constexpr int NB = U8Step<MODE, NW, P>::NB;
+  constexpr int LPU = u8_lpu<MODE, NW>();          // lanes per unit
+  constexpr int NWL = NW / LPU;                    // words held by one lane
+  constexpr int RWL = u8_pad4(NWL);                // its slice of a delta record (16B aligned)
+  constexpr int RREC = LPU * RWL;                  // words per delta record
+  constexpr int GPW = 32 / LPU;                    // lane groups per warp
+  constexpr int K = u8_unroll<MODE, NWL, P>();
+  using STEP = U8Step<MODE, NWL, P, LPU>;
+  constexpr int NB = STEP::NB;
   extern __shared__ __align__(16) uint32_t sT[];
   const int lane = threadIdx.x & 31;
+  const int half = (LPU == 2) ? (lane & 1) : 0, slot = lane / LPU;
   const int sw = p.s - LN_U8_PAIR;                 // walked digits (row r-1 paired, not walked)
-  const int total = 2 * sw * RW;
+  const int total = 2 * sw * RREC;
   for (int i = lane; i < total; i += 32) sT[i] = gTab[i];
   __syncwarp();
   const uint32_t nblk = 1u << (sw - K);
@@ -233,12 +260,12 @@ walk_u8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int3
   bool have = false;
   const int64_t u_end = p.unit_begin + p.unit_count;
   const int64_t g0 = p.unit_begin / P, g_end = (u_end + P - 1) / P;
-  const int64_t nchunks = (g_end - g0 + 31) / 32;
+  const int64_t nchunks = (g_end - g0 + GPW - 1) / GPW;
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sT);
   for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
-    const int64_t g = g0 + ch * 32 + lane;
+    const int64_t g = g0 + ch * GPW + slot;
     const int64_t uh = min(max(g * P, p.unit_begin), u_end - 1);   // a valid unit of the group
-    uint32_t A[P][NW];
+    uint32_t A[P][NWL];
     uint32_t B[NB];
     uint32_t Kc[2];
     int32_t best[P];
@@ -249,7 +276,8 @@ walk_u8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int3
       for (int x = 0; x <= kh; ++x) neg |= (uint64_t)(prefix_digit(p, uh, x) != 0) << x;
       int32_t kap = 0, kapb = 0;
 #pragma unroll
-      for (int q = 0; q < NW; ++q) {
+      for (int ql = 0; ql < NWL; ++ql) {
+        const int q = half * NWL + ql;             // global word of this lane's column slice
         int32_t Pv[4] = {0, 0, 0, 0};              // high prefix part of columns 4q..4q+3
         for (int x = 0; x <= kh; ++x) {
           // L_1 / L_marg: a_x = +1 (digit 0) or -1; L_2: only rows in group 0 count
@@ -288,8 +316,8 @@ walk_u8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int3
         }
 #pragma unroll
         for (int h = 0; h <= LN_U8_PAIR; ++h) {
-          B[h * G * NW + q] = w[h][0];
-          if (G == 2) B[h * G * NW + NW + q] = w[h][1];
+          B[h * G * NWL + ql] = w[h][0];
+          if (G == 2) B[h * G * NWL + NWL + ql] = w[h][1];
         }
       }
       Kc[0] = (uint32_t)kap;
@@ -303,7 +331,8 @@ walk_u8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int3
 #pragma unroll
       for (int b = 0; b < LG; ++b) lowdig[b] = prefix_digit(p, u, kh + 1 + b);
 #pragma unroll
-      for (int q = 0; q < NW; ++q) {
+      for (int ql = 0; ql < NWL; ++ql) {
+        const int q = half * NWL + ql;
         int32_t a[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) a[e] = __ldg(abRec + 4 * q + e);
@@ -314,8 +343,8 @@ walk_u8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int3
           const int4 v = __ldg(reinterpret_cast<const int4*>(gInit + (kh + 1 + b) * CW) + q);
           a[0] += f * v.x; a[1] += f * v.y; a[2] += f * v.z; a[3] += f * v.w;
         }
-        A[j][q] = (uint32_t)(a[0] & 0xFF) | ((uint32_t)(a[1] & 0xFF) << 8) | ((uint32_t)(a[2] & 0xFF) << 16) |
-                  ((uint32_t)(a[3] & 0xFF) << 24);
+        A[j][ql] = (uint32_t)(a[0] & 0xFF) | ((uint32_t)(a[1] & 0xFF) << 8) | ((uint32_t)(a[2] & 0xFF) << 16) |
+                   ((uint32_t)(a[3] & 0xFF) << 24);
       }
       // value of the unit's start word (strategy A, and B when paired)
       int32_t v0 = 0;
@@ -323,10 +352,11 @@ walk_u8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int3
       for (int h = 0; h <= LN_U8_PAIR; ++h) {
         uint32_t acc = Kc[h];
 #pragma unroll
-        for (int q = 0; q < NW; ++q) {
-          acc = sad4(A[j][q], B[h * G * NW + q], acc);
-          if (G == 2) acc = sad4(A[j][q], B[h * G * NW + NW + q], acc);
+        for (int q = 0; q < NWL; ++q) {
+          acc = sad4(A[j][q], B[h * G * NWL + q], acc);
+          if (G == 2) acc = sad4(A[j][q], B[h * G * NWL + NWL + q], acc);
         }
+        if (LPU == 2) acc += __shfl_xor_sync(0xffffffffu, acc, 1);
         v0 = h == 0 ? (int32_t)acc : max(v0, (int32_t)acc);
       }
       best[j] = v0;
@@ -337,19 +367,19 @@ walk_u8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int3
         const int tz = __ffs((int)t) - 1;
         const int b = K + tz;
         const int sg = 1 ^ (int)((t >> (tz + 1)) & 1u);
-        U8Step<MODE, NW, P>::run(A, B, Kc, best, sbase, (2 * b + sg) * RW, p.one);
+        STEP::run(A, B, Kc, best, sbase, (2 * b + sg) * RREC + half * RWL, p.one);
       }
 #pragma unroll
       for (int jj = 1; jj < (1 << K); ++jj) {
         const int b = u8_cctz(jj);
         const int sg = (b < K - 1) ? (1 ^ ((jj >> (b + 1)) & 1)) : (1 ^ (int)(t & 1u));
-        U8Step<MODE, NW, P>::run(A, B, Kc, best, sbase, (2 * b + sg) * RW, p.one);
+        STEP::run(A, B, Kc, best, sbase, (2 * b + sg) * RREC + half * RWL, p.one);
       }
     }
 #pragma unroll
     for (int j = 0; j < P; ++j) {
       const int64_t u = g * P + j;
-      if (u >= p.unit_begin && u < u_end) {
+      if (u >= p.unit_begin && u < u_end && half == 0) {
         if (p.unit_max) p.unit_max[u - p.unit_begin] = best[j];
         if (!have || best[j] > best_all) { best_all = best[j]; best_u = (uint32_t)u; have = true; }
       }
@@ -363,9 +393,10 @@ walk_u8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int3
 // Delta table (walked digit b <-> row r-1-b, sign sg = new digit value) and init
 // records; the byte window covers the last s + lg rows (lg = log2 of the lane group).
 template <int MODE>
-__global__ void build_u8_kernel(const int32_t* M, int r, int c, int NW, int k, int s, int lg, uint32_t* tab,
+__global__ void build_u8_kernel(const int32_t* M, int r, int c, int NW, int k, int s, int lg, int lpu, uint32_t* tab,
                                 int32_t* init) {
-  const int RW = u8_pad4(NW), CW = 4 * NW;
+  // a record holds lpu slices of pad4(NW / lpu) words (one per lane of a lane pair)
+  const int NWL = NW / lpu, RWL = u8_pad4(NWL), RW = lpu * RWL, CW = 4 * NW;
   const int scale = (MODE == MODE_LD) ? 1 : 2;
   const int tid = threadIdx.x;
   const int sw = s - LN_U8_PAIR;
@@ -374,10 +405,11 @@ __global__ void build_u8_kernel(const int32_t* M, int r, int c, int NW, int k, i
     const int32_t* row = M + (int64_t)(r - 1 - LN_U8_PAIR - b) * c;   // walked digit b
     const int f = sg ? -scale : scale;     // digit -> 1: a_x = -1 (m -= 2M) or group 1 (m_0 -= M)
     for (int i = 0; i < RW; ++i) {
+      const int h = i / RWL, ql = i % RWL, q = h * NWL + ql;   // slice h, word q of the row
       uint32_t w = 0;
       for (int e = 0; e < 4; ++e) {
-        const int y = 4 * i + e;
-        const int32_t v = (i < NW && y < c) ? f * row[y] : 0;
+        const int y = 4 * q + e;
+        const int32_t v = (ql < NWL && y < c) ? f * row[y] : 0;
         w += (uint32_t)v << (8 * e);       // packed signed delta sum_e 256^e delta_e (mod 2^32)
       }
       tab[rec * RW + i] = w;
@@ -404,7 +436,10 @@ __global__ void build_u8_kernel(const int32_t* M, int r, int c, int NW, int k, i
 }
 
 template <int MODE, int NW>
-size_t u8_smem(int s) { return sizeof(uint32_t) * (size_t)(2 * (s - LN_U8_PAIR) * U8Layout<MODE, NW>::RW); }
+size_t u8_smem(int s) {
+  constexpr int LPU = u8_lpu<MODE, NW>();
+  return sizeof(uint32_t) * (size_t)(2 * (s - LN_U8_PAIR) * LPU * u8_pad4(NW / LPU));
+}
 
 template <int MODE, int NW>
 cudaError_t launch_u8(const WalkParams& p, const uint32_t* tab, const int32_t* init, int grid, cudaStream_t st) {
@@ -430,7 +465,10 @@ template <int MODE, int NW>
 int upl_u8() { return u8_units_per_lane<MODE, NW>(); }
 
 template <int MODE, int NW>
-int unroll_u8() { return u8_unroll<MODE, NW, u8_units_per_lane<MODE, NW>()>(); }
+int lpu_u8() { return u8_lpu<MODE, NW>(); }
+
+template <int MODE, int NW>
+int unroll_u8() { return u8_unroll<MODE, NW / u8_lpu<MODE, NW>(), u8_units_per_lane<MODE, NW>()>(); }
 
 #ifdef LN_U8_ONLY_NW   // experiment builds (tools/build_variant.py): one instance only
 #define LN_U8_SWITCH(MODE, NW_, FN, ...)                                                             \
@@ -475,8 +513,9 @@ cudaError_t walk_u8_launch_mode<LN_BIN_MODE>(const WalkParams& p, int32_t* scrat
   if (NW == 0) return cudaErrorInvalidValue;
   uint32_t* tab = reinterpret_cast<uint32_t*>(scratch_tab);
   const int P = [&]() -> int { LN_U8_SWITCH(LN_BIN_MODE, NW, upl_u8) return 1; }();
-  build_u8_kernel<LN_BIN_MODE><<<1, 256, 0, st>>>(p.M, p.r, p.c, NW, p.k, p.s, P >= 8 ? 3 : P >= 4 ? 2 : (P == 2 ? 1 : 0), tab,
-                                                  scratch_init);
+  const int lpu = [&]() -> int { LN_U8_SWITCH(LN_BIN_MODE, NW, lpu_u8) return 1; }();
+  build_u8_kernel<LN_BIN_MODE><<<1, 256, 0, st>>>(p.M, p.r, p.c, NW, p.k, p.s, P >= 8 ? 3 : P >= 4 ? 2 : (P == 2 ? 1 : 0),
+                                                  lpu, tab, scratch_init);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   LN_U8_SWITCH(LN_BIN_MODE, NW, launch_u8, p, tab, scratch_init, grid, st)
@@ -492,6 +531,12 @@ int walk_u8_occupancy_mode<LN_BIN_MODE>(int c, int s) {
 template <>
 int walk_u8_units_per_lane_mode<LN_BIN_MODE>(int c) {
   LN_U8_SWITCH(LN_BIN_MODE, walk_u8_words_mode<LN_BIN_MODE>(c), upl_u8)
+  return 1;
+}
+
+template <>
+int walk_u8_lanes_per_unit_mode<LN_BIN_MODE>(int c) {
+  LN_U8_SWITCH(LN_BIN_MODE, walk_u8_words_mode<LN_BIN_MODE>(c), lpu_u8)
   return 1;
 }
 

@@ -122,6 +122,7 @@ HOT_SHAPES = [
     (3, False, 9, 7), (3, False, 10, 32), (3, False, 8, 13), (4, False, 7, 5), (4, False, 8, 29),
     (5, False, 6, 4), (1, False, 9, 70), (2, False, 8, 100),
     (1, True, 10, 97), (1, False, 11, 190), (1, False, 12, 128),      # wide rows (config 5a m = 4n)
+    (1, True, 12, 150), (1, False, 13, 133),                           # > 128 columns: lane pairs
 ]
 
 
