@@ -159,6 +159,7 @@ template <int MODE> cudaError_t walk_u8_launch_mode(const WalkParams& p, int32_t
 template <int MODE> int walk_u8_occupancy_mode(int c, int s);
 template <int MODE> int walk_u8_units_per_lane_mode(int c);
 template <int MODE> int walk_u8_lanes_per_unit_mode(int c);
+template <int MODE> int walk_u8_paired_rows_mode();
 int walk_u8_lanes_per_unit(int mode, int c);
 template <int MODE> int walk_u8_unroll_mode(int c);
 // Byte-packed d-ary walk, last row paired (L_d, d in {3,4}; guard: every column's

@@ -100,11 +100,11 @@ cudaError_t walk_pair16_launch(const WalkParams& p, int32_t* scratch_tab, int32_
 }
 
 bool walk_u8_supported(int mode, int c, int s) {
-  int NW = 0, K = 4;
-  if (mode == MODE_L1) { NW = walk_u8_words_mode<MODE_L1>(c); if (NW) K = walk_u8_unroll_mode<MODE_L1>(c); }
-  else if (mode == MODE_MARG) { NW = walk_u8_words_mode<MODE_MARG>(c); if (NW) K = walk_u8_unroll_mode<MODE_MARG>(c); }
-  else if (mode == MODE_LD) { NW = walk_u8_words_mode<MODE_LD>(c); if (NW) K = walk_u8_unroll_mode<MODE_LD>(c); }
-  if (NW == 0 || s < K + 1 || s > 31) return false;    // K unrolled digits + the paired last row
+  int NW = 0, K = 4, PR = 1;
+  if (mode == MODE_L1) { NW = walk_u8_words_mode<MODE_L1>(c); if (NW) K = walk_u8_unroll_mode<MODE_L1>(c); PR = walk_u8_paired_rows_mode<MODE_L1>(); }
+  else if (mode == MODE_MARG) { NW = walk_u8_words_mode<MODE_MARG>(c); if (NW) K = walk_u8_unroll_mode<MODE_MARG>(c); PR = walk_u8_paired_rows_mode<MODE_MARG>(); }
+  else if (mode == MODE_LD) { NW = walk_u8_words_mode<MODE_LD>(c); if (NW) K = walk_u8_unroll_mode<MODE_LD>(c); PR = walk_u8_paired_rows_mode<MODE_LD>(); }
+  if (NW == 0 || s < K + PR || s > 31) return false;   // K unrolled digits + the paired last rows
   const int RW = 2 * (((NW + 1) / 2 + 3) & ~3);         // record words incl. lane-pair slice padding
   return 2 * s * RW <= 16384;     // delta table staged in shared memory (dTab holds 32768 words)
 }

@@ -78,6 +78,9 @@ struct U8Layout {
 #ifndef LN_U8_PAIR
 #define LN_U8_PAIR 1
 #endif
+// paired rows per mode (L_2 holds two bias sets per strategy already: at most one row)
+template <int MODE>
+__host__ __device__ constexpr int u8_pr() { return MODE == MODE_LD ? (LN_U8_PAIR < 1 ? LN_U8_PAIR : 1) : LN_U8_PAIR; }
 
 // units per lane: the row quad loaded once per step is shared by P units
 #ifndef LN_U8_PWIDE
@@ -94,7 +97,7 @@ struct U8Layout {
 #define LN_U8_LPU2 0
 #endif
 template <int MODE, int NW>
-__host__ __device__ constexpr int u8_lpu() { return (U8Layout<MODE, NW>::G == 1 && NW > 32 && LN_U8_LPU2 && LN_U8_PAIR) ? 2 : 1; }
+__host__ __device__ constexpr int u8_lpu() { return (U8Layout<MODE, NW>::G == 1 && NW > 32 && LN_U8_LPU2 && u8_pr<MODE>() >= 1) ? 2 : 1; }
 template <int MODE, int NW>
 __host__ __device__ constexpr int u8_units_per_lane() {
   return u8_lpu<MODE, NW>() == 2 ? (NW / 2 <= 8 ? 4 : 2)
@@ -117,7 +120,7 @@ __device__ __forceinline__ uint32_t u8_add(uint32_t a, uint32_t d, uint32_t one)
 
 template <int MODE, int NW, int P>
 __host__ __device__ constexpr int u8_step_instr() {
-  return P * ((1 + LN_U8_PAIR) * U8Layout<MODE, NW>::G + 1) * NW + P + U8Layout<MODE, NW>::RW / 4;
+  return P * ((1 << u8_pr<MODE>()) * U8Layout<MODE, NW>::G + 1) * NW + P + U8Layout<MODE, NW>::RW / 4;
 }
 
 template <int MODE, int NW, int P>
@@ -130,15 +133,16 @@ __host__ __device__ constexpr int u8_unroll() {
 template <int MODE, int NW, int P, int LPU = 1>
 struct U8Step {
   // NW here = the words THIS lane holds (half of the unit's words when LPU = 2)
-  static_assert(LPU == 1 || LN_U8_PAIR, "lane pairs need the paired epilogue");
+  static constexpr int PR = u8_pr<MODE>(), NS = 1 << PR;   // paired rows, bias sets
+  static_assert(LPU == 1 || PR >= 1, "lane pairs need the paired epilogue");
   static constexpr int G = U8Layout<MODE, NW>::G, RW = U8Layout<MODE, NW>::RW;
-  static constexpr int NB = (1 + LN_U8_PAIR) * G * NW;   // bias words: B (G*NW) [, B' (G*NW)]
+  static constexpr int NB = NS * G * NW;        // bias words: set h (paired-row signs h) x group
   // One Gray step: add the packed delta record at sbase + off to every unit's bytes,
   // re-accumulate sum |a - B| (and sum |a - B'| for the paired strategy), keep the max.
   static __device__ __forceinline__ void run(uint32_t (&A)[P][NW], const uint32_t (&B)[NB],
-                                             const uint32_t (&K)[2], int32_t (&best)[P], uint32_t sbase, int off,
+                                             const uint32_t (&K)[NS], int32_t (&best)[P], uint32_t sbase, int off,
                                              uint32_t one) {
-    uint32_t a0[P], a1[P], b0[P], b1[P];
+    uint32_t a0[P], a1[P], hs[P][NS][G];
 #pragma unroll
     for (int v = 0; v < RW / 4; ++v) {
       const uint4 x4 = lds128(sbase + 4u * (uint32_t)(off + 4 * v));
@@ -150,13 +154,12 @@ struct U8Step {
 #pragma unroll
           for (int j = 0; j < P; ++j) {
             A[j][i] = u8_add(A[j][i], rq[e], one);
-            if (LN_U8_PAIR) {
-              a0[j] = sad4(A[j][i], B[i], i == 0 ? K[0] : a0[j]);
-              b0[j] = sad4(A[j][i], B[G * NW + i], i == 0 ? K[1] : b0[j]);
-              if (G == 2) {
-                a1[j] = sad4(A[j][i], B[NW + i], i == 0 ? 0u : a1[j]);
-                b1[j] = sad4(A[j][i], B[G * NW + NW + i], i == 0 ? 0u : b1[j]);
-              }
+            if (PR >= 1) {
+#pragma unroll
+              for (int h = 0; h < NS; ++h)
+#pragma unroll
+                for (int gg = 0; gg < G; ++gg)
+                  hs[j][h][gg] = sad4(A[j][i], B[(h * G + gg) * NW + i], i == 0 ? (gg == 0 ? K[h] : 0u) : hs[j][h][gg]);
             } else if (G == 2) {
               a0[j] = sad4(A[j][i], B[i], i == 0 ? K[0] : a0[j]);
               a1[j] = sad4(A[j][i], B[NW + i], i == 0 ? 0u : a1[j]);
@@ -175,16 +178,17 @@ struct U8Step {
         }
       }
     }
-    if (LN_U8_PAIR) {
+    if (PR >= 1) {
 #pragma unroll
       for (int j = 0; j < P; ++j) {
-        int32_t va = (G == 2) ? (int32_t)(a0[j] + a1[j]) : (int32_t)a0[j];
-        int32_t vb = (G == 2) ? (int32_t)(b0[j] + b1[j]) : (int32_t)b0[j];
-        if (LPU == 2) {                          // the partner lane holds the other half of the words
-          va += __shfl_xor_sync(0xffffffffu, va, 1);
-          vb += __shfl_xor_sync(0xffffffffu, vb, 1);
+        int32_t v[NS];
+#pragma unroll
+        for (int h = 0; h < NS; ++h) {
+          v[h] = (G == 2) ? (int32_t)(hs[j][h][0] + hs[j][h][1]) : (int32_t)hs[j][h][0];
+          if (LPU == 2) v[h] += __shfl_xor_sync(0xffffffffu, v[h], 1);   // partner lane: other half of the words
         }
-        best[j] = __vimax3_s32(best[j], va, vb);
+#pragma unroll
+        for (int h = 0; h < NS; h += 2) best[j] = __vimax3_s32(best[j], v[h], v[h + 1]);
       }
     } else if (G == 1 && (NW == 1 || LN_U8_CHAINS == 1)) {
 #pragma unroll
@@ -219,7 +223,7 @@ struct U8Step {
 #define LN_U8_MINB_MID 14
 #endif
 template <int MODE, int NW, int P>
-__host__ __device__ constexpr int u8_foot() { return U8Layout<MODE, NW>::G * (NW / u8_lpu<MODE, NW>()) * (P + 1 + LN_U8_PAIR); }
+__host__ __device__ constexpr int u8_foot() { return U8Layout<MODE, NW>::G * (NW / u8_lpu<MODE, NW>()) * (P + (1 << u8_pr<MODE>())); }
 template <int MODE, int NW, int P>
 __host__ __device__ constexpr int u8_min_blocks() {
   return u8_lpu<MODE, NW>() == 2 ? (u8_foot<MODE, NW, P>() <= 40 ? 12 : 1)
@@ -245,7 +249,8 @@ walk_u8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int3
   extern __shared__ __align__(16) uint32_t sT[];
   const int lane = threadIdx.x & 31;
   const int half = (LPU == 2) ? (lane & 1) : 0, slot = lane / LPU;
-  const int sw = p.s - LN_U8_PAIR;                 // walked digits (row r-1 paired, not walked)
+  constexpr int PR = STEP::PR, NS = STEP::NS;
+  const int sw = p.s - PR;                         // walked digits (the last PR rows are paired, not walked)
   const int total = 2 * sw * RREC;
   for (int i = lane; i < total; i += 32) sT[i] = gTab[i];
   __syncwarp();
@@ -267,14 +272,16 @@ walk_u8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int3
     const int64_t uh = min(max(g * P, p.unit_begin), u_end - 1);   // a valid unit of the group
     uint32_t A[P][NWL];
     uint32_t B[NB];
-    uint32_t Kc[2];
+    uint32_t Kc[NS];
     int32_t best[P];
     // ---- lane init (PAPER.md:253's per-thread product): shared high part -> B, K;
     //      per unit: its low prefix rows -> start bytes
     {
       uint64_t neg = 0;                            // bit x: digit of row x (0..kh) is 1
       for (int x = 0; x <= kh; ++x) neg |= (uint64_t)(prefix_digit(p, uh, x) != 0) << x;
-      int32_t kap = 0, kapb = 0;
+      int32_t kap[NS];
+#pragma unroll
+      for (int h = 0; h < NS; ++h) kap[h] = 0;
 #pragma unroll
       for (int ql = 0; ql < NWL; ++ql) {
         const int q = half * NWL + ql;             // global word of this lane's column slice
@@ -286,16 +293,22 @@ walk_u8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int3
           const int4 v = __ldg(reinterpret_cast<const int4*>(gInit + x * CW) + q);
           Pv[0] += f * v.x; Pv[1] += f * v.y; Pv[2] += f * v.z; Pv[3] += f * v.w;
         }
-        uint32_t w[2][2] = {{0u, 0u}, {0u, 0u}};   // [paired][bias set]
+        uint32_t w[NS][2];                         // [paired-row signs][bias set]
+#pragma unroll
+        for (int h = 0; h < NS; ++h) w[h][0] = w[h][1] = 0u;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int y = 4 * q + e;
           const int32_t lo = Pv[e] + __ldg(loRec + y);
-          const int32_t srho = LN_U8_PAIR ? __ldg(rhoRec + y) : 0;
+          int32_t srho[PR > 0 ? PR : 1];
 #pragma unroll
-          for (int h = 0; h <= LN_U8_PAIR; ++h) {  // h = 1: strategy B, row r-1 flipped (m -= scale rho)
-            const int32_t sh = h ? srho : 0;
-            int32_t& kk = h ? kapb : kap;
+          for (int i = 0; i < PR; ++i) srho[i] = __ldg(rhoRec + i * CW + y);
+#pragma unroll
+          for (int h = 0; h < NS; ++h) {           // bit i of h: paired row r-1-i flipped (m -= scale rho_i)
+            int32_t sh = 0;
+#pragma unroll
+            for (int i = 0; i < PR; ++i) sh += ((h >> i) & 1) ? srho[i] : 0;
+            int32_t& kk = kap[h];
             const int32_t c0 = -lo + sh;
             int32_t b0;
             if (MODE == MODE_MARG && y == 0) {     // linear column: m_0 = a_0 + Lo_0 (- 2 rho_0)
@@ -315,13 +328,13 @@ walk_u8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int3
           }
         }
 #pragma unroll
-        for (int h = 0; h <= LN_U8_PAIR; ++h) {
+        for (int h = 0; h < NS; ++h) {
           B[h * G * NWL + ql] = w[h][0];
           if (G == 2) B[h * G * NWL + NWL + ql] = w[h][1];
         }
       }
-      Kc[0] = (uint32_t)kap;
-      Kc[1] = (uint32_t)kapb;
+#pragma unroll
+      for (int h = 0; h < NS; ++h) Kc[h] = (uint32_t)kap[h];
     }
 #pragma unroll
     for (int j = 0; j < P; ++j) {
@@ -349,7 +362,7 @@ walk_u8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int3
       // value of the unit's start word (strategy A, and B when paired)
       int32_t v0 = 0;
 #pragma unroll
-      for (int h = 0; h <= LN_U8_PAIR; ++h) {
+      for (int h = 0; h < NS; ++h) {
         uint32_t acc = Kc[h];
 #pragma unroll
         for (int q = 0; q < NWL; ++q) {
@@ -399,10 +412,11 @@ __global__ void build_u8_kernel(const int32_t* M, int r, int c, int NW, int k, i
   const int NWL = NW / lpu, RWL = u8_pad4(NWL), RW = lpu * RWL, CW = 4 * NW;
   const int scale = (MODE == MODE_LD) ? 1 : 2;
   const int tid = threadIdx.x;
-  const int sw = s - LN_U8_PAIR;
+  const int PR = u8_pr<MODE>();
+  const int sw = s - PR;
   for (int rec = tid; rec < 2 * sw; rec += blockDim.x) {
     const int b = rec >> 1, sg = rec & 1;
-    const int32_t* row = M + (int64_t)(r - 1 - LN_U8_PAIR - b) * c;   // walked digit b
+    const int32_t* row = M + (int64_t)(r - 1 - PR - b) * c;   // walked digit b
     const int f = sg ? -scale : scale;     // digit -> 1: a_x = -1 (m -= 2M) or group 1 (m_0 -= M)
     for (int i = 0; i < RW; ++i) {
       const int h = i / RWL, ql = i % RWL, q = h * NWL + ql;   // slice h, word q of the row
@@ -431,14 +445,14 @@ __global__ void build_u8_kernel(const int32_t* M, int r, int c, int NW, int k, i
     init[(k + 1) * CW + y] = (MODE == MODE_LD) ? N : -W;
     init[(k + 2) * CW + y] = (MODE == MODE_LD) ? T : 0;
     init[(k + 3) * CW + y] = (MODE == MODE_LD) ? Ssuf - N : Ssuf + W;
-    init[(k + 4) * CW + y] = y < c ? scale * M[(int64_t)(r - 1) * c + y] : 0;
+    for (int i = 0; i < PR; ++i) init[(k + 4 + i) * CW + y] = y < c ? scale * M[(int64_t)(r - 1 - i) * c + y] : 0;
   }
 }
 
 template <int MODE, int NW>
 size_t u8_smem(int s) {
   constexpr int LPU = u8_lpu<MODE, NW>();
-  return sizeof(uint32_t) * (size_t)(2 * (s - LN_U8_PAIR) * LPU * u8_pad4(NW / LPU));
+  return sizeof(uint32_t) * (size_t)(2 * (s - u8_pr<MODE>()) * LPU * u8_pad4(NW / LPU));
 }
 
 template <int MODE, int NW>
@@ -533,6 +547,9 @@ int walk_u8_units_per_lane_mode<LN_BIN_MODE>(int c) {
   LN_U8_SWITCH(LN_BIN_MODE, walk_u8_words_mode<LN_BIN_MODE>(c), upl_u8)
   return 1;
 }
+
+template <>
+int walk_u8_paired_rows_mode<LN_BIN_MODE>() { return u8_pr<LN_BIN_MODE>(); }
 
 template <>
 int walk_u8_lanes_per_unit_mode<LN_BIN_MODE>(int c) {
