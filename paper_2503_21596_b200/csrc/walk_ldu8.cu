@@ -33,6 +33,17 @@ constexpr int kTabWordsLU = 16384;
 
 __host__ __device__ constexpr int lu_pad4(int x) { return (x + 3) & ~3; }
 
+#ifndef LN_LDU8_EPI
+#define LN_LDU8_EPI 2
+#endif
+// a + b as IMAD (FMA-heavy pipe) with `one` a uniform operand ptxas cannot fold: keeps the
+// epilogue's adds off the ALU pipe, which the VABSDIFF4s saturate
+__device__ __forceinline__ int32_t lu_fadd(int32_t a, int32_t b, uint32_t one) {
+  int32_t r;
+  asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(one), "r"(b));
+  return r;
+}
+
 __device__ __forceinline__ uint32_t lu_sad4(uint32_t a, uint32_t b, uint32_t acc) {
   uint32_t d;
   asm("vabsdiff4.u32.u32.u32.add %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(acc));
@@ -92,8 +103,65 @@ struct LdU8 {
   // best paired-row extension of the current word, relative to S.  E[m - 1] serves the
   // subset m of paired rows (bit 0 = row r-1, bit 1 = row r-2, bit 2 = row r-3); the
   // labellings of the paired rows are the set partitions of them into distinct groups.
-  static __device__ __forceinline__ int32_t ext(const Unit& U) {
-    if constexpr (PR == 1) {
+  // max of n candidate values with 3-input maxes (VIMNMX3): (n - 1) / 2 ALU instructions
+  template <int N>
+  static __device__ __forceinline__ int32_t max_tree(const int32_t (&v)[N]) {
+    if constexpr (N == 1) {
+      return v[0];
+    } else if constexpr (N == 2) {
+      return max(v[0], v[1]);
+    } else {
+      constexpr int M = (N + 2) / 3;
+      int32_t w[M];
+#pragma unroll
+      for (int i = 0; i < M; ++i) {
+        if (3 * i + 2 < N) w[i] = __vimax3_s32(v[3 * i], v[3 * i + 1], v[3 * i + 2]);
+        else if (3 * i + 1 < N) w[i] = max(v[3 * i], v[3 * i + 1]);
+        else w[i] = v[3 * i];
+      }
+      return max_tree<M>(w);
+    }
+  }
+  // d = 3: every labelling of the paired rows as an explicit candidate (sums on the FMA
+  // pipe), then one max tree on the ALU pipe
+  static __device__ __forceinline__ int32_t ext_flat(const Unit& U, uint32_t one) {
+    if constexpr (PR == 2) {
+      int32_t v[9];
+      int n = 0;
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+          if (a != b) v[n++] = lu_fadd(U.E[0][a], U.E[1][b], one);
+#pragma unroll
+      for (int a = 0; a < 3; ++a) v[n++] = U.E[2][a];
+      return max_tree<9>(v);
+    } else {
+      int32_t v[27];
+      int n = 0;
+#pragma unroll
+      for (int a = 0; a < 3; ++a)                                    // {1}{2}{3}
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+          if (a != b) v[n++] = lu_fadd(lu_fadd(U.E[0][a], U.E[1][b], one), U.E[3][3 - a - b], one);
+#pragma unroll
+      for (int a = 0; a < 3; ++a)                                    // {12}{3}, {13}{2}, {23}{1}
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+          if (a != b) {
+            v[n++] = lu_fadd(U.E[2][a], U.E[3][b], one);
+            v[n++] = lu_fadd(U.E[4][a], U.E[1][b], one);
+            v[n++] = lu_fadd(U.E[5][a], U.E[0][b], one);
+          }
+#pragma unroll
+      for (int a = 0; a < 3; ++a) v[n++] = U.E[6][a];                // {123}
+      return max_tree<27>(v);
+    }
+  }
+  static __device__ __forceinline__ int32_t ext(const Unit& U, uint32_t one) {
+    if constexpr (D == 3 && PR >= 2 && LN_LDU8_EPI == 2) {
+      return ext_flat(U, one);
+    } else if constexpr (PR == 1) {
       return max_of(U.E[0]);
     } else if constexpr (PR == 2) {
       return max(pairmax(U.E[0], U.E[1]), max_of(U.E[2]));
@@ -105,16 +173,23 @@ struct LdU8 {
       return __vimax3_s32(t1, t2, max_of(U.E[6]));                  // {123}
     }
   }
-  static __device__ __forceinline__ void refresh(Unit& U, int g, const uint32_t (&h)[NS]) {
-    U.S += (int32_t)h[0] - U.H[g];
-    U.H[g] = (int32_t)h[0];
+  static __device__ __forceinline__ void refresh(Unit& U, int g, const uint32_t (&h)[NS], uint32_t one) {
+    if (LN_LDU8_EPI == 2 && D == 3) {
+      U.S = lu_fadd(U.S, lu_fadd((int32_t)h[0], -U.H[g], one), one);
+      U.H[g] = (int32_t)h[0];
 #pragma unroll
-    for (int m = 1; m < NS; ++m) U.E[m - 1][g] = (int32_t)h[m] - (int32_t)h[0];
+      for (int m = 1; m < NS; ++m) U.E[m - 1][g] = lu_fadd((int32_t)h[m], -(int32_t)h[0], one);
+    } else {
+      U.S += (int32_t)h[0] - U.H[g];
+      U.H[g] = (int32_t)h[0];
+#pragma unroll
+      for (int m = 1; m < NS; ++m) U.E[m - 1][g] = (int32_t)h[m] - (int32_t)h[0];
+    }
   }
   // move the walked row of record `off` from group PG to group QG in every unit
   template <int PG, int QG>
   static __device__ __forceinline__ void move(Unit (&U)[P], const uint32_t (&Bs)[NS * NW], const uint32_t (&Ks)[NS],
-                                              uint32_t sbase, int off) {
+                                              uint32_t sbase, int off, uint32_t one) {
     uint32_t hp[P][NS], hq[P][NS];
 #pragma unroll
     for (int v = 0; v < RW / 4; ++v) {
@@ -140,24 +215,24 @@ struct LdU8 {
     }
 #pragma unroll
     for (int j = 0; j < P; ++j) {
-      refresh(U[j], PG, hp[j]);
-      refresh(U[j], QG, hq[j]);
-      U[j].best = max(U[j].best, U[j].S + ext(U[j]));
+      refresh(U[j], PG, hp[j], one);
+      refresh(U[j], QG, hq[j], one);
+      U[j].best = __viaddmax_s32(U[j].S, ext(U[j], one), U[j].best);
     }
   }
   static __device__ __forceinline__ void move_dyn(Unit (&U)[P], const uint32_t (&Bs)[NS * NW], const uint32_t (&Ks)[NS],
-                                                  uint32_t sbase, int off, int p, int q) {
+                                                  uint32_t sbase, int off, int p, int q, uint32_t one) {
     switch (p * D + q) {
-      case 0 * D + 1: move<0, 1>(U, Bs, Ks, sbase, off); return;
-      case 1 * D + 0: move<1, 0>(U, Bs, Ks, sbase, off); return;
-      case 1 * D + 2: move<1, 2>(U, Bs, Ks, sbase, off); return;
-      case 2 * D + 1: move<2, 1>(U, Bs, Ks, sbase, off); return;
+      case 0 * D + 1: move<0, 1>(U, Bs, Ks, sbase, off, one); return;
+      case 1 * D + 0: move<1, 0>(U, Bs, Ks, sbase, off, one); return;
+      case 1 * D + 2: move<1, 2>(U, Bs, Ks, sbase, off, one); return;
+      case 2 * D + 1: move<2, 1>(U, Bs, Ks, sbase, off, one); return;
       default: break;
     }
     if constexpr (D >= 4) {
       switch (p * D + q) {
-        case 2 * D + 3: move<2, 3>(U, Bs, Ks, sbase, off); return;
-        case 3 * D + 2: move<3, 2>(U, Bs, Ks, sbase, off); return;
+        case 2 * D + 3: move<2, 3>(U, Bs, Ks, sbase, off, one); return;
+        case 3 * D + 2: move<3, 2>(U, Bs, Ks, sbase, off, one); return;
         default: break;
       }
     }
@@ -242,22 +317,22 @@ walk_ldu8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const in
 #pragma unroll
         for (int m = 1; m < NS; ++m) U[j].E[m - 1][g] = (int32_t)h[m] - (int32_t)h[0];
       }
-      U[j].best = U[j].S + WK::ext(U[j]);
+      U[j].best = U[j].S + WK::ext(U[j], p.one);
     }
     for (uint32_t t = 0; t < nblk; ++t) {
       if (t != 0) {
         uint32_t i, from, to;
         dary_block_start<D>(t, &i, &from, &to);
-        WK::move_dyn(U, Bs, Ks, sbase, (int)i * RD, (int)from, (int)to);
+        WK::move_dyn(U, Bs, Ks, sbase, (int)i * RD, (int)from, (int)to, p.one);
       }
       if ((t & 1u) == 0) {
-        WK::template move<0, 1>(U, Bs, Ks, sbase, 0);
-        WK::template move<1, 2>(U, Bs, Ks, sbase, 0);
-        if constexpr (D >= 4) WK::template move<2, 3>(U, Bs, Ks, sbase, 0);
+        WK::template move<0, 1>(U, Bs, Ks, sbase, 0, p.one);
+        WK::template move<1, 2>(U, Bs, Ks, sbase, 0, p.one);
+        if constexpr (D >= 4) WK::template move<2, 3>(U, Bs, Ks, sbase, 0, p.one);
       } else {
-        if constexpr (D >= 4) WK::template move<3, 2>(U, Bs, Ks, sbase, 0);
-        WK::template move<2, 1>(U, Bs, Ks, sbase, 0);
-        WK::template move<1, 0>(U, Bs, Ks, sbase, 0);
+        if constexpr (D >= 4) WK::template move<3, 2>(U, Bs, Ks, sbase, 0, p.one);
+        WK::template move<2, 1>(U, Bs, Ks, sbase, 0, p.one);
+        WK::template move<1, 0>(U, Bs, Ks, sbase, 0, p.one);
       }
     }
 #pragma unroll
