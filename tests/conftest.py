@@ -14,6 +14,11 @@ if HERE not in sys.path:
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA B200 (runs the sm_100a kernels through the C ABI)")
     config.addinivalue_line("markers", "slow: longer CPU test")
+    # the C-ABI library and the C oracle are built in-tree (__graft_entry__.build());
+    # build them here too if a fresh checkout runs the tests first
+    from paper_2503_21596_b200 import build as B
+    if not os.path.exists(B.OUT):
+        B.build()
 
 
 def gpu_available() -> bool:
