@@ -106,8 +106,8 @@ void suffix_guard(const int32_t* M, int m, Problem* p) {
 
 // log2 of the u8 kernel's lane group: its units differ in the last lane_bits prefix
 // rows, which join the byte window (walk_u8_impl.cuh "Lane groups")
-int u8_lane_bits(const Problem& p) {
-  const int P = walk_u8_units_per_lane(p.mode, p.c);
+int u8_lane_bits(const Problem& p, int lpu = 1) {
+  const int P = walk_u8_units_per_lane(p.mode, p.c, lpu);
   return P >= 8 ? 3 : P >= 4 ? 2 : (P == 2 ? 1 : 0);
 }
 
@@ -187,6 +187,7 @@ int kernel_override() {
 struct Plan {
   int kernel = K_GEN;
   int k = 0, s = 0;
+  int u8_lpu = 1;                // byte walk: lanes per unit
   int64_t units = 1;
   std::vector<uint64_t> table;   // packed prefixes (RGS for d >= 3, explicit for hooks); empty = arithmetic
   // RGS plans: the process-wide immutable prefix list for (k, d), shared instead of copied
@@ -250,19 +251,24 @@ int make_plan(const Problem& pr, int world, Plan* pl, int64_t target_override = 
     // byte-packed walk first: its guard bounds the suffix length from above, so the
     // split takes at least f - su prefix digits (units must stay below 2^32)
     if (ov < 0 && allow_u8) {
-      const int lg = u8_lane_bits(pr);
-      int su = 0;
-      for (int s_ = 1; s_ <= f - lg && s_ <= 31; ++s_)
-        if (u8_fits(pr, s_ + lg) && walk_u8_supported(pr.mode, pr.c, s_)) su = s_;
-      int s_lo = 0;
-      for (int s_ = 1; s_ <= su; ++s_) if (walk_u8_supported(pr.mode, pr.c, s_)) { s_lo = s_; break; }
-      if (su > 0 && s_lo > 0 && f - su <= 31) {
-        int k = std::max(lg, f - su);
-        while (k < f - s_lo && k < 31 && (1LL << k) < target) ++k;
-        p.k = k; p.s = f - k; p.units = 1LL << k;
-        p.kernel = K_U8;
-        *pl = std::move(p);
-        return LNORM_OK;
+      // lane pairs (lpu 2) first where the instance offers them: their second unit per lane
+      // adds a prefix row to the byte window, so fall back to one lane per unit if it no longer fits
+      for (int lpu = walk_u8_lanes_per_unit(pr.mode, pr.c); lpu >= 1; --lpu) {
+        const int lg = u8_lane_bits(pr, lpu);
+        int su = 0;
+        for (int s_ = 1; s_ <= f - lg && s_ <= 31; ++s_)
+          if (u8_fits(pr, s_ + lg) && walk_u8_supported(pr.mode, pr.c, s_, lpu)) su = s_;
+        int s_lo = 0;
+        for (int s_ = 1; s_ <= su; ++s_) if (walk_u8_supported(pr.mode, pr.c, s_, lpu)) { s_lo = s_; break; }
+        if (su > 0 && s_lo > 0 && f - su <= 31) {
+          int k = std::max(lg, f - su);
+          while (k < f - s_lo && k < 31 && (1LL << k) < target) ++k;
+          p.k = k; p.s = f - k; p.units = 1LL << k;
+          p.kernel = K_U8;
+          p.u8_lpu = lpu;
+          *pl = std::move(p);
+          return LNORM_OK;
+        }
       }
     }
     const int sp = (pr.fitsPair && ov != K_BIN16 && ov != K_BIN && ov != K_GEN) ? min_s(K_PAIR16) : -1;
@@ -473,7 +479,7 @@ int launch_walk(DevCtx& cx, const Problem& pr, const Plan& pl, WalkParams& wp, i
   else if (pl.kernel == K_BIN16) occ = walk_bin16_occupancy(pr.mode, pr.c, pl.k, pl.s, &block);
   else if (pl.kernel == K_LD16) occ = walk_ld16_occupancy(pr.dl, pr.c, pl.k, pl.s, &block);
   else if (pl.kernel == K_PAIR16) occ = walk_pair16_occupancy(pr.mode, pr.c, pl.s, &block);
-  else if (pl.kernel == K_U8) occ = walk_u8_occupancy(pr.mode, pr.c, pl.s, &block);
+  else if (pl.kernel == K_U8) occ = walk_u8_occupancy(pr.mode, pr.c, pl.s, pl.u8_lpu, &block);
   else if (pl.kernel == K_LDPAIR16) occ = walk_ldpair16_occupancy(pr.dl, pr.c, pl.s, &block);
   else if (pl.kernel == K_LDU8) occ = walk_ldu8_occupancy(pr.dl, pr.c, pl.s, &block);
   else if (pl.kernel == K_LD) occ = walk_ld_occupancy(pr.dl, pr.c, &block);
@@ -483,7 +489,8 @@ int launch_walk(DevCtx& cx, const Problem& pr, const Plan& pl, WalkParams& wp, i
   if (pl.kernel == K_BIN16) per_block *= walk_bin16_units_per_lane(pr.mode, pr.c);
   if (pl.kernel == K_LD16) per_block *= walk_ld16_units_per_lane(pr.dl, pr.c);
   if (pl.kernel == K_PAIR16) per_block *= walk_pair16_units_per_lane(pr.mode, pr.c);
-  if (pl.kernel == K_U8) per_block = per_block * walk_u8_units_per_lane(pr.mode, pr.c) / walk_u8_lanes_per_unit(pr.mode, pr.c);
+  if (pl.kernel == K_U8) per_block = per_block * walk_u8_units_per_lane(pr.mode, pr.c, pl.u8_lpu) / pl.u8_lpu;
+  wp.u8_lpu = pl.u8_lpu;
   if (pl.kernel == K_LDPAIR16) per_block *= walk_ldpair16_units_per_lane(pr.dl, pr.c);
   if (pl.kernel == K_LDU8) per_block *= walk_ldu8_units_per_lane(pr.dl, pr.c, pl.s);
   int64_t want = (wp.unit_count + per_block - 1) / per_block;
@@ -1091,16 +1098,20 @@ int lnorm_prefix_maxima(const int32_t* M, int32_t n, int32_t m, int32_t d, int32
       pl.kernel = K_PAIR16;
     // the u8 kernel needs aligned lane groups: prefix i*P + j equals prefix i*P on rows
     // 0..k-lg and carries the bits of j on the last lg prefix rows (row k = bit 0)
-    const int lg = u8_lane_bits(pr), P = 1 << lg;
-    bool grouped = ov < 0 && pl.k >= lg && count % P == 0 && u8_fits(pr, pl.s + lg) &&
-                   walk_u8_supported(pr.mode, pr.c, pl.s);
-    for (int64_t i = 0; grouped && i < count; ++i) {
-      const int64_t h = i - i % P;
-      for (int x = 0; x <= pl.k && grouped; ++x) {
-        const int v = prefixes[i * nfixed + x];
-        if (x <= pl.k - lg) grouped = v == prefixes[h * nfixed + x];
-        else grouped = v == (int)(((i % P) >> (pl.k - x)) & 1);
+    bool grouped = false;
+    for (int lpu = walk_u8_lanes_per_unit(pr.mode, pr.c); lpu >= 1 && !grouped; --lpu) {
+      const int lg = u8_lane_bits(pr, lpu), P = 1 << lg;
+      grouped = ov < 0 && pl.k >= lg && count % P == 0 && u8_fits(pr, pl.s + lg) &&
+                walk_u8_supported(pr.mode, pr.c, pl.s, lpu);
+      for (int64_t i = 0; grouped && i < count; ++i) {
+        const int64_t h = i - i % P;
+        for (int x = 0; x <= pl.k && grouped; ++x) {
+          const int v = prefixes[i * nfixed + x];
+          if (x <= pl.k - lg) grouped = v == prefixes[h * nfixed + x];
+          else grouped = v == (int)(((i % P) >> (pl.k - x)) & 1);
+        }
       }
+      if (grouped) pl.u8_lpu = lpu;
     }
     if (grouped) pl.kernel = K_U8;
   }
@@ -1238,6 +1249,7 @@ int lnorm_plan(const int32_t* M, int32_t n, int32_t m, int32_t d, int32_t with_m
   I.prefix_digits = pl.k; I.suffix_digits = pl.s; I.variant = pl.kernel; I.packed_ok = pr.fits16;
   I.units = pl.units;
   I.steps = (double)pl.units * (double)ipow(pr.dl, pl.s);
+  I.lanes_per_unit = pl.kernel == K_U8 ? pl.u8_lpu : 1;
   *out = I;
   return LNORM_OK;
 }

@@ -41,11 +41,13 @@ struct WalkParams {
   int64_t units_per;
   int64_t m_stride, tab_stride, init_stride;
   uint32_t one;                  // = 1 (a uniform operand the compiler cannot fold)
+  int32_t u8_lpu;                // byte walk: lanes per unit (1, or 2 for > 128 columns)
 };
 
 // Defaults for a single-matrix launch.
 inline void walk_params_single(WalkParams& p) {
   p.one = 1;
+  if (p.u8_lpu < 1) p.u8_lpu = 1;
   p.batch = 1;
   p.units_per = p.unit_count;
   p.m_stride = p.tab_stride = p.init_stride = 0;
@@ -148,20 +150,20 @@ cudaError_t walk_ldpair16_launch(const WalkParams& p, int32_t* scratch_tab, int3
                                  cudaStream_t st, int* block_out);
 // Byte-packed binary walk (L_1, L_marg, L_2): four column sums per register as offset
 // bytes; exact when every column's suffix window fits a byte (guard checked by the caller).
-bool walk_u8_supported(int mode, int c, int s);
-int walk_u8_units_per_lane(int mode, int c);
-int walk_u8_occupancy(int mode, int c, int s, int* block_out);
+bool walk_u8_supported(int mode, int c, int s, int lpu = 1);
+int walk_u8_units_per_lane(int mode, int c, int lpu = 1);
+int walk_u8_occupancy(int mode, int c, int s, int lpu, int* block_out);
 cudaError_t walk_u8_launch(const WalkParams& p, int32_t* scratch_tab, int32_t* scratch_init, int grid,
                            cudaStream_t st, int* block_out);
 template <int MODE> int walk_u8_words_mode(int c);
 template <int MODE> cudaError_t walk_u8_launch_mode(const WalkParams& p, int32_t* scratch_tab, int32_t* scratch_init,
                                                     int grid, cudaStream_t st);
-template <int MODE> int walk_u8_occupancy_mode(int c, int s);
-template <int MODE> int walk_u8_units_per_lane_mode(int c);
+template <int MODE> int walk_u8_occupancy_mode(int c, int s, int lpu);
+template <int MODE> int walk_u8_units_per_lane_mode(int c, int lpu);
 template <int MODE> int walk_u8_lanes_per_unit_mode(int c);
 template <int MODE> int walk_u8_paired_rows_mode();
 int walk_u8_lanes_per_unit(int mode, int c);
-template <int MODE> int walk_u8_unroll_mode(int c);
+template <int MODE> int walk_u8_unroll_mode(int c, int lpu);
 // Byte-packed d-ary walk, last row paired (L_d, d in {3,4}; guard: every column's
 // sum_x |M_xy| <= 255, checked by the caller).
 bool walk_ldu8_supported(int d, int c, int s);

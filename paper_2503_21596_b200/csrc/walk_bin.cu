@@ -99,33 +99,35 @@ cudaError_t walk_pair16_launch(const WalkParams& p, int32_t* scratch_tab, int32_
   return walk_pair16_launch_mode<MODE_LD>(p, scratch_tab, scratch_init, grid, st);
 }
 
-bool walk_u8_supported(int mode, int c, int s) {
+bool walk_u8_supported(int mode, int c, int s, int lpu) {
   int NW = 0, K = 4, PR = 1;
-  if (mode == MODE_L1) { NW = walk_u8_words_mode<MODE_L1>(c); if (NW) K = walk_u8_unroll_mode<MODE_L1>(c); PR = walk_u8_paired_rows_mode<MODE_L1>(); }
-  else if (mode == MODE_MARG) { NW = walk_u8_words_mode<MODE_MARG>(c); if (NW) K = walk_u8_unroll_mode<MODE_MARG>(c); PR = walk_u8_paired_rows_mode<MODE_MARG>(); }
-  else if (mode == MODE_LD) { NW = walk_u8_words_mode<MODE_LD>(c); if (NW) K = walk_u8_unroll_mode<MODE_LD>(c); PR = walk_u8_paired_rows_mode<MODE_LD>(); }
+  if (mode == MODE_L1) { NW = walk_u8_words_mode<MODE_L1>(c); if (NW) K = walk_u8_unroll_mode<MODE_L1>(c, lpu); PR = walk_u8_paired_rows_mode<MODE_L1>(); }
+  else if (mode == MODE_MARG) { NW = walk_u8_words_mode<MODE_MARG>(c); if (NW) K = walk_u8_unroll_mode<MODE_MARG>(c, lpu); PR = walk_u8_paired_rows_mode<MODE_MARG>(); }
+  else if (mode == MODE_LD) { NW = walk_u8_words_mode<MODE_LD>(c); if (NW) K = walk_u8_unroll_mode<MODE_LD>(c, lpu); PR = walk_u8_paired_rows_mode<MODE_LD>(); }
   if (NW == 0 || s < K + PR || s > 31) return false;   // K unrolled digits + the paired last rows
+  if (lpu > walk_u8_lanes_per_unit(mode, c)) return false;
   const int RW = 2 * (((NW + 1) / 2 + 3) & ~3);         // record words incl. lane-pair slice padding
-  return 2 * s * RW <= 16384;     // delta table staged in shared memory (dTab holds 32768 words)
+  return 2 * s * RW <= 16384;
 }
 
+// largest lanes-per-unit an instance offers for c columns (1 or 2)
 int walk_u8_lanes_per_unit(int mode, int c) {
   if (mode == MODE_L1) return walk_u8_lanes_per_unit_mode<MODE_L1>(c);
   if (mode == MODE_MARG) return walk_u8_lanes_per_unit_mode<MODE_MARG>(c);
   return walk_u8_lanes_per_unit_mode<MODE_LD>(c);
 }
 
-int walk_u8_units_per_lane(int mode, int c) {
-  if (mode == MODE_L1) return walk_u8_units_per_lane_mode<MODE_L1>(c);
-  if (mode == MODE_MARG) return walk_u8_units_per_lane_mode<MODE_MARG>(c);
-  return walk_u8_units_per_lane_mode<MODE_LD>(c);
+int walk_u8_units_per_lane(int mode, int c, int lpu) {
+  if (mode == MODE_L1) return walk_u8_units_per_lane_mode<MODE_L1>(c, lpu);
+  if (mode == MODE_MARG) return walk_u8_units_per_lane_mode<MODE_MARG>(c, lpu);
+  return walk_u8_units_per_lane_mode<MODE_LD>(c, lpu);
 }
 
-int walk_u8_occupancy(int mode, int c, int s, int* block_out) {
+int walk_u8_occupancy(int mode, int c, int s, int lpu, int* block_out) {
   *block_out = 32;
-  if (mode == MODE_L1) return walk_u8_occupancy_mode<MODE_L1>(c, s);
-  if (mode == MODE_MARG) return walk_u8_occupancy_mode<MODE_MARG>(c, s);
-  return walk_u8_occupancy_mode<MODE_LD>(c, s);
+  if (mode == MODE_L1) return walk_u8_occupancy_mode<MODE_L1>(c, s, lpu);
+  if (mode == MODE_MARG) return walk_u8_occupancy_mode<MODE_MARG>(c, s, lpu);
+  return walk_u8_occupancy_mode<MODE_LD>(c, s, lpu);
 }
 
 cudaError_t walk_u8_launch(const WalkParams& p, int32_t* scratch_tab, int32_t* scratch_init, int grid,

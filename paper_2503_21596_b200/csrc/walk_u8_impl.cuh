@@ -86,21 +86,23 @@ __host__ __device__ constexpr int u8_pr() { return MODE == MODE_LD ? (LN_U8_PAIR
 #ifndef LN_U8_PWIDE
 #define LN_U8_PWIDE 1
 #endif
-// Lanes per unit (experiment knob, off by default): wide L_1 / L_marg rows (more than 128
-// columns) split over a lane PAIR (each lane holds half of the words of the same units; the
-// two partial sums of a strategy are combined with one SHFL), so a lane keeps two units
-// sharing one bias set instead of one unit with its own.  Measured +7-9 % on 144-190 columns,
-// but the second unit adds a prefix row to the byte window, which pushed the 48x192 config
-// past the guard (k > 31) onto the 16-bit kernel; a planner choice between both instances
-// would be needed to enable it.
+// Lanes per unit: wide L_1 / L_marg rows (more than 128 columns) split over a lane PAIR
+// (each lane holds half of the words of the same units; the two partial sums of a strategy
+// are combined with one SHFL), so a lane keeps two units sharing one bias set instead of one
+// unit with its own (measured +7-9 % on 144-190 columns).  The second unit adds a prefix
+// row to the byte window, so the planner falls back to the one-lane instance where that row
+// no longer fits (48x192: k would exceed 31).  The 192-column lane-pair instance spills a
+// few registers in its unit init (none inside the walk loop).
 #ifndef LN_U8_LPU2
-#define LN_U8_LPU2 0
+#define LN_U8_LPU2 1
 #endif
+// lanes per unit an instance can run with (the planner picks 2 where the byte guard allows
+// the extra window row, else 1; both instances are compiled for those NW)
 template <int MODE, int NW>
-__host__ __device__ constexpr int u8_lpu() { return (U8Layout<MODE, NW>::G == 1 && NW > 32 && LN_U8_LPU2 && u8_pr<MODE>() >= 1) ? 2 : 1; }
-template <int MODE, int NW>
+__host__ __device__ constexpr int u8_lpu_max() { return (U8Layout<MODE, NW>::G == 1 && NW > 32 && LN_U8_LPU2 && u8_pr<MODE>() >= 1) ? 2 : 1; }
+template <int MODE, int NW, int LPU = 1>
 __host__ __device__ constexpr int u8_units_per_lane() {
-  return u8_lpu<MODE, NW>() == 2 ? (NW / 2 <= 8 ? 4 : 2)
+  return LPU == 2 ? (NW / 2 <= 8 ? 4 : 2)
        : U8Layout<MODE, NW>::G * NW <= 16 ? LN_U8_P
        : (U8Layout<MODE, NW>::G * NW <= 32 ? 2 : (U8Layout<MODE, NW>::G == 1 ? LN_U8_PWIDE : 1));
 }
@@ -223,23 +225,22 @@ struct U8Step {
 #define LN_U8_MINB_MID 14
 #endif
 template <int MODE, int NW, int P>
-__host__ __device__ constexpr int u8_foot() { return U8Layout<MODE, NW>::G * (NW / u8_lpu<MODE, NW>()) * (P + (1 << u8_pr<MODE>())); }
-template <int MODE, int NW, int P>
+__host__ __device__ constexpr int u8_foot() { return U8Layout<MODE, NW>::G * NW * (P + (1 << u8_pr<MODE>())); }
+template <int MODE, int NW, int P, int LPU>
 __host__ __device__ constexpr int u8_min_blocks() {
-  return u8_lpu<MODE, NW>() == 2 ? (u8_foot<MODE, NW, P>() <= 40 ? 12 : 1)
+  return LPU == 2 ? (u8_foot<MODE, NW / 2, P>() <= 40 ? 12 : 1)
        : (U8Layout<MODE, NW>::G == 1 && u8_foot<MODE, NW, P>() <= 56) ? LN_U8_MINB
        : (U8Layout<MODE, NW>::G == 1 && u8_foot<MODE, NW, P>() <= 70) ? LN_U8_MINB_MID
        : ((u8_foot<MODE, NW, P>() <= 96 && P >= 4) || u8_foot<MODE, NW, P>() <= 54) ? 12 : 1;
 }
 
-template <int MODE, int NW, int P>
-__global__ void __launch_bounds__(kBlockU8, u8_min_blocks<MODE, NW, P>())
+template <int MODE, int NW, int P, int LPU>
+__global__ void __launch_bounds__(kBlockU8, u8_min_blocks<MODE, NW, P, LPU>())
 walk_u8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int32_t* __restrict__ gInit) {
   using LY = U8Layout<MODE, NW>;
   constexpr int G = LY::G, CW = LY::CW;
   constexpr int LG = (P >= 8) ? 3 : (P >= 4) ? 2 : (P == 2 ? 1 : 0);
-  constexpr int LPU = u8_lpu<MODE, NW>();          // lanes per unit
-  constexpr int NWL = NW / LPU;                    // words held by one lane
+  constexpr int NWL = NW / LPU;                    // LPU = lanes per unit                    // words held by one lane
   constexpr int RWL = u8_pad4(NWL);                // its slice of a delta record (16B aligned)
   constexpr int RREC = LPU * RWL;                  // words per delta record
   constexpr int GPW = 32 / LPU;                    // lane groups per warp
@@ -449,40 +450,63 @@ __global__ void build_u8_kernel(const int32_t* M, int r, int c, int NW, int k, i
   }
 }
 
-template <int MODE, int NW>
-size_t u8_smem(int s) {
-  constexpr int LPU = u8_lpu<MODE, NW>();
-  return sizeof(uint32_t) * (size_t)(2 * (s - u8_pr<MODE>()) * LPU * u8_pad4(NW / LPU));
-}
+template <int MODE, int NW, int LPU>
+size_t u8_smem(int s) { return sizeof(uint32_t) * (size_t)(2 * (s - u8_pr<MODE>()) * LPU * u8_pad4(NW / LPU)); }
 
-template <int MODE, int NW>
-cudaError_t launch_u8(const WalkParams& p, const uint32_t* tab, const int32_t* init, int grid, cudaStream_t st) {
-  constexpr int P = u8_units_per_lane<MODE, NW>();
-  const size_t sm = u8_smem<MODE, NW>(p.s);
-  cudaError_t e = cudaFuncSetAttribute(walk_u8_kernel<MODE, NW, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+template <int MODE, int NW, int LPU>
+cudaError_t launch_u8_l(const WalkParams& p, const uint32_t* tab, const int32_t* init, int grid, cudaStream_t st) {
+  constexpr int P = u8_units_per_lane<MODE, NW, LPU>();
+  const size_t sm = u8_smem<MODE, NW, LPU>(p.s);
+  cudaError_t e = cudaFuncSetAttribute(walk_u8_kernel<MODE, NW, P, LPU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
-  walk_u8_kernel<MODE, NW, P><<<grid, kBlockU8, sm, st>>>(p, tab, init);
+  walk_u8_kernel<MODE, NW, P, LPU><<<grid, kBlockU8, sm, st>>>(p, tab, init);
   return cudaGetLastError();
 }
 
 template <int MODE, int NW>
-int occ_u8(int s) {
-  constexpr int P = u8_units_per_lane<MODE, NW>();
-  const size_t sm = u8_smem<MODE, NW>(s);
-  cudaFuncSetAttribute(walk_u8_kernel<MODE, NW, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+cudaError_t launch_u8(const WalkParams& p, const uint32_t* tab, const int32_t* init, int grid, cudaStream_t st) {
+  if constexpr (u8_lpu_max<MODE, NW>() == 2) {
+    if (p.u8_lpu == 2) return launch_u8_l<MODE, NW, 2>(p, tab, init, grid, st);
+  }
+  return launch_u8_l<MODE, NW, 1>(p, tab, init, grid, st);
+}
+
+template <int MODE, int NW, int LPU>
+int occ_u8_l(int s) {
+  constexpr int P = u8_units_per_lane<MODE, NW, LPU>();
+  const size_t sm = u8_smem<MODE, NW, LPU>(s);
+  cudaFuncSetAttribute(walk_u8_kernel<MODE, NW, P, LPU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   int nb = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, walk_u8_kernel<MODE, NW, P>, kBlockU8, sm);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, walk_u8_kernel<MODE, NW, P, LPU>, kBlockU8, sm);
   return nb;
 }
 
 template <int MODE, int NW>
-int upl_u8() { return u8_units_per_lane<MODE, NW>(); }
+int occ_u8(int s, int lpu) {
+  if constexpr (u8_lpu_max<MODE, NW>() == 2) {
+    if (lpu == 2) return occ_u8_l<MODE, NW, 2>(s);
+  }
+  return occ_u8_l<MODE, NW, 1>(s);
+}
 
 template <int MODE, int NW>
-int lpu_u8() { return u8_lpu<MODE, NW>(); }
+int upl_u8(int lpu) {
+  if constexpr (u8_lpu_max<MODE, NW>() == 2) {
+    if (lpu == 2) return u8_units_per_lane<MODE, NW, 2>();
+  }
+  return u8_units_per_lane<MODE, NW, 1>();
+}
 
 template <int MODE, int NW>
-int unroll_u8() { return u8_unroll<MODE, NW / u8_lpu<MODE, NW>(), u8_units_per_lane<MODE, NW>()>(); }
+int lpu_u8() { return u8_lpu_max<MODE, NW>(); }
+
+template <int MODE, int NW>
+int unroll_u8(int lpu) {
+  if constexpr (u8_lpu_max<MODE, NW>() == 2) {
+    if (lpu == 2) return u8_unroll<MODE, NW / 2, u8_units_per_lane<MODE, NW, 2>()>();
+  }
+  return u8_unroll<MODE, NW, u8_units_per_lane<MODE, NW, 1>()>();
+}
 
 #ifdef LN_U8_ONLY_NW   // experiment builds (tools/build_variant.py): one instance only
 #define LN_U8_SWITCH(MODE, NW_, FN, ...)                                                             \
@@ -526,8 +550,9 @@ cudaError_t walk_u8_launch_mode<LN_BIN_MODE>(const WalkParams& p, int32_t* scrat
   const int NW = walk_u8_words_mode<LN_BIN_MODE>(p.c);
   if (NW == 0) return cudaErrorInvalidValue;
   uint32_t* tab = reinterpret_cast<uint32_t*>(scratch_tab);
-  const int P = [&]() -> int { LN_U8_SWITCH(LN_BIN_MODE, NW, upl_u8) return 1; }();
-  const int lpu = [&]() -> int { LN_U8_SWITCH(LN_BIN_MODE, NW, lpu_u8) return 1; }();
+  const int lmax = [&]() -> int { LN_U8_SWITCH(LN_BIN_MODE, NW, lpu_u8) return 1; }();
+  const int lpu = (p.u8_lpu == 2 && lmax == 2) ? 2 : 1;
+  const int P = [&]() -> int { LN_U8_SWITCH(LN_BIN_MODE, NW, upl_u8, lpu) return 1; }();
   build_u8_kernel<LN_BIN_MODE><<<1, 256, 0, st>>>(p.M, p.r, p.c, NW, p.k, p.s, P >= 8 ? 3 : P >= 4 ? 2 : (P == 2 ? 1 : 0),
                                                   lpu, tab, scratch_init);
   cudaError_t e = cudaGetLastError();
@@ -537,14 +562,14 @@ cudaError_t walk_u8_launch_mode<LN_BIN_MODE>(const WalkParams& p, int32_t* scrat
 }
 
 template <>
-int walk_u8_occupancy_mode<LN_BIN_MODE>(int c, int s) {
-  LN_U8_SWITCH(LN_BIN_MODE, walk_u8_words_mode<LN_BIN_MODE>(c), occ_u8, s)
+int walk_u8_occupancy_mode<LN_BIN_MODE>(int c, int s, int lpu) {
+  LN_U8_SWITCH(LN_BIN_MODE, walk_u8_words_mode<LN_BIN_MODE>(c), occ_u8, s, lpu)
   return 0;
 }
 
 template <>
-int walk_u8_units_per_lane_mode<LN_BIN_MODE>(int c) {
-  LN_U8_SWITCH(LN_BIN_MODE, walk_u8_words_mode<LN_BIN_MODE>(c), upl_u8)
+int walk_u8_units_per_lane_mode<LN_BIN_MODE>(int c, int lpu) {
+  LN_U8_SWITCH(LN_BIN_MODE, walk_u8_words_mode<LN_BIN_MODE>(c), upl_u8, lpu)
   return 1;
 }
 
@@ -558,8 +583,8 @@ int walk_u8_lanes_per_unit_mode<LN_BIN_MODE>(int c) {
 }
 
 template <>
-int walk_u8_unroll_mode<LN_BIN_MODE>(int c) {
-  LN_U8_SWITCH(LN_BIN_MODE, walk_u8_words_mode<LN_BIN_MODE>(c), unroll_u8)
+int walk_u8_unroll_mode<LN_BIN_MODE>(int c, int lpu) {
+  LN_U8_SWITCH(LN_BIN_MODE, walk_u8_words_mode<LN_BIN_MODE>(c), unroll_u8, lpu)
   return 4;
 }
 

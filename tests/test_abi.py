@@ -196,6 +196,16 @@ def test_plan_packed_guard_and_fallback():
     assert L.plan(np.eye(3, dtype=np.int32))["variant_name"] == "generic"     # suffix shorter than the unroll
 
 
+def test_plan_lane_pairs_for_wide_rows():
+    """Beyond 128 columns the byte walk splits a unit over a lane pair where the extra window
+    row still fits the byte guard, else it keeps one lane per unit (48x192: k would exceed 31)."""
+    from paper_2503_21596_b200 import synth
+    assert L.plan(synth.random_matrix(42, 168, 142))["lanes_per_unit"] == 2
+    P = L.plan(synth.random_matrix(48, 192, 148))
+    assert P["variant_name"] == "bin_u8" and P["lanes_per_unit"] == 1 and P["prefix_digits"] == 31
+    assert L.plan(synth.random_matrix(42, 42, 2))["lanes_per_unit"] == 1
+
+
 def test_plan_is_identical_for_every_rank_and_grows_with_world():
     from paper_2503_21596_b200 import synth
     M = synth.random_matrix(42, 42, 2)

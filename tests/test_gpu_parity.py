@@ -197,6 +197,7 @@ def test_planted_40x40_marg(lib):
 @pytest.mark.parametrize("d,marg,n,m,nfixed", [
     (1, False, 42, 42, 25), (1, True, 40, 40, 24), (2, False, 24, 24, 10), (3, False, 24, 24, 14),
     (1, False, 48, 48, 33), (1, False, 48, 192, 35), (1, True, 40, 160, 28), (3, False, 26, 26, 16),
+    (1, False, 48, 192, 32),            # the full search's split: one lane per unit (lane pairs no longer fit)
     (4, False, 18, 18, 10),
 ])
 def test_sampled_prefixes_full_size(lib, d, marg, n, m, nfixed):
