@@ -263,6 +263,9 @@ int make_plan(const Problem& pr, int world, Plan* pl, int64_t target_override = 
         if (su > 0 && s_lo > 0 && f - su <= 31) {
           int k = std::max(lg, f - su);
           while (k < f - s_lo && k < 31 && (1LL << k) < target) ++k;
+          // short suffixes spend their time in the lane init: keep s >= 10 while the split
+          // still leaves ~2^21 units (several chunks per resident warp)
+          while (f - k < 10 && k > std::max(lg, 21) && f - k < su) --k;
           p.k = k; p.s = f - k; p.units = 1LL << k;
           p.kernel = K_U8;
           p.u8_lpu = lpu;
