@@ -185,6 +185,26 @@ def test_planted_42x42_l1(lib):
     assert oracle.value(M, arg) == v and arg[0] == 1
 
 
+@pytest.mark.parametrize("marg", [False, True], ids=["L1_42x42", "marg_40x40"])
+def test_bench_workload_families_and_metamorphic(lib, marg, monkeypatch):
+    """The bench workloads in full (BASELINE configs 2 and 3, 2^41 / 2^39 strategies): the byte
+    kernel and the independent strategy-paired 16-bit kernel return the same value and the same
+    canonical argmax; the argmax attains the value (oracle, from scratch); L_1(M) = L_1(M^T) and
+    L_marg(M) = L_marg(M^T)."""
+    n = 40 if marg else 42
+    M = synth.random_matrix(n, n, 3 if marg else 2)
+    assert lib.plan(M, with_marginals=marg)["variant_name"] == "bin_u8"
+    v, arg = lib.compute(M, with_marginals=marg)
+    assert oracle.value(M, arg, marg=marg) == v
+    monkeypatch.setenv("LNORM_KERNEL", "pair16")
+    assert lib.plan(M, with_marginals=marg)["variant_name"] == "bin_pair16"
+    v2, arg2 = lib.compute(M, with_marginals=marg)
+    assert v2 == v and list(arg2) == list(arg)
+    monkeypatch.setenv("LNORM_KERNEL", "auto")
+    vt, _ = lib.compute(np.ascontiguousarray(M.T), with_marginals=marg)
+    assert vt == v
+
+
 def test_planted_40x40_marg(lib):
     """BASELINE config 3 planted twin: shared-corner marginal direct sum."""
     M, c, subs = synth.planted_marg()
