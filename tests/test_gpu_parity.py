@@ -205,6 +205,21 @@ def test_bench_workload_families_and_metamorphic(lib, marg, monkeypatch):
     assert vt == v
 
 
+@pytest.mark.parametrize("d,n,seed", [(3, 24, 4), (3, 26, 226), (4, 18, 218)])
+def test_ld_workload_families_agree(lib, d, n, seed, monkeypatch):
+    """BASELINE config 4 / 5b sizes in full: the byte d-ary walk (three rows paired) and the
+    independent last-row-paired 16-bit walk agree on value and canonical (RGS) argmax; the
+    argmax attains the value (oracle, from scratch)."""
+    M = synth.random_matrix(n, n, seed)
+    assert lib.plan(M, d=d)["variant_name"] == "ld_u8"
+    v, arg = lib.compute(M, d=d)
+    assert oracle.value(M, arg, d=d) == v
+    monkeypatch.setenv("LNORM_KERNEL", "pair16")
+    assert lib.plan(M, d=d)["variant_name"] == "ld_pair16"
+    v2, arg2 = lib.compute(M, d=d)
+    assert v2 == v and list(arg2) == list(arg)
+
+
 def test_planted_40x40_marg(lib):
     """BASELINE config 3 planted twin: shared-corner marginal direct sum."""
     M, c, subs = synth.planted_marg()
