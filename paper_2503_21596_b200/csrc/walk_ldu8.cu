@@ -30,6 +30,9 @@ constexpr int kTabWordsLU = 16384;
 #ifndef LN_LDU8_MINB
 #define LN_LDU8_MINB 12
 #endif
+#ifndef LN_LDU8_MINB3
+#define LN_LDU8_MINB3 14                 // d = 3, three paired rows, <= 28 columns: measured +2-3 %
+#endif
 
 __host__ __device__ constexpr int lu_pad4(int x) { return (x + 3) & ~3; }
 
@@ -246,7 +249,7 @@ struct LdU8 {
 // Init records (global int32, stride CW = 4 NW): prefix rows 0..k, the base (walked
 // rows at label 0), -N_y, then the packed bias words of the NS sets and their K_m.
 template <int D, int NW, int P, int PR>
-__global__ void __launch_bounds__(kBlockLU, (D * NW * P * (PR >= 2 ? PR : 1) <= 72 ? LN_LDU8_MINB : 1))
+__global__ void __launch_bounds__(kBlockLU, ((PR == 3 && D == 3 && D * NW * P * PR <= 63) ? LN_LDU8_MINB3 : (D * NW * P * (PR >= 2 ? PR : 1) <= 72 ? LN_LDU8_MINB : 1)))
 walk_ldu8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int32_t* __restrict__ gInit) {
   using WK = LdU8<D, NW, P, PR>;
   constexpr int RD = WK::RD, CW = 4 * NW, NS = WK::NS;
@@ -419,7 +422,10 @@ __global__ void build_ldu8_kernel(const int32_t* M, int r, int c, int NW, int k,
 // per-unit bytes and the 2^PR bias sets would not fit the register budget)
 template <int D, int NW, int PR>
 constexpr int ldu8_units_per_lane() {
-  return PR == 3 ? (D * NW <= 12 ? 2 : 1)
+#ifndef LN_LDU8_P3
+#define LN_LDU8_P3 12
+#endif
+  return PR == 3 ? (D * NW <= LN_LDU8_P3 ? 2 : 1)
        : D * NW * (PR == 2 ? 2 : 1) <= 24 ? LN_LDU8_PMAX : (D * NW <= 48 ? (LN_LDU8_PMAX < 2 ? LN_LDU8_PMAX : 2) : 1);
 }
 
