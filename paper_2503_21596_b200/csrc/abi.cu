@@ -757,7 +757,7 @@ const char* lnorm_status_string(int status) {
   }
 }
 
-int32_t lnorm_version(void) { return (1 << 16) | 0; }
+int32_t lnorm_version(void) { return (1 << 16) | 1; }   // 1.1: lnorm_plan_info.lanes_per_unit
 
 int lnorm_compute(const int32_t* M, int32_t n, int32_t m, int32_t d, int32_t with_marginals,
                   int64_t* value, int8_t* argmax) {
