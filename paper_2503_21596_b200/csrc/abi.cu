@@ -188,6 +188,7 @@ struct Plan {
   int kernel = K_GEN;
   int k = 0, s = 0;
   int u8_lpu = 1;                // byte walk: lanes per unit
+  int key_shift = 0;             // reduction keys carry unit >> key_shift (units > 2^32, byte walk)
   int64_t units = 1;
   std::vector<uint64_t> table;   // packed prefixes (RGS for d >= 3, explicit for hooks); empty = arithmetic
   // RGS plans: the process-wide immutable prefix list for (k, d), shared instead of copied
@@ -196,6 +197,7 @@ struct Plan {
 };
 
 constexpr int64_t kNominalLanes = 148LL * 1024;   // plan is hardware-independent => identical on every rank
+constexpr int kMaxKeyShift = 4;                    // byte walk: up to 2^35 units (the recovery re-walks 16)
 constexpr int64_t kTableCap = 1LL << 22;
 
 // All restricted-growth prefixes of length k+1 with labels < d, in lexicographic order.
@@ -260,7 +262,7 @@ int make_plan(const Problem& pr, int world, Plan* pl, int64_t target_override = 
           if (u8_fits(pr, s_ + lg) && walk_u8_supported(pr.mode, pr.c, s_, lpu)) su = s_;
         int s_lo = 0;
         for (int s_ = 1; s_ <= su; ++s_) if (walk_u8_supported(pr.mode, pr.c, s_, lpu)) { s_lo = s_; break; }
-        if (su > 0 && s_lo > 0 && f - su <= 31) {
+        if (su > 0 && s_lo > 0 && f - su <= 31 + kMaxKeyShift) {
           int k = std::max(lg, f - su);
           while (k < f - s_lo && k < 31 && (1LL << k) < target) ++k;
           // short suffixes spend their time in the lane init: keep s >= 10 while the split
@@ -269,6 +271,9 @@ int make_plan(const Problem& pr, int world, Plan* pl, int64_t target_override = 
           p.k = k; p.s = f - k; p.units = 1LL << k;
           p.kernel = K_U8;
           p.u8_lpu = lpu;
+          p.key_shift = std::max(0, k - 31);
+          if (const char* e = getenv("LNORM_KEY_SHIFT"))       // test hook: force coarse keys
+            p.key_shift = std::max(p.key_shift, std::min(atoi(e), std::min(k, kMaxKeyShift)));
           *pl = std::move(p);
           return LNORM_OK;
         }
@@ -282,6 +287,8 @@ int make_plan(const Problem& pr, int world, Plan* pl, int64_t target_override = 
     else if (si > 0) { kern = K_BIN; smin = si; }
     int k = 0;
     while (k < f - smin && k < 31 && (1LL << k) < target) ++k;
+    // a unit's walk counts its words in 32 bits: at most 31 suffix digits (r <= 63)
+    if (f - k > 31) k = std::min(31, f - 31);
     p.k = k; p.s = f - k; p.units = 1LL << k;
     p.kernel = kern;
     if (kern == K_BIN16 && !walk_bin16_table_fits(pr.mode, pr.c, p.k, p.s))
@@ -328,7 +335,7 @@ int make_plan(const Problem& pr, int world, Plan* pl, int64_t target_override = 
   // per-unit word count must fit 32-bit block counters
   long double words = 1;
   for (int i = 0; i < p.s; ++i) words *= pr.dl;
-  if (words >= 4.0e9L || p.units >= (1LL << 32)) return LNORM_ETOOLARGE;
+  if (words >= 4.0e9L || (p.units >> p.key_shift) >= (1LL << 32)) return LNORM_ETOOLARGE;
   *pl = std::move(p);
   return LNORM_OK;
 }
@@ -356,7 +363,7 @@ struct FinalizeArgs {
   const unsigned long long* lex;   // [batch] smallest optimal suffix keys
   const uint64_t* table;   // full prefix table or null (binary arithmetic)
   const int32_t* Min;      // original (un-oriented) input, n x m
-  int n, m, r, k, s, base, mode, transposed, pbits;
+  int n, m, r, k, s, base, mode, transposed, pbits, key_shift;
   int64_t* value_out;      // [batch]
   int8_t* argmax_out;      // int8[batch][n]
 };
@@ -370,12 +377,13 @@ __global__ void finalize_kernel(FinalizeArgs a) {
   const unsigned long long key = a.key[blockIdx.x], lex = a.lex[blockIdx.x];
   a.Min += (int64_t)blockIdx.x * a.n * a.m;
   a.argmax_out += (int64_t)blockIdx.x * a.n;
-  const int64_t u = (int64_t)key_unit(key);
+  // unit = key group start + the group offset recovery found (high word of lex)
+  const int64_t u = ((int64_t)key_unit(key) << a.key_shift) + (int64_t)(lex >> 32);
   if (threadIdx.x == 0) {
     a.value_out[blockIdx.x] = (int64_t)key_value(key);
     for (int x = 0; x <= a.k; ++x)
       dig[x] = a.table ? (int8_t)((a.table[u] >> (a.pbits * x)) & ((1ull << a.pbits) - 1ull)) : (int8_t)(x == 0 ? 0 : (u >> (a.k - x)) & 1);
-    uint64_t q = lex;
+    uint64_t q = lex & 0xFFFFFFFFull;
     for (int i = 0; i < a.s; ++i) { dig[a.r - 1 - i] = (int8_t)(q % (uint64_t)a.base); q /= (uint64_t)a.base; }
   }
   __syncthreads();
@@ -589,6 +597,7 @@ int run_device(DevCtx& cx, const int32_t* dIn, const Problem& pr, int rank, int 
   WalkParams wp{};
   wp.M = cx.dM; wp.r = pr.r; wp.c = pr.c; wp.mode = pr.mode; wp.d = pr.dl; wp.k = pl.k; wp.s = pl.s;
   wp.pbits = prefix_bits(pr.dl);
+  wp.key_shift = pl.key_shift;
   wp.counter = cx.dCtl; wp.key = cx.dCtl + 1; wp.unit_max = nullptr;
   CU(cudaEventRecord(cx.ev[1], s));
   if (ck && ck->path && world == 1 && vslices <= 1) {
@@ -668,6 +677,7 @@ int run_device(DevCtx& cx, const int32_t* dIn, const Problem& pr, int rank, int 
   FinalizeArgs fa;
   fa.key = cx.dCtl + 1; fa.lex = cx.dCtl + 2; fa.table = rp.prefix_table; fa.Min = dIn; fa.n = pr.n; fa.m = pr.m; fa.r = pr.r;
   fa.k = pl.k; fa.s = pl.s; fa.base = pr.dl; fa.mode = pr.mode; fa.transposed = pr.transposed ? 1 : 0; fa.pbits = prefix_bits(pr.dl);
+  fa.key_shift = pl.key_shift;
   fa.value_out = cx.dRes; fa.argmax_out = reinterpret_cast<int8_t*>(cx.dRes + 1);
   finalize_kernel<<<1, 256, 0, s>>>(fa);
   ++launches;
@@ -1032,6 +1042,7 @@ int lnorm_compute_batch(const int32_t* M, int32_t batch, int32_t n, int32_t m, i
   FinalizeArgs fa;
   fa.key = keys; fa.lex = lex; fa.table = nullptr; fa.Min = dIn; fa.n = n; fa.m = m; fa.r = pr.r;
   fa.k = pl.k; fa.s = pl.s; fa.base = 2; fa.mode = pr.mode; fa.transposed = pr.transposed ? 1 : 0; fa.pbits = 1;
+  fa.key_shift = 0;
   fa.value_out = vals; fa.argmax_out = args;
   finalize_kernel<<<batch, 128, 0, s>>>(fa);
   CU(cudaGetLastError());

@@ -42,6 +42,11 @@ struct WalkParams {
   int64_t m_stride, tab_stride, init_stride;
   uint32_t one;                  // = 1 (a uniform operand the compiler cannot fold)
   int32_t u8_lpu;                // byte walk: lanes per unit (1, or 2 for > 128 columns)
+  // reduction keys carry unit >> key_shift (a 32-bit "key unit"): splits with more than 2^32
+  // units (byte walk only) compare groups of 2^key_shift consecutive units; the recovery then
+  // re-walks the whole winning group (lex order = unit order, so the smallest group holding
+  // an optimum holds the smallest optimal unit)
+  int32_t key_shift;
 };
 
 // Defaults for a single-matrix launch.
@@ -175,8 +180,9 @@ cudaError_t walk_ldu8_launch(const WalkParams& p, int32_t* scratch_tab, int32_t*
 bool walk_generic_supported(int d, int c);
 cudaError_t walk_generic_launch(const WalkParams& p, int grid, cudaStream_t st, int* block_out);
 int walk_generic_occupancy(int d, int c, int* block_out);
-// Argmax recovery: re-walk unit key_unit(*key) and write the smallest
-// lexicographic suffix key attaining key_value(*key) into *lex_out (atomicMin).
+// Argmax recovery: re-walk the units key_unit(*key) << key_shift .. + 2^key_shift - 1 and
+// write the smallest (unit offset << 32 | lexicographic suffix key) attaining
+// key_value(*key) into *lex_out (atomicMin).
 cudaError_t recover_launch(const WalkParams& p, unsigned long long* lex_out, cudaStream_t st);
 // Trace: per-step values of one unit (test hook).
 cudaError_t trace_launch(const WalkParams& p, int64_t max_steps, int64_t* values, int8_t* digits,

@@ -118,24 +118,31 @@ __global__ void __launch_bounds__(32 * kGenWarps) recover_kernel(const WalkParam
   const uint64_t words = ipow64(base, p.s);
   const unsigned long long key = *p.key;
   const int32_t target = key_value(key);
-  const int64_t u = (int64_t)key_unit(key);
+  const int64_t g0 = (int64_t)key_unit(key) << p.key_shift;    // first unit of the winning key group
+  const int64_t gcount = 1LL << p.key_shift;
   const uint64_t T = (uint64_t)gridDim.x * kGenWarps;
   const uint64_t t = (uint64_t)blockIdx.x * kGenWarps + wib;
   const uint64_t J = words / T, R = words % T;
   const uint64_t lo = t * J + (t < R ? t : R);
   const uint64_t hi = lo + J + (t < R ? 1 : 0);
   if (lo >= hi) return;
-  gen_init(p, u, lo, G, lane);
-  uint64_t lex = 0;
-  for (int i = 0; i < p.s; ++i) lex += (uint64_t)dary_digit(base, (uint32_t)i, lo) * ipow64(base, i);
   unsigned long long bestlex = ~0ull;
-  if (gen_value(p, G, lane) == target) bestlex = lex;
-  for (uint64_t w = lo + 1; w < hi; ++w) {
-    uint32_t i, from, to;
-    dary_change_values(base, w, &i, &from, &to);
-    gen_move(p, G, p.r - 1 - (int)i, (int)from, (int)to, lane);
-    lex = lex + (uint64_t)to * ipow64(base, (int)i) - (uint64_t)from * ipow64(base, (int)i);
-    if (gen_value(p, G, lane) == target && lex < bestlex) bestlex = lex;
+  for (int64_t o = 0; o < gcount; ++o) {
+    const int64_t u = g0 + o;
+    if (u >= p.unit_begin + p.unit_count) break;              // (a group may run past the last unit)
+    gen_init(p, u, lo, G, lane);
+    uint64_t lex = 0;
+    for (int i = 0; i < p.s; ++i) lex += (uint64_t)dary_digit(base, (uint32_t)i, lo) * ipow64(base, i);
+    const unsigned long long hiword = (unsigned long long)o << 32;
+    if (gen_value(p, G, lane) == target && (hiword | lex) < bestlex) bestlex = hiword | lex;
+    for (uint64_t w = lo + 1; w < hi; ++w) {
+      uint32_t i, from, to;
+      dary_change_values(base, w, &i, &from, &to);
+      gen_move(p, G, p.r - 1 - (int)i, (int)from, (int)to, lane);
+      lex = lex + (uint64_t)to * ipow64(base, (int)i) - (uint64_t)from * ipow64(base, (int)i);
+      if (gen_value(p, G, lane) == target && (hiword | lex) < bestlex) bestlex = hiword | lex;
+    }
+    if (bestlex != ~0ull) break;                              // an earlier unit of the group wins
   }
   if (lane == 0 && bestlex != ~0ull) atomicMin(lex_out, bestlex);
 }

@@ -395,7 +395,7 @@ walk_u8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int3
       const int64_t u = g * P + j;
       if (u >= p.unit_begin && u < u_end && half == 0) {
         if (p.unit_max) p.unit_max[u - p.unit_begin] = best[j];
-        if (!have || best[j] > best_all) { best_all = best[j]; best_u = (uint32_t)u; have = true; }
+        if (!have || best[j] > best_all) { best_all = best[j]; best_u = (uint32_t)(u >> p.key_shift); have = true; }
       }
     }
   }

@@ -197,13 +197,24 @@ def test_plan_packed_guard_and_fallback():
 
 
 def test_plan_lane_pairs_for_wide_rows():
-    """Beyond 128 columns the byte walk splits a unit over a lane pair where the extra window
-    row still fits the byte guard, else it keeps one lane per unit (48x192: k would exceed 31)."""
+    """Beyond 128 columns the byte walk splits a unit over a lane pair; the extra window row
+    shortens the suffix, and splits beyond 2^31 units use coarse reduction keys (48x192: k = 32)."""
     from paper_2503_21596_b200 import synth
     assert L.plan(synth.random_matrix(42, 168, 142))["lanes_per_unit"] == 2
     P = L.plan(synth.random_matrix(48, 192, 148))
-    assert P["variant_name"] == "bin_u8" and P["lanes_per_unit"] == 1 and P["prefix_digits"] == 31
+    assert P["variant_name"] == "bin_u8" and P["lanes_per_unit"] == 2 and P["prefix_digits"] == 32
     assert L.plan(synth.random_matrix(42, 42, 2))["lanes_per_unit"] == 1
+
+
+def test_plan_large_rows_use_byte_walk_and_reach_63_rows():
+    """50-52 rows keep the byte walk (more than 2^31 units: coarse keys); up to 63 rows plan
+     with at most 31 suffix digits per unit."""
+    from paper_2503_21596_b200 import synth
+    P = L.plan(synth.random_matrix(50, 50, 7))
+    assert P["variant_name"] == "bin_u8" and P["prefix_digits"] > 31
+    for n in (56, 60, 63):
+        P = L.plan(synth.random_matrix(n, n, 7))
+        assert P["suffix_digits"] <= 31 and P["prefix_digits"] <= 31 and P["steps"] == 2.0 ** (n - 1)
 
 
 def test_plan_is_identical_for_every_rank_and_grows_with_world():

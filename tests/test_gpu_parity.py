@@ -220,6 +220,27 @@ def test_ld_workload_families_agree(lib, d, n, seed, monkeypatch):
     assert v2 == v and list(arg2) == list(arg)
 
 
+@pytest.mark.parametrize("shift", [1, 3, 4])
+def test_coarse_reduction_keys_exact(lib, shift, monkeypatch):
+    """Splits with more than 2^31 units (50+ rows) reduce on unit >> shift and recover the
+    whole winning group; forced here on small inputs (LNORM_KEY_SHIFT): same value and the
+    same lexicographically smallest argmax as the oracle, including tie-heavy inputs and the
+    multi-rank slices."""
+    monkeypatch.setenv("LNORM_KEY_SHIFT", str(shift))
+    cases = [(synth.random_matrix(14, 16, 65_000 + shift), 1, False),
+             (synth.random_matrix(13, 15, 65_100 + shift), 1, True),
+             (synth.random_matrix(12, 14, 65_200 + shift), 2, False),
+             (np.eye(12, dtype=np.int32), 1, False), (np.ones((11, 13), dtype=np.int32), 2, False),
+             (synth.random_matrix(14, 16, 65_300 + shift, -1, 1), 1, False)]
+    for M, d, marg in cases:
+        assert lib.plan(M, d=d, with_marginals=marg)["variant_name"] == "bin_u8"
+        check(lib, M, d=d, marg=marg)
+        ref = oracle.norm(M, d=d, with_marginals=marg)
+        for sl in (3, 8):
+            got = lib.compute_sliced(M, sl, d=d, with_marginals=marg)
+            assert got[0] == ref[0] and list(got[1]) == list(ref[1])
+
+
 def test_planted_40x40_marg(lib):
     """BASELINE config 3 planted twin: shared-corner marginal direct sum."""
     M, c, subs = synth.planted_marg()
