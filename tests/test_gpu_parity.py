@@ -241,6 +241,32 @@ def test_coarse_reduction_keys_exact(lib, shift, monkeypatch):
             assert got[0] == ref[0] and list(got[1]) == list(ref[1])
 
 
+def test_maximum_sizes(lib):
+    """The ABI limits: 1024 columns (and 1024 rows, searched transposed), 63 enumerated rows
+    (sampled through the hook with the byte kernel's lane groups), one past each limit rejected."""
+    check(lib, synth.random_matrix(5, 1024, 66_000), d=1)
+    check(lib, synth.random_matrix(5, 1024, 66_001), d=3)
+    T = synth.random_matrix(1024, 5, 66_002)                      # searched as its 5 x 1024 transpose
+    v, arg = lib.compute(T)
+    assert v == oracle.l1(np.ascontiguousarray(T.T))[0] and oracle.value(T, arg) == v
+    with pytest.raises(Exception):
+        lib.compute(synth.random_matrix(5, 1025, 66_003))
+    with pytest.raises(Exception):
+        lib.compute(synth.random_matrix(64, 64, 66_004))
+    # a full 63-row search is 2^62 strategies (and 63 x 20 would be searched transposed): the
+    # hook walks the 63 rows of per-prefix sub-searches instead (no orientation)
+    M = synth.random_matrix(63, 20, 66_005, -2, 2)
+    P = np.zeros((8, 55), dtype=np.int8)
+    g = synth.SplitMix64(66_006)
+    for i in range(8):
+        P[i, 1:53] = [g.next() % 2 for _ in range(52)]
+        P[i, :53] = P[i - i % 4, :53]
+        P[i, 53], P[i, 54] = (i % 4) >> 1, (i % 4) & 1
+    got = lib.prefix_maxima(M, P)
+    for i in range(8):
+        assert got[i] == oracle.prefix_max(M, P[i])[0]
+
+
 def test_planted_40x40_marg(lib):
     """BASELINE config 3 planted twin: shared-corner marginal direct sum."""
     M, c, subs = synth.planted_marg()
