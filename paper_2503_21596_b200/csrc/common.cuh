@@ -176,6 +176,10 @@ int walk_ldu8_units_per_lane(int d, int c, int s);
 int walk_ldu8_occupancy(int d, int c, int s, int* block_out);
 cudaError_t walk_ldu8_launch(const WalkParams& p, int32_t* scratch_tab, int32_t* scratch_init, int grid,
                              cudaStream_t st, int* block_out);
+template <int D, int PART> int walk_ldu8_upl_part(int NW, int s);
+template <int D, int PART> int walk_ldu8_occ_part(int NW, int s);
+template <int D, int PART> cudaError_t walk_ldu8_launch_part(const WalkParams& p, const uint32_t* tab, const int32_t* init,
+                                                             int grid, cudaStream_t st, int NW);
 // Generic warp-per-unit walk (any mode, d, c, s).
 bool walk_generic_supported(int d, int c);
 cudaError_t walk_generic_launch(const WalkParams& p, int grid, cudaStream_t st, int* block_out);
