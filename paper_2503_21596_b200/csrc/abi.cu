@@ -197,7 +197,7 @@ struct Plan {
 };
 
 constexpr int64_t kNominalLanes = 148LL * 1024;   // plan is hardware-independent => identical on every rank
-constexpr int kMaxKeyShift = 4;                    // byte walk: up to 2^35 units (the recovery re-walks 16)
+constexpr int kMaxKeyShift = 8;                    // byte walk: up to 2^39 units (the recovery re-walks <= 256)
 constexpr int64_t kTableCap = 1LL << 22;
 
 // All restricted-growth prefixes of length k+1 with labels < d, in lexicographic order.

@@ -207,14 +207,16 @@ def test_plan_lane_pairs_for_wide_rows():
 
 
 def test_plan_large_rows_use_byte_walk_and_reach_63_rows():
-    """50-52 rows keep the byte walk (more than 2^31 units: coarse keys); up to 63 rows plan
-     with at most 31 suffix digits per unit."""
+    """50-56 rows keep the byte walk (more than 2^31 units: coarse keys, up to 2^39 units);
+    up to 63 rows plan with at most 31 suffix digits per unit."""
     from paper_2503_21596_b200 import synth
-    P = L.plan(synth.random_matrix(50, 50, 7))
-    assert P["variant_name"] == "bin_u8" and P["prefix_digits"] > 31
+    for n in (50, 56):
+        P = L.plan(synth.random_matrix(n, n, 7))
+        assert P["variant_name"] == "bin_u8" and 31 < P["prefix_digits"] <= 39
     for n in (56, 60, 63):
         P = L.plan(synth.random_matrix(n, n, 7))
-        assert P["suffix_digits"] <= 31 and P["prefix_digits"] <= 31 and P["steps"] == 2.0 ** (n - 1)
+        assert P["suffix_digits"] <= 31 and P["steps"] == 2.0 ** (n - 1)
+        assert P["prefix_digits"] <= (39 if P["variant_name"] == "bin_u8" else 31)
 
 
 def test_plan_is_identical_for_every_rank_and_grows_with_world():
