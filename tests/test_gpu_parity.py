@@ -267,6 +267,17 @@ def test_maximum_sizes(lib):
         assert got[i] == oracle.prefix_max(M, P[i])[0]
 
 
+def test_coarse_keys_full_size_planted(lib, monkeypatch):
+    """Coarse keys at the bench size: the planted 42x42 twin with groups of 256 units per key
+    gives the exact value (sum of the blocks) and the same canonical argmax as exact keys."""
+    M, blocks = synth.planted_l1()
+    expect = sum(oracle.l1(B)[0] for B in blocks)
+    v0, a0 = lib.compute(M)
+    monkeypatch.setenv("LNORM_KEY_SHIFT", "8")
+    v8, a8 = lib.compute(M)
+    assert v0 == v8 == expect and list(a8) == list(a0) and oracle.value(M, a8) == v8
+
+
 def test_planted_40x40_marg(lib):
     """BASELINE config 3 planted twin: shared-corner marginal direct sum."""
     M, c, subs = synth.planted_marg()
