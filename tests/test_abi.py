@@ -219,6 +219,30 @@ def test_plan_large_rows_use_byte_walk_and_reach_63_rows():
         assert P["prefix_digits"] <= (39 if P["variant_name"] == "bin_u8" else 31)
 
 
+@pytest.mark.parametrize("hi", [10, 40])
+def test_plan_invariants_over_shapes(hi):
+    """Every plan covers exactly the canonical strategy space (2^(r-1) words for +-1 / L_2):
+    units x 2^s = steps, s <= 31, units below the key range, byte plans only where the window
+    guard holds, for every row count up to 63 and several column counts."""
+    from paper_2503_21596_b200 import synth
+    for n in list(range(2, 64, 3)) + [63]:
+        for m in (n, 7, 64, 130, 192):
+            M = synth.random_matrix(n, m, 3 * n + m + hi, -hi, hi)
+            for d, marg in ((1, False), (1, True), (2, False)):
+                try:
+                    P = L.plan(M, d=d, with_marginals=marg)
+                except L.LNormError:
+                    continue                                      # ETOOLARGE / EOVERFLOW limits
+                r = P["rows"]
+                assert P["units"] * 2.0 ** P["suffix_digits"] == P["steps"] == 2.0 ** (r - 1)
+                assert P["suffix_digits"] <= 31 and P["prefix_digits"] + P["suffix_digits"] == r - 1
+                assert P["prefix_digits"] <= (39 if P["variant_name"] == "bin_u8" else 31)
+                if P["variant_name"] == "bin_u8":     # the byte window holds at least the suffix rows
+                    A = np.abs(np.asarray(M if not P["transposed"] else M.T, dtype=np.int64))
+                    W = A[r - P["suffix_digits"]:].sum(axis=0).max()
+                    assert (2 * W <= 255) if d == 1 else (W <= 255)
+
+
 def test_plan_is_identical_for_every_rank_and_grows_with_world():
     from paper_2503_21596_b200 import synth
     M = synth.random_matrix(42, 42, 2)
