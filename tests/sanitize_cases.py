@@ -1,7 +1,7 @@
 """Small searches through every kernel family, for compute-sanitizer runs:
 
-compute-sanitizer --tool memcheck  python tools/sanitize_cases.py
-compute-sanitizer --tool racecheck python tools/sanitize_cases.py
+compute-sanitizer --tool memcheck  python tests/sanitize_cases.py
+compute-sanitizer --tool racecheck python tests/sanitize_cases.py
 
 Covers the byte kernels (L_1 / L_marg / L_2, aligned and unaligned Algorithm-1 slices, the
 grouped prefix hook; L_3 / L_4 with 1, 2 and 3 paired rows), the 16-bit and int32 families

@@ -1,8 +1,8 @@
-"""At-scale validation of the coarse-key byte walk: full 50x50 L_1 (2^49 strategies, 2^32
+"""(Test infrastructure: uses the oracle.) At-scale validation of the coarse-key byte walk: full 50x50 L_1 (2^49 strategies, 2^32
 units, key groups of 2) through the byte kernel and through the independent strategy-paired
 16-bit kernel; same value and canonical argmax, argmax attains the value (oracle, from scratch).
 
-python tools/validate_50x50.py [--out profiles/r01/validate_50x50.json]
+python tests/validate_50x50.py [--out profiles/r01/validate_50x50.json]
 """
 import argparse
 import json
