@@ -1,6 +1,8 @@
-"""(Test infrastructure: uses the oracle.) At-scale validation of the coarse-key byte walk: full 50x50 L_1 (2^49 strategies, 2^32
-units, key groups of 2) through the byte kernel and through the independent strategy-paired
-16-bit kernel; same value and canonical argmax, argmax attains the value (oracle, from scratch).
+"""At-scale validation of the coarse-key byte walk (test infrastructure: uses the oracle).
+
+Full 50x50 L_1 (2^49 strategies; seed 150 plans 2^36 units, reduced in key groups of 32)
+through the byte kernel and through the independent strategy-paired 16-bit kernel: same value
+and canonical argmax, and the argmax attains the value (oracle, from scratch).
 
 python tests/validate_50x50.py [--out profiles/r01/validate_50x50.json]
 """
