@@ -37,8 +37,18 @@
  *          after orientation for d = 1, or d^(n-1) >= 2^63 for d >= 2), or the
  *          problem exceeds the kernels' column limit (m > 1024 after
  *          orientation).  LNORM_ENODEV / ECUDA / ENCCL / ENOMEM: runtime.
+ *          LNORM_EINTERNAL: the always-on self-check of the argmax recovery
+ *          failed (the re-walk of the winning unit did not reproduce the
+ *          reduced maximum exactly: no strategy of the unit attains the key's
+ *          value, or one exceeds it); value and argmax are then untouched.
  *  Threads re-entrant per device (an internal per-device context is guarded by
  *          a mutex); all calls synchronise before returning.
+ *  Streams entry points taking `cuda_stream` (a cudaStream_t; NULL = the
+ *          library's internal non-blocking stream) enqueue ALL their device
+ *          work -- copies, kernels, the NCCL all-reduce -- on that stream, in
+ *          stream order after whatever the caller enqueued before the call,
+ *          and synchronise it before returning.  The other entry points use the
+ *          internal stream.
  *
  * Every step of the search runs in the library's sm_100a kernels; there is no
  * CPU fallback (no device => LNORM_ENODEV).
@@ -60,7 +70,8 @@ typedef enum {
   LNORM_ENODEV = 4,
   LNORM_ECUDA = 5,
   LNORM_ENCCL = 6,
-  LNORM_ENOMEM = 7
+  LNORM_ENOMEM = 7,
+  LNORM_EINTERNAL = 8
 } lnorm_status;
 
 /* Human-readable name of a status code (static storage). */
@@ -79,9 +90,14 @@ int lnorm_compute(const int32_t* M, int32_t n, int32_t m, int32_t d, int32_t wit
 
 /*
  * Same as lnorm_compute but M is a DEVICE pointer on the current device
- * (row-major n*m int32) and work is enqueued on `cuda_stream` (a
- * cudaStream_t; NULL = the library's internal stream).  Used to time the
- * search with its input already resident in HBM.  Synchronises before return.
+ * (row-major n*m int32, caller-owned, read-only) and the work is enqueued on
+ * `cuda_stream` (see "Streams"), so a producer kernel enqueued earlier on the
+ * same stream is complete before M is read.  Used to time the search with its
+ * input already resident in HBM.  The exactness guards (sum |M|, per-column
+ * window sums) are computed on the device by a one-block kernel; its ~0.5 KB
+ * result is copied back on the same stream and synchronised, because the plan
+ * (kernel family, prefix/suffix split) depends on them -- the only host round
+ * trip before the walk.  Synchronises before return.
  */
 int lnorm_compute_device(const int32_t* M_device, int32_t n, int32_t m, int32_t d,
                          int32_t with_marginals, void* cuda_stream,
@@ -99,25 +115,42 @@ int lnorm_compute_multi(const int32_t* M, int32_t n, int32_t m, int32_t d, int32
                         int64_t* value, int8_t* argmax);
 
 /*
- * One rank per GPU (torchrun): a communicator handle owned by the library.
+ * One rank per GPU (torchrun): rank `rank` of `world` walks its
+ * Algorithm-1 slice of the unit list, the 8-byte reduction key is
+ * all-reduced with ncclMax on `cuda_stream` (no host round trip), and every
+ * rank recovers and returns the same value and argmax (bit-identical).
+ * nccl_comm: a caller-owned ncclComm_t of exactly `world` ranks whose rank
+ * `rank` lives on the CURRENT CUDA device -- e.g. the communicator of a
+ * torch.distributed NCCL process group, or one made by lnorm_comm_create.  The
+ * library never destroys it.  nccl_comm == NULL is allowed only with world == 1
+ * (no collective).  With a non-NULL comm the all-reduce runs even at world == 1.
+ * M: host matrix (replicated on every rank); _device: M resident on the rank's
+ * device (as lnorm_compute_device).  Errors after the slice walk started still
+ * take part in the collective, so a failing rank never leaves its peers hanging.
+ */
+int lnorm_compute_rank(const int32_t* M, int32_t n, int32_t m, int32_t d, int32_t with_marginals,
+                       void* nccl_comm, int32_t rank, int32_t world, void* cuda_stream,
+                       int64_t* value, int8_t* argmax);
+int lnorm_compute_rank_device(const int32_t* M_device, int32_t n, int32_t m, int32_t d, int32_t with_marginals,
+                              void* nccl_comm, int32_t rank, int32_t world, void* cuda_stream,
+                              int64_t* value, int8_t* argmax);
+
+/*
+ * A library-made NCCL communicator for callers without one.
  * lnorm_comm_unique_id writes a 128-byte ncclUniqueId (rank 0 calls it and
  * broadcasts the bytes, e.g. through torch.distributed); every rank then calls
- * lnorm_comm_create with its rank, the world size and its CUDA device.
- * lnorm_compute_rank: rank r walks its Algorithm-1 slice of the units, the
- * 8-byte key is all-reduced (ncclMax) on the compute stream and every rank
- * returns the same value and argmax.  world == 1 with comm == NULL is allowed
- * (no collective).  Host buffer M (replicated on every rank).
+ * lnorm_comm_create with its rank, the world size and its CUDA device
+ * (ncclCommInitRank; a real communicator for every world >= 1 when `id` is
+ * given; id == NULL is allowed only with world == 1 and yields a handle without
+ * a communicator).  lnorm_comm_nccl returns the ncclComm_t (or NULL) to pass to
+ * lnorm_compute_rank; the handle owns it until lnorm_comm_destroy.
  */
 typedef struct lnorm_comm lnorm_comm;
 int lnorm_comm_unique_id(uint8_t id_out[128]);
 int lnorm_comm_create(const uint8_t id[128], int32_t rank, int32_t world, int32_t device,
                       lnorm_comm** comm_out);
+int lnorm_comm_nccl(lnorm_comm* comm, void** nccl_comm_out);
 int lnorm_comm_destroy(lnorm_comm* comm);
-int lnorm_compute_rank(lnorm_comm* comm, const int32_t* M, int32_t n, int32_t m, int32_t d,
-                       int32_t with_marginals, int64_t* value, int8_t* argmax);
-/* lnorm_compute_rank with M already resident on the rank's device (row-major n*m int32). */
-int lnorm_compute_rank_device(lnorm_comm* comm, const int32_t* M_device, int32_t n, int32_t m, int32_t d,
-                              int32_t with_marginals, int64_t* value, int8_t* argmax);
 
 /*
  * Checkpoint / resume for long searches: the unit list is walked in
@@ -138,10 +171,12 @@ int lnorm_compute_checkpointed(const int32_t* M, int32_t n, int32_t m, int32_t d
  * Batched search (the inner oracle of see-saw / branch-and-bound
  * loops): `batch` matrices of the same shape, contiguous
  * (batch x n x m int32, host).  values: int64[batch]; argmax: int8[batch][n]
- * (may be NULL), same conventions as lnorm_compute.  When every matrix is within
- * the strategy-paired packed path's guard (sum |M| <= 16383, d <= 2) one walk
- * launch covers the whole batch (units of all matrices in one grid, per-matrix
- * keys, batched recovery); otherwise the matrices are searched one after another.
+ * (may be NULL), same conventions as lnorm_compute.  One walk launch covers the
+ * whole batch (units of all matrices in one grid, per-matrix keys, batched
+ * recovery and finalisation): the strategy-paired packed kernel when every
+ * matrix is within its guard (sum |M| <= 16383, d <= 2) and the shape has a
+ * long enough suffix, else the generic warp-per-unit kernel (any d, any shape).
+ * Any batch size (launches are chunked internally).
  */
 int lnorm_compute_batch(const int32_t* M, int32_t batch, int32_t n, int32_t m, int32_t d, int32_t with_marginals,
                         int64_t* values, int8_t* argmax);
@@ -186,6 +221,21 @@ int lnorm_compute_sliced(const int32_t* M, int32_t n, int32_t m, int32_t d, int3
  */
 int lnorm_prefix_maxima(const int32_t* M, int32_t n, int32_t m, int32_t d, int32_t with_marginals,
                         int32_t nfixed, const int8_t* prefixes, int64_t count, int64_t* out);
+
+/*
+ * SURVEY 8(b)'s sampled-parity hook in unit coordinates: the per-unit maxima of
+ * `count` units of the split with `prefix_digits` = k prefix rows beyond row 0
+ * (unit prefix = rows 0..k).  units[i] indexes the lexicographically ordered
+ * unit list lnorm_compute walks: for +-1 strategies and L_2 the digits of rows
+ * 1..k are the bits of units[i] (row k least significant, bit 1 = -1 / label 1),
+ * row 0 fixed; for d >= 3 units[i] is the index of the restricted-growth prefix
+ * (length k+1, at most min(d, n) labels) in lexicographic order.  unit_max[i]
+ * receives the maximum over all completions of unit i (no orientation: the
+ * rows are the caller's).  Same kernels as lnorm_prefix_maxima.  EINVAL if a
+ * unit index is out of range or k >= n.
+ */
+int lnorm_unit_maxima(const int32_t* M, int32_t n, int32_t m, int32_t d, int32_t with_marginals,
+                      int32_t prefix_digits, const uint64_t* units, int64_t count, int32_t* unit_max);
 
 /*
  * Test hook: the device walk of ONE unit, step by step.  Rows 0..nfixed-1 are

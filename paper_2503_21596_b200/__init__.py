@@ -18,7 +18,8 @@ import threading
 import numpy as np
 
 __all__ = [
-    "LNormError", "load", "compute", "compute_device", "compute_reduced", "compute_batch", "compute_multi", "Comm", "prefix_maxima",
+    "LNormError", "load", "compute", "compute_device", "compute_reduced", "compute_batch", "compute_multi", "Comm",
+    "compute_rank", "compute_rank_device", "torch_nccl_comm", "prefix_maxima", "unit_maxima",
     "walk_trace", "gray_digit", "gray_change", "partition", "last_stats", "status_string", "SYMBOLS", "plan",
 ]
 
@@ -28,14 +29,15 @@ LIB_PATH = os.environ.get("LNORM_LIB") or os.path.join(_HERE, "liblnorm.so")   #
 # every function include/lnorm.h declares (checked by tests/test_abi.py)
 SYMBOLS = [
     "lnorm_status_string", "lnorm_version", "lnorm_compute", "lnorm_compute_device", "lnorm_compute_multi",
-    "lnorm_comm_unique_id", "lnorm_comm_create", "lnorm_comm_destroy", "lnorm_compute_rank",
+    "lnorm_comm_unique_id", "lnorm_comm_create", "lnorm_comm_nccl", "lnorm_comm_destroy", "lnorm_compute_rank",
     "lnorm_compute_rank_device",
-    "lnorm_prefix_maxima", "lnorm_walk_trace", "lnorm_gray_digit", "lnorm_gray_change", "lnorm_partition",
+    "lnorm_prefix_maxima", "lnorm_unit_maxima", "lnorm_walk_trace", "lnorm_gray_digit", "lnorm_gray_change", "lnorm_partition",
     "lnorm_last_stats", "lnorm_plan", "lnorm_compute_sliced", "lnorm_compute_reduced", "lnorm_compute_batch",
     "lnorm_compute_checkpointed",
 ]
 
-STATUS = {0: "OK", 1: "EINVAL", 2: "EOVERFLOW", 3: "ETOOLARGE", 4: "ENODEV", 5: "ECUDA", 6: "ENCCL", 7: "ENOMEM"}
+STATUS = {0: "OK", 1: "EINVAL", 2: "EOVERFLOW", 3: "ETOOLARGE", 4: "ENODEV", 5: "ECUDA", 6: "ENCCL", 7: "ENOMEM",
+          8: "EINTERNAL"}
 
 
 class LNormError(RuntimeError):
@@ -99,10 +101,12 @@ def load():
             "lnorm_compute_multi": ([i32p, i32, i32, i32, i32, i32, i32p, i64p, i8p], ctypes.c_int),
             "lnorm_comm_unique_id": ([P(ctypes.c_uint8)], ctypes.c_int),
             "lnorm_comm_create": ([P(ctypes.c_uint8), i32, i32, i32, P(vp)], ctypes.c_int),
+            "lnorm_comm_nccl": ([vp, P(vp)], ctypes.c_int),
             "lnorm_comm_destroy": ([vp], ctypes.c_int),
-            "lnorm_compute_rank": ([vp, i32p, i32, i32, i32, i32, i64p, i8p], ctypes.c_int),
-            "lnorm_compute_rank_device": ([vp, vp, i32, i32, i32, i32, i64p, i8p], ctypes.c_int),
+            "lnorm_compute_rank": ([i32p, i32, i32, i32, i32, vp, i32, i32, vp, i64p, i8p], ctypes.c_int),
+            "lnorm_compute_rank_device": ([vp, i32, i32, i32, i32, vp, i32, i32, vp, i64p, i8p], ctypes.c_int),
             "lnorm_prefix_maxima": ([i32p, i32, i32, i32, i32, i32, i8p, i64, i64p], ctypes.c_int),
+            "lnorm_unit_maxima": ([i32p, i32, i32, i32, i32, i32, P(u64), i64, i32p], ctypes.c_int),
             "lnorm_walk_trace": ([i32p, i32, i32, i32, i32, i32, i8p, i64, i64p, i8p], ctypes.c_int),
             "lnorm_gray_digit": ([i32, i32, u64], i32),
             "lnorm_gray_change": ([i32, u64, i32p, i32p, i32p], ctypes.c_int),
@@ -139,11 +143,33 @@ def _check(rc: int, what: str):
         raise LNormError(rc, what)
 
 
+_I32 = np.iinfo(np.int32)
+
+
+def _int32(M, ndim: int, what: str):
+    """Exact int32 copy of an integer array: non-integer dtypes and out-of-range entries raise
+    (never a silent wrap or truncation, which would search a different matrix)."""
+    A = np.asarray(M)
+    if A.ndim != ndim:
+        raise ValueError(f"{what} must be a {ndim}-D integer array")
+    if A.dtype == np.bool_ or not np.issubdtype(A.dtype, np.integer):
+        raise TypeError(f"{what} must have an integer dtype, got {A.dtype}")
+    if A.size and A.dtype != np.int32 and (int(A.min()) < _I32.min or int(A.max()) > _I32.max):
+        raise LNormError(2, f"{what} has entries outside int32")
+    return np.ascontiguousarray(A, dtype=np.int32)
+
+
 def _mat(M):
-    A = np.ascontiguousarray(np.asarray(M), dtype=np.int32)
-    if A.ndim != 2:
-        raise ValueError("M must be a 2-D integer matrix")
-    return A
+    return _int32(M, 2, "M")
+
+
+def _stream_ptr(stream):
+    """cudaStream_t of a torch.cuda.Stream, a raw int handle, or None (library stream)."""
+    if stream is None:
+        return None
+    if hasattr(stream, "cuda_stream"):
+        return ctypes.c_void_p(int(stream.cuda_stream))
+    return ctypes.c_void_p(int(stream))
 
 
 def _p(a, ct):
@@ -163,16 +189,29 @@ def compute(M, d: int = 1, with_marginals: bool = False):
     return int(v.value), arg
 
 
+def _dev_mat(M_dev):
+    if len(M_dev.shape) != 2:
+        raise ValueError("M_dev must be 2-D")
+    dt = getattr(M_dev, "dtype", None)
+    if dt is not None and "int32" not in str(dt):
+        raise TypeError(f"M_dev must be int32, got {dt}")
+    if hasattr(M_dev, "is_contiguous") and not M_dev.is_contiguous():
+        raise ValueError("M_dev must be contiguous")
+    return int(M_dev.shape[0]), int(M_dev.shape[1])
+
+
 def compute_device(M_dev, d: int = 1, with_marginals: bool = False, stream=None):
     """Same as compute() for a matrix already resident on the device.
 
-    M_dev: a CUDA tensor-like object with ``data_ptr()`` and ``shape`` (int32, contiguous)."""
-    n, m = int(M_dev.shape[0]), int(M_dev.shape[1])
+    M_dev: a CUDA tensor-like object with ``data_ptr()`` and ``shape`` (int32, contiguous).
+    stream: torch.cuda.Stream / raw cudaStream_t / None; the search is enqueued on it, after
+    the work the caller queued there (e.g. the kernel that produced M_dev)."""
+    n, m = _dev_mat(M_dev)
     v = ctypes.c_int64()
     arg = np.zeros(n, dtype=np.int8)
-    st = ctypes.c_void_p(stream) if stream else None
-    _check(load().lnorm_compute_device(ctypes.c_void_p(M_dev.data_ptr()), n, m, d, int(with_marginals), st,
-                                       ctypes.byref(v), _p(arg, ctypes.c_int8)), "lnorm_compute_device")
+    _check(load().lnorm_compute_device(ctypes.c_void_p(M_dev.data_ptr()), n, m, d, int(with_marginals),
+                                       _stream_ptr(stream), ctypes.byref(v), _p(arg, ctypes.c_int8)),
+           "lnorm_compute_device")
     return int(v.value), arg
 
 
@@ -196,9 +235,7 @@ def compute_batch(Ms, d: int = 1, with_marginals: bool = False):
     """Many same-shape matrices in one call (batched walk when the packed guard holds).
 
     Ms: array-like (batch, n, m).  Returns (values int64[batch], argmax int8[batch, n])."""
-    A = np.ascontiguousarray(np.asarray(Ms), dtype=np.int32)
-    if A.ndim != 3:
-        raise ValueError("Ms must be (batch, n, m)")
+    A = _int32(Ms, 3, "Ms (batch, n, m)")
     b, n, m = A.shape
     vals = np.zeros(b, dtype=np.int64)
     args = np.zeros((b, n), dtype=np.int8)
@@ -248,11 +285,52 @@ def compute_multi(M, d: int = 1, with_marginals: bool = False, devices=None):
     return int(v.value), arg
 
 
-class Comm:
-    """A library-owned NCCL communicator for one rank of a torchrun job.
+def compute_rank(M, nccl_comm, rank: int, world: int, d: int = 1, with_marginals: bool = False, stream=None):
+    """One rank of a multi-GPU search (lnorm_compute_rank): `nccl_comm` is a caller-owned
+    ncclComm_t (int / c_void_p, e.g. ``torch_nccl_comm()``) spanning `world` ranks, or None
+    when world == 1.  Every rank returns the same (value, argmax)."""
+    A = _mat(M)
+    n, m = A.shape
+    v = ctypes.c_int64()
+    arg = np.zeros(n, dtype=np.int8)
+    _check(load().lnorm_compute_rank(_p(A, ctypes.c_int32), n, m, d, int(with_marginals),
+                                     ctypes.c_void_p(int(nccl_comm) if nccl_comm else 0), rank, world,
+                                     _stream_ptr(stream), ctypes.byref(v), _p(arg, ctypes.c_int8)),
+           "lnorm_compute_rank")
+    return int(v.value), arg
 
-    Rank 0 creates the 128-byte unique id with ``Comm.unique_id()`` and
-    broadcasts it (e.g. ``torch.distributed.broadcast_object_list``)."""
+
+def compute_rank_device(M_dev, nccl_comm, rank: int, world: int, d: int = 1, with_marginals: bool = False,
+                        stream=None):
+    """compute_rank with the matrix resident on this rank's device."""
+    n, m = _dev_mat(M_dev)
+    v = ctypes.c_int64()
+    arg = np.zeros(n, dtype=np.int8)
+    _check(load().lnorm_compute_rank_device(ctypes.c_void_p(M_dev.data_ptr()), n, m, d, int(with_marginals),
+                                            ctypes.c_void_p(int(nccl_comm) if nccl_comm else 0), rank, world,
+                                            _stream_ptr(stream), ctypes.byref(v), _p(arg, ctypes.c_int8)),
+           "lnorm_compute_rank_device")
+    return int(v.value), arg
+
+
+def torch_nccl_comm(group=None, device=None) -> int:
+    """The ncclComm_t of a torch.distributed NCCL process group (caller-owned; torch keeps it).
+
+    The group must have been initialised eagerly (``init_process_group(..., device_id=dev)``)
+    or have run a collective on `device`."""
+    import torch
+    import torch.distributed as dist
+    pg = group if group is not None else dist.distributed_c10d._get_default_group()
+    dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+    return int(pg._get_backend(dev)._comm_ptr())
+
+
+class Comm:
+    """A library-made NCCL communicator for one rank (lnorm_comm_create / _destroy).
+
+    Rank 0 creates the 128-byte unique id with ``Comm.unique_id()`` and broadcasts it
+    (e.g. ``torch.distributed.broadcast_object_list``).  uid=None is allowed for world 1
+    and gives a handle without a communicator (no collective)."""
 
     def __init__(self, uid: bytes | None, rank: int, world: int, device: int):
         self._h = ctypes.c_void_p()
@@ -266,23 +344,19 @@ class Comm:
         _check(load().lnorm_comm_unique_id(buf), "lnorm_comm_unique_id")
         return bytes(buf)
 
-    def compute(self, M, d: int = 1, with_marginals: bool = False):
-        A = _mat(M)
-        n, m = A.shape
-        v = ctypes.c_int64()
-        arg = np.zeros(n, dtype=np.int8)
-        _check(load().lnorm_compute_rank(self._h, _p(A, ctypes.c_int32), n, m, d, int(with_marginals),
-                                         ctypes.byref(v), _p(arg, ctypes.c_int8)), "lnorm_compute_rank")
-        return int(v.value), arg
+    @property
+    def nccl(self) -> int:
+        """The ncclComm_t this handle owns (0 if none)."""
+        out = ctypes.c_void_p()
+        _check(load().lnorm_comm_nccl(self._h, ctypes.byref(out)), "lnorm_comm_nccl")
+        return int(out.value or 0)
 
-    def compute_device(self, M_dev, d: int = 1, with_marginals: bool = False):
-        n, m = int(M_dev.shape[0]), int(M_dev.shape[1])
-        v = ctypes.c_int64()
-        arg = np.zeros(n, dtype=np.int8)
-        _check(load().lnorm_compute_rank_device(self._h, ctypes.c_void_p(M_dev.data_ptr()), n, m, d,
-                                                int(with_marginals), ctypes.byref(v), _p(arg, ctypes.c_int8)),
-               "lnorm_compute_rank_device")
-        return int(v.value), arg
+    def compute(self, M, d: int = 1, with_marginals: bool = False, stream=None):
+        return compute_rank(M, self.nccl, self.rank, self.world, d=d, with_marginals=with_marginals, stream=stream)
+
+    def compute_device(self, M_dev, d: int = 1, with_marginals: bool = False, stream=None):
+        return compute_rank_device(M_dev, self.nccl, self.rank, self.world, d=d, with_marginals=with_marginals,
+                                   stream=stream)
 
     def close(self):
         if self._h:
@@ -307,6 +381,17 @@ def prefix_maxima(M, prefixes, d: int = 1, with_marginals: bool = False):
     _check(load().lnorm_prefix_maxima(_p(A, ctypes.c_int32), n, m, d, int(with_marginals), P.shape[1],
                                       _p(P, ctypes.c_int8), P.shape[0], _p(out, ctypes.c_int64)),
            "lnorm_prefix_maxima")
+    return out
+
+
+def unit_maxima(M, prefix_digits: int, units, d: int = 1, with_marginals: bool = False):
+    """Per-unit maxima in the library's unit coordinates (lnorm_unit_maxima)."""
+    A = _mat(M)
+    n, m = A.shape
+    U = np.ascontiguousarray(np.asarray(units, dtype=np.uint64).reshape(-1))
+    out = np.zeros(U.shape[0], dtype=np.int32)
+    _check(load().lnorm_unit_maxima(_p(A, ctypes.c_int32), n, m, d, int(with_marginals), prefix_digits,
+                                    _p(U, ctypes.c_uint64), U.shape[0], _p(out, ctypes.c_int32)), "lnorm_unit_maxima")
     return out
 
 

@@ -13,6 +13,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -44,6 +45,9 @@ struct Nccl {
   ncclResult_t (*CommInitAll)(ncclComm_t*, int, const int*) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
+  ncclResult_t (*CommCount)(const ncclComm_t, int*) = nullptr;
+  ncclResult_t (*CommUserRank)(const ncclComm_t, int*) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
 };
@@ -65,9 +69,13 @@ Nccl& nccl() {
     n.CommInitAll = (decltype(n.CommInitAll))dlsym(h, "ncclCommInitAll");
     n.AllReduce = (decltype(n.AllReduce))dlsym(h, "ncclAllReduce");
     n.CommDestroy = (decltype(n.CommDestroy))dlsym(h, "ncclCommDestroy");
+    n.CommAbort = (decltype(n.CommAbort))dlsym(h, "ncclCommAbort");
+    n.CommCount = (decltype(n.CommCount))dlsym(h, "ncclCommCount");
+    n.CommUserRank = (decltype(n.CommUserRank))dlsym(h, "ncclCommUserRank");
     n.GroupStart = (decltype(n.GroupStart))dlsym(h, "ncclGroupStart");
     n.GroupEnd = (decltype(n.GroupEnd))dlsym(h, "ncclGroupEnd");
-    n.ok = n.GetUniqueId && n.CommInitRank && n.CommInitAll && n.AllReduce && n.CommDestroy;
+    n.ok = n.GetUniqueId && n.CommInitRank && n.CommInitAll && n.AllReduce && n.CommDestroy && n.CommAbort &&
+           n.CommCount && n.CommUserRank;
   });
   return n;
 }
@@ -86,22 +94,97 @@ struct Problem {
   int64_t sufW[kMaxRows + 1] = {};
 };
 
-// Byte-packed path guard (walk_u8_impl.cuh): a unit's window of column y spans
-// 2 W_y (L_1, L_marg: +-1 on every suffix row) or W_y (L_2), W_y = sum over the s
-// suffix rows of |M_xy|; it must fit an unsigned byte.
-void suffix_guard(const int32_t* M, int m, Problem* p) {
-  std::vector<int64_t> colw(p->c, 0);
-  p->sufW[0] = 0;
-  for (int s = 1; s <= p->r && s <= kMaxRows; ++s) {
-    const int x = p->r - s;
+// Exactness-guard statistics of the oriented matrix (the data-dependent half of
+// validation; the host computes them for host input, guard_stats_kernel for device
+// input -- same definitions):
+//   S       = sum |M_ij| (int64; > 2^31-1 => EOVERFLOW, P:259 integer exactness)
+//   par[i]  = packed column-pair guard: sum over the columns y >= c0 with (y - c0) & 1 == i
+//             of sum_x |M_xy| (c0 = 1 for L_marg's linear column, else 0)
+//   sufW[s] = byte-path guard: max over columns y of sum over the last s enumerated rows
+//             of |M_xy| (s = 1..r)
+struct GuardStats {
+  int64_t S = 0;
+  int64_t par[2] = {0, 0};
+  int64_t sufW[kMaxRows + 1] = {};
+};
+
+// Entry (x, y) of the ORIENTED r x c matrix from the caller's n x m M.
+inline int64_t oriented(const int32_t* M, int m, bool transposed, int x, int y) {
+  return transposed ? M[(int64_t)y * m + x] : M[(int64_t)x * m + y];
+}
+
+void host_stats(const int32_t* M, const Problem& p, GuardStats* g) {
+  std::vector<int64_t> colw(p.c, 0);
+  g->sufW[0] = 0;
+  for (int s = 1; s <= p.r; ++s) {
+    const int x = p.r - s;
     int64_t mx = 0;
-    for (int y = 0; y < p->c; ++y) {
-      int64_t v = p->transposed ? M[(int64_t)y * m + x] : M[(int64_t)x * m + y];
+    for (int y = 0; y < p.c; ++y) {
+      const int64_t v = oriented(M, p.m, p.transposed, x, y);
       colw[y] += v < 0 ? -v : v;
       mx = std::max(mx, colw[y]);
     }
-    p->sufW[s] = mx;
+    g->sufW[s] = mx;
   }
+  const int c0 = p.mode == MODE_MARG ? 1 : 0;
+  g->S = 0; g->par[0] = g->par[1] = 0;
+  for (int y = 0; y < p.c; ++y) {
+    g->S += colw[y];
+    if (y >= c0) g->par[(y - c0) & 1] += colw[y];
+  }
+}
+
+// One block: each thread owns columns y = tid, tid + blockDim, ... (c <= 1024).
+__global__ void guard_stats_kernel(const int32_t* M, int m, int transposed, int r, int c, int marg,
+                                   long long* out) {
+  __shared__ long long red[32];
+  constexpr int kPer = kMaxCols / 256;
+  long long colw[kPer];
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) colw[i] = 0;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  auto block_reduce = [&](long long v, bool is_max) -> long long {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const long long w = __shfl_xor_sync(0xffffffffu, v, o);
+      v = is_max ? (w > v ? w : v) : v + w;
+    }
+    __syncthreads();
+    if (lane == 0) red[wid] = v;
+    __syncthreads();
+    long long t = is_max ? red[0] : 0;
+    for (int i = is_max ? 1 : 0; i < nw; ++i) t = is_max ? (red[i] > t ? red[i] : t) : t + red[i];
+    return t;
+  };
+  for (int s = 1; s <= r; ++s) {
+    const int x = r - s;
+    long long mx = 0;
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      const int y = threadIdx.x + i * blockDim.x;
+      if (y < c) {
+        const long long v = transposed ? M[(int64_t)y * m + x] : M[(int64_t)x * m + y];
+        colw[i] += v < 0 ? -v : v;
+        mx = colw[i] > mx ? colw[i] : mx;
+      }
+    }
+    mx = block_reduce(mx, true);
+    if (threadIdx.x == 0) out[3 + s - 1] = mx;
+  }
+  long long S = 0, p0 = 0, p1 = 0;
+  const int c0 = marg ? 1 : 0;
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) {
+    const int y = threadIdx.x + i * blockDim.x;
+    if (y < c) {
+      S += colw[i];
+      if (y >= c0) { if ((y - c0) & 1) p1 += colw[i]; else p0 += colw[i]; }
+    }
+  }
+  S = block_reduce(S, false);
+  p0 = block_reduce(p0, false);
+  p1 = block_reduce(p1, false);
+  if (threadIdx.x == 0) { out[0] = S; out[1] = p0; out[2] = p1; }
 }
 
 // log2 of the u8 kernel's lane group: its units differ in the last lane_bits prefix
@@ -111,37 +194,18 @@ int u8_lane_bits(const Problem& p, int lpu = 1) {
   return P >= 8 ? 3 : P >= 4 ? 2 : (P == 2 ? 1 : 0);
 }
 
+// Byte-packed path guard (walk_u8_impl.cuh): a unit's window of column y spans
+// 2 W_y (L_1, L_marg: +-1 on every window row) or W_y (L_2 / L_d), W_y = sum over the
+// window rows of |M_xy|; it must fit an unsigned byte.
 bool u8_fits(const Problem& p, int s) {
   if (s < 1 || s > p.r) return false;
   return p.mode == MODE_LD ? p.sufW[s] <= 255 : 2 * p.sufW[s] <= 255;
 }
 
-// Packed guard: for each parity class of the packed columns,
-// sum over its columns of sum_x |M_xy| <= 32767 bounds every 16-bit column sum and
-// every accumulator half.  M is the caller's n x m matrix; p gives the orientation.
-bool packed_guard(const int32_t* M, int m, const Problem& p) {
-  int64_t par[2] = {0, 0};
-  const int c0 = p.mode == MODE_MARG ? 1 : 0;
-  for (int y = c0; y < p.c; ++y) {
-    int64_t ca = 0;
-    for (int x = 0; x < p.r; ++x) {
-      int64_t v = p.transposed ? M[(int64_t)y * m + x] : M[(int64_t)x * m + y];
-      ca += v < 0 ? -v : v;
-    }
-    par[(y - c0) & 1] += ca;
-  }
-  return par[0] <= 32767 && par[1] <= 32767;
-}
-
-int validate(const int32_t* M, int n, int m, int d, int marg, Problem* pr) {
-  if (!M || n < 1 || m < 1 || d < 1 || d > kMaxD || (marg != 0 && marg != 1)) return LNORM_EINVAL;
+// Shape half of validation (no entries read): argument checks, orientation, limits.
+int validate_shape(int n, int m, int d, int marg, Problem* pr) {
+  if (n < 1 || m < 1 || d < 1 || d > kMaxD || (marg != 0 && marg != 1)) return LNORM_EINVAL;
   if (marg && d != 1) return LNORM_EINVAL;
-  int64_t S = 0;
-  for (int64_t i = 0; i < (int64_t)n * m; ++i) {
-    int64_t v = M[i];
-    S += v < 0 ? -v : v;
-    if (S > INT32_MAX) return LNORM_EOVERFLOW;
-  }
   Problem p;
   p.n = n; p.m = m; p.d = d; p.marg = marg;
   if (d == 1) {
@@ -156,14 +220,32 @@ int validate(const int32_t* M, int n, int m, int d, int marg, Problem* pr) {
     p.r = n; p.c = m;                     // never transposed
   }
   if (p.r > kMaxRows - 1 || p.c > kMaxCols) return LNORM_ETOOLARGE;
-  p.fits16 = packed_guard(M, m, p);
-  suffix_guard(M, m, &p);
-  p.fitsPair = S <= 16383;
-  p.fitsLdPair = S <= 32767;
   // search space d^(r-1) must fit a 63-bit word index
   long double space = 1;
   for (int i = 0; i < p.r - 1; ++i) space *= p.dl;
   if (space >= 9.2e18L) return LNORM_ETOOLARGE;
+  *pr = p;
+  return LNORM_OK;
+}
+
+// Data half: the guards that pick the exact kernel families.
+int apply_stats(const GuardStats& g, Problem* p) {
+  if (g.S > INT32_MAX) return LNORM_EOVERFLOW;
+  p->fits16 = g.par[0] <= 32767 && g.par[1] <= 32767;
+  for (int s = 0; s <= kMaxRows; ++s) p->sufW[s] = g.sufW[s];
+  p->fitsPair = g.S <= 16383;
+  p->fitsLdPair = g.S <= 32767;
+  return LNORM_OK;
+}
+
+int validate(const int32_t* M, int n, int m, int d, int marg, Problem* pr) {
+  if (!M) return LNORM_EINVAL;
+  Problem p;
+  int rc = validate_shape(n, m, d, marg, &p);
+  if (rc) return rc;
+  GuardStats g;
+  host_stats(M, p, &g);
+  if ((rc = apply_stats(g, &p))) return rc;
   *pr = p;
   return LNORM_OK;
 }
@@ -322,8 +404,9 @@ int make_plan(const Problem& pr, int world, Plan* pl, int64_t target_override = 
         auto v = std::make_shared<std::vector<uint64_t>>();
         rgs_enumerate(k + 1, d, *v, kTableCap + 1);
         std::lock_guard<std::mutex> g(mu);
-        cache[{k, d}] = v;
-        tab = v;
+        // a concurrent miss may have inserted the list first: keep that one (never replace
+        // an entry a device context may mirror)
+        tab = cache.emplace(std::make_pair(k, d), std::move(v)).first->second;
       }
       p.shared = tab;
     }
@@ -341,21 +424,38 @@ int make_plan(const Problem& pr, int world, Plan* pl, int64_t target_override = 
 }
 
 // --------------------------------------------------------------- kernels --
-__global__ void orient_kernel(const int32_t* in, int n, int m, int transpose, int32_t* out) {
+// Batched launches: matrices b = blockIdx.y, blockIdx.y + gridDim.y, ... < batch.
+__global__ void orient_kernel(const int32_t* in, int n, int m, int transpose, int32_t* out, int batch = 1) {
   const int64_t total = (int64_t)n * m;
-  in += blockIdx.y * total;     // batched launches: blockIdx.y = matrix
-  out += blockIdx.y * total;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    if (!transpose) out[i] = in[i];
-    else { const int64_t x = i / m, y = i % m; out[y * n + x] = in[i]; }
+  for (int b = blockIdx.y; b < batch; b += gridDim.y) {
+    const int32_t* ib = in + b * total;
+    int32_t* ob = out + b * total;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+      if (!transpose) ob[i] = ib[i];
+      else { const int64_t x = i / m, y = i % m; ob[y * n + x] = ib[i]; }
+    }
   }
 }
 
+// Control block of one search (device):
+//   [0] work counter (generic kernel)   [1] max reduction key   [2] error flag
+//   [3] min lexicographic suffix key (recovery)   [4] max value the recovery re-walk
+//   saw, biased like the key (self-check).  [1] and [2] are adjacent: the multi-rank
+//   all-reduce(max) combines the key and the "some rank failed" flag in ONE call.
+constexpr int kCtlWords = 5;
 __global__ void init_ctl_kernel(unsigned long long* ctl) {
-  ctl[0] = 0ull;        // work counter
-  ctl[1] = 0ull;        // max key
-  ctl[2] = ~0ull;       // min lexicographic suffix key
-  ctl[3] = 0ull;
+  ctl[0] = 0ull;
+  ctl[1] = 0ull;
+  ctl[2] = 0ull;
+  ctl[3] = ~0ull;
+  ctl[4] = 0ull;
+}
+
+// Test hook (LNORM_TEST_CORRUPT_KEY=delta): shift the reduced key's value by delta so
+// that the recovery self-check must fail.
+__global__ void corrupt_key_kernel(unsigned long long* key, int delta) {
+  const int32_t v = key_value(*key) + delta;
+  *key = make_key(v, key_unit(*key));
 }
 
 struct FinalizeArgs {
@@ -364,6 +464,7 @@ struct FinalizeArgs {
   const uint64_t* table;   // full prefix table or null (binary arithmetic)
   const int32_t* Min;      // original (un-oriented) input, n x m
   int n, m, r, k, s, base, mode, transposed, pbits, key_shift;
+  int64_t units;           // units per matrix (bounds the decoded winning unit)
   int64_t* value_out;      // [batch]
   int8_t* argmax_out;      // int8[batch][n]
 };
@@ -379,6 +480,13 @@ __global__ void finalize_kernel(FinalizeArgs a) {
   a.argmax_out += (int64_t)blockIdx.x * a.n;
   // unit = key group start + the group offset recovery found (high word of lex)
   const int64_t u = ((int64_t)key_unit(key) << a.key_shift) + (int64_t)(lex >> 32);
+  if (lex == ~0ull || u < 0 || u >= a.units) {
+    // the recovery found no strategy attaining the key (the host reports LNORM_EINTERNAL):
+    // decode nothing
+    if (threadIdx.x == 0) a.value_out[blockIdx.x] = INT64_MIN;
+    for (int x = threadIdx.x; x < a.n; x += blockDim.x) a.argmax_out[x] = 0;
+    return;
+  }
   if (threadIdx.x == 0) {
     a.value_out[blockIdx.x] = (int64_t)key_value(key);
     for (int x = 0; x <= a.k; ++x)
@@ -418,7 +526,13 @@ struct DevCtx {
   int32_t* dInit = nullptr;
   unsigned long long* dCtl = nullptr;
   uint64_t* dPre = nullptr; size_t capPre = 0;
-  const void* preSrc = nullptr;     // host list dPre currently mirrors (immutable RGS lists only)
+  // the immutable process-wide RGS list dPre currently mirrors (held, so its address
+  // cannot be reused by another list while this context refers to it); null = none
+  std::shared_ptr<const std::vector<uint64_t>> preHold;
+  long long* dStats = nullptr;      // guard_stats_kernel output (device input)
+  long long* hStats = nullptr;      // pinned mirror
+  unsigned long long* hCtl = nullptr;   // pinned mirror of the control block (self-check)
+  cudaStream_t cur = nullptr;       // stream of the call in progress (caller's or `stream`)
   int64_t* dRes = nullptr;          // [0] value, then int8 argmax[kMaxCols]
   int64_t* dUnit = nullptr; size_t capUnit = 0;
   int32_t* dRed = nullptr; size_t capRed = 0;      // reduction scratch + reduced matrix + maps
@@ -445,9 +559,13 @@ int ctx_get(int device, DevCtx** out) {
     CU(cudaDeviceGetAttribute(&c.nsm, cudaDevAttrMultiProcessorCount, device));
     CU(cudaMalloc(&c.dTab, sizeof(int32_t) * 32768));
     CU(cudaMalloc(&c.dInit, sizeof(int32_t) * 16384));
-    CU(cudaMalloc(&c.dCtl, sizeof(unsigned long long) * 4));
+    CU(cudaMalloc(&c.dCtl, sizeof(unsigned long long) * kCtlWords));
     CU(cudaMalloc(&c.dRes, 8 + kMaxCols + 64));
     CU(cudaMallocHost(&c.hRes, 8 + kMaxCols + 64));
+    CU(cudaMalloc(&c.dStats, sizeof(long long) * (3 + kMaxRows)));
+    CU(cudaMallocHost(&c.hStats, sizeof(long long) * (3 + kMaxRows)));
+    CU(cudaMallocHost(&c.hCtl, sizeof(unsigned long long) * kCtlWords));
+    c.cur = c.stream;
     c.device = device;
     c.ready = true;
   }
@@ -507,15 +625,16 @@ int launch_walk(DevCtx& cx, const Problem& pr, const Plan& pl, WalkParams& wp, i
   int64_t want = (wp.unit_count + per_block - 1) / per_block;
   int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)occ * cx.nsm, want));
   cudaError_t e;
-  if (pl.kernel == K_BIN) e = walk_bin_launch(wp, cx.dTab, grid, cx.stream, &block);
-  else if (pl.kernel == K_BIN16) e = walk_bin16_launch(wp, cx.dTab, grid, cx.stream, &block);
-  else if (pl.kernel == K_LD16) e = walk_ld16_launch(wp, cx.dTab, grid, cx.stream, &block);
-  else if (pl.kernel == K_PAIR16) e = walk_pair16_launch(wp, cx.dTab, cx.dInit, grid, cx.stream, &block);
-  else if (pl.kernel == K_U8) e = walk_u8_launch(wp, cx.dTab, cx.dInit, grid, cx.stream, &block);
-  else if (pl.kernel == K_LDPAIR16) e = walk_ldpair16_launch(wp, cx.dTab, cx.dInit, grid, cx.stream, &block);
-  else if (pl.kernel == K_LDU8) e = walk_ldu8_launch(wp, cx.dTab, cx.dInit, grid, cx.stream, &block);
-  else if (pl.kernel == K_LD) e = walk_ld_launch(wp, cx.dTab, grid, cx.stream, &block);
-  else e = walk_generic_launch(wp, grid, cx.stream, &block);
+  cudaStream_t st = cx.cur ? cx.cur : cx.stream;
+  if (pl.kernel == K_BIN) e = walk_bin_launch(wp, cx.dTab, grid, st, &block);
+  else if (pl.kernel == K_BIN16) e = walk_bin16_launch(wp, cx.dTab, grid, st, &block);
+  else if (pl.kernel == K_LD16) e = walk_ld16_launch(wp, cx.dTab, grid, st, &block);
+  else if (pl.kernel == K_PAIR16) e = walk_pair16_launch(wp, cx.dTab, cx.dInit, grid, st, &block);
+  else if (pl.kernel == K_U8) e = walk_u8_launch(wp, cx.dTab, cx.dInit, grid, st, &block);
+  else if (pl.kernel == K_LDPAIR16) e = walk_ldpair16_launch(wp, cx.dTab, cx.dInit, grid, st, &block);
+  else if (pl.kernel == K_LDU8) e = walk_ldu8_launch(wp, cx.dTab, cx.dInit, grid, st, &block);
+  else if (pl.kernel == K_LD) e = walk_ld_launch(wp, cx.dTab, grid, st, &block);
+  else e = walk_generic_launch(wp, grid, st, &block);
   if (e != cudaSuccess) { (void)cudaGetLastError(); return LNORM_ECUDA; }
   *grid_out = grid; *block_out = block;
   return LNORM_OK;
@@ -563,128 +682,172 @@ bool ck_save(const char* path, const CkState& st) {
   return ok && rename(tmp.c_str(), path) == 0;
 }
 
+// Recovery self-check: the re-walk of the winning unit
+// must reproduce the reduced maximum exactly -- some strategy of the unit attains
+// key_value(key) (lex found) and none exceeds it (rmax == key value).  Any mismatch
+// means the hot walk or the reduction is wrong: LNORM_EINTERNAL, never a silent answer.
+bool recovery_consistent(unsigned long long key, unsigned long long lex, unsigned long long rmax) {
+  return key != 0ull && lex != ~0ull && (uint32_t)(rmax & 0xFFFFFFFFull) == (uint32_t)(key >> 32);
+}
+
+int corrupt_key_delta() {
+  const char* e = getenv("LNORM_TEST_CORRUPT_KEY");
+  return (e && *e) ? atoi(e) : 0;
+}
+
 // vslices > 1 (test hook, world == 1): walk the Algorithm-1 slices of `vslices`
 // virtual ranks one after the other on this device; the shared key then holds
 // exactly what the multi-rank all-reduce(max) would.
+// comm != null: this rank walks its Algorithm-1 slice of `world` and ONE
+// ncclAllReduce(max) over {key, error flag} combines the ranks (also at world == 1).
 int run_device(DevCtx& cx, const int32_t* dIn, const Problem& pr, int rank, int world, ncclComm_t comm,
                RunOut* out, lnorm_stats* st, int vslices = 1, const Checkpoint* ck = nullptr,
                const int32_t* hostM = nullptr) {
   Plan pl;
+  // the plan depends only on (M, world): identical on every rank, so a planning error
+  // is raised by all ranks alike before any of them reaches the collective
   int rc = make_plan(pr, std::max(world, vslices), &pl);
   if (rc) return rc;
-  cudaStream_t s = cx.stream;
-  if ((rc = grow(&cx.dM, &cx.capM, (size_t)pr.n * pr.m))) return rc;
+  cudaStream_t s = cx.cur ? cx.cur : cx.stream;
+  const bool collective = comm != nullptr;
   const std::vector<uint64_t>& ptab = pl.prefixes();
-  if (!ptab.empty() && cx.preSrc != (const void*)&ptab) {
-    cx.preSrc = nullptr;
-    if ((rc = grow(&cx.dPre, &cx.capPre, ptab.size()))) return rc;
-  }
-  CU(cudaEventRecord(cx.ev[0], s));
-  int launches = 0;
-  orient_kernel<<<std::min(1024, (pr.n * pr.m + 255) / 256), 256, 0, s>>>(dIn, pr.n, pr.m, pr.transposed ? 1 : 0, cx.dM);
-  ++launches;
-  CU(cudaGetLastError());
-  if (!ptab.empty() && cx.preSrc != (const void*)&ptab) {
-    // the RGS list for (k, d) is immutable and lives for the process: upload it once per device
-    CU(cudaMemcpyAsync(cx.dPre, ptab.data(), sizeof(uint64_t) * ptab.size(), cudaMemcpyHostToDevice, s));
-    if (pl.shared) cx.preSrc = (const void*)&ptab;
-  }
-  init_ctl_kernel<<<1, 1, 0, s>>>(cx.dCtl);
-  ++launches;
-  // Algorithm 1 over the unit list: rank slice [lo, hi]
-  int grid = 0, block = 0;
-  int64_t lo = 0, cnt = pl.units, walked = 0;
+  int grid = 0, block = 0, launches = 0;
+  int64_t cnt = pl.units, walked = 0;
   WalkParams wp{};
-  wp.M = cx.dM; wp.r = pr.r; wp.c = pr.c; wp.mode = pr.mode; wp.d = pr.dl; wp.k = pl.k; wp.s = pl.s;
-  wp.pbits = prefix_bits(pr.dl);
-  wp.key_shift = pl.key_shift;
-  wp.counter = cx.dCtl; wp.key = cx.dCtl + 1; wp.unit_max = nullptr;
-  CU(cudaEventRecord(cx.ev[1], s));
-  if (ck && ck->path && world == 1 && vslices <= 1) {
-    // ---- checkpointed walk: chunks of the unit list, state persisted after each
-    uint64_t fp = 1469598103934665603ull;
-    const int32_t hdr[8] = {pr.n, pr.m, pr.d, pr.marg, pl.k, pl.s, pl.kernel, (int32_t)pr.transposed};
-    fp = fnv1a(fp, hdr, sizeof(hdr));
-    if (hostM) fp = fnv1a(fp, hostM, sizeof(int32_t) * (size_t)pr.n * pr.m);
-    CkState cs{0x4c4e4f524d434b31ull, fp, 0, 0ull};
-    ck_load(ck->path, fp, &cs);
-    if (cs.key) CU(cudaMemcpyAsync(cx.dCtl + 1, &cs.key, sizeof(cs.key), cudaMemcpyHostToDevice, s));
-    const int64_t chunk = ck->chunk_units > 0 ? ck->chunk_units : pl.units;
-    int32_t chunks = 0;
-    while (cs.next_unit < pl.units && (ck->max_chunks <= 0 || chunks < ck->max_chunks)) {
-      const int64_t c0 = cs.next_unit, c1 = std::min<int64_t>(pl.units, c0 + chunk);
-      wp.unit_begin = c0; wp.unit_count = c1 - c0;
-      walk_params_single(wp);
-      wp.prefix_table = ptab.empty() ? nullptr : cx.dPre + c0;
-      if (pl.kernel == K_GEN) CU(cudaMemsetAsync(cx.dCtl, 0, sizeof(unsigned long long), s));
-      if ((rc = launch_walk(cx, pr, pl, wp, &grid, &block))) return rc;
-      launches += pl.kernel == K_GEN ? 1 : 2;
-      walked += c1 - c0;
-      CU(cudaMemcpyAsync(&cs.key, cx.dCtl + 1, sizeof(cs.key), cudaMemcpyDeviceToHost, s));
-      CU(cudaStreamSynchronize(s));
-      cs.next_unit = c1;
-      if (!ck_save(ck->path, cs)) return LNORM_EINVAL;
-      ++chunks;
+  // ---- everything up to the collective: on error the rank still joins the all-reduce
+  //      with its error flag raised, so its peers return instead of hanging
+  auto pre = [&]() -> int {
+    int e;
+    if ((e = grow(&cx.dM, &cx.capM, (size_t)pr.n * pr.m))) return e;
+    const bool mirror = !ptab.empty() && pl.shared && cx.preHold.get() == pl.shared.get();
+    if (!ptab.empty() && !mirror) {
+      cx.preHold.reset();
+      if ((e = grow(&cx.dPre, &cx.capPre, ptab.size()))) return e;
     }
-    if (ck->units_done) *ck->units_done = cs.next_unit;
-    if (cs.next_unit < pl.units) {               // partial: report the best so far, no recovery yet
-      if (ck->done) *ck->done = 0;
-      out->value = cs.key ? (int64_t)key_value(cs.key) : INT64_MIN;
-      out->argmax.assign(pr.n, 0);
-      lnorm_stats S{};
-      S.rows = pr.r; S.cols = pr.c; S.units = walked; S.units_total = pl.units; S.launches = launches;
-      S.variant = pl.kernel;
-      *st = S;
+    CU(cudaEventRecord(cx.ev[0], s));
+    orient_kernel<<<std::min(1024, (pr.n * pr.m + 255) / 256), 256, 0, s>>>(dIn, pr.n, pr.m, pr.transposed ? 1 : 0, cx.dM);
+    ++launches;
+    CU(cudaGetLastError());
+    if (!ptab.empty() && !mirror) {
+      // the RGS list for (k, d) is immutable and lives for the process: upload it once per device
+      CU(cudaMemcpyAsync(cx.dPre, ptab.data(), sizeof(uint64_t) * ptab.size(), cudaMemcpyHostToDevice, s));
+      if (pl.shared) cx.preHold = pl.shared;
+    }
+    init_ctl_kernel<<<1, 1, 0, s>>>(cx.dCtl);
+    ++launches;
+    CU(cudaGetLastError());
+    wp.M = cx.dM; wp.r = pr.r; wp.c = pr.c; wp.mode = pr.mode; wp.d = pr.dl; wp.k = pl.k; wp.s = pl.s;
+    wp.pbits = prefix_bits(pr.dl);
+    wp.key_shift = pl.key_shift;
+    wp.counter = cx.dCtl; wp.key = cx.dCtl + 1; wp.unit_max = nullptr;
+    CU(cudaEventRecord(cx.ev[1], s));
+    if (ck && ck->path && world == 1 && vslices <= 1 && !collective) {
+      // ---- checkpointed walk: chunks of the unit list, state persisted after each
+      uint64_t fp = 1469598103934665603ull;
+      const int32_t hdr[8] = {pr.n, pr.m, pr.d, pr.marg, pl.k, pl.s, pl.kernel, (int32_t)pr.transposed};
+      fp = fnv1a(fp, hdr, sizeof(hdr));
+      if (hostM) fp = fnv1a(fp, hostM, sizeof(int32_t) * (size_t)pr.n * pr.m);
+      CkState cs{0x4c4e4f524d434b31ull, fp, 0, 0ull};
+      ck_load(ck->path, fp, &cs);
+      if (cs.key) CU(cudaMemcpyAsync(cx.dCtl + 1, &cs.key, sizeof(cs.key), cudaMemcpyHostToDevice, s));
+      const int64_t chunk = ck->chunk_units > 0 ? ck->chunk_units : pl.units;
+      int32_t chunks = 0;
+      while (cs.next_unit < pl.units && (ck->max_chunks <= 0 || chunks < ck->max_chunks)) {
+        const int64_t c0 = cs.next_unit, c1 = std::min<int64_t>(pl.units, c0 + chunk);
+        wp.unit_begin = c0; wp.unit_count = c1 - c0;
+        walk_params_single(wp);
+        wp.prefix_table = ptab.empty() ? nullptr : cx.dPre + c0;
+        if (pl.kernel == K_GEN) CU(cudaMemsetAsync(cx.dCtl, 0, sizeof(unsigned long long), s));
+        if ((e = launch_walk(cx, pr, pl, wp, &grid, &block))) return e;
+        launches += pl.kernel == K_GEN ? 1 : 2;
+        walked += c1 - c0;
+        CU(cudaMemcpyAsync(&cs.key, cx.dCtl + 1, sizeof(cs.key), cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+        cs.next_unit = c1;
+        if (!ck_save(ck->path, cs)) return LNORM_EINVAL;
+        ++chunks;
+      }
+      if (ck->units_done) *ck->units_done = cs.next_unit;
+      if (cs.next_unit < pl.units) {               // partial: report the best so far, no recovery yet
+        if (ck->done) *ck->done = 0;
+        out->value = cs.key ? (int64_t)key_value(cs.key) : INT64_MIN;
+        out->argmax.assign(pr.n, 0);
+        lnorm_stats S{};
+        S.rows = pr.r; S.cols = pr.c; S.units = walked; S.units_total = pl.units; S.launches = launches;
+        S.variant = pl.kernel;
+        *st = S;
+        return -1;                                 // (not an error: partial result, no recovery)
+      }
+      if (ck->done) *ck->done = 1;
       return LNORM_OK;
     }
-    if (ck->done) *ck->done = 1;
-  }
-  const int nslices = (ck && ck->path) ? 0 : (world > 1 ? 1 : std::max(1, vslices));
-  for (int sl = 0; sl < nslices; ++sl) {
-    const int T = world > 1 ? world : nslices, t = world > 1 ? rank : sl;
-    if (T > 1) {
-      int64_t jmin = 0, jmax = -1;
-      algorithm1((uint64_t)pl.units, T, t, &jmin, &jmax);
-      lo = jmin;
-      cnt = jmax - jmin + 1;
-    }
-    wp.unit_begin = lo; wp.unit_count = cnt;
-    walk_params_single(wp);
-    wp.prefix_table = ptab.empty() ? nullptr : cx.dPre + lo;
-    if (cnt > 0) {
-      if (sl > 0 && pl.kernel == K_GEN) {   // the generic kernel's work counter restarts per slice
-        CU(cudaMemsetAsync(cx.dCtl, 0, sizeof(unsigned long long), s));
+    const int nslices = collective ? 1 : std::max(1, vslices);
+    int64_t lo = 0;
+    for (int sl = 0; sl < nslices; ++sl) {
+      const int T = collective ? world : nslices, t = collective ? rank : sl;
+      if (T > 1) {
+        int64_t jmin = 0, jmax = -1;
+        algorithm1((uint64_t)pl.units, T, t, &jmin, &jmax);
+        lo = jmin;
+        cnt = jmax - jmin + 1;
       }
-      if ((rc = launch_walk(cx, pr, pl, wp, &grid, &block))) return rc;
-      launches += pl.kernel == K_GEN ? 1 : 2;   // table build + walk
-      walked += cnt;
+      wp.unit_begin = lo; wp.unit_count = cnt;
+      walk_params_single(wp);
+      wp.prefix_table = ptab.empty() ? nullptr : cx.dPre + lo;
+      if (cnt > 0) {
+        if (sl > 0 && pl.kernel == K_GEN) {   // the generic kernel's work counter restarts per slice
+          CU(cudaMemsetAsync(cx.dCtl, 0, sizeof(unsigned long long), s));
+        }
+        if ((e = launch_walk(cx, pr, pl, wp, &grid, &block))) return e;
+        launches += pl.kernel == K_GEN ? 1 : 2;   // table build + walk
+        walked += cnt;
+      }
     }
-  }
+    return LNORM_OK;
+  };
+  int pre_rc = pre();
+  if (pre_rc == -1) return LNORM_OK;           // checkpoint: partial result already written
   cnt = walked;
-  CU(cudaEventRecord(cx.ev[2], s));
-  if (world > 1) {
+  if (pre_rc != LNORM_OK) {
+    if (!collective) return pre_rc;
+    (void)cudaGetLastError();
+    (void)cudaMemsetAsync(cx.dCtl + 2, 0xFF, sizeof(unsigned long long), s);   // raise the error flag
+  }
+  (void)cudaEventRecord(cx.ev[2], s);
+  if (collective) {
     Nccl& nc = nccl();
-    if (!nc.ok || !comm) return LNORM_ENCCL;
-    if (nc.AllReduce(cx.dCtl + 1, cx.dCtl + 1, 1, ncclUint64, ncclMax, comm, s) != ncclSuccess) return LNORM_ENCCL;
+    if (!nc.ok) return LNORM_ENCCL;
+    if (nc.AllReduce(cx.dCtl + 1, cx.dCtl + 1, 2, ncclUint64, ncclMax, comm, s) != ncclSuccess) return LNORM_ENCCL;
+    ++launches;
+    if (pre_rc != LNORM_OK) { (void)cudaStreamSynchronize(s); return pre_rc; }
+  }
+  if (const int delta = corrupt_key_delta()) {
+    corrupt_key_kernel<<<1, 1, 0, s>>>(cx.dCtl + 1, delta);
+    CU(cudaGetLastError());
+    ++launches;
   }
   // recovery over the full unit space (same winning unit on every rank)
   WalkParams rp = wp;
   rp.unit_begin = 0; rp.unit_count = pl.units;
   walk_params_single(rp);
   rp.prefix_table = ptab.empty() ? nullptr : cx.dPre;
-  if (recover_launch(rp, cx.dCtl + 2, s) != cudaSuccess) { (void)cudaGetLastError(); return LNORM_ECUDA; }
+  if (recover_launch(rp, cx.dCtl + 3, cx.dCtl + 4, s) != cudaSuccess) { (void)cudaGetLastError(); return LNORM_ECUDA; }
   ++launches;
   FinalizeArgs fa;
-  fa.key = cx.dCtl + 1; fa.lex = cx.dCtl + 2; fa.table = rp.prefix_table; fa.Min = dIn; fa.n = pr.n; fa.m = pr.m; fa.r = pr.r;
+  fa.key = cx.dCtl + 1; fa.lex = cx.dCtl + 3; fa.table = rp.prefix_table; fa.Min = dIn; fa.n = pr.n; fa.m = pr.m; fa.r = pr.r;
   fa.k = pl.k; fa.s = pl.s; fa.base = pr.dl; fa.mode = pr.mode; fa.transposed = pr.transposed ? 1 : 0; fa.pbits = prefix_bits(pr.dl);
   fa.key_shift = pl.key_shift;
+  fa.units = pl.units;
   fa.value_out = cx.dRes; fa.argmax_out = reinterpret_cast<int8_t*>(cx.dRes + 1);
   finalize_kernel<<<1, 256, 0, s>>>(fa);
   ++launches;
   CU(cudaGetLastError());
   CU(cudaMemcpyAsync(cx.hRes, cx.dRes, 8 + pr.n, cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(cx.hCtl, cx.dCtl, sizeof(unsigned long long) * kCtlWords, cudaMemcpyDeviceToHost, s));
   CU(cudaEventRecord(cx.ev[3], s));
   CU(cudaStreamSynchronize(s));
+  if (cx.hCtl[2]) return LNORM_ENCCL;                 // a peer rank failed before the collective
+  if (!recovery_consistent(cx.hCtl[1], cx.hCtl[3], cx.hCtl[4])) return LNORM_EINTERNAL;
   out->value = cx.hRes[0];
   out->argmax.assign(reinterpret_cast<int8_t*>(cx.hRes + 1), reinterpret_cast<int8_t*>(cx.hRes + 1) + pr.n);
   float wms = 0, tms = 0;
@@ -713,27 +876,47 @@ void write_out(const RunOut& ro, int64_t* value, int8_t* argmax) {
   if (argmax) std::memcpy(argmax, ro.argmax.data(), ro.argmax.size());
 }
 
+// Restores the context's default stream when a call that borrowed the caller's ends.
+struct StreamScope {
+  DevCtx* c;
+  StreamScope(DevCtx* cx, cudaStream_t user) : c(cx) { c->cur = user ? user : c->stream; }
+  ~StreamScope() { c->cur = c->stream; }
+};
+
+// Guard statistics of a device-resident matrix: one-block kernel on the call's stream,
+// ~0.5 KB copied back (the plan depends on them: the only host round trip before the walk).
+int device_stats(DevCtx& cx, const int32_t* devM, Problem* pr) {
+  cudaStream_t s = cx.cur;
+  guard_stats_kernel<<<1, 256, 0, s>>>(devM, pr->m, pr->transposed ? 1 : 0, pr->r, pr->c,
+                                       pr->mode == MODE_MARG ? 1 : 0, cx.dStats);
+  CU(cudaGetLastError());
+  CU(cudaMemcpyAsync(cx.hStats, cx.dStats, sizeof(long long) * (3 + pr->r), cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  GuardStats g;
+  g.S = cx.hStats[0]; g.par[0] = cx.hStats[1]; g.par[1] = cx.hStats[2];
+  for (int q = 1; q <= pr->r; ++q) g.sufW[q] = cx.hStats[3 + q - 1];
+  return apply_stats(g, pr);
+}
+
 int compute_on(int device, const int32_t* hostM, const int32_t* devM, int n, int m, int d, int marg,
-               int rank, int world, ncclComm_t comm, int64_t* value, int8_t* argmax, int vslices = 1) {
-  if (!value) return LNORM_EINVAL;
+               int rank, int world, ncclComm_t comm, cudaStream_t user_stream, int64_t* value, int8_t* argmax,
+               int vslices = 1) {
+  if (!value || (!hostM && !devM)) return LNORM_EINVAL;
   Problem pr;
-  std::vector<int32_t> hcopy;
   DevCtx* cx = nullptr;
   int rc = ctx_get(device, &cx);
   if (rc) return rc;
   std::lock_guard<std::mutex> g(cx->mu);
   CU(cudaSetDevice(device));
-  if (devM) {   // validation needs the entries: bring the (small) matrix to the host once
-    if (n < 1 || m < 1) return LNORM_EINVAL;
-    hcopy.resize((size_t)n * m);
-    CU(cudaMemcpy(hcopy.data(), devM, sizeof(int32_t) * hcopy.size(), cudaMemcpyDeviceToHost));
-    hostM = hcopy.data();
-  }
-  if ((rc = validate(hostM, n, m, d, marg, &pr))) return rc;
+  StreamScope scope(cx, user_stream);
   const int32_t* dIn = devM;
-  if (!devM) {
+  if (devM) {
+    if ((rc = validate_shape(n, m, d, marg, &pr))) return rc;
+    if ((rc = device_stats(*cx, devM, &pr))) return rc;
+  } else {
+    if ((rc = validate(hostM, n, m, d, marg, &pr))) return rc;
     if ((rc = grow(&cx->dIn, &cx->capIn, (size_t)n * m))) return rc;
-    CU(cudaMemcpyAsync(cx->dIn, hostM, sizeof(int32_t) * n * m, cudaMemcpyHostToDevice, cx->stream));
+    CU(cudaMemcpyAsync(cx->dIn, hostM, sizeof(int32_t) * n * m, cudaMemcpyHostToDevice, cx->cur));
     dIn = cx->dIn;
   }
   RunOut ro;
@@ -742,6 +925,18 @@ int compute_on(int device, const int32_t* hostM, const int32_t* devM, int n, int
   g_stats = st;
   write_out(ro, value, argmax);
   return LNORM_OK;
+}
+
+// Rank entry points: the communicator (if any) must span `world` ranks with this
+// process at `rank`.
+int check_comm(ncclComm_t comm, int rank, int world) {
+  if (world < 1 || rank < 0 || rank >= world) return LNORM_EINVAL;
+  if (!comm) return world == 1 ? LNORM_OK : LNORM_EINVAL;
+  Nccl& nc = nccl();
+  if (!nc.ok) return LNORM_ENCCL;
+  int cnt = 0, me = -1;
+  if (nc.CommCount(comm, &cnt) != ncclSuccess || nc.CommUserRank(comm, &me) != ncclSuccess) return LNORM_ENCCL;
+  return (cnt == world && me == rank) ? LNORM_OK : LNORM_EINVAL;
 }
 
 }  // namespace
@@ -763,27 +958,28 @@ const char* lnorm_status_string(int status) {
     case LNORM_ECUDA: return "CUDA runtime error";
     case LNORM_ENCCL: return "NCCL unavailable or failed";
     case LNORM_ENOMEM: return "out of device memory";
+    case LNORM_EINTERNAL: return "internal self-check failed (argmax recovery did not reproduce the reduced maximum)";
     default: return "unknown status";
   }
 }
 
-int32_t lnorm_version(void) { return (1 << 16) | 1; }   // 1.1: lnorm_plan_info.lanes_per_unit
+int32_t lnorm_version(void) { return (2 << 16) | 0; }   // 2.0: caller-owned NCCL comm + stream in lnorm_compute_rank, EINTERNAL
 
 int lnorm_compute(const int32_t* M, int32_t n, int32_t m, int32_t d, int32_t with_marginals,
                   int64_t* value, int8_t* argmax) {
   if (!M) return LNORM_EINVAL;
   int dev = 0, rc = current_device(&dev);
   if (rc) return rc;
-  return compute_on(dev, M, nullptr, n, m, d, with_marginals, 0, 1, nullptr, value, argmax);
+  return compute_on(dev, M, nullptr, n, m, d, with_marginals, 0, 1, nullptr, nullptr, value, argmax);
 }
 
 int lnorm_compute_device(const int32_t* M_device, int32_t n, int32_t m, int32_t d, int32_t with_marginals,
                          void* cuda_stream, int64_t* value, int8_t* argmax) {
-  (void)cuda_stream;   // work runs on the context stream; the call synchronises before returning
   if (!M_device) return LNORM_EINVAL;
   int dev = 0, rc = current_device(&dev);
   if (rc) return rc;
-  return compute_on(dev, nullptr, M_device, n, m, d, with_marginals, 0, 1, nullptr, value, argmax);
+  return compute_on(dev, nullptr, M_device, n, m, d, with_marginals, 0, 1, nullptr,
+                    static_cast<cudaStream_t>(cuda_stream), value, argmax);
 }
 
 int lnorm_comm_unique_id(uint8_t id_out[128]) {
@@ -799,10 +995,10 @@ int lnorm_comm_unique_id(uint8_t id_out[128]) {
 
 int lnorm_comm_create(const uint8_t id[128], int32_t rank, int32_t world, int32_t device, lnorm_comm** comm_out) {
   if (!comm_out || world < 1 || rank < 0 || rank >= world || device < 0) return LNORM_EINVAL;
+  if (!id && world > 1) return LNORM_EINVAL;
   lnorm_comm* c = new lnorm_comm;
   c->rank = rank; c->world = world; c->device = device;
-  if (world > 1) {
-    if (!id) { delete c; return LNORM_EINVAL; }
+  if (id) {   // a real communicator for every world >= 1 (world 1 exercises the all-reduce path)
     Nccl& nc = nccl();
     if (!nc.ok) { delete c; return LNORM_ENCCL; }
     if (cudaSetDevice(device) != cudaSuccess) { (void)cudaGetLastError(); delete c; return LNORM_ENODEV; }
@@ -814,6 +1010,12 @@ int lnorm_comm_create(const uint8_t id[128], int32_t rank, int32_t world, int32_
   return LNORM_OK;
 }
 
+int lnorm_comm_nccl(lnorm_comm* comm, void** nccl_comm_out) {
+  if (!comm || !nccl_comm_out) return LNORM_EINVAL;
+  *nccl_comm_out = static_cast<void*>(comm->comm);
+  return LNORM_OK;
+}
+
 int lnorm_comm_destroy(lnorm_comm* comm) {
   if (!comm) return LNORM_EINVAL;
   if (comm->comm) { Nccl& nc = nccl(); if (nc.ok) nc.CommDestroy(comm->comm); }
@@ -821,28 +1023,30 @@ int lnorm_comm_destroy(lnorm_comm* comm) {
   return LNORM_OK;
 }
 
-int lnorm_compute_rank(lnorm_comm* comm, const int32_t* M, int32_t n, int32_t m, int32_t d,
-                       int32_t with_marginals, int64_t* value, int8_t* argmax) {
+int lnorm_compute_rank(const int32_t* M, int32_t n, int32_t m, int32_t d, int32_t with_marginals,
+                       void* nccl_comm, int32_t rank, int32_t world, void* cuda_stream,
+                       int64_t* value, int8_t* argmax) {
   if (!M) return LNORM_EINVAL;
-  if (!comm) {
-    int dev = 0, rc = current_device(&dev);
-    if (rc) return rc;
-    return compute_on(dev, M, nullptr, n, m, d, with_marginals, 0, 1, nullptr, value, argmax);
-  }
-  return compute_on(comm->device, M, nullptr, n, m, d, with_marginals, comm->rank, comm->world, comm->comm,
-                    value, argmax);
+  ncclComm_t comm = static_cast<ncclComm_t>(nccl_comm);
+  int rc = check_comm(comm, rank, world);
+  if (rc) return rc;
+  int dev = 0;
+  if ((rc = current_device(&dev))) return rc;
+  return compute_on(dev, M, nullptr, n, m, d, with_marginals, rank, world, comm,
+                    static_cast<cudaStream_t>(cuda_stream), value, argmax);
 }
 
-int lnorm_compute_rank_device(lnorm_comm* comm, const int32_t* M_device, int32_t n, int32_t m, int32_t d,
-                              int32_t with_marginals, int64_t* value, int8_t* argmax) {
+int lnorm_compute_rank_device(const int32_t* M_device, int32_t n, int32_t m, int32_t d, int32_t with_marginals,
+                              void* nccl_comm, int32_t rank, int32_t world, void* cuda_stream,
+                              int64_t* value, int8_t* argmax) {
   if (!M_device) return LNORM_EINVAL;
-  if (!comm) {
-    int dev = 0, rc = current_device(&dev);
-    if (rc) return rc;
-    return compute_on(dev, nullptr, M_device, n, m, d, with_marginals, 0, 1, nullptr, value, argmax);
-  }
-  return compute_on(comm->device, nullptr, M_device, n, m, d, with_marginals, comm->rank, comm->world, comm->comm,
-                    value, argmax);
+  ncclComm_t comm = static_cast<ncclComm_t>(nccl_comm);
+  int rc = check_comm(comm, rank, world);
+  if (rc) return rc;
+  int dev = 0;
+  if ((rc = current_device(&dev))) return rc;
+  return compute_on(dev, nullptr, M_device, n, m, d, with_marginals, rank, world, comm,
+                    static_cast<cudaStream_t>(cuda_stream), value, argmax);
 }
 
 int lnorm_compute_multi(const int32_t* M, int32_t n, int32_t m, int32_t d, int32_t with_marginals,
@@ -853,28 +1057,52 @@ int lnorm_compute_multi(const int32_t* M, int32_t n, int32_t m, int32_t d, int32
   int cnt = 0;
   if (cudaGetDeviceCount(&cnt) != cudaSuccess) { (void)cudaGetLastError(); return LNORM_ENODEV; }
   for (int dv : devs) if (dv < 0 || dv >= cnt) return LNORM_ENODEV;
-  if (num_devices == 1) return compute_on(devs[0], M, nullptr, n, m, d, with_marginals, 0, 1, nullptr, value, argmax);
+  {   // argument / shape / overflow errors are the same on every device: report them before any comm
+    Problem pr;
+    const int rc = validate(M, n, m, d, with_marginals, &pr);
+    if (rc) return rc;
+  }
   Nccl& nc = nccl();
   if (!nc.ok) return LNORM_ENCCL;
+  // one communicator per device (also for a single device: the all-reduce path always runs)
   std::vector<ncclComm_t> comms(num_devices);
   if (nc.CommInitAll(comms.data(), num_devices, devs.data()) != ncclSuccess) return LNORM_ENCCL;
   std::vector<int> rcs(num_devices, 0);
   std::vector<int64_t> vals(num_devices, 0);
   std::vector<std::vector<int8_t>> args(num_devices, std::vector<int8_t>(n, 0));
   std::vector<lnorm_stats> sts(num_devices);
+  std::atomic<int> finished{0}, failed{0};
   std::vector<std::thread> th;
   for (int g = 0; g < num_devices; ++g) {
     th.emplace_back([&, g] {
-      rcs[g] = compute_on(devs[g], M, nullptr, n, m, d, with_marginals, g, num_devices, comms[g], &vals[g],
+      rcs[g] = compute_on(devs[g], M, nullptr, n, m, d, with_marginals, g, num_devices, comms[g], nullptr, &vals[g],
                           args[g].data());
       sts[g] = g_stats;
+      if (rcs[g]) failed.fetch_add(1);
+      finished.fetch_add(1);
     });
   }
+  // A device that fails before reaching the collective (context or allocation failure)
+  // would leave its peers blocked in the all-reduce: once any device has failed and the
+  // others make no progress for 2 s, abort every communicator (unblocks them with an error).
+  bool aborted = false;
+  auto t_fail = std::chrono::steady_clock::time_point{};
+  while (finished.load() < num_devices) {
+    std::this_thread::sleep_for(std::chrono::milliseconds(1));
+    if (!aborted && failed.load() > 0) {
+      const auto now = std::chrono::steady_clock::now();
+      if (t_fail == std::chrono::steady_clock::time_point{}) t_fail = now;
+      else if (now - t_fail > std::chrono::seconds(2)) {
+        for (auto& cm : comms) nc.CommAbort(cm);
+        aborted = true;
+      }
+    }
+  }
   for (auto& t : th) t.join();
-  for (auto& cm : comms) nc.CommDestroy(cm);
+  if (!aborted) for (auto& cm : comms) nc.CommDestroy(cm);
   for (int g = 0; g < num_devices; ++g) if (rcs[g]) return rcs[g];
   for (int g = 1; g < num_devices; ++g)
-    if (vals[g] != vals[0] || args[g] != args[0]) return LNORM_ECUDA;   // ranks must agree bit-for-bit
+    if (vals[g] != vals[0] || args[g] != args[0]) return LNORM_EINTERNAL;   // ranks must agree bit-for-bit
   *value = vals[0];
   if (argmax) std::memcpy(argmax, args[0].data(), n);
   lnorm_stats S = sts[0];
@@ -972,7 +1200,7 @@ int lnorm_compute_batch(const int32_t* M, int32_t batch, int32_t n, int32_t m, i
   int dev = 0, rc = current_device(&dev);
   if (rc) return rc;
   const size_t nm = (size_t)n * m;
-  // validate every matrix; the batched kernel needs the strategy-paired path for all of them
+  // validate every matrix; the paired batched kernel needs its guard for all of them
   Problem pr;
   bool all_pair = true;
   for (int b = 0; b < batch; ++b) {
@@ -981,16 +1209,19 @@ int lnorm_compute_batch(const int32_t* M, int32_t batch, int32_t n, int32_t m, i
     if (b == 0) pr = q;
     all_pair = all_pair && q.fitsPair;
   }
+  // path: the strategy-paired packed kernel (one launch, units of all matrices), else the
+  // generic warp-per-unit kernel batched the same way for small search spaces (tiny shapes,
+  // any d), else one search per matrix through the hot single-matrix kernels
   Plan pl;
   const int64_t target = std::max<int64_t>(1, kNominalLanes * 8 / batch);
-  if (all_pair && pr.dl == 2) {
-    if ((rc = make_plan(pr, 1, &pl, target, /*allow_u8=*/false))) return rc;
-  }
-  if (!all_pair || pr.dl != 2 || pl.kernel != K_PAIR16) {
-    // outside the batched kernel's reach (L_d, d >= 3, or a matrix beyond the packed
-    // guard): one search per matrix through the same device path
+  bool pair = false;
+  if (all_pair && pr.dl == 2 && make_plan(pr, 1, &pl, target, /*allow_u8=*/false) == LNORM_OK && pl.kernel == K_PAIR16)
+    pair = true;
+  long double space = 1;
+  for (int i = 0; i < pr.r - 1; ++i) space *= pr.dl;
+  if (!pair && space > (long double)(1 << 20)) {
     for (int b = 0; b < batch; ++b) {
-      if ((rc = compute_on(dev, M + b * nm, nullptr, n, m, d, with_marginals, 0, 1, nullptr, values + b,
+      if ((rc = compute_on(dev, M + b * nm, nullptr, n, m, d, with_marginals, 0, 1, nullptr, nullptr, values + b,
                            argmax ? argmax + (size_t)b * n : nullptr)))
         return rc;
     }
@@ -1001,13 +1232,36 @@ int lnorm_compute_batch(const int32_t* M, int32_t batch, int32_t n, int32_t m, i
   std::lock_guard<std::mutex> g(cx->mu);
   CU(cudaSetDevice(dev));
   cudaStream_t s = cx->stream;
+  if (!pair) {
+    // generic batched plan: the smallest prefix length giving ~64 warps of work per SM
+    pl = Plan{};
+    pl.kernel = K_GEN;
+    const int f = pr.r - 1;
+    auto units_of = [&](int k) -> int64_t { return pr.dl == 2 ? (1LL << k) : rgs_count(k + 1, pr.dl); };
+    int k = 0;
+    while (k < f && (int64_t)batch * units_of(k) < (int64_t)cx->nsm * 64 && units_of(k + 1) <= kTableCap &&
+           (k + 2) * prefix_bits(pr.dl) <= 64)
+      ++k;
+    pl.k = k; pl.s = f - k; pl.units = units_of(k);
+    if (pr.dl > 2 && k > 0) {
+      auto v = std::make_shared<std::vector<uint64_t>>();
+      rgs_enumerate(k + 1, pr.dl, *v, kTableCap + 1);
+      pl.shared = v;
+    }
+  }
   int64_t tabw = 0, initw = 0;
-  walk_pair16_table_sizes(pr.mode, pr.c, pl.k, pl.s, &tabw, &initw);
+  if (pair) walk_pair16_table_sizes(pr.mode, pr.c, pl.k, pl.s, &tabw, &initw);
   auto up8 = [](size_t x) { return (x + 7) & ~(size_t)7; };
   const size_t oIn = 0, oM = oIn + up8(batch * nm), oTab = oM + up8(batch * nm), oInit = oTab + up8(batch * (size_t)tabw);
   const size_t oKey = oInit + up8(batch * (size_t)initw);                 // int32 units so far
-  const size_t words32 = oKey + 4 * (size_t)batch + 2 * (size_t)batch + up8((size_t)batch * n) / 4 + 8;
+  // keys, lex, rmax, values: int64 each per matrix; then argmax bytes
+  const size_t words32 = oKey + 8 * (size_t)batch + up8((size_t)batch * n) / 4 + 8;
   if ((rc = grow(&cx->dBatch, &cx->capBatch, words32 / 2 + 1))) return rc;
+  const std::vector<uint64_t>& ptab = pl.prefixes();
+  if (!ptab.empty()) {
+    cx->preHold.reset();
+    if ((rc = grow(&cx->dPre, &cx->capPre, ptab.size()))) return rc;
+  }
   int32_t* base = reinterpret_cast<int32_t*>(cx->dBatch);
   int32_t* dIn = base + oIn;
   int32_t* dMo = base + oM;
@@ -1015,50 +1269,76 @@ int lnorm_compute_batch(const int32_t* M, int32_t batch, int32_t n, int32_t m, i
   int32_t* dInit = base + oInit;
   unsigned long long* keys = reinterpret_cast<unsigned long long*>(base + oKey);
   unsigned long long* lex = keys + batch;
-  int64_t* vals = reinterpret_cast<int64_t*>(lex + batch);
+  unsigned long long* rmax = lex + batch;
+  int64_t* vals = reinterpret_cast<int64_t*>(rmax + batch);
   int8_t* args = reinterpret_cast<int8_t*>(vals + batch);
   CU(cudaEventRecord(cx->ev[0], s));
   CU(cudaMemcpyAsync(dIn, M, sizeof(int32_t) * batch * nm, cudaMemcpyHostToDevice, s));
-  orient_kernel<<<dim3(std::min(64, (int)((nm + 255) / 256)), batch), 256, 0, s>>>(dIn, n, m, pr.transposed ? 1 : 0, dMo);
+  if (!ptab.empty()) CU(cudaMemcpyAsync(cx->dPre, ptab.data(), sizeof(uint64_t) * ptab.size(), cudaMemcpyHostToDevice, s));
+  orient_kernel<<<dim3(std::min(64, (int)((nm + 255) / 256)), std::min(batch, 65535)), 256, 0, s>>>(
+      dIn, n, m, pr.transposed ? 1 : 0, dMo, batch);
   CU(cudaGetLastError());
   CU(cudaMemsetAsync(keys, 0, sizeof(unsigned long long) * batch, s));
   CU(cudaMemsetAsync(lex, 0xFF, sizeof(unsigned long long) * batch, s));
+  CU(cudaMemsetAsync(rmax, 0, sizeof(unsigned long long) * batch, s));
+  CU(cudaMemsetAsync(cx->dCtl, 0, sizeof(unsigned long long), s));     // generic kernel's work counter
   WalkParams wp{};
   wp.M = dMo; wp.r = pr.r; wp.c = pr.c; wp.mode = pr.mode; wp.d = pr.dl; wp.k = pl.k; wp.s = pl.s;
-  wp.pbits = prefix_bits(pr.dl); wp.prefix_table = nullptr; wp.counter = nullptr; wp.key = keys; wp.unit_max = nullptr;
+  wp.pbits = prefix_bits(pr.dl); wp.prefix_table = ptab.empty() ? nullptr : cx->dPre;
+  wp.counter = cx->dCtl; wp.key = keys; wp.unit_max = nullptr;
   wp.unit_begin = 0; wp.unit_count = pl.units * batch;
   wp.batch = batch; wp.units_per = pl.units; wp.m_stride = (int64_t)nm; wp.tab_stride = tabw; wp.init_stride = initw; wp.one = 1;
-  int block = 32;
-  const int occ = std::max(1, walk_pair16_occupancy(pr.mode, pr.c, pl.s, &block));
-  const int64_t P = walk_pair16_units_per_lane(pr.mode, pr.c);
-  const int64_t chunks = (int64_t)batch * ((pl.units + 32 * P - 1) / (32 * P));
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)occ * cx->nsm, chunks));
+  wp.u8_lpu = 1;
+  int block = 32, grid = 1;
   CU(cudaEventRecord(cx->ev[1], s));
-  if (walk_pair16_launch(wp, reinterpret_cast<int32_t*>(dTab), dInit, grid, s, &block) != cudaSuccess) {
-    (void)cudaGetLastError(); return LNORM_ECUDA;
+  if (pair) {
+    const int occ = std::max(1, walk_pair16_occupancy(pr.mode, pr.c, pl.s, &block));
+    const int64_t P = walk_pair16_units_per_lane(pr.mode, pr.c);
+    const int64_t chunks = (int64_t)batch * ((pl.units + 32 * P - 1) / (32 * P));
+    grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)occ * cx->nsm, chunks));
+    if (walk_pair16_launch(wp, reinterpret_cast<int32_t*>(dTab), dInit, grid, s, &block) != cudaSuccess) {
+      (void)cudaGetLastError(); return LNORM_ECUDA;
+    }
+  } else {
+    const int occ = std::max(1, walk_generic_occupancy(pr.dl, pr.c, &block));
+    const int64_t want = (wp.unit_count + block / 32 - 1) / (block / 32);
+    grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)occ * cx->nsm, want));
+    if (walk_generic_launch(wp, grid, s, &block) != cudaSuccess) { (void)cudaGetLastError(); return LNORM_ECUDA; }
   }
   CU(cudaEventRecord(cx->ev[2], s));
-  if (recover_launch(wp, lex, s) != cudaSuccess) { (void)cudaGetLastError(); return LNORM_ECUDA; }
+  WalkParams rp = wp;
+  rp.unit_count = pl.units;          // recovery: units of one matrix (blockIdx.y = matrix)
+  if (recover_launch(rp, lex, rmax, s) != cudaSuccess) { (void)cudaGetLastError(); return LNORM_ECUDA; }
   FinalizeArgs fa;
-  fa.key = keys; fa.lex = lex; fa.table = nullptr; fa.Min = dIn; fa.n = n; fa.m = m; fa.r = pr.r;
-  fa.k = pl.k; fa.s = pl.s; fa.base = 2; fa.mode = pr.mode; fa.transposed = pr.transposed ? 1 : 0; fa.pbits = 1;
+  fa.key = keys; fa.lex = lex; fa.table = wp.prefix_table; fa.Min = dIn; fa.n = n; fa.m = m; fa.r = pr.r;
+  fa.k = pl.k; fa.s = pl.s; fa.base = pr.dl; fa.mode = pr.mode; fa.transposed = pr.transposed ? 1 : 0;
+  fa.pbits = prefix_bits(pr.dl);
   fa.key_shift = 0;
+  fa.units = pl.units;
   fa.value_out = vals; fa.argmax_out = args;
   finalize_kernel<<<batch, 128, 0, s>>>(fa);
   CU(cudaGetLastError());
-  CU(cudaMemcpyAsync(values, vals, sizeof(int64_t) * batch, cudaMemcpyDeviceToHost, s));
-  if (argmax) CU(cudaMemcpyAsync(argmax, args, (size_t)batch * n, cudaMemcpyDeviceToHost, s));
+  std::vector<unsigned long long> hk(3 * (size_t)batch);
+  std::vector<int64_t> hv((size_t)batch);
+  std::vector<int8_t> ha(argmax ? (size_t)batch * n : 0);
+  CU(cudaMemcpyAsync(hk.data(), keys, sizeof(unsigned long long) * 3 * batch, cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(hv.data(), vals, sizeof(int64_t) * batch, cudaMemcpyDeviceToHost, s));
+  if (argmax) CU(cudaMemcpyAsync(ha.data(), args, (size_t)batch * n, cudaMemcpyDeviceToHost, s));
   CU(cudaEventRecord(cx->ev[3], s));
   CU(cudaStreamSynchronize(s));
+  for (int b = 0; b < batch; ++b)
+    if (!recovery_consistent(hk[b], hk[batch + b], hk[2 * (size_t)batch + b])) return LNORM_EINTERNAL;
+  std::memcpy(values, hv.data(), sizeof(int64_t) * batch);
+  if (argmax) std::memcpy(argmax, ha.data(), (size_t)batch * n);
   float wms = 0, tms = 0;
   cudaEventElapsedTime(&wms, cx->ev[1], cx->ev[2]);
   cudaEventElapsedTime(&tms, cx->ev[0], cx->ev[3]);
   lnorm_stats S{};
   S.rows = pr.r; S.cols = pr.c; S.transposed = pr.transposed; S.prefix_digits = pl.k; S.suffix_digits = pl.s;
-  S.d = 1; S.units = pl.units * batch; S.units_total = S.units;
-  S.steps = (double)S.units * (double)ipow(2, pl.s);
-  S.column_updates = S.steps * pr.c;
-  S.walk_ms = wms; S.total_ms = tms; S.launches = 5; S.variant = pl.kernel; S.block_threads = block; S.grid_blocks = grid;
+  S.d = pr.d == 1 ? 1 : pr.dl; S.units = pl.units * batch; S.units_total = S.units;
+  S.steps = (double)S.units * (double)ipow(pr.dl, pl.s);
+  S.column_updates = S.steps * pr.c * (pr.mode == MODE_LD && pr.dl >= 3 ? 2 : 1);
+  S.walk_ms = wms; S.total_ms = tms; S.launches = 6; S.variant = pl.kernel; S.block_threads = block; S.grid_blocks = grid;
   g_stats = S;
   return LNORM_OK;
 }
@@ -1068,7 +1348,7 @@ int lnorm_compute_sliced(const int32_t* M, int32_t n, int32_t m, int32_t d, int3
   if (!M || slices < 1 || slices > 4096) return LNORM_EINVAL;
   int dev = 0, rc = current_device(&dev);
   if (rc) return rc;
-  return compute_on(dev, M, nullptr, n, m, d, with_marginals, 0, 1, nullptr, value, argmax, slices);
+  return compute_on(dev, M, nullptr, n, m, d, with_marginals, 0, 1, nullptr, nullptr, value, argmax, slices);
 }
 
 int lnorm_prefix_maxima(const int32_t* M, int32_t n, int32_t m, int32_t d, int32_t with_marginals,
@@ -1081,9 +1361,12 @@ int lnorm_prefix_maxima(const int32_t* M, int32_t n, int32_t m, int32_t d, int32
   // no orientation, no label reduction: the hook walks exactly the suffix of the given rows
   pr.transposed = false; pr.r = n; pr.c = m;
   pr.dl = d == 1 ? 2 : d;
-  pr.fits16 = packed_guard(M, m, pr);
   if (pr.r > kMaxRows - 1 || pr.c > kMaxCols) return LNORM_ETOOLARGE;
-  suffix_guard(M, m, &pr);
+  {
+    GuardStats gs;
+    host_stats(M, pr, &gs);
+    if ((rc = apply_stats(gs, &pr))) return rc;
+  }
   const int base = pr.dl;
   Plan pl;
   pl.k = nfixed - 1; pl.s = n - nfixed; pl.units = count;
@@ -1152,7 +1435,7 @@ int lnorm_prefix_maxima(const int32_t* M, int32_t n, int32_t m, int32_t d, int32
   if ((rc = grow(&cx->dUnit, &cx->capUnit, (size_t)count))) return rc;
   cudaStream_t s = cx->stream;
   CU(cudaMemcpyAsync(cx->dM, M, sizeof(int32_t) * n * m, cudaMemcpyHostToDevice, s));
-  cx->preSrc = nullptr;
+  cx->preHold.reset();
   CU(cudaMemcpyAsync(cx->dPre, pl.table.data(), sizeof(uint64_t) * count, cudaMemcpyHostToDevice, s));
   init_ctl_kernel<<<1, 1, 0, s>>>(cx->dCtl);
   WalkParams wp{};
@@ -1176,6 +1459,37 @@ int lnorm_prefix_maxima(const int32_t* M, int32_t n, int32_t m, int32_t d, int32
   S.walk_ms = wms; S.total_ms = wms; S.launches = pl.kernel == K_GEN ? 1 : 2; S.variant = pl.kernel;
   S.block_threads = block; S.grid_blocks = grid;
   g_stats = S;
+  return LNORM_OK;
+}
+
+int lnorm_unit_maxima(const int32_t* M, int32_t n, int32_t m, int32_t d, int32_t with_marginals,
+                      int32_t prefix_digits, const uint64_t* units, int64_t count, int32_t* unit_max) {
+  if (!M || !units || !unit_max || count < 1 || prefix_digits < 0 || prefix_digits >= n) return LNORM_EINVAL;
+  Problem pr;
+  int rc = validate(M, n, m, d, with_marginals, &pr);
+  if (rc) return rc;
+  const int k = prefix_digits, nfixed = k + 1;
+  std::vector<int8_t> pre((size_t)count * nfixed, 0);
+  if (d == 1 || pr.dl == 2) {
+    if (k > 62) return LNORM_EINVAL;
+    for (int64_t i = 0; i < count; ++i) {
+      if (units[i] >> k) return LNORM_EINVAL;
+      for (int x = 1; x <= k; ++x) pre[(size_t)i * nfixed + x] = (int8_t)((units[i] >> (k - x)) & 1ull);
+    }
+  } else {
+    const int dl = pr.dl, pb = prefix_bits(dl);
+    if (nfixed * pb > 64 || rgs_count(nfixed, dl) > kTableCap) return LNORM_EINVAL;
+    std::vector<uint64_t> list;
+    rgs_enumerate(nfixed, dl, list, kTableCap + 1);
+    for (int64_t i = 0; i < count; ++i) {
+      if (units[i] >= list.size()) return LNORM_EINVAL;
+      for (int x = 0; x < nfixed; ++x)
+        pre[(size_t)i * nfixed + x] = (int8_t)((list[units[i]] >> (pb * x)) & ((1ull << pb) - 1ull));
+    }
+  }
+  std::vector<int64_t> out((size_t)count);
+  if ((rc = lnorm_prefix_maxima(M, n, m, d, with_marginals, nfixed, pre.data(), count, out.data()))) return rc;
+  for (int64_t i = 0; i < count; ++i) unit_max[i] = (int32_t)out[i];
   return LNORM_OK;
 }
 
@@ -1209,7 +1523,7 @@ int lnorm_walk_trace(const int32_t* M, int32_t n, int32_t m, int32_t d, int32_t 
   if ((rc = grow(&cx->dUnit, &cx->capUnit, (size_t)nw + (size_t)(nw * n + 7) / 8))) return rc;
   cudaStream_t s = cx->stream;
   CU(cudaMemcpyAsync(cx->dM, M, sizeof(int32_t) * n * m, cudaMemcpyHostToDevice, s));
-  cx->preSrc = nullptr;
+  cx->preHold.reset();
   CU(cudaMemcpyAsync(cx->dPre, &w, sizeof(uint64_t), cudaMemcpyHostToDevice, s));
   WalkParams wp{};
   wp.M = cx->dM; wp.r = n; wp.c = m; wp.mode = pr.mode; wp.d = base; wp.k = nfixed - 1; wp.s = s_;

@@ -186,8 +186,11 @@ cudaError_t walk_generic_launch(const WalkParams& p, int grid, cudaStream_t st, 
 int walk_generic_occupancy(int d, int c, int* block_out);
 // Argmax recovery: re-walk the units key_unit(*key) << key_shift .. + 2^key_shift - 1 and
 // write the smallest (unit offset << 32 | lexicographic suffix key) attaining
-// key_value(*key) into *lex_out (atomicMin).
-cudaError_t recover_launch(const WalkParams& p, unsigned long long* lex_out, cudaStream_t st);
+// key_value(*key) into *lex_out (atomicMin), and the largest value seen (biased as the
+// key's high word) into *rmax_out (atomicMax) for the self-check.  Batched launches:
+// lex_out / rmax_out / key are per matrix; the batch is passed in p.batch (<= 65535).
+cudaError_t recover_launch(const WalkParams& p, unsigned long long* lex_out, unsigned long long* rmax_out,
+                           cudaStream_t st);
 // Trace: per-step values of one unit (test hook).
 cudaError_t trace_launch(const WalkParams& p, int64_t max_steps, int64_t* values, int8_t* digits,
                          cudaStream_t st);

@@ -70,6 +70,8 @@ __device__ __forceinline__ uint64_t ipow64(uint32_t b, int e) {
   return r;
 }
 
+// Batched launches (p.batch > 1, many small matrices): work item t is unit
+// t % units_per of matrix t / units_per (matrix b at M + b*m_stride, key[b]).
 __global__ void __launch_bounds__(32 * kGenWarps) walk_generic_kernel(const WalkParams p) {
   extern __shared__ int32_t smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -78,24 +80,28 @@ __global__ void __launch_bounds__(32 * kGenWarps) walk_generic_kernel(const Walk
   const uint32_t base = (uint32_t)base_of(p);
   const uint64_t words = ipow64(base, p.s);
   unsigned long long best_key = 0;
+  WalkParams q = p;
   while (true) {
     unsigned long long t = 0;
     if (lane == 0) t = atomicAdd(p.counter, 1ull);
     t = __shfl_sync(0xffffffffu, t, 0);
     if ((int64_t)t >= p.unit_count) break;
-    const int64_t u = p.unit_begin + (int64_t)t;
-    gen_init(p, u, 0, G, lane);
-    int32_t best = gen_value(p, G, lane);
+    int64_t lu = (int64_t)t, b = 0;
+    if (p.batch > 1) { b = lu / p.units_per; lu -= b * p.units_per; q.M = p.M + b * p.m_stride; }
+    const int64_t u = p.unit_begin + lu;
+    gen_init(q, u, 0, G, lane);
+    int32_t best = gen_value(q, G, lane);
     for (uint64_t w = 1; w < words; ++w) {
       uint32_t i, from, to;
       dary_change_values(base, w, &i, &from, &to);
-      gen_move(p, G, p.r - 1 - (int)i, (int)from, (int)to, lane);
-      int32_t v = gen_value(p, G, lane);
+      gen_move(q, G, p.r - 1 - (int)i, (int)from, (int)to, lane);
+      int32_t v = gen_value(q, G, lane);
       best = v > best ? v : best;
     }
     if (p.unit_max && lane == 0) p.unit_max[t] = best;
     unsigned long long kk = make_key(best, (uint32_t)u);
-    best_key = kk > best_key ? kk : best_key;
+    if (p.batch > 1) { if (lane == 0) atomicMax(p.key + b, kk); }
+    else best_key = kk > best_key ? kk : best_key;
   }
   if (lane == 0 && best_key) atomicMax(p.key, best_key);
 }
@@ -103,17 +109,12 @@ __global__ void __launch_bounds__(32 * kGenWarps) walk_generic_kernel(const Walk
 // Recovery: the words of the winning unit are split into contiguous chunks
 // (Algorithm 1), one per warp; each warp starts from its
 // chunk's first word by the closed form and walks it, keeping the smallest
-// lexicographic suffix key among words whose value equals the optimum.
-__global__ void __launch_bounds__(32 * kGenWarps) recover_kernel(const WalkParams pin, unsigned long long* lex_out) {
-  extern __shared__ int32_t smem[];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  // batched launches: blockIdx.y = matrix
-  WalkParams p = pin;
-  p.M = pin.M + (int64_t)blockIdx.y * pin.m_stride;
-  p.key = pin.key + blockIdx.y;
-  lex_out += blockIdx.y;
-  const int nG = groups_of(p);
-  int32_t* G = smem + wib * nG * p.c;
+// lexicographic suffix key among words whose value equals the optimum.  The
+// re-walk recomputes every value with independent int32 group sums, so it also
+// checks the hot kernels: the largest value it sees goes to rmax_out (biased like
+// the key) and must equal the key's value (host check, LNORM_EINTERNAL otherwise).
+__device__ void recover_one(const WalkParams& p, unsigned long long* lex_out, unsigned long long* rmax_out,
+                            int32_t* G, int lane, int wib) {
   const uint32_t base = (uint32_t)base_of(p);
   const uint64_t words = ipow64(base, p.s);
   const unsigned long long key = *p.key;
@@ -126,7 +127,9 @@ __global__ void __launch_bounds__(32 * kGenWarps) recover_kernel(const WalkParam
   const uint64_t lo = t * J + (t < R ? t : R);
   const uint64_t hi = lo + J + (t < R ? 1 : 0);
   if (lo >= hi) return;
+  if (key == 0ull || g0 < p.unit_begin || g0 >= p.unit_begin + p.unit_count) return;   // no valid key: report nothing
   unsigned long long bestlex = ~0ull;
+  int32_t vmax = INT32_MIN;
   for (int64_t o = 0; o < gcount; ++o) {
     const int64_t u = g0 + o;
     if (u >= p.unit_begin + p.unit_count) break;              // (a group may run past the last unit)
@@ -134,17 +137,39 @@ __global__ void __launch_bounds__(32 * kGenWarps) recover_kernel(const WalkParam
     uint64_t lex = 0;
     for (int i = 0; i < p.s; ++i) lex += (uint64_t)dary_digit(base, (uint32_t)i, lo) * ipow64(base, i);
     const unsigned long long hiword = (unsigned long long)o << 32;
-    if (gen_value(p, G, lane) == target && (hiword | lex) < bestlex) bestlex = hiword | lex;
+    int32_t v = gen_value(p, G, lane);
+    vmax = max(vmax, v);
+    if (v == target && (hiword | lex) < bestlex) bestlex = hiword | lex;
     for (uint64_t w = lo + 1; w < hi; ++w) {
       uint32_t i, from, to;
       dary_change_values(base, w, &i, &from, &to);
       gen_move(p, G, p.r - 1 - (int)i, (int)from, (int)to, lane);
       lex = lex + (uint64_t)to * ipow64(base, (int)i) - (uint64_t)from * ipow64(base, (int)i);
-      if (gen_value(p, G, lane) == target && (hiword | lex) < bestlex) bestlex = hiword | lex;
+      v = gen_value(p, G, lane);
+      vmax = max(vmax, v);
+      if (v == target && (hiword | lex) < bestlex) bestlex = hiword | lex;
     }
     if (bestlex != ~0ull) break;                              // an earlier unit of the group wins
   }
-  if (lane == 0 && bestlex != ~0ull) atomicMin(lex_out, bestlex);
+  if (lane == 0) {
+    if (bestlex != ~0ull) atomicMin(lex_out, bestlex);
+    atomicMax(rmax_out, (unsigned long long)((uint32_t)vmax ^ 0x80000000u));
+  }
+}
+
+// Batched launches: matrices b = blockIdx.y, blockIdx.y + gridDim.y, ... (any batch size).
+__global__ void __launch_bounds__(32 * kGenWarps) recover_kernel(const WalkParams pin, unsigned long long* lex_out,
+                                                                 unsigned long long* rmax_out) {
+  extern __shared__ int32_t smem[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  int32_t* G = smem + wib * groups_of(pin) * pin.c;
+  const int nb = pin.batch > 0 ? pin.batch : 1;
+  for (int b = blockIdx.y; b < nb; b += gridDim.y) {
+    WalkParams p = pin;
+    p.M = pin.M + (int64_t)b * pin.m_stride;
+    p.key = pin.key + b;
+    recover_one(p, lex_out + b, rmax_out + b, G, lane, wib);
+  }
 }
 
 // Trace: one warp walks unit p.unit_begin and records every step.
@@ -203,7 +228,8 @@ cudaError_t walk_generic_launch(const WalkParams& p, int grid, cudaStream_t st, 
   return cudaGetLastError();
 }
 
-cudaError_t recover_launch(const WalkParams& p, unsigned long long* lex_out, cudaStream_t st) {
+cudaError_t recover_launch(const WalkParams& p, unsigned long long* lex_out, unsigned long long* rmax_out,
+                           cudaStream_t st) {
   const int nG = p.mode == MODE_LD ? p.d : 2;
   size_t sm = gen_smem(nG, p.c, kGenWarps);
   cudaError_t e = cudaFuncSetAttribute(recover_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -217,7 +243,8 @@ cudaError_t recover_launch(const WalkParams& p, unsigned long long* lex_out, cud
   for (int i = 0; i < p.s; ++i) words *= (uint64_t)(p.mode == MODE_LD ? p.d : 2);
   int gx = (int)std::min<uint64_t>((uint64_t)nsm * 4, std::max<uint64_t>(1, words / (64ull * kGenWarps)));
   if (p.batch > 1) gx = std::max(1, std::min(gx, (nsm * 8 + p.batch - 1) / p.batch));
-  recover_kernel<<<dim3(gx, p.batch > 0 ? p.batch : 1), 32 * kGenWarps, sm, st>>>(p, lex_out);
+  const int gy = std::max(1, std::min(p.batch > 0 ? p.batch : 1, 65535));
+  recover_kernel<<<dim3(gx, gy), 32 * kGenWarps, sm, st>>>(p, lex_out, rmax_out);
   return cudaGetLastError();
 }
 

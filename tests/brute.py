@@ -57,3 +57,44 @@ def ld_dual(M, d):
             v += max(sum(M[x][y] * b[k][y] for y in range(m)) for k in range(d))
         best = v if best is None or v > best else best
     return best
+
+
+def strategy_value_bilinear(M, x, marg=False):
+    """Value of one +-1 strategy x as max over Bob's y of x^T M y (y_0 = +1 for L_marg)."""
+    n, m = len(M), len(M[0])
+    best = None
+    ys = product((1, -1), repeat=m - 1) if marg else product((1, -1), repeat=m)
+    for yr in ys:
+        y = ((1,) + yr) if marg else yr
+        v = sum(x[i] * M[i][j] * y[j] for i in range(n) for j in range(m))
+        best = v if best is None or v > best else best
+    return best
+
+
+def labelling_value_eq5(M, a, d):
+    """Value of one labelling a by Eq. (5) with a fixed: max over outputs b^g_y, column by column."""
+    n, m = len(M), len(M[0])
+    v = 0
+    for g in range(d):
+        for y in range(m):
+            v += max(sum(M[x][y] * b for x in range(n) if a[x] == g) for b in (1, -1))
+    return v
+
+
+def prefix_max_brute(M, fixed, d=1, marg=False):
+    """Max over completions of a fixed prefix of rows 0..len(fixed)-1, and the lexicographically
+    smallest maximising completion (digits: 0/1 <-> +1/-1 for d = 1, labels for d >= 2).
+    Completions are enumerated with itertools in lexicographic order; the value of each comes
+    from the bilinear form (d = 1) or Eq. (5) (d >= 2), not from the oracle's column sums."""
+    n = len(M)
+    base = 2 if d == 1 else d
+    best, arg = None, None
+    for rest in product(range(base), repeat=n - len(fixed)):
+        dig = tuple(fixed) + rest
+        if d == 1:
+            v = strategy_value_bilinear(M, [1 - 2 * t for t in dig], marg)
+        else:
+            v = labelling_value_eq5(M, dig, d)
+        if best is None or v > best:
+            best, arg = v, dig
+    return best, list(arg)

@@ -30,11 +30,11 @@ def test_library_exports_every_header_symbol():
     for f in funcs:
         assert hasattr(lib, f), f
     assert sorted(funcs) == sorted(L.SYMBOLS)
-    assert L.load().lnorm_version() >> 16 == 1
+    assert L.load().lnorm_version() >> 16 == 2
 
 
 def test_status_strings():
-    for s in range(8):
+    for s in range(9):
         assert L.status_string(s)
 
 
@@ -276,3 +276,34 @@ def test_dary_block_start_matches_eq17():
                 ip += 1
             S = list(range(d)) + list(range(d - 1, -1, -1))
             assert (dig, frm, to) == (1 + ip, S[(tt - 1) % (2 * d)], S[tt % (2 * d)])
+
+
+def test_binding_rejects_lossy_matrix_casts():
+    """The binding never wraps or truncates entries into int32: non-integer dtypes and
+    out-of-range integers raise before any library call."""
+    from paper_2503_21596_b200 import LNormError
+    with pytest.raises(TypeError):
+        L.compute(np.ones((3, 3)) * 1.7)
+    with pytest.raises(TypeError):
+        L.compute(np.ones((3, 3), dtype=bool))
+    with pytest.raises(LNormError) as e:
+        L.compute(np.array([[2 ** 33 + 3, 1], [1, 1]], dtype=np.int64))
+    assert e.value.name == "EOVERFLOW"
+    with pytest.raises(LNormError):
+        L.compute_batch(np.full((2, 2, 2), -(2 ** 31) - 1, dtype=np.int64))
+    with pytest.raises(ValueError):
+        L.compute(np.ones(4, dtype=np.int32))
+    # int64 input within range is accepted by the binding (then needs a device on this host)
+    A = L._mat(np.array([[5, -7], [2 ** 31 - 1, -(2 ** 31)]], dtype=np.int64))
+    assert A.dtype == np.int32 and A[1, 0] == 2 ** 31 - 1 and A[1, 1] == -(2 ** 31)
+
+
+def test_rank_entry_checks_communicator_arguments_before_the_device():
+    """lnorm_compute_rank: world > 1 without a communicator, or a rank outside [0, world), is
+    EINVAL (checked before any device work, so also on this GPU-less host)."""
+    from paper_2503_21596_b200 import LNormError
+    M = np.eye(3, dtype=np.int32)
+    for rank, world in ((0, 2), (2, 2), (-1, 1), (0, 0)):
+        with pytest.raises(LNormError) as e:
+            L.compute_rank(M, None, rank, world)
+        assert e.value.name == "EINVAL", (rank, world)

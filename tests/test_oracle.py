@@ -285,3 +285,28 @@ def test_thread_count_independence(threads):
     assert oracle.l1(M, threads=threads)[0] == oracle.l1(M, threads=1)[0]
     assert list(oracle.l1(M, threads=threads)[1]) == list(oracle.l1(M, threads=1)[1])
     assert list(oracle.ld(M, 3, threads=threads)[1]) == list(oracle.ld(M, 3, threads=1)[1])
+
+
+@pytest.mark.parametrize("d,marg,n,m", [(1, False, 6, 4), (1, True, 6, 4), (2, False, 6, 3), (3, False, 5, 3),
+                                        (4, False, 5, 2)])
+def test_prefix_max_brute_force_pin(d, marg, n, m):
+    """oracle.prefix_max with 1 < nfixed < n against an independent brute force (tests/brute.py:
+    lexicographic itertools enumeration of the completions, bilinear / Eq. (5) values): the
+    maximum over the completions of the fixed rows AND its lexicographically smallest maximiser.
+    A prefix that is ignored, mis-ordered or read with the wrong digit convention fails here: the
+    cases include prefixes whose constrained maximum is strictly below the norm."""
+    base = 2 if d == 1 else d
+    below = 0
+    for seed in range(6):
+        M = rnd(n, m, 9900 + 10 * seed + d + 5 * marg, -4, 4)
+        full = oracle.norm(M, d=d, with_marginals=marg)[0]
+        g = synth.SplitMix64(991 + seed)
+        for nfixed in range(2, n):
+            fixed = [0] + [g.next() % base for _ in range(nfixed - 1)]
+            v, arg = oracle.prefix_max(M, fixed, d=d, with_marginals=marg)
+            bv, barg = brute.prefix_max_brute(M.tolist(), fixed, d=d, marg=marg)
+            assert v == bv, (seed, fixed)
+            assert list(arg) == barg, (seed, fixed, list(arg), barg)
+            assert v <= full
+            below += v < full
+    assert below > 0
