@@ -10,7 +10,8 @@ recovery).  Prints ONE JSON line (rank 0).
 value  : Gray-code steps (strategies) per second of the whole job, matrix resident in HBM
 e2e    : the same metric through lnorm_compute / lnorm_compute_rank with a pinned host matrix
          (H2D of M and D2H of value+argmax inside every timed step)
-roofline: integer-issue roofline of the walk kernel
+roofline: ALU-pipe roofline of the walk kernel: the kernel family's binding-pipe
+         instruction floor per strategy x strategies / walk time, against 64 lane-instr/clk/SM x SMs x f_max
 cpu_baseline: the naive oracle (oracle/) on the box's host cores, bounded sample (rank 0, N = 1)
 --impl reference: the oracle as the reference arm (host cores, bounded sample per step)
 """
@@ -37,7 +38,45 @@ CONFIGS = {
     "marg_40x40": (40, 40, 1, True, 3, "L_marg of a 40x40 marginal-augmented correlator matrix, entries in [-10,10], seed 3"),
     "l2_24x24": (24, 24, 2, False, 4, "L_2 of a random 24x24 witness matrix, entries in [-10,10], seed 4"),
     "l3_24x24": (24, 24, 3, False, 4, "L_3 of a random 24x24 witness matrix, entries in [-10,10], seed 4"),
+    # config-5 sweep points used for profiles (not the headline)
+    "l3_26x26": (26, 26, 3, False, 226, "L_3 of a random 26x26 matrix, entries in [-10,10], seed 226 (config 5b top)"),
+    "l4_18x18": (18, 18, 4, False, 218, "L_4 of a random 18x18 matrix, entries in [-10,10], seed 218 (P:371)"),
+    "l1_36x144": (36, 144, 1, False, 136, "L_1 of a random 36x144 matrix, entries in [-10,10], seed 136 (config 5a, m = 4n)"),
+    "l1_40x160": (40, 160, 1, False, 140, "L_1 of a random 40x160 matrix, entries in [-10,10], seed 140 (config 5a, m = 4n)"),
 }
+
+
+def alu_floor(variant, d, c, s, d_walked):
+    """Binding-pipe instruction floor per strategy of the kernel family's own algorithm
+    (DESIGN.md "Roofline"): (instructions per strategy, pipe, lane-instructions/clk/SM of that pipe).
+
+    7 byte walk (L_1/L_marg/L_2): per walked word, per unit, G*c/4 VABSDIFF4 per bias set (two
+      sets: the paired last row's two signs) + one VIMNMX3 per two strategies
+      -> G*c/4 + 1/2 per strategy on the ALU pipe (G = 2 for L_2's two groups).
+    8 byte d-ary walk (L_3/L_4), PR paired rows (3 if s >= 4, 2 if s = 3, 1 if s = 2): a move
+      recomputes 2^PR bias sums of the two changed groups: 2*2^PR*c/4 VABSDIFF4, then the max of
+      the T = d^PR labellings (ceil((T-1)/2) VIMNMX3) and one VIADDMNMX for the running best,
+      shared by T strategies, on the ALU pipe.
+    16-bit / int32 families: issue-bound (both integer pipes), instructions per strategy."""
+    if variant == 7:
+        G = 2 if d == 2 else 1
+        return G * c / 4.0 + 0.5, "alu", 64.0
+    if variant == 8:
+        pr = 3 if s >= 4 else (2 if s == 3 else 1)
+        T = d_walked ** pr
+        per_word = 2 * (2 ** pr) * c / 4.0 + (T - 1 + 1) // 2 + 1   # ceil((T-1)/2) = T // 2
+        return per_word / T, "alu", 64.0
+    if variant in (3, 5):
+        return float(c), "issue", 128.0
+    if variant == 6:
+        return 4.0 * c / d_walked, "issue", 128.0
+    if variant == 4:
+        return 2.0 * c, "issue", 128.0
+    if variant == 0:
+        return 2.0 * c, "issue", 128.0
+    if variant == 1:
+        return 4.0 * c, "issue", 128.0
+    return None, None, None
 
 def metric_name(n, m, d, marg):
     norm = "L_marg" if marg else ("L_1" if d == 1 else f"L_{d}")
@@ -113,6 +152,24 @@ def cpu_baseline(M, d, marg, target_s=12.0):
                       f"from-scratch int64 evaluation, {dt2:.1f} s"}
 
 
+VARIANT_NAMES = {0: "bin_int32", 1: "ld_int32", 2: "generic", 3: "bin_packed16", 4: "ld_packed16", 5: "bin_pair16",
+                 6: "ld_pair16", 7: "bin_u8", 8: "ld_u8"}
+ALU_FLOOR_NOTE = {
+    7: "per strategy: G*c/4 VABSDIFF4 (four |.|-accumulates each) + 1/2 VIMNMX3, ALU pipe (c columns, G = 1; L_2: 2)",
+    8: "per walked word: 2*2^PR*c/4 VABSDIFF4 + ceil((d^PR-1)/2) VIMNMX3 + 1 VIADDMNMX for d^PR strategies, ALU pipe",
+}
+
+
+def load_walk_profile(config):
+    """ncu numbers of the walk kernel for this config (profiles/r02/walk_profiles.json, captured with
+    `ncu --set full` on this bench's own launch; tools/ncu_bench.py)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02", "walk_profiles.json")) as f:
+            return json.load(f).get(config)
+    except Exception:
+        return None
+
+
 def flush_l2(buf):
     buf.add_(1)   # 256 MiB write > 126 MB L2
 
@@ -179,14 +236,19 @@ def main():
     import paper_2503_21596_b200 as L
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    # launched by torchrun (also with --nproc-per-node 1): one rank per GPU, torch's own NCCL
+    # communicator is handed to the library (caller-owned comm, lnorm_compute_rank), which
+    # all-reduces the 8-byte key (+ error flag) on our stream
+    distributed = "RANK" in os.environ and "WORLD_SIZE" in os.environ
     dist = None
     comm = None
-    if world > 1:
+    if distributed:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
-        obj = [L.Comm.unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        comm = L.Comm(obj[0], rank, world, local)
+        t0 = torch.ones(1, device=dev)
+        dist.all_reduce(t0)
+        comm = L.torch_nccl_comm(device=dev)
+    stream = torch.cuda.Stream(device=dev)
 
     Md = torch.from_numpy(M).to(dev)
     pinned = torch.from_numpy(M).pin_memory()
@@ -194,91 +256,115 @@ def main():
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device=dev)
 
     def run_device():
-        if comm is not None:
-            return comm.compute_device(Md, d=d, with_marginals=marg)
-        return L.compute_device(Md, d=d, with_marginals=marg)
+        if distributed:
+            return L.compute_rank_device(Md, comm, rank, world, d=d, with_marginals=marg, stream=stream)
+        return L.compute_device(Md, d=d, with_marginals=marg, stream=stream)
 
     def run_host():
-        if comm is not None:
-            return comm.compute(Mh, d=d, with_marginals=marg)
+        if distributed:
+            return L.compute_rank(Mh, comm, rank, world, d=d, with_marginals=marg, stream=stream)
         return L.compute(Mh, d=d, with_marginals=marg)
 
     def barrier():
+        torch.cuda.synchronize()
         if dist is not None:
-            dist.barrier()
+            dist.barrier(device_ids=[local])
         torch.cuda.synchronize()
 
-    for _ in range(max(3, args.warmup)):
-        res = run_device()
-    barrier()
-
-    stats_walk = []
-    times = []
-    launches = 0
-    with ClockSampler(local) as clk:
-        for _ in range(args.steps):
-            flush_l2(flush)
-            barrier()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
+    with torch.cuda.stream(stream):
+        for _ in range(max(3, args.warmup)):
             res = run_device()
-            e1.record()
-            barrier()
-            times.append(e0.elapsed_time(e1))
-            st = L.last_stats()
-            stats_walk.append(st["walk_ms"])
-            launches += st["launches"]
-        # e2e: host buffers through the public API, H2D + D2H inside the timed region
-        e2e_times = []
-        for _ in range(args.steps):
-            flush_l2(flush)
-            barrier()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            res_h = run_host()
-            e1.record()
-            barrier()
-            e2e_times.append(e0.elapsed_time(e1))
+        barrier()
+
+        stats_walk = []
+        times = []
+        launches = 0
+        with ClockSampler(local) as clk:
+            for _ in range(args.steps):
+                flush_l2(flush)
+                barrier()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                res = run_device()
+                e1.record(stream)
+                barrier()
+                times.append(e0.elapsed_time(e1))
+                st = L.last_stats()
+                stats_walk.append(st["walk_ms"])
+                launches += st["launches"]
+            # e2e: host buffers through the public API, H2D + D2H inside the timed region
+            e2e_times = []
+            for _ in range(args.steps):
+                flush_l2(flush)
+                barrier()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                res_h = run_host()
+                e1.record(stream)
+                barrier()
+                e2e_times.append(e0.elapsed_time(e1))
     st = L.last_stats()
     value, argmax = res
     assert res_h[0] == value and list(res_h[1]) == list(argmax), "host and device paths disagree"
 
-    t = torch.tensor([sum(times), sum(e2e_times), sum(stats_walk)], dtype=torch.float64, device=dev)
+    mine = torch.tensor([sum(times), sum(e2e_times), sum(stats_walk), float(st["steps"])], dtype=torch.float64, device=dev)
     if dist is not None:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    T, TE, TW = [float(x) for x in t.tolist()]
+        allr = [torch.zeros_like(mine) for _ in range(world)]
+        dist.all_gather(allr, mine)
+        per_rank = torch.stack(allr).cpu().tolist()
+    else:
+        per_rank = [mine.cpu().tolist()]
+    T = max(r[0] for r in per_rank)
+    TE = max(r[1] for r in per_rank)
+    TW = per_rank[0][2]
     if total_steps is None:
-        total_steps = st["steps"] * (world if world > 1 else 1)
+        total_steps = sum(r[3] for r in per_rank)
     ms_per_step = T / args.steps
     val = total_steps / (ms_per_step / 1e3)
     e2e = total_steps / (TE / args.steps / 1e3)
 
     if rank == 0:
         c = clk.summary()
-        col_updates = total_steps * (st["cols"] if st["d"] <= 2 else 2 * st["cols"])
+        cols = st["cols"]
+        col_updates = total_steps * (cols if st["d"] <= 2 else 2 * cols)
         walk_ms = TW / args.steps
-        achieved_ops = 2.0 * col_updates / (walk_ms / 1e3) / 1e12     # Tops/s (add + |.|-accumulate)
         nsm = torch.cuda.get_device_properties(dev).multi_processor_count
         peak_mhz = load_peak_clock()
-        simd = 4 if st["variant"] in (7, 8) else (2 if st["variant"] in (3, 4, 5, 6) else 1)   # u8x4 / s16x2 / int32 lanes per register
-        packed = simd > 1
-        lanes = 128.0 * simd
-        peak = lanes * nsm * peak_mhz * 1e6 * world / 1e12             # integer lane-ops/clk/SM x SMs x f_max
-        dtype = {4: "u8x4", 2: "int16x2", 1: "int32"}[simd]
-        traffic = None
-        tf = os.path.join(ROOT, "profiles", "r01", "walk_traffic.json")
-        if os.path.exists(tf):
-            try:
-                traffic = json.load(open(tf)).get("dram_bytes_per_launch")
-            except Exception:
-                traffic = None
+        variant = st["variant"]
+        per_strat, pipe, lanes = alu_floor(variant, d, cols, st["suffix_digits"], st["d"] if d > 1 else 2)
+        dtype = {7: "u8x4", 8: "u8x4", 3: "int16x2", 4: "int16x2", 5: "int16x2", 6: "int16x2"}.get(variant, "int32")
+        rank_steps = per_rank[0][3]
+        roof = {"bound": "alu", "achieved": None, "peak": None, "unit": None, "frac": None, "traffic": None}
+        if per_strat is not None:
+            floor_instr = rank_steps * per_strat                         # binding-pipe lane-instructions per launch
+            achieved = floor_instr / (walk_ms / 1e3) / 1e12
+            peak = lanes * nsm * peak_mhz * 1e6 / 1e12
+            roof.update({
+                "achieved": achieved, "peak": peak,
+                "unit": f"T lane-instr/s on the {'ALU pipe' if pipe == 'alu' else 'issue slots (ALU + FMA-heavy integer pipes)'}",
+                "frac": achieved / peak,
+                "frac_at_measured_clock": (achieved / (peak * c["sm_mhz"] / peak_mhz)) if c.get("sm_mhz") else None,
+                "kernel": f"walk variant {variant} ({VARIANT_NAMES.get(variant, '?')}), 1 launch per search per GPU",
+                "walk_ms_per_launch": walk_ms,
+                "floor_instr_per_strategy": per_strat,
+                "floor_model": ALU_FLOOR_NOTE.get(variant, ""),
+                "peak_basis": (f"{lanes:.0f} lane-instr/clk/SM ({'ALU pipe: VABSDIFF4 measured 64/clk/SM, profiles/r01/peaks_u8.jsonl' if pipe == 'alu' else 'issue limit, 4 SMSPs x 32 lanes'})"
+                               f" x {nsm} SMs x {peak_mhz:.0f} MHz (sm_max_mhz, MEASURED_PEAKS.json)"),
+            })
+        prof = load_walk_profile(args.config)
+        if prof:
+            roof["traffic"] = prof.get("dram_bytes_per_launch")
+            roof["ncu"] = {k: prof.get(k) for k in ("alu_pipe_pct", "issue_active_pct", "fma_pipe_pct",
+                                                      "smem_bank_conflicts", "dram_bytes_per_launch", "source")}
         line = {
             "metric": metric_name(n, m, d, marg),
             "value": val, "unit": "steps/s", "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup),
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": dtype, "data": "synthetic",
-            "config": {"workload": desc, "n": n, "m": m, "d": d, "with_marginals": marg,
-                       "strategies_per_step": total_steps, "parallelism": f"units split over {world} GPU(s) (Algorithm 1) + 1 NCCL all-reduce(max)",
+            "config": {"workload": desc, "name": args.config, "n": n, "m": m, "d": d, "with_marginals": marg,
+                       "strategies_per_step": total_steps,
+                       "parallelism": (f"units split over {world} GPU rank(s) (Algorithm 1) + 1 ncclAllReduce(max) through "
+                                       f"torch's NCCL communicator" if distributed else "1 GPU, no collective"),
                        "l2": "256 MiB buffer written between timed steps (flush); matrix 7 KB"},
             "result": {"value": value, "argmax": [int(x) for x in argmax]},
             "wall_s_per_search": ms_per_step / 1e3,
@@ -286,30 +372,17 @@ def main():
             "e2e": {"value": e2e, "unit": "steps/s", "h2d_bytes_per_step": int(M.nbytes),
                     "d2h_bytes_per_step": 8 + n, "ms_per_step": TE / args.steps},
             "gpu_launches": int(launches),
-            "roofline": {"bound": "alu", "achieved": achieved_ops, "peak": peak,
-                         "unit": "Tops/s (" + ({4: "u8x4 SIMD lanes", 2: "int16x2 SIMD lanes", 1: "int32"}[simd]) + ")",
-                         "frac": achieved_ops / peak, "traffic": traffic,
-                         "kernel": "walk (dominant)", "walk_ms_per_launch": walk_ms,
-                         "peak_basis": (f"128 lane-instr/clk/SM (ALU + FMA-heavy integer pipes = issue limit; VIADD+VABSDIFF mix "
-                                        f"measured 127, profiles/r01/peaks_b4.jsonl) x {({4: '4 u8 bytes x ', 2: '2 s16 halves x ', 1: ''})[simd]}"
-                                        f"{nsm} SMs x {peak_mhz:.0f} MHz; algorithmic work = 2 ops per column update"),
-                         "kernel_variant": st["variant"],
-                         "frac_at_measured_clock": (achieved_ops / (peak * (c["sm_mhz"] or peak_mhz) / peak_mhz)) if c["sm_mhz"] else None,
-                         "note": ("algorithmic work counts 2 ops per column update of a plain walk (SURVEY 8(d)); "
-                                  "frac > 1 means the kernel's row pairing (last rows evaluated for all labels per "
-                                  "walked word) needs fewer instructions per strategy than that count"
-                                  if achieved_ops > peak else
-                                  "algorithmic work counts 2 ops per column update of a plain walk (SURVEY 8(d))")},
+            "per_rank": [{"rank": i, "ms_per_step": r[0] / args.steps, "walk_ms": r[2] / args.steps,
+                          "e2e_ms_per_step": r[1] / args.steps, "strategies": r[3]} for i, r in enumerate(per_rank)],
+            "roofline": roof,
             "clocks": c,
             "stats": st,
         }
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(M, d, marg)
         print(json.dumps(line), flush=True)
-    if comm is not None:
-        comm.close()
     if dist is not None:
-        dist.barrier()
+        dist.barrier(device_ids=[local])
         dist.destroy_process_group()
 
 
