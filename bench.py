@@ -46,14 +46,14 @@ CONFIGS = {
 }
 
 
-def alu_floor(variant, d, c, s, d_walked):
+def alu_floor(variant, d, c, s, d_walked, pr=None):
     """Binding-pipe instruction floor per strategy of the kernel family's own algorithm
     (DESIGN.md "Roofline"): (instructions per strategy, pipe, lane-instructions/clk/SM of that pipe).
 
     7 byte walk (L_1/L_marg/L_2): per walked word, per unit, G*c/4 VABSDIFF4 per bias set (two
       sets: the paired last row's two signs) + one VIMNMX3 per two strategies
       -> G*c/4 + 1/2 per strategy on the ALU pipe (G = 2 for L_2's two groups).
-    8 byte d-ary walk (L_3/L_4), PR paired rows (3 if s >= 4, 2 if s = 3, 1 if s = 2): a move
+    8 byte d-ary walk (L_3/L_4), PR paired rows (lnorm_stats.paired_rows; L_3: 4 if s >= 5): a move
       recomputes 2^PR bias sums of the two changed groups: 2*2^PR*c/4 VABSDIFF4, then the max of
       the T = d^PR labellings (ceil((T-1)/2) VIMNMX3) and one VIADDMNMX for the running best,
       shared by T strategies, on the ALU pipe.
@@ -62,7 +62,8 @@ def alu_floor(variant, d, c, s, d_walked):
         G = 2 if d == 2 else 1
         return G * c / 4.0 + 0.5, "alu", 64.0
     if variant == 8:
-        pr = 3 if s >= 4 else (2 if s == 3 else 1)
+        if not pr:
+            pr = 3 if s >= 4 else (2 if s == 3 else 1)
         T = d_walked ** pr
         per_word = 2 * (2 ** pr) * c / 4.0 + (T - 1 + 1) // 2 + 1   # ceil((T-1)/2) = T // 2
         return per_word / T, "alu", 64.0
@@ -331,7 +332,8 @@ def main():
         nsm = torch.cuda.get_device_properties(dev).multi_processor_count
         peak_mhz = load_peak_clock()
         variant = st["variant"]
-        per_strat, pipe, lanes = alu_floor(variant, d, cols, st["suffix_digits"], st["d"] if d > 1 else 2)
+        per_strat, pipe, lanes = alu_floor(variant, d, cols, st["suffix_digits"], st["d"] if d > 1 else 2,
+                                           st.get("paired_rows"))
         dtype = {7: "u8x4", 8: "u8x4", 3: "int16x2", 4: "int16x2", 5: "int16x2", 6: "int16x2"}.get(variant, "int32")
         rank_steps = per_rank[0][3]
         roof = {"bound": "alu", "achieved": None, "peak": None, "unit": None, "frac": None, "traffic": None}

@@ -306,6 +306,8 @@ typedef struct {
   int32_t launches;            /* kernels launched by the call */
   int32_t variant;             /* kernel variant id */
   int32_t block_threads, grid_blocks;
+  int32_t paired_rows;         /* packed kernels: last rows evaluated for all labels per walked word (0: none) */
+  int32_t reserved;
 } lnorm_stats;
 int lnorm_last_stats(lnorm_stats* out);
 

@@ -378,15 +378,16 @@ int make_plan(const Problem& pr, int world, Plan* pl, int64_t target_override = 
   } else {
     const int d = pr.dl;
     const int ov = kernel_override();
-    const bool hot = walk_ld_supported(d, pr.c, 1) && f >= 1;
-    int kern = hot ? K_LD : K_GEN;
-    int smin = hot ? 1 : 0;
-    if (hot && ov != K_BIN && ov != K_GEN) {
+    // the fastest exact d-ary family (byte > last-row-paired 16-bit > 16-bit > int32 > generic);
+    // each is checked on its own column limit (the int32 walk stops at 32 columns, the byte
+    // walk at 48, the 16-bit ones at 64), LNORM_KERNEL starts the order lower
+    int kern = K_GEN, smin = 0;
+    if (f >= 1 && ov != K_GEN) {
       if (ov < 0 && pr.mode == MODE_LD && pr.sufW[pr.r] <= 255 && f >= 2 && walk_ldu8_supported(d, pr.c, 2)) { kern = K_LDU8; smin = 2; }
-      else if (pr.fitsLdPair && f >= 2 && walk_ldpair16_supported(d, pr.c, 2) && ov != K_BIN16) { kern = K_LDPAIR16; smin = 2; }
-      else if (pr.fits16 && walk_ld16_supported(d, pr.c, 1)) { kern = K_LD16; smin = 1; }
+      else if (ov != K_BIN && ov != K_BIN16 && pr.fitsLdPair && f >= 2 && walk_ldpair16_supported(d, pr.c, 2)) { kern = K_LDPAIR16; smin = 2; }
+      else if (ov != K_BIN && pr.fits16 && walk_ld16_supported(d, pr.c, 1)) { kern = K_LD16; smin = 1; }
+      else if (walk_ld_supported(d, pr.c, 1)) { kern = K_LD; smin = 1; }
     }
-    if (ov == K_GEN) { kern = K_GEN; smin = 0; }
     int k = 0;
     while (k < f - smin && (k + 2) * prefix_bits(d) <= 64 && rgs_count(k + 2, d) <= kTableCap && rgs_count(k + 1, d) < target) ++k;
     p.k = k; p.s = f - k;
@@ -412,8 +413,11 @@ int make_plan(const Problem& pr, int world, Plan* pl, int64_t target_override = 
     }
     p.units = (int64_t)p.shared->size();
     p.kernel = kern;
-    if (kern == K_LDU8 && !walk_ldu8_supported(d, pr.c, p.s)) kern = p.kernel = K_LDPAIR16;
-    if (kern == K_LDPAIR16 && !walk_ldpair16_supported(d, pr.c, p.s)) p.kernel = pr.fits16 && walk_ld16_supported(d, pr.c, p.s) ? K_LD16 : K_LD;
+    // the split may leave a suffix a family cannot take: step down the order
+    if (p.kernel == K_LDU8 && !walk_ldu8_supported(d, pr.c, p.s)) p.kernel = pr.fitsLdPair ? K_LDPAIR16 : K_LD16;
+    if (p.kernel == K_LDPAIR16 && !walk_ldpair16_supported(d, pr.c, p.s)) p.kernel = K_LD16;
+    if (p.kernel == K_LD16 && !(pr.fits16 && walk_ld16_supported(d, pr.c, p.s))) p.kernel = K_LD;
+    if (p.kernel == K_LD && !walk_ld_supported(d, pr.c, p.s)) p.kernel = K_GEN;
   }
   // per-unit word count must fit 32-bit block counters
   long double words = 1;
@@ -860,6 +864,7 @@ int run_device(DevCtx& cx, const int32_t* dIn, const Problem& pr, int rank, int 
   S.column_updates = S.steps * pr.c * (pr.mode == MODE_LD && pr.dl >= 3 ? 2 : 1);
   S.walk_ms = wms; S.total_ms = tms; S.launches = launches; S.variant = pl.kernel;
   S.block_threads = block; S.grid_blocks = grid;
+  S.paired_rows = pl.kernel == K_LDU8 ? walk_ldu8_paired_rows(pr.dl, pl.s) : (pl.kernel == K_U8 ? 1 : 0);
   *st = S;
   return LNORM_OK;
 }
@@ -1413,14 +1418,15 @@ int lnorm_prefix_maxima(const int32_t* M, int32_t n, int32_t m, int32_t d, int32
     if (grouped) pl.kernel = K_U8;
   }
   else {
-    pl.kernel = walk_ld_supported(base, pr.c, pl.s) ? K_LD : K_GEN;
-    if (pl.kernel == K_LD && pr.fits16 && walk_ld16_supported(base, pr.c, pl.s)) pl.kernel = K_LD16;
-    if ((pl.kernel == K_LD || pl.kernel == K_LD16) && pr.fitsLdPair && walk_ldpair16_supported(base, pr.c, pl.s))
-      pl.kernel = K_LDPAIR16;
+    // same family order as make_plan, each on its own column limit
     const int ov = kernel_override();
-    if (ov < 0 && pl.kernel == K_LDPAIR16 && pr.sufW[pr.r] <= 255 && walk_ldu8_supported(base, pr.c, pl.s))
-      pl.kernel = K_LDU8;
-    if (ov == K_GEN || (ov == K_BIN && pl.kernel != K_GEN)) pl.kernel = ov == K_GEN ? K_GEN : K_LD;
+    pl.kernel = K_GEN;
+    if (ov != K_GEN) {
+      if (ov < 0 && pr.sufW[pr.r] <= 255 && walk_ldu8_supported(base, pr.c, pl.s)) pl.kernel = K_LDU8;
+      else if (ov != K_BIN && ov != K_BIN16 && pr.fitsLdPair && walk_ldpair16_supported(base, pr.c, pl.s)) pl.kernel = K_LDPAIR16;
+      else if (ov != K_BIN && pr.fits16 && walk_ld16_supported(base, pr.c, pl.s)) pl.kernel = K_LD16;
+      else if (walk_ld_supported(base, pr.c, pl.s)) pl.kernel = K_LD;
+    }
   }
   long double words = 1;
   for (int i = 0; i < pl.s; ++i) words *= base;

@@ -172,6 +172,8 @@ template <int MODE> int walk_u8_unroll_mode(int c, int lpu);
 // Byte-packed d-ary walk, last row paired (L_d, d in {3,4}; guard: every column's
 // sum_x |M_xy| <= 255, checked by the caller).
 bool walk_ldu8_supported(int d, int c, int s);
+// rows the byte d-ary walk pairs for a unit of s suffix digits (the all-H kernel's 3-4 for L_3)
+int walk_ldu8_paired_rows(int d, int s);
 int walk_ldu8_units_per_lane(int d, int c, int s);
 int walk_ldu8_occupancy(int d, int c, int s, int* block_out);
 cudaError_t walk_ldu8_launch(const WalkParams& p, int32_t* scratch_tab, int32_t* scratch_init, int grid,
@@ -180,6 +182,12 @@ template <int D, int PART> int walk_ldu8_upl_part(int NW, int s);
 template <int D, int PART> int walk_ldu8_occ_part(int NW, int s);
 template <int D, int PART> cudaError_t walk_ldu8_launch_part(const WalkParams& p, const uint32_t* tab, const int32_t* init,
                                                              int grid, cudaStream_t st, int NW);
+// Byte-packed L_3 walk, 3 or 4 paired rows, all-H form, bias words in shared memory
+// (walk_ldu8w_impl.cuh); dispatched by walk_ldu8_launch when d = 3 and the suffix allows.
+template <int PART> cudaError_t walk_ldu8w_launch_part(const WalkParams& p, const uint32_t* tab, const int32_t* init,
+                                                       int grid, cudaStream_t st, int NW, int pr);
+template <int PART> int walk_ldu8w_occ_part(int NW, int pr, int s);
+template <int PART> int walk_ldu8w_upl_part(int NW, int pr);
 // Generic warp-per-unit walk (any mode, d, c, s).
 bool walk_generic_supported(int d, int c);
 cudaError_t walk_generic_launch(const WalkParams& p, int grid, cudaStream_t st, int* block_out);

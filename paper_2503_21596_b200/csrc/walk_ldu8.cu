@@ -1,12 +1,33 @@
 // Byte-packed d-ary walk: dispatch, exactness limits and the table builder (the kernels
 // are instantiated in walk_ldu8_d{3,4}{a,b}.cu; see walk_ldu8_impl.cuh).
+#include <algorithm>
+#include <cstdlib>
+
 #include "walk_ldu8_impl.cuh"
 
 namespace lnorm {
 
 namespace {
 int part_of(int NW) { return NW <= 6 ? 0 : 1; }
+
+// Paired rows of the all-H L_3 kernel (walk_ldu8w_impl.cuh) for a unit of s suffix digits:
+// 4 when at least one walked digit remains, 3 at s = 4, else 0 (the all-E kernel runs).
+// LNORM_LDU8W=0 disables it (A/B); LNORM_LDU8W_PR=3 caps it at three paired rows.
+int ldu8w_rows(int d, int s) {
+  if (d != 3) return 0;
+  const char* em = getenv("LNORM_LDU8W");
+  const char* ec = getenv("LNORM_LDU8W_PR");
+  const int mode = (em && *em) ? atoi(em) : 1, cap = (ec && *ec) ? atoi(ec) : 4;
+  if (!mode) return 0;
+  const int pr = s >= 5 ? 4 : (s == 4 ? 3 : 0);
+  return std::min(pr, cap) >= 3 ? std::min(pr, cap) : 0;
+}
 }  // namespace
+
+int walk_ldu8_paired_rows(int d, int s) {
+  const int wr = ldu8w_rows(d, s);
+  return wr ? wr : ldu8_rows(s);
+}
 
 bool walk_ldu8_supported(int d, int c, int s) {
   if ((d != 3 && d != 4) || c < 1 || s < 2) return false;
@@ -17,6 +38,7 @@ bool walk_ldu8_supported(int d, int c, int s) {
 
 int walk_ldu8_units_per_lane(int d, int c, int s) {
   const int NW = words_of(c), pt = part_of(NW);
+  if (const int wr = ldu8w_rows(d, s)) return pt ? walk_ldu8w_upl_part<1>(NW, wr) : walk_ldu8w_upl_part<0>(NW, wr);
   if (d == 3) return pt ? walk_ldu8_upl_part<3, 1>(NW, s) : walk_ldu8_upl_part<3, 0>(NW, s);
   if (d == 4) return pt ? walk_ldu8_upl_part<4, 1>(NW, s) : walk_ldu8_upl_part<4, 0>(NW, s);
   return 1;
@@ -25,6 +47,7 @@ int walk_ldu8_units_per_lane(int d, int c, int s) {
 int walk_ldu8_occupancy(int d, int c, int s, int* block_out) {
   *block_out = kBlockLU;
   const int NW = words_of(c), pt = part_of(NW);
+  if (const int wr = ldu8w_rows(d, s)) return pt ? walk_ldu8w_occ_part<1>(NW, wr, s) : walk_ldu8w_occ_part<0>(NW, wr, s);
   if (d == 3) return pt ? walk_ldu8_occ_part<3, 1>(NW, s) : walk_ldu8_occ_part<3, 0>(NW, s);
   if (d == 4) return pt ? walk_ldu8_occ_part<4, 1>(NW, s) : walk_ldu8_occ_part<4, 0>(NW, s);
   return 0;
@@ -34,12 +57,15 @@ cudaError_t walk_ldu8_launch(const WalkParams& p, int32_t* scratch_tab, int32_t*
                              cudaStream_t st, int* block_out) {
   *block_out = kBlockLU;
   const int NW = words_of(p.c), pt = part_of(NW);
-  const int pr = ldu8_rows(p.s);
+  const int wr = ldu8w_rows(p.d, p.s);
+  const int pr = wr ? wr : ldu8_rows(p.s);
   if ((p.s - pr) * 2 * lu_pad4(NW) > kTabWordsLU || (p.k + 3) * 4 * NW + (NW + 1) * (1 << pr) > 16384) return cudaErrorInvalidValue;
   uint32_t* tab = reinterpret_cast<uint32_t*>(scratch_tab);
   build_ldu8_kernel<<<1, 128, 0, st>>>(p.M, p.r, p.c, NW, p.k, p.s, pr, tab, scratch_init);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
+  if (wr) return pt ? walk_ldu8w_launch_part<1>(p, tab, scratch_init, grid, st, NW, wr)
+                    : walk_ldu8w_launch_part<0>(p, tab, scratch_init, grid, st, NW, wr);
   if (p.d == 3) return pt ? walk_ldu8_launch_part<3, 1>(p, tab, scratch_init, grid, st, NW)
                           : walk_ldu8_launch_part<3, 0>(p, tab, scratch_init, grid, st, NW);
   if (p.d == 4) return pt ? walk_ldu8_launch_part<4, 1>(p, tab, scratch_init, grid, st, NW)

@@ -498,7 +498,7 @@ int words_of(int c) { return (c + 3) / 4; }
 #ifdef LN_LDU8_PART
 // part 0: 1-6 words (<= 24 columns), part 1: 7-12 words
 #define LN_LDU8_PSWITCH(D, NW_, FN, ...)                                                     \
-  if (LN_LDU8_PART == 0) {                                                                   \
+  if constexpr (LN_LDU8_PART == 0) {                                                         \
     switch (NW_) {                                                                           \
       case 1: return FN<D, 1>(__VA_ARGS__); case 2: return FN<D, 2>(__VA_ARGS__);            \
       case 3: return FN<D, 3>(__VA_ARGS__); case 4: return FN<D, 4>(__VA_ARGS__);            \

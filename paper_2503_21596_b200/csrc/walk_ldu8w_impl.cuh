@@ -1,0 +1,409 @@
+// Hot d-ary Gray walk for L_3, column sums packed four per register as offset bytes,
+// the LAST PR (3 or 4) rows evaluated for all 3^PR labellings at every walked word, with
+// every group's 2^PR bias sums kept as plain |.|-sums ("all-H" form) and the bias words
+// staged in shared memory.
+//
+// Same units, restricted-growth prefixes, warp-uniform reflected ternary walk (PAPER.md
+// Eqs. 13-17) and byte encoding as walk_ldu8_impl.cuh (read its header first): group g's
+// column sum m_g,y lives in [N_y, N_y + W_y], a_g,y = m_g,y - N_y is one unsigned byte
+// when every W_y <= 255, one 32-bit add of a packed row moves a row between two groups
+// (Eqs. 18-19), and VABSDIFF4.U8.ACC accumulates four |.| per instruction.
+//
+// What differs.  For a subset T of the paired rows let
+//     H[T][g] = sum_y |m_g,y + sum_{i in T} rho_i,y|        (T = {} is the plain ||m_g||_1)
+// = sum_y |a_g,y - B_T,y| + kappa_T  with B_T = clamp(-N - sum_{i in T} rho_i, 0, 255).  A
+// labelling of the paired rows is the partition (T_0, T_1, T_2) of them by label, and by
+// Eq. (6) the strategy's value is exactly
+//     L*(walked word, labelling) = H[T_0][0] + H[T_1][1] + H[T_2][2]
+// -- three non-negative terms, no running S or differences to maintain.  A move p -> q
+// re-accumulates the 2^PR sums of the two changed groups (2 * 2^PR * NW VABSDIFF4 on the
+// ALU pipe), the 3^PR candidate values are two IMADs each (FMA-heavy pipe) and one max
+// tree over them and the running best (ceil(3^PR / 2) VIMNMX3, ALU).  Per strategy that is
+// (2 * 2^PR * c/4 + 3^PR / 2) / 3^PR ALU instructions: 4.07 at PR = 3, 2.88 at PR = 4 for
+// 24 columns (the all-E form of walk_ldu8_impl.cuh at PR = 3 needs the same 4.07).
+//
+// The 2^PR * NW bias words do not fit the register file next to 48 H sums at PR = 4, so they
+// are read per move from shared memory with warp-uniform LDS.128 broadcasts (four bias sets of
+// one word each, shared by the two moved groups); the K_T constants stay in registers.
+//
+// Control: a move of the reflected ternary walk is 0->1, 1->2, 2->1 or 1->0; the kernel holds
+// TWO sum bodies (groups {0,1} and {1,2}; the direction only picks which of the delta
+// record's +row / -row each group adds, a uniform shared-memory offset) and ONE copy of the
+// max tree, so the hot code stays small for the instruction cache.  The changed digit, old
+// and new label come from the uniform word counter: inside a block of three
+// words the low digit moves 0->1->2 (even block) or 2->1->0 (odd block: label complement),
+// the block start is dary_block_start (Eq. 17).
+#include <type_traits>
+#include <utility>
+
+#include "common.cuh"
+
+namespace lnorm {
+
+namespace {
+
+constexpr int kBlockW = 32;
+// resident warps per SM asked of ptxas: 16 (<= 128 registers, four warps per SMSP) where that
+// needs no spills (every instance but NW = 10 and 12 at PR = 4), else 12
+#ifndef LN_LDU8W_MINB
+#define LN_LDU8W_MINB 16
+#endif
+template <int NW, int PR>
+__host__ __device__ constexpr int w_minb() { return (PR == 4 && (NW == 10 || NW == 12)) ? 12 : LN_LDU8W_MINB; }
+constexpr int kTabWordsW = 16384;
+
+__host__ __device__ constexpr int w_pad4(int x) { return (x + 3) & ~3; }
+__host__ __device__ constexpr int w_pow3(int e) { return e == 0 ? 1 : 3 * w_pow3(e - 1); }
+// bitmask of the paired rows labelled g in labelling L (base-3 digits of L, paired row b = digit b)
+__host__ __device__ constexpr int w_mask(int L, int g, int PR) {
+  return PR == 0 ? 0 : ((L % 3 == g) ? 1 : 0) | (w_mask(L / 3, g, PR - 1) << 1);
+}
+
+__device__ __forceinline__ uint32_t w_sad4(uint32_t a, uint32_t b, uint32_t acc) {
+  uint32_t d;
+  asm("vabsdiff4.u32.u32.u32.add %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(acc));
+  return d;
+}
+// The candidate sums and their max.  Every value here is a non-negative integer below 2^23
+// (at most 3 * sum |M| <= 3 * 255 * 48 under the byte guard), and read as IEEE-754 single
+// bits such an integer v is the subnormal v * 2^-149: subnormal addition is exact and
+// bit-additive while the sum stays below 2^23 (a carry into the exponent field at 2^23 is
+// still the integer v), and subnormal max orders like the integers.  So, with denormals
+// kept (add.f32 / max.f32 without .ftz -- no fast-math in this build), FADD computes the
+// integer sum on EITHER FMA pipe (full rate, where IMAD runs on the FMA-heavy pipe only at
+// half rate) and FMNMX3 the integer max.  LN_LDU8W_FP=0 keeps integer IMAD / VIMNMX3.
+#ifndef LN_LDU8W_FP
+#define LN_LDU8W_FP 1
+#endif
+__device__ __forceinline__ int32_t w_fadd(int32_t a, int32_t b, uint32_t one) {
+#if LN_LDU8W_FP
+  (void)one;
+  float r;
+  asm("add.f32 %0, %1, %2;" : "=f"(r) : "f"(__int_as_float(a)), "f"(__int_as_float(b)));
+  return __float_as_int(r);
+#else
+  int32_t r;   // IMAD with a uniform operand ptxas cannot fold: stays on the FMA-heavy pipe
+  asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(one), "r"(b));
+  return r;
+#endif
+}
+__device__ __forceinline__ int32_t w_max3(int32_t a, int32_t b, int32_t c) {
+#if LN_LDU8W_FP
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(__int_as_float(a)), "f"(__int_as_float(b)), "f"(__int_as_float(c)));
+  return __float_as_int(r);
+#else
+  return __vimax3_s32(a, b, c);
+#endif
+}
+__device__ __forceinline__ int32_t w_max2(int32_t a, int32_t b) {
+#if LN_LDU8W_FP
+  float r;
+  asm("max.f32 %0, %1, %2;" : "=f"(r) : "f"(__int_as_float(a)), "f"(__int_as_float(b)));
+  return __float_as_int(r);
+#else
+  return max(a, b);
+#endif
+}
+
+// max of N non-negative values with three-input maxes: ceil((N - 1) / 2) ALU instructions
+template <int N>
+__device__ __forceinline__ int32_t w_max_tree(const int32_t (&v)[N]) {
+  if constexpr (N == 1) {
+    return v[0];
+  } else if constexpr (N == 2) {
+    return w_max2(v[0], v[1]);
+  } else {
+    constexpr int M = (N + 2) / 3;
+    int32_t w[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+      if (3 * i + 2 < N) w[i] = w_max3(v[3 * i], v[3 * i + 1], v[3 * i + 2]);
+      else if (3 * i + 1 < N) w[i] = w_max2(v[3 * i], v[3 * i + 1]);
+      else w[i] = v[3 * i];
+    }
+    return w_max_tree<M>(w);
+  }
+}
+
+template <int NW, int PR>
+struct LdW {
+  static constexpr int RW = w_pad4(NW);
+  static constexpr int RD = 2 * RW;          // delta record: +row at [0, NW), -row at [RW, RW + NW)
+  static constexpr int NS = 1 << PR;         // bias sets (subsets of the paired rows)
+  static constexpr int NL = w_pow3(PR);      // labellings of the paired rows
+
+  // the value of labelling L: H[T_0][0] + H[T_1][1] + H[T_2][2] (masks forced to compile time)
+  template <int L>
+  static __device__ __forceinline__ int32_t cand(const int32_t (&H)[NS][3], uint32_t one) {
+    constexpr int m0 = std::integral_constant<int, w_mask(L, 0, PR)>::value;
+    constexpr int m1 = std::integral_constant<int, w_mask(L, 1, PR)>::value;
+    constexpr int m2 = std::integral_constant<int, w_mask(L, 2, PR)>::value;
+    return w_fadd(w_fadd(H[m0][0], H[m1][1], one), H[m2][2], one);
+  }
+  template <int... Ls>
+  static __device__ __forceinline__ int32_t best_seq(const int32_t (&H)[NS][3], int32_t best, uint32_t one,
+                                                     std::integer_sequence<int, Ls...>) {
+    int32_t v[NL + 1] = {cand<Ls>(H, one)..., best};
+    return w_max_tree<NL + 1>(v);
+  }
+  // max(best, every labelling's value of the current word)
+  static __device__ __forceinline__ int32_t best_of(const int32_t (&H)[NS][3], int32_t best, uint32_t one) {
+    return best_seq(H, best, one, std::make_integer_sequence<int, NL>{});
+  }
+
+  // A move between groups GA < GB (either direction): the lower group adds the packed row at
+  // shared address rowA, the higher one the row at rowB (the +row or the -row of the walked
+  // digit's delta record, chosen by the direction), then both groups' 2^PR bias sums are
+  // re-accumulated.  The max over the labellings follows at the single call site.
+  // Shared-memory bias layout: word-major, sBias[i * NS + m] = B_m word i, so the 2^PR bias
+  // words of one packed word are NS / 4 LDS.128.  Instruction order: per packed word i and per
+  // half of the bias sets, all VABSDIFF4 of one group back to back -- they share the byte
+  // operand A[g][i] (operand reuse cache), so each reads two registers (bias word, accumulator)
+  // instead of three; the register-file read ports, not the ALU pipe, bound a 3-source mix.
+  template <int GA, int GB, int P>
+  static __device__ __forceinline__ void sums(uint32_t (&A)[P][3][NW], int32_t (&H)[P][NS][3], const uint32_t (&Ks)[NS],
+                                              uint32_t rowA, uint32_t rowB, uint32_t sbias) {
+#ifndef LN_LDU8W_HB
+#define LN_LDU8W_HB 8
+#endif
+    constexpr int HB = NS >= LN_LDU8W_HB ? LN_LDU8W_HB : NS;     // bias sets per batch of loads
+#pragma unroll
+    for (int v = 0; v < RW / 4; ++v) {
+      const uint4 xa = lds128(rowA + 16u * (uint32_t)v);
+      const uint4 xb = lds128(rowB + 16u * (uint32_t)v);
+      const uint32_t ra[4] = {xa.x, xa.y, xa.z, xa.w}, rb[4] = {xb.x, xb.y, xb.z, xb.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int i = 4 * v + e;
+        if (i < NW) {
+#pragma unroll
+          for (int j = 0; j < P; ++j) {
+            A[j][GA][i] += ra[e];
+            A[j][GB][i] += rb[e];
+          }
+#pragma unroll
+          for (int h = 0; h < NS / HB; ++h) {
+            uint32_t bb[HB];
+#pragma unroll
+            for (int q = 0; q < HB / 4; ++q) {
+              const uint4 bq = lds128(sbias + 4u * (uint32_t)(i * NS + h * HB + 4 * q));
+              bb[4 * q] = bq.x; bb[4 * q + 1] = bq.y; bb[4 * q + 2] = bq.z; bb[4 * q + 3] = bq.w;
+            }
+#pragma unroll
+            for (int j = 0; j < P; ++j) {
+#pragma unroll
+              for (int m = 0; m < HB; ++m)
+                H[j][h * HB + m][GA] =
+                    (int32_t)w_sad4(A[j][GA][i], bb[m], i == 0 ? Ks[h * HB + m] : (uint32_t)H[j][h * HB + m][GA]);
+#pragma unroll
+              for (int m = 0; m < HB; ++m)
+                H[j][h * HB + m][GB] =
+                    (int32_t)w_sad4(A[j][GB][i], bb[m], i == 0 ? Ks[h * HB + m] : (uint32_t)H[j][h * HB + m][GB]);
+            }
+          }
+        }
+      }
+    }
+  }
+};
+
+// Init records: as build_ldu8_kernel writes them (prefix rows 0..k, the walked base, -N,
+// then NS * NW bias words and the NS kappa sums), stride CW = 4 NW.
+// Units per lane: P units of a lane move the same rows at every word, so one shared-memory
+// load of a row or bias quad serves all P and the P max trees of a word can overlap the other
+// units' VABSDIFF4 streams.  Measured on 24x24 L_3 (profiles/r02): P = 2 needs 212 registers
+// (two warps per SMSP) and runs 2 % slower than P = 1 at 128 registers; default 1.
+#ifndef LN_LDU8W_P
+#define LN_LDU8W_P 1
+#endif
+template <int NW, int PR>
+__host__ __device__ constexpr int w_units() { return (NW <= 6) ? LN_LDU8W_P : 1; }
+
+template <int NW, int PR>
+__global__ void __launch_bounds__(kBlockW, (w_minb<NW, PR>()))
+walk_ldu8w_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int32_t* __restrict__ gInit) {
+  using WK = LdW<NW, PR>;
+  constexpr int P = w_units<NW, PR>();
+  constexpr int RD = WK::RD, RW = WK::RW, CW = 4 * NW, NS = WK::NS;
+  extern __shared__ __align__(16) uint32_t sT[];
+  const int lane = threadIdx.x & 31;
+  const int sw = p.s - PR;                         // walked digits
+  const int32_t* baseRec = gInit + (p.k + 1) * CW;
+  const int32_t* negRec = baseRec + CW;
+  const uint32_t* biasRec = reinterpret_cast<const uint32_t*>(negRec + CW);
+  uint32_t* sBias = sT + sw * RD;
+  for (int i = lane; i < sw * RD; i += 32) sT[i] = gTab[i];
+  for (int i = lane; i < NS * NW; i += 32) {     // word-major: sBias[q * NS + m]
+    const int q = i / NS, m = i % NS;
+    sBias[i] = biasRec[m * NW + q];
+  }
+  __syncwarp();
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sT);
+  const uint32_t sbias = (uint32_t)__cvta_generic_to_shared(sBias);
+  // LN_LDU8W_KVEC: XOR with threadIdx.y (always 0 in these one-dimensional blocks, but not
+  // provably uniform) keeps the kappa sums in vector registers, where VABSDIFF4 reads them,
+  // instead of uniform registers copied over at every use (IMAD.U32 on the FMA pipe)
+#ifndef LN_LDU8W_KVEC
+#define LN_LDU8W_KVEC 1
+#endif
+  uint32_t Ks[NS];
+#pragma unroll
+  for (int m = 0; m < NS; ++m) Ks[m] = __ldg(biasRec + NS * NW + m) ^ (LN_LDU8W_KVEC ? (uint32_t)threadIdx.y : 0u);
+  uint32_t nwords = 1;
+  for (int i = 0; i < sw; ++i) nwords *= 3;
+  int32_t best_all = INT32_MIN;
+  uint32_t best_u = 0;
+  bool have = false;
+  const int64_t nchunks = (p.unit_count + 32 * P - 1) / (32 * P);
+  for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    uint32_t A[P][3][NW];
+    int32_t H[P][NS][3];
+    int32_t best[P];
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
+      // ---- unit init: prefix labels -> the three groups' bytes at the start word (suffix all 0)
+      const int64_t rel = ch * 32 * P + j * 32 + lane;
+      const int64_t u = p.unit_begin + (rel < p.unit_count ? rel : 0);
+      uint64_t lab = 0;
+      if (p.prefix_table) lab = p.prefix_table[u - p.unit_begin];
+      else for (int x = 0; x <= p.k; ++x) lab |= (uint64_t)prefix_digit(p, u, x) << (p.pbits * x);
+      const uint64_t lmask = (1ull << p.pbits) - 1ull;
+#pragma unroll
+      for (int q = 0; q < NW; ++q) {
+        int32_t a[3][4];
+#pragma unroll
+        for (int g = 0; g < 3; ++g)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) a[g][e] = __ldg(negRec + 4 * q + e) + (g == 0 ? __ldg(baseRec + 4 * q + e) : 0);
+        for (int x = 0; x <= p.k; ++x) {
+          const int dig = (int)((lab >> (p.pbits * x)) & lmask);
+          const int4 v = __ldg(reinterpret_cast<const int4*>(gInit + x * CW) + q);
+#pragma unroll
+          for (int g = 0; g < 3; ++g) {
+            const int32_t f = dig == g ? 1 : 0;
+            a[g][0] += f * v.x; a[g][1] += f * v.y; a[g][2] += f * v.z; a[g][3] += f * v.w;
+          }
+        }
+#pragma unroll
+        for (int g = 0; g < 3; ++g)
+          A[j][g][q] = (uint32_t)(a[g][0] & 0xFF) | ((uint32_t)(a[g][1] & 0xFF) << 8) |
+                       ((uint32_t)(a[g][2] & 0xFF) << 16) | ((uint32_t)(a[g][3] & 0xFF) << 24);
+      }
+#pragma unroll
+      for (int g = 0; g < 3; ++g)
+#pragma unroll
+        for (int m = 0; m < NS; ++m) {
+          uint32_t h = Ks[m];
+#pragma unroll
+          for (int q = 0; q < NW; ++q) h = w_sad4(A[j][g][q], sBias[q * NS + m], h);
+          H[j][m][g] = (int32_t)h;
+        }
+      best[j] = WK::best_of(H[j], 0, p.one);          // every value is >= 0 (a sum of |.|)
+    }
+    // ---- the walk: words 1 .. 3^sw - 1, one dispatch site for the four move cases
+    uint32_t t = 0, jj = 0;
+    for (uint32_t w = 1; w < nwords; ++w) {
+      uint32_t i, from, to;
+      if (++jj == 3) { jj = 0; ++t; }
+      if (jj == 0) {
+        dary_block_start<3>(t, &i, &from, &to);
+      } else {
+        i = 0;
+        const bool odd = (t & 1u) != 0;
+        from = odd ? 3 - jj : jj - 1;
+        to = odd ? 2 - jj : jj;
+      }
+      // walked digit i's delta record: +row at srow, -row at srow + 4 RW bytes; the group the
+      // row leaves (from) adds the -row, the group it joins (to) the +row
+      const uint32_t srow = sbase + 4u * i * (uint32_t)RD;
+      const uint32_t rlo = from < to ? srow + 4u * (uint32_t)RW : srow;   // row for the lower group
+      const uint32_t rhi = from < to ? srow : srow + 4u * (uint32_t)RW;   // row for the higher group
+      if (from + to == 1) WK::template sums<0, 1, P>(A, H, Ks, rlo, rhi, sbias);
+      else WK::template sums<1, 2, P>(A, H, Ks, rlo, rhi, sbias);
+#pragma unroll
+      for (int j = 0; j < P; ++j) best[j] = WK::best_of(H[j], best[j], p.one);
+    }
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
+      const int64_t rel = ch * 32 * P + j * 32 + lane;
+      if (rel < p.unit_count) {
+        if (p.unit_max) p.unit_max[rel] = best[j];
+        if (!have || best[j] > best_all) { best_all = best[j]; best_u = (uint32_t)(p.unit_begin + rel); have = true; }
+      }
+    }
+  }
+  unsigned long long key = have ? make_key(best_all, best_u) : 0ull;
+  key = warp_max_u64(key);
+  if (lane == 0 && key) atomicMax(p.key, key);
+}
+
+template <int NW, int PR>
+size_t w_smem(int s) { return sizeof(uint32_t) * (size_t)((s - PR) * 2 * w_pad4(NW) + (1 << PR) * NW); }
+
+template <int NW, int PR>
+cudaError_t launch_w(const WalkParams& p, const uint32_t* tab, const int32_t* init, int grid, cudaStream_t st) {
+  const size_t sm = w_smem<NW, PR>(p.s);
+  cudaError_t e = cudaFuncSetAttribute(walk_ldu8w_kernel<NW, PR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  walk_ldu8w_kernel<NW, PR><<<grid, kBlockW, sm, st>>>(p, tab, init);
+  return cudaGetLastError();
+}
+
+template <int NW, int PR>
+int occ_w(int s) {
+  const size_t sm = w_smem<NW, PR>(s);
+  int nb = 0;
+  cudaFuncSetAttribute(walk_ldu8w_kernel<NW, PR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, walk_ldu8w_kernel<NW, PR>, kBlockW, sm);
+  return nb;
+}
+
+}  // namespace
+
+#ifdef LN_LDU8W_PART
+// part 0: 1-6 packed words (<= 24 columns), part 1: 7-12
+#define LN_LDU8W_SWITCH(NW_, FN, PR, ...)                                                          \
+  if constexpr (LN_LDU8W_PART == 0) {                                                              \
+    switch (NW_) {                                                                                 \
+      case 1: return FN<1, PR>(__VA_ARGS__); case 2: return FN<2, PR>(__VA_ARGS__);                \
+      case 3: return FN<3, PR>(__VA_ARGS__); case 4: return FN<4, PR>(__VA_ARGS__);                \
+      case 5: return FN<5, PR>(__VA_ARGS__); case 6: return FN<6, PR>(__VA_ARGS__);                \
+      default: break;                                                                              \
+    }                                                                                              \
+  } else {                                                                                         \
+    switch (NW_) {                                                                                 \
+      case 7: return FN<7, PR>(__VA_ARGS__);   case 8: return FN<8, PR>(__VA_ARGS__);              \
+      case 9: return FN<9, PR>(__VA_ARGS__);   case 10: return FN<10, PR>(__VA_ARGS__);            \
+      case 11: return FN<11, PR>(__VA_ARGS__); case 12: return FN<12, PR>(__VA_ARGS__);            \
+      default: break;                                                                              \
+    }                                                                                              \
+  }
+
+template <>
+cudaError_t walk_ldu8w_launch_part<LN_LDU8W_PART>(const WalkParams& p, const uint32_t* tab, const int32_t* init, int grid,
+                                                   cudaStream_t st, int NW, int pr) {
+  if (pr == 4) { LN_LDU8W_SWITCH(NW, launch_w, 4, p, tab, init, grid, st) }
+  else if (pr == 3) { LN_LDU8W_SWITCH(NW, launch_w, 3, p, tab, init, grid, st) }
+  return cudaErrorInvalidValue;
+}
+
+template <int NW, int PR>
+int upl_w() { return w_units<NW, PR>(); }
+
+template <>
+int walk_ldu8w_upl_part<LN_LDU8W_PART>(int NW, int pr) {
+  if (pr == 4) { LN_LDU8W_SWITCH(NW, upl_w, 4) }
+  else if (pr == 3) { LN_LDU8W_SWITCH(NW, upl_w, 3) }
+  return 1;
+}
+
+template <>
+int walk_ldu8w_occ_part<LN_LDU8W_PART>(int NW, int pr, int s) {
+  if (pr == 4) { LN_LDU8W_SWITCH(NW, occ_w, 4, s) }
+  else if (pr == 3) { LN_LDU8W_SWITCH(NW, occ_w, 3, s) }
+  return 0;
+}
+#endif
+
+}  // namespace lnorm

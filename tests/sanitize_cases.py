@@ -4,8 +4,9 @@ compute-sanitizer --tool memcheck  python tests/sanitize_cases.py
 compute-sanitizer --tool racecheck python tests/sanitize_cases.py
 
 Covers the byte kernels (L_1 / L_marg / L_2, aligned and unaligned Algorithm-1 slices, the
-grouped prefix hook; L_3 / L_4 with 1, 2 and 3 paired rows), the 16-bit and int32 families
-(LNORM_KERNEL), the generic kernel, the reductions and the batched API.  Every value is checked
+grouped prefix hook; L_3 / L_4 with 1, 2 and 3 paired rows; the all-H L_3 kernel with 3 and 4),
+the 16-bit and int32 families (LNORM_KERNEL), the generic kernel (also batched), the reductions,
+the batched API and the device-input path (guard-statistics kernel, caller stream).  Every value is checked
 against the oracle so a silent corruption also fails.
 """
 import os
@@ -44,8 +45,14 @@ def main():
     got = L.prefix_maxima(M, P)
     assert all(got[i] == oracle.prefix_max(M, P[i])[0] for i in range(8))
     for d in (3, 4):
-        for n in (8, 10, 12):
+        for n in (8, 10, 12, 14):
             seen.add(check(synth.random_matrix(n, 14, 510 + n + d), d))
+    # L_3 all-H kernel with 3 and 4 paired rows, and past 32 columns; the all-E kernel
+    for n, m in [(13, 14), (12, 40)]:
+        seen.add(check(synth.random_matrix(n, m, 515 + n + m), 3))
+    os.environ["LNORM_LDU8W"] = "0"
+    seen.add(check(synth.random_matrix(13, 14, 516), 3))
+    os.environ["LNORM_LDU8W"] = "1"
     for fam in ("pair16", "packed", "int32", "generic"):
         os.environ["LNORM_KERNEL"] = fam
         for d, marg in [(1, False), (1, True), (2, False), (3, False)]:
@@ -59,6 +66,13 @@ def main():
     Ms = np.stack([synth.random_matrix(10, 10, 540 + i) for i in range(16)])
     vals, _ = L.compute_batch(Ms)
     assert all(int(vals[i]) == oracle.l1(Ms[i])[0] for i in range(16))
+    Ts = np.stack([synth.random_matrix(4, 3, 550 + i, -1, 1) for i in range(40)])     # generic batched walk
+    for d in (1, 3):
+        vals, _ = L.compute_batch(Ts, d=d)
+        assert all(int(vals[i]) == oracle.norm(Ts[i], d=d)[0] for i in range(40))
+    import torch                                                                  # device input + stream
+    Md = torch.from_numpy(synth.random_matrix(12, 13, 560)).cuda()
+    assert L.compute_device(Md, stream=torch.cuda.Stream())[0] == oracle.l1(Md.cpu().numpy())[0]
     print("sanitize cases ok; kernel variants:", sorted(L.VARIANTS[v] for v in seen))
 
 

@@ -114,6 +114,8 @@ HOT_SHAPES = [
     (5, False, 6, 4), (1, False, 9, 70), (2, False, 8, 100),
     (1, True, 10, 97), (1, False, 11, 190), (1, False, 12, 128),      # wide rows (config 5a m = 4n)
     (1, True, 12, 150), (1, False, 13, 133),                           # > 128 columns: lane pairs
+    (3, False, 12, 40), (3, False, 13, 44), (4, False, 10, 36),        # d-ary byte walk beyond 32 columns
+    (3, False, 11, 33), (3, False, 9, 48),
 ]
 
 
@@ -161,6 +163,12 @@ def test_config4_l2_24x24_full(lib):
 def test_l3_l4_medium_full(lib):
     check(lib, synth.random_matrix(13, 24, 4), d=3)
     check(lib, synth.random_matrix(10, 16, 5), d=4)
+    # more than 32 columns: the byte walk (the int32 d-ary walk stops at 32 columns)
+    M = synth.random_matrix(14, 40, 6)
+    check(lib, M, d=3)
+    assert lib.last_stats()["variant"] == 8
+    check(lib, synth.random_matrix(11, 44, 7), d=4)
+    assert lib.last_stats()["variant"] == 8
 
 
 def test_marg_medium_full(lib):
@@ -293,12 +301,15 @@ def test_sampled_prefixes_ungrouped(lib, d, marg):
         assert got[i] == oracle.prefix_max(M, P[i], d=d, with_marginals=marg)[0]
 
 
+@pytest.mark.parametrize("allh", ["1", "0"], ids=["allH", "allE"])
 @pytest.mark.parametrize("d", [3, 4])
-@pytest.mark.parametrize("s", [2, 3, 4, 6])
-def test_ldu8_paired_rows_every_suffix_length(lib, d, s):
+@pytest.mark.parametrize("s", [2, 3, 4, 5, 6])
+def test_ldu8_paired_rows_every_suffix_length(lib, d, s, allh, monkeypatch):
     """The byte d-ary walk pairs the last 1, 2 or 3 rows depending on the suffix length
-    (s = 2, 3, >= 4): per-prefix maxima for every case against the oracle, and the value
-    of the full search (whose planner picks its own split)."""
+    (s = 2, 3, >= 4; L_3: the all-H kernel pairs 3 rows at s = 4 and 4 rows from s = 5,
+    LNORM_LDU8W=0 keeps the all-E kernel): per-prefix maxima for every case against the oracle,
+    and the value of the full search (whose planner picks its own split)."""
+    monkeypatch.setenv("LNORM_LDU8W", allh)
     n, m = 11, 13
     M = synth.random_matrix(n, m, 64_000 + 10 * d + s)
     nfixed = n - s

@@ -50,16 +50,24 @@ enum {
   OP_MAD_SAD4,       // 1:1 mad (packed u8x4 update) + vabsdiff4.add
   OP_ADD_SAD4,       // 1:1 add (uniform operand) + vabsdiff4.add
   OP_MAD_SAD4V,      // 1:1 mad + vabsdiff4.add with a DISTINCT bias register per chain (3 live sources)
+  OP_VIMNMX3,        // __vimax3_s32       -> VIMNMX3
+  OP_SAD4_VIMNMX3,   // 1:1 vabsdiff4.add + VIMNMX3
+  OP_FMNMX3,         // max.f32 d,a,b,c    -> FMNMX3 (sm_100 three-input float max)
+  OP_SAD4_FMNMX3,    // 1:1 vabsdiff4.add + FMNMX3 (does the float max leave the ALU pipe free?)
+  OP_FMNMX,          // max.f32 d,a,b      -> FMNMX
+  OP_SAD4_FMNMX,     // 1:1 vabsdiff4.add + FMNMX
+  OP_SAD4_MAD_FMNMX3,// 2:1:1 vabsdiff4.add, mad, FMNMX3 (the byte d-ary walk's mix with a float max tree)
   OP_N
 };
 static const char* kNames[OP_N] = {
   "add.s32(uniform operand)", "mad.lo.s32", "sad.s32", "add+sad", "mad+sad", "vadd2", "viaddmax_s16x2",
   "vadd2+viaddmax_s16x2", "vmaxu2", "mad+vmaxu2+mad", "hadd2", "hfma2_abs", "hadd2+hfma2_abs",
   "add_constbank+sad", "lds128_bcast", "iadd3", "viaddmax_s32", "mad+viaddmax_s16x2", "vabsdiff4_acc",
-  "mad+vabsdiff4_acc", "add+vabsdiff4_acc", "mad+vabsdiff4_acc(per-chain bias)"};
+  "mad+vabsdiff4_acc", "add+vabsdiff4_acc", "mad+vabsdiff4_acc(per-chain bias)", "vimnmx3", "vabsdiff4_acc+vimnmx3",
+  "fmnmx3", "vabsdiff4_acc+fmnmx3", "fmnmx", "vabsdiff4_acc+fmnmx", "2 vabsdiff4_acc+mad+fmnmx3"};
 // SASS instructions per chain per unrolled iteration, read off `cuobjdump -sass`
 // (ptxas fuses two u16x2 maxes into one VIMNMX3; the constant-bank probe adds one LDCU.128 per 4 adds)
-static const double kInstr[OP_N] = {1,1,1,2,2,1,1,2,0.5,3,1,1,2,2.25,1,1,1,2,1,2,2,2};
+static const double kInstr[OP_N] = {1,1,1,2,2,1,1,2,0.5,3,1,1,2,2.25,1,1,1,2,1,2,2,2,1,2,1,2,1,2,4};
 
 template <int OP>
 __global__ void __launch_bounds__(256) probe(int32_t* out, Rec* rec, int trips, int32_t a_in, int32_t one_in, int32_t zero_in) {
@@ -153,6 +161,30 @@ __global__ void __launch_bounds__(256) probe(int32_t* out, Rec* rec, int trips, 
         } else if constexpr (OP == OP_MAD_SAD4V) {
           asm volatile("mad.lo.s32 %0, %1, %2, %0;" : "+r"(y[c]) : "r"(a), "r"(one));
           asm volatile("vabsdiff4.u32.u32.u32.add %0, %1, %2, %0;" : "+r"(x[c]) : "r"(y[c]), "r"(bv[c]));
+        } else if constexpr (OP == OP_VIMNMX3) {
+          const int32_t t3 = __vimax3_s32(x[c], y[c], a); y[c] = x[c]; x[c] = t3; asm volatile("" : "+r"(x[c]));
+        } else if constexpr (OP == OP_SAD4_VIMNMX3) {
+          asm volatile("vabsdiff4.u32.u32.u32.add %0, %1, %2, %0;" : "+r"(x[c]) : "r"(y[c]), "r"(bias));
+          y[c] = __vimax3_s32(y[c], x[c], a); asm volatile("" : "+r"(y[c]));
+        } else if constexpr (OP == OP_FMNMX3) {
+          int32_t t3;
+          asm volatile("max.f32 %0, %1, %2, %3;" : "=r"(t3) : "r"(x[c]), "r"(y[c]), "r"(a));
+          y[c] = x[c]; x[c] = t3;
+        } else if constexpr (OP == OP_SAD4_FMNMX3) {
+          asm volatile("vabsdiff4.u32.u32.u32.add %0, %1, %2, %0;" : "+r"(x[c]) : "r"(y[c]), "r"(bias));
+          asm volatile("max.f32 %0, %0, %1, %2;" : "+r"(y[c]) : "r"(x[c]), "r"(a));
+        } else if constexpr (OP == OP_FMNMX) {
+          int32_t t2;
+          asm volatile("max.f32 %0, %1, %2;" : "=r"(t2) : "r"(x[c]), "r"(y[c]));
+          y[c] = x[c]; x[c] = t2;
+        } else if constexpr (OP == OP_SAD4_FMNMX) {
+          asm volatile("vabsdiff4.u32.u32.u32.add %0, %1, %2, %0;" : "+r"(x[c]) : "r"(y[c]), "r"(bias));
+          asm volatile("max.f32 %0, %0, %1;" : "+r"(y[c]) : "r"(x[c]));
+        } else if constexpr (OP == OP_SAD4_MAD_FMNMX3) {
+          asm volatile("vabsdiff4.u32.u32.u32.add %0, %1, %2, %0;" : "+r"(x[c]) : "r"(y[c]), "r"(bias));
+          asm volatile("mad.lo.s32 %0, %1, %2, %0;" : "+r"(y[c]) : "r"(a), "r"(one));
+          asm volatile("vabsdiff4.u32.u32.u32.add %0, %1, %2, %0;" : "+r"(x[c]) : "r"(y[c]), "r"(bv[c]));
+          asm volatile("max.f32 %0, %0, %1, %2;" : "+r"(y[c]) : "r"(x[c]), "r"(a));
         } else if constexpr (OP == OP_ADD_SAD4) {
           asm volatile("add.s32 %0, %0, %1;" : "+r"(y[c]) : "r"(a));
           asm volatile("vabsdiff4.u32.u32.u32.add %0, %1, %2, %0;" : "+r"(x[c]) : "r"(y[c]), "r"(bias));
@@ -216,6 +248,7 @@ int main(int argc, char** argv) {
   std::vector<Rec> h;
   All<OP_ADD, OP_MAD, OP_SAD, OP_ADD_SAD, OP_MAD_SAD, OP_VADD2, OP_VIADDMAX2, OP_VADD2_VIADDMAX2, OP_VMAXU2,
       OP_MAD_VMAXU2_MAD, OP_HADD2, OP_HFMA2ABS, OP_HADD2_HFMA2ABS, OP_ADDC_SAD, OP_LDS128, OP_IADD3,
-      OP_VIADDMAX32, OP_MAD_VIADDMAX2, OP_SAD4, OP_MAD_SAD4, OP_ADD_SAD4, OP_MAD_SAD4V>::go(nsm, bps, threads, trips, dout, drec, h);
+      OP_VIADDMAX32, OP_MAD_VIADDMAX2, OP_SAD4, OP_MAD_SAD4, OP_ADD_SAD4, OP_MAD_SAD4V, OP_VIMNMX3, OP_SAD4_VIMNMX3,
+      OP_FMNMX3, OP_SAD4_FMNMX3, OP_FMNMX, OP_SAD4_FMNMX, OP_SAD4_MAD_FMNMX3>::go(nsm, bps, threads, trips, dout, drec, h);
   return 0;
 }
