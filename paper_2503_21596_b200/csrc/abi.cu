@@ -134,57 +134,66 @@ void host_stats(const int32_t* M, const Problem& p, GuardStats* g) {
   }
 }
 
-// One block: each thread owns columns y = tid, tid + blockDim, ... (c <= 1024).
-__global__ void guard_stats_kernel(const int32_t* M, int m, int transposed, int r, int c, int marg,
-                                   long long* out) {
-  __shared__ long long red[32];
-  constexpr int kPer = kMaxCols / 256;
+// One block of 256 threads: each thread owns columns y = tid, tid + 256, ... (c <= 1024);
+// per suffix length a warp max goes to shared memory (no block barrier per row), one barrier
+// at the end combines the eight warps.
+__global__ void __launch_bounds__(256) guard_stats_kernel(const int32_t* M, int m, int transposed, int r, int c,
+                                                          int marg, long long* out) {
+  constexpr int kW = 8, kPer = kMaxCols / 256;
+  __shared__ long long red[kMaxRows][kW];
+  __shared__ long long red3[3][kW];
   long long colw[kPer];
 #pragma unroll
   for (int i = 0; i < kPer; ++i) colw[i] = 0;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  auto block_reduce = [&](long long v, bool is_max) -> long long {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  auto wmax = [](long long v) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const long long w = __shfl_xor_sync(0xffffffffu, v, o);
-      v = is_max ? (w > v ? w : v) : v + w;
-    }
-    __syncthreads();
-    if (lane == 0) red[wid] = v;
-    __syncthreads();
-    long long t = is_max ? red[0] : 0;
-    for (int i = is_max ? 1 : 0; i < nw; ++i) t = is_max ? (red[i] > t ? red[i] : t) : t + red[i];
-    return t;
+    for (int o = 16; o > 0; o >>= 1) { const long long w = __shfl_xor_sync(0xffffffffu, v, o); v = w > v ? w : v; }
+    return v;
+  };
+  auto wsum = [](long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
   };
   for (int s = 1; s <= r; ++s) {
     const int x = r - s;
     long long mx = 0;
 #pragma unroll
     for (int i = 0; i < kPer; ++i) {
-      const int y = threadIdx.x + i * blockDim.x;
+      const int y = threadIdx.x + i * 256;
       if (y < c) {
         const long long v = transposed ? M[(int64_t)y * m + x] : M[(int64_t)x * m + y];
         colw[i] += v < 0 ? -v : v;
         mx = colw[i] > mx ? colw[i] : mx;
       }
     }
-    mx = block_reduce(mx, true);
-    if (threadIdx.x == 0) out[3 + s - 1] = mx;
+    mx = wmax(mx);
+    if (lane == 0) red[s - 1][wid] = mx;
   }
   long long S = 0, p0 = 0, p1 = 0;
   const int c0 = marg ? 1 : 0;
 #pragma unroll
   for (int i = 0; i < kPer; ++i) {
-    const int y = threadIdx.x + i * blockDim.x;
+    const int y = threadIdx.x + i * 256;
     if (y < c) {
       S += colw[i];
       if (y >= c0) { if ((y - c0) & 1) p1 += colw[i]; else p0 += colw[i]; }
     }
   }
-  S = block_reduce(S, false);
-  p0 = block_reduce(p0, false);
-  p1 = block_reduce(p1, false);
-  if (threadIdx.x == 0) { out[0] = S; out[1] = p0; out[2] = p1; }
+  S = wsum(S); p0 = wsum(p0); p1 = wsum(p1);
+  if (lane == 0) { red3[0][wid] = S; red3[1][wid] = p0; red3[2][wid] = p1; }
+  __syncthreads();
+  if (threadIdx.x < r) {
+    long long v = red[threadIdx.x][0];
+    for (int w = 1; w < kW; ++w) v = red[threadIdx.x][w] > v ? red[threadIdx.x][w] : v;
+    out[3 + threadIdx.x] = v;
+  }
+  if (threadIdx.x < 3) {
+    long long v = 0;
+    for (int w = 0; w < kW; ++w) v += red3[threadIdx.x][w];
+    out[threadIdx.x] = v;
+  }
 }
 
 // log2 of the u8 kernel's lane group: its units differ in the last lane_bits prefix
@@ -429,7 +438,12 @@ int make_plan(const Problem& pr, int world, Plan* pl, int64_t target_override = 
 
 // --------------------------------------------------------------- kernels --
 // Batched launches: matrices b = blockIdx.y, blockIdx.y + gridDim.y, ... < batch.
-__global__ void orient_kernel(const int32_t* in, int n, int m, int transpose, int32_t* out, int batch = 1) {
+// ctl (single searches): the search's control block is initialised here too (one launch less).
+__global__ void orient_kernel(const int32_t* in, int n, int m, int transpose, int32_t* out, int batch = 1,
+                              unsigned long long* ctl = nullptr) {
+  if (ctl && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+    ctl[0] = 0ull; ctl[1] = 0ull; ctl[2] = 0ull; ctl[3] = ~0ull; ctl[4] = 0ull;
+  }
   const int64_t total = (int64_t)n * m;
   for (int b = blockIdx.y; b < batch; b += gridDim.y) {
     const int32_t* ib = in + b * total;
@@ -729,7 +743,9 @@ int run_device(DevCtx& cx, const int32_t* dIn, const Problem& pr, int rank, int 
       if ((e = grow(&cx.dPre, &cx.capPre, ptab.size()))) return e;
     }
     CU(cudaEventRecord(cx.ev[0], s));
-    orient_kernel<<<std::min(1024, (pr.n * pr.m + 255) / 256), 256, 0, s>>>(dIn, pr.n, pr.m, pr.transposed ? 1 : 0, cx.dM);
+    // orientation + control-block init in one launch (init_ctl_kernel's job folded in)
+    orient_kernel<<<std::min(1024, (pr.n * pr.m + 255) / 256), 256, 0, s>>>(dIn, pr.n, pr.m, pr.transposed ? 1 : 0, cx.dM,
+                                                                             1, cx.dCtl);
     ++launches;
     CU(cudaGetLastError());
     if (!ptab.empty() && !mirror) {
@@ -737,9 +753,6 @@ int run_device(DevCtx& cx, const int32_t* dIn, const Problem& pr, int rank, int 
       CU(cudaMemcpyAsync(cx.dPre, ptab.data(), sizeof(uint64_t) * ptab.size(), cudaMemcpyHostToDevice, s));
       if (pl.shared) cx.preHold = pl.shared;
     }
-    init_ctl_kernel<<<1, 1, 0, s>>>(cx.dCtl);
-    ++launches;
-    CU(cudaGetLastError());
     wp.M = cx.dM; wp.r = pr.r; wp.c = pr.c; wp.mode = pr.mode; wp.d = pr.dl; wp.k = pl.k; wp.s = pl.s;
     wp.pbits = prefix_bits(pr.dl);
     wp.key_shift = pl.key_shift;

@@ -2,6 +2,11 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include "gray.cuh"
 
 namespace lnorm {
@@ -95,6 +100,52 @@ __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v)
     v = w > v ? w : v;
   }
   return v;
+}
+
+// Host: raise a kernel's dynamic shared-memory limit to >= bytes once per (kernel, device)
+// instead of at every launch, and the SM count per device (cached; launch paths call these
+// per search, so they must be cheap).
+inline cudaError_t ensure_dyn_smem(const void* fn, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(mu);
+  size_t& have = done[{fn, dev}];
+  if (have >= bytes) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) have = bytes;
+  return e;
+}
+// Resident blocks per SM of a kernel at (block, dynamic smem), computed once per device.
+inline int occupancy_cached(const void* fn, int block, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::pair<std::pair<const void*, int>, std::pair<int, size_t>>, int> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  {
+    std::lock_guard<std::mutex> g(mu);
+    auto it = done.find({{fn, dev}, {block, smem}});
+    if (it != done.end()) return it->second;
+  }
+  if (smem > 48 * 1024 && ensure_dyn_smem(fn, smem) != cudaSuccess) return 0;
+  int nb = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, block, smem) != cudaSuccess) { (void)cudaGetLastError(); return 0; }
+  std::lock_guard<std::mutex> g(mu);
+  done[{{fn, dev}, {block, smem}}] = nb;
+  return nb;
+}
+inline int device_sms() {
+  static int nsm[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return 148;
+  if (!nsm[dev]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    nsm[dev] = v > 0 ? v : 148;
+  }
+  return nsm[dev];
 }
 
 }  // namespace lnorm

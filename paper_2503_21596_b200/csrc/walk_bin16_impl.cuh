@@ -271,7 +271,7 @@ template <int MODE, int W>
 cudaError_t launch_one16(const WalkParams& p, const uint32_t* tab, int grid, cudaStream_t st) {
   constexpr int P = units_per_lane<MODE, W>();
   const size_t sm = smem16<MODE, W>(p.k, p.s);
-  cudaError_t e = cudaFuncSetAttribute(walk_bin16_kernel<MODE, W, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  cudaError_t e = ensure_dyn_smem((const void*)walk_bin16_kernel<MODE, W, P>, sm);
   if (e != cudaSuccess) return e;
   walk_bin16_kernel<MODE, W, P><<<grid, kBlock, sm, st>>>(p, tab);
   return cudaGetLastError();
@@ -282,11 +282,9 @@ int upl_one16() { return units_per_lane<MODE, W>(); }
 
 template <int MODE, int W>
 int occ_one16(int k, int s) {
-  int nb = 0;
   constexpr int P = units_per_lane<MODE, W>();
   const size_t sm = smem16<MODE, W>(k, s);
-  cudaFuncSetAttribute(walk_bin16_kernel<MODE, W, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, walk_bin16_kernel<MODE, W, P>, kBlock, sm);
+  const int nb = occupancy_cached((const void*)walk_bin16_kernel<MODE, W, P>, kBlock, sm);
   return nb;
 }
 

@@ -161,8 +161,7 @@ cudaError_t launch_one(const WalkParams& p, int grid, cudaStream_t st) {
 
 template <int MODE, int C>
 int occ_one() {
-  int nb = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, walk_bin_kernel<MODE, C>, kBlock, 0);
+  const int nb = occupancy_cached((const void*)walk_bin_kernel<MODE, C>, kBlock, 0);
   return nb;
 }
 

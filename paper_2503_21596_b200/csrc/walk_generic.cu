@@ -158,16 +158,26 @@ __device__ void recover_one(const WalkParams& p, unsigned long long* lex_out, un
 }
 
 // Batched launches: matrices b = blockIdx.y, blockIdx.y + gridDim.y, ... (any batch size).
+// stage_m: the block first copies the (oriented) matrix into shared memory, so every Gray step
+// reads its row there instead of through L2 (the recovery is latency-bound: one unit, short
+// chunks per warp).
 __global__ void __launch_bounds__(32 * kGenWarps) recover_kernel(const WalkParams pin, unsigned long long* lex_out,
-                                                                 unsigned long long* rmax_out) {
+                                                                 unsigned long long* rmax_out, int stage_m) {
   extern __shared__ int32_t smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  int32_t* G = smem + wib * groups_of(pin) * pin.c;
+  const int rc = pin.r * pin.c;
+  int32_t* G = smem + (stage_m ? rc : 0) + wib * groups_of(pin) * pin.c;
   const int nb = pin.batch > 0 ? pin.batch : 1;
   for (int b = blockIdx.y; b < nb; b += gridDim.y) {
     WalkParams p = pin;
     p.M = pin.M + (int64_t)b * pin.m_stride;
     p.key = pin.key + b;
+    if (stage_m) {
+      __syncthreads();
+      for (int i = threadIdx.x; i < rc; i += blockDim.x) smem[i] = p.M[i];
+      __syncthreads();
+      p.M = smem;
+    }
     recover_one(p, lex_out + b, rmax_out + b, G, lane, wib);
   }
 }
@@ -211,9 +221,7 @@ bool walk_generic_supported(int d, int c) {
 int walk_generic_occupancy(int d, int c, int* block_out) {
   const int nG = d < 2 ? 2 : d;
   size_t sm = gen_smem(nG, c, kGenWarps);
-  cudaFuncSetAttribute(walk_generic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  int nb = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, walk_generic_kernel, 32 * kGenWarps, sm);
+  const int nb = occupancy_cached((const void*)walk_generic_kernel, 32 * kGenWarps, sm);
   *block_out = 32 * kGenWarps;
   return nb;
 }
@@ -221,7 +229,7 @@ int walk_generic_occupancy(int d, int c, int* block_out) {
 cudaError_t walk_generic_launch(const WalkParams& p, int grid, cudaStream_t st, int* block_out) {
   const int nG = p.mode == MODE_LD ? p.d : 2;
   size_t sm = gen_smem(nG, p.c, kGenWarps);
-  cudaError_t e = cudaFuncSetAttribute(walk_generic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  cudaError_t e = ensure_dyn_smem((const void*)walk_generic_kernel, sm);
   if (e != cudaSuccess) return e;
   walk_generic_kernel<<<grid, 32 * kGenWarps, sm, st>>>(p);
   *block_out = 32 * kGenWarps;
@@ -231,20 +239,21 @@ cudaError_t walk_generic_launch(const WalkParams& p, int grid, cudaStream_t st, 
 cudaError_t recover_launch(const WalkParams& p, unsigned long long* lex_out, unsigned long long* rmax_out,
                            cudaStream_t st) {
   const int nG = p.mode == MODE_LD ? p.d : 2;
-  size_t sm = gen_smem(nG, p.c, kGenWarps);
-  cudaError_t e = cudaFuncSetAttribute(recover_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  const size_t gsm = gen_smem(nG, p.c, kGenWarps);
+  const size_t msm = sizeof(int32_t) * (size_t)p.r * p.c;
+  const int stage = gsm + msm <= 96 * 1024 ? 1 : 0;
+  const size_t sm = gsm + (stage ? msm : 0);
+  const int nsm = device_sms();
+  cudaError_t e = ensure_dyn_smem((const void*)recover_kernel, std::max<size_t>(sm, 96 * 1024));
   if (e != cudaSuccess) return e;
-  int dev = 0, nsm = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  // blocks per matrix: enough warps for ~64-word chunks (a d-ary step of this generic
-  // walk costs ~1k cycles: runtime-d digit arithmetic + a full re-evaluation), at most 4 per SM
+  // blocks per matrix: enough warps for ~16-word chunks (the recovery is latency-bound: a
+  // d-ary step of this generic walk is a few hundred cycles), at most 4 per SM
   uint64_t words = 1;
   for (int i = 0; i < p.s; ++i) words *= (uint64_t)(p.mode == MODE_LD ? p.d : 2);
-  int gx = (int)std::min<uint64_t>((uint64_t)nsm * 4, std::max<uint64_t>(1, words / (64ull * kGenWarps)));
+  int gx = (int)std::min<uint64_t>((uint64_t)nsm * 4, std::max<uint64_t>(1, words / (16ull * kGenWarps)));
   if (p.batch > 1) gx = std::max(1, std::min(gx, (nsm * 8 + p.batch - 1) / p.batch));
   const int gy = std::max(1, std::min(p.batch > 0 ? p.batch : 1, 65535));
-  recover_kernel<<<dim3(gx, gy), 32 * kGenWarps, sm, st>>>(p, lex_out, rmax_out);
+  recover_kernel<<<dim3(gx, gy), 32 * kGenWarps, sm, st>>>(p, lex_out, rmax_out, stage);
   return cudaGetLastError();
 }
 
@@ -252,7 +261,7 @@ cudaError_t trace_launch(const WalkParams& p, int64_t max_steps, int64_t* values
                          cudaStream_t st) {
   const int nG = p.mode == MODE_LD ? p.d : 2;
   size_t sm = gen_smem(nG, p.c, 1);
-  cudaError_t e = cudaFuncSetAttribute(trace_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  cudaError_t e = ensure_dyn_smem((const void*)trace_kernel, sm);
   if (e != cudaSuccess) return e;
   trace_kernel<<<1, 32, sm, st>>>(p, max_steps, values, digits);
   return cudaGetLastError();

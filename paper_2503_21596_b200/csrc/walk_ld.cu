@@ -170,8 +170,7 @@ cudaError_t launch_one(const WalkParams& p, int grid, cudaStream_t st) {
 }
 template <int D, int C>
 int occ_one() {
-  int nb = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, walk_ld_kernel<D, C>, kBlock, 0);
+  const int nb = occupancy_cached((const void*)walk_ld_kernel<D, C>, kBlock, 0);
   return nb;
 }
 

@@ -215,7 +215,7 @@ template <int D, int W>
 cudaError_t launch_one(const WalkParams& p, const uint32_t* tab, int grid, cudaStream_t st) {
   constexpr int P = ld16_units_per_lane<D, W>();
   const size_t sm = ld16_smem(W, p.k, p.s);
-  cudaError_t e = cudaFuncSetAttribute(walk_ld16_kernel<D, W, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  cudaError_t e = ensure_dyn_smem((const void*)walk_ld16_kernel<D, W, P>, sm);
   if (e != cudaSuccess) return e;
   walk_ld16_kernel<D, W, P><<<grid, kBlock, sm, st>>>(p, tab);
   return cudaGetLastError();
@@ -225,9 +225,7 @@ template <int D, int W>
 int occ_one(int k, int s) {
   constexpr int P = ld16_units_per_lane<D, W>();
   const size_t sm = ld16_smem(W, k, s);
-  cudaFuncSetAttribute(walk_ld16_kernel<D, W, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  int nb = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, walk_ld16_kernel<D, W, P>, kBlock, sm);
+  const int nb = occupancy_cached((const void*)walk_ld16_kernel<D, W, P>, kBlock, sm);
   return nb;
 }
 

@@ -265,7 +265,7 @@ template <int D, int C>
 cudaError_t launch_one(const WalkParams& p, const uint32_t* tab, const int32_t* init, int grid, cudaStream_t st) {
   constexpr int P = ldpair_units_per_lane<D, C>();
   const size_t sm = ldpair_smem(C, p.s);
-  cudaError_t e = cudaFuncSetAttribute(walk_ldpair16_kernel<D, C, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  cudaError_t e = ensure_dyn_smem((const void*)walk_ldpair16_kernel<D, C, P>, sm);
   if (e != cudaSuccess) return e;
   walk_ldpair16_kernel<D, C, P><<<grid, kBlock, sm, st>>>(p, tab, init);
   return cudaGetLastError();
@@ -275,9 +275,7 @@ template <int D, int C>
 int occ_one(int s) {
   constexpr int P = ldpair_units_per_lane<D, C>();
   const size_t sm = ldpair_smem(C, s);
-  cudaFuncSetAttribute(walk_ldpair16_kernel<D, C, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  int nb = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, walk_ldpair16_kernel<D, C, P>, kBlock, sm);
+  const int nb = occupancy_cached((const void*)walk_ldpair16_kernel<D, C, P>, kBlock, sm);
   return nb;
 }
 

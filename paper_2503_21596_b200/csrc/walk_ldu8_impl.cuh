@@ -442,7 +442,7 @@ template <int D, int NW, int PR>
 cudaError_t launch_lu_pr(const WalkParams& p, const uint32_t* tab, const int32_t* init, int grid, cudaStream_t st) {
   constexpr int P = ldu8_units_per_lane<D, NW, PR>();
   const size_t sm = ldu8_smem(NW, p.s);
-  cudaError_t e = cudaFuncSetAttribute(walk_ldu8_kernel<D, NW, P, PR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  cudaError_t e = ensure_dyn_smem((const void*)walk_ldu8_kernel<D, NW, P, PR>, sm);
   if (e != cudaSuccess) return e;
   walk_ldu8_kernel<D, NW, P, PR><<<grid, kBlockLU, sm, st>>>(p, tab, init);
   return cudaGetLastError();
@@ -463,9 +463,7 @@ template <int D, int NW, int PR>
 int occ_lu_pr(int s) {
   constexpr int P = ldu8_units_per_lane<D, NW, PR>();
   const size_t sm = ldu8_smem(NW, s);
-  int nb = 0;
-  cudaFuncSetAttribute(walk_ldu8_kernel<D, NW, P, PR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, walk_ldu8_kernel<D, NW, P, PR>, kBlockLU, sm);
+  const int nb = occupancy_cached((const void*)walk_ldu8_kernel<D, NW, P, PR>, kBlockLU, sm);
   return nb;
 }
 

@@ -344,7 +344,7 @@ size_t w_smem(int s) { return sizeof(uint32_t) * (size_t)((s - PR) * 2 * w_pad4(
 template <int NW, int PR>
 cudaError_t launch_w(const WalkParams& p, const uint32_t* tab, const int32_t* init, int grid, cudaStream_t st) {
   const size_t sm = w_smem<NW, PR>(p.s);
-  cudaError_t e = cudaFuncSetAttribute(walk_ldu8w_kernel<NW, PR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  cudaError_t e = ensure_dyn_smem((const void*)walk_ldu8w_kernel<NW, PR>, sm);
   if (e != cudaSuccess) return e;
   walk_ldu8w_kernel<NW, PR><<<grid, kBlockW, sm, st>>>(p, tab, init);
   return cudaGetLastError();
@@ -353,9 +353,7 @@ cudaError_t launch_w(const WalkParams& p, const uint32_t* tab, const int32_t* in
 template <int NW, int PR>
 int occ_w(int s) {
   const size_t sm = w_smem<NW, PR>(s);
-  int nb = 0;
-  cudaFuncSetAttribute(walk_ldu8w_kernel<NW, PR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, walk_ldu8w_kernel<NW, PR>, kBlockW, sm);
+  const int nb = occupancy_cached((const void*)walk_ldu8w_kernel<NW, PR>, kBlockW, sm);
   return nb;
 }
 

@@ -371,7 +371,7 @@ template <int MODE, int C>
 cudaError_t launch_pair(const WalkParams& p, const uint32_t* tab, const int32_t* init, int grid, cudaStream_t st) {
   constexpr int P = pair_units_per_lane<MODE, C>();
   const size_t sm = pair_smem<MODE, C>(p.s);
-  cudaError_t e = cudaFuncSetAttribute(walk_pair16_kernel<MODE, C, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  cudaError_t e = ensure_dyn_smem((const void*)walk_pair16_kernel<MODE, C, P>, sm);
   if (e != cudaSuccess) return e;
   walk_pair16_kernel<MODE, C, P><<<grid, kBlock, sm, st>>>(p, tab, init);
   return cudaGetLastError();
@@ -381,9 +381,7 @@ template <int MODE, int C>
 int occ_pair(int s) {
   constexpr int P = pair_units_per_lane<MODE, C>();
   const size_t sm = pair_smem<MODE, C>(s);
-  cudaFuncSetAttribute(walk_pair16_kernel<MODE, C, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  int nb = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, walk_pair16_kernel<MODE, C, P>, kBlock, sm);
+  const int nb = occupancy_cached((const void*)walk_pair16_kernel<MODE, C, P>, kBlock, sm);
   return nb;
 }
 

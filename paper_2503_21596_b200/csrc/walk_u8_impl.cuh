@@ -457,7 +457,7 @@ template <int MODE, int NW, int LPU>
 cudaError_t launch_u8_l(const WalkParams& p, const uint32_t* tab, const int32_t* init, int grid, cudaStream_t st) {
   constexpr int P = u8_units_per_lane<MODE, NW, LPU>();
   const size_t sm = u8_smem<MODE, NW, LPU>(p.s);
-  cudaError_t e = cudaFuncSetAttribute(walk_u8_kernel<MODE, NW, P, LPU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  cudaError_t e = ensure_dyn_smem((const void*)walk_u8_kernel<MODE, NW, P, LPU>, sm);
   if (e != cudaSuccess) return e;
   walk_u8_kernel<MODE, NW, P, LPU><<<grid, kBlockU8, sm, st>>>(p, tab, init);
   return cudaGetLastError();
@@ -475,9 +475,7 @@ template <int MODE, int NW, int LPU>
 int occ_u8_l(int s) {
   constexpr int P = u8_units_per_lane<MODE, NW, LPU>();
   const size_t sm = u8_smem<MODE, NW, LPU>(s);
-  cudaFuncSetAttribute(walk_u8_kernel<MODE, NW, P, LPU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  int nb = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, walk_u8_kernel<MODE, NW, P, LPU>, kBlockU8, sm);
+  const int nb = occupancy_cached((const void*)walk_u8_kernel<MODE, NW, P, LPU>, kBlockU8, sm);
   return nb;
 }
 
