@@ -192,7 +192,8 @@ def test_plan_packed_guard_and_fallback():
     assert P["packed_ok"] == 0 and P["variant_name"] == "bin_int32"
     assert L.plan(synth.random_matrix(24, 24, 4), d=3)["variant_name"] == "ld_u8"       # column |.|-sums <= 255
     assert L.plan(synth.random_matrix(24, 24, 4) * 3, d=3)["variant_name"] == "ld_pair16"
-    assert L.plan(synth.random_matrix(24, 40, 4), d=3)["variant_name"] == "generic"
+    # 40 columns: the byte d-ary walk is not limited by the int32 walk's 32-column constant bank
+    assert L.plan(synth.random_matrix(24, 40, 4), d=3)["variant_name"] == "ld_u8"
     assert L.plan(np.eye(3, dtype=np.int32))["variant_name"] == "generic"     # suffix shorter than the unroll
 
 
