@@ -290,6 +290,28 @@ typedef struct {
 int lnorm_plan(const int32_t* M, int32_t n, int32_t m, int32_t d, int32_t with_marginals, int32_t world,
                lnorm_plan_info* out);
 
+/*
+ * SURVEY.md §8(f4) experiment -- the tcgen05 kind::i8 (integer tensor-core) formulation of
+ * the L_1 search (Eq. 1), measured against the byte walk and NOT used by
+ * lnorm_compute.  Strategies (row 0 fixed to +1) are numbered
+ * (t, i, l): rows 1, 2 carry the two bits of i in [0, 4), rows 3..n-8 the bits of the
+ * reflected Gray word t ^ (t >> 1), rows n-7..n-1 the bits of l in [0, 128)
+ * (set bit = -1).  Tile t = all (i, l) = 512 strategies, whose column sums one tcgen05.mma
+ * (M = 128, N = 4 * ceil4(m), K = 32, int8 x int8 -> int32 in TMEM) forms; the kernel covers
+ * tiles [tile_begin, tile_begin + tile_count) of the 2^(n-10) tiles (tile_count = 0: all of
+ * them, i.e. the exact L_1 of M with rows as given, no orientation).
+ * M: host, row-major n x m int32, caller-owned.  Limits: 10 <= n <= 43, 1 <= m <= 64,
+ * |M_xy| <= 127 on rows 1, 2 and the last 7 rows, sum over rows 0 and 3..n-8 of |M_xy| <= 508
+ * per column (four int8 pieces), sum |M| < 2^21 (key layout): else LNORM_EINVAL /
+ * ETOOLARGE / EOVERFLOW.
+ * Outputs: value = the maximum over the covered strategies; argmax (int8[n], may be NULL)
+ * = one strategy attaining it (not necessarily the lexicographically smallest);
+ * strategies (may be NULL) = strategies covered; kernel_ms (may be NULL) = CUDA-event time
+ * of the kernel.  Synchronises before return.
+ */
+int lnorm_imma_l1(const int32_t* M, int32_t n, int32_t m, uint64_t tile_begin, uint64_t tile_count,
+                  int64_t* value, int8_t* argmax, uint64_t* strategies, double* kernel_ms);
+
 /* Statistics of the last successful compute call on the calling thread. */
 typedef struct {
   int32_t rows, cols;          /* enumerated rows / columns after orientation */

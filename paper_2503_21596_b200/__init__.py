@@ -20,7 +20,7 @@ import numpy as np
 __all__ = [
     "LNormError", "load", "compute", "compute_device", "compute_reduced", "compute_batch", "compute_multi", "Comm",
     "compute_rank", "compute_rank_device", "torch_nccl_comm", "prefix_maxima", "unit_maxima",
-    "walk_trace", "gray_digit", "gray_change", "partition", "last_stats", "status_string", "SYMBOLS", "plan",
+    "walk_trace", "imma_l1", "gray_digit", "gray_change", "partition", "last_stats", "status_string", "SYMBOLS", "plan",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -33,7 +33,7 @@ SYMBOLS = [
     "lnorm_compute_rank_device",
     "lnorm_prefix_maxima", "lnorm_unit_maxima", "lnorm_walk_trace", "lnorm_gray_digit", "lnorm_gray_change", "lnorm_partition",
     "lnorm_last_stats", "lnorm_plan", "lnorm_compute_sliced", "lnorm_compute_reduced", "lnorm_compute_batch",
-    "lnorm_compute_checkpointed",
+    "lnorm_compute_checkpointed", "lnorm_imma_l1",
 ]
 
 STATUS = {0: "OK", 1: "EINVAL", 2: "EOVERFLOW", 3: "ETOOLARGE", 4: "ENODEV", 5: "ECUDA", 6: "ENCCL", 7: "ENOMEM",
@@ -118,6 +118,7 @@ def load():
             "lnorm_compute_reduced": ([i32p, i32, i32, i32, i32, i64p, i8p, i32p], ctypes.c_int),
             "lnorm_compute_sliced": ([i32p, i32, i32, i32, i32, i32, i64p, i8p], ctypes.c_int),
             "lnorm_plan": ([i32p, i32, i32, i32, i32, i32, P(PlanInfo)], ctypes.c_int),
+            "lnorm_imma_l1": ([i32p, i32, i32, u64, u64, i64p, i8p, P(u64), P(ctypes.c_double)], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
             f = getattr(lib, name)
@@ -393,6 +394,19 @@ def unit_maxima(M, prefix_digits: int, units, d: int = 1, with_marginals: bool =
     _check(load().lnorm_unit_maxima(_p(A, ctypes.c_int32), n, m, d, int(with_marginals), prefix_digits,
                                     _p(U, ctypes.c_uint64), U.shape[0], _p(out, ctypes.c_int32)), "lnorm_unit_maxima")
     return out
+
+
+def imma_l1(M, tile_begin: int = 0, tile_count: int = 0):
+    """SURVEY §8(f4) experiment: max of Eq. (1) over tiles [tile_begin, tile_begin + tile_count) of
+    512 strategies whose column sums come from one tcgen05 kind::i8 MMA each (tile_count = 0: all
+    tiles = the exact L_1 of M, rows as given).  Returns (value, argmax, strategies, kernel_ms)."""
+    A = _mat(M)
+    n, m = A.shape
+    v, cnt, ms = ctypes.c_int64(), ctypes.c_uint64(), ctypes.c_double()
+    arg = np.zeros(n, dtype=np.int8)
+    _check(load().lnorm_imma_l1(_p(A, ctypes.c_int32), n, m, tile_begin, tile_count, ctypes.byref(v),
+                                _p(arg, ctypes.c_int8), ctypes.byref(cnt), ctypes.byref(ms)), "lnorm_imma_l1")
+    return int(v.value), arg, int(cnt.value), float(ms.value)
 
 
 def walk_trace(M, prefix, d: int = 1, with_marginals: bool = False):

@@ -96,6 +96,15 @@ __host__ __device__ constexpr int u8_pr() { return MODE == MODE_LD ? (LN_U8_PAIR
 #ifndef LN_U8_LPU2
 #define LN_U8_LPU2 1
 #endif
+#ifndef LN_U8_WIDE_EVEN
+#define LN_U8_WIDE_EVEN 1
+#endif
+// resident blocks asked of ptxas for the wide lane-pair instances (10: 168 registers, a few
+// spills in the unit init only; measured 3-4 % faster than the unbounded 244-register build on
+// 144-160 columns, profiles/r02/ab_wide_rows.jsonl)
+#ifndef LN_U8_MINB_LP
+#define LN_U8_MINB_LP 10
+#endif
 // lanes per unit an instance can run with (the planner picks 2 where the byte guard allows
 // the extra window row, else 1; both instances are compiled for those NW)
 template <int MODE, int NW>
@@ -228,7 +237,7 @@ template <int MODE, int NW, int P>
 __host__ __device__ constexpr int u8_foot() { return U8Layout<MODE, NW>::G * NW * (P + (1 << u8_pr<MODE>())); }
 template <int MODE, int NW, int P, int LPU>
 __host__ __device__ constexpr int u8_min_blocks() {
-  return LPU == 2 ? (u8_foot<MODE, NW / 2, P>() <= 40 ? 12 : 1)
+  return LPU == 2 ? (u8_foot<MODE, NW / 2, P>() <= 40 ? 12 : LN_U8_MINB_LP)
        : (U8Layout<MODE, NW>::G == 1 && u8_foot<MODE, NW, P>() <= 56) ? LN_U8_MINB
        : (U8Layout<MODE, NW>::G == 1 && u8_foot<MODE, NW, P>() <= 70) ? LN_U8_MINB_MID
        : ((u8_foot<MODE, NW, P>() <= 96 && P >= 4) || u8_foot<MODE, NW, P>() <= 54) ? 12 : 1;
@@ -506,6 +515,19 @@ int unroll_u8(int lpu) {
   return u8_unroll<MODE, NW, u8_units_per_lane<MODE, NW, 1>()>();
 }
 
+// Wide rows (more than 128 columns, lane pairs): L_1 / L_marg instances for every EVEN word
+// count, so a 144-column row is 36 words, not 40 (round 1 rounded to multiples of 8: up to
+// 15 % padding VABSDIFF4 on the m = 4n sweep); L_2 (two bias sets, one lane per unit) keeps
+// multiples of 8.
+#if LN_BIN_MODE != 2 && LN_U8_WIDE_EVEN
+#define LN_U8_WIDE_CASES(MODE, FN, ...)                                                              \
+    case 34: return FN<MODE, 34>(__VA_ARGS__); case 36: return FN<MODE, 36>(__VA_ARGS__);            \
+    case 38: return FN<MODE, 38>(__VA_ARGS__); case 42: return FN<MODE, 42>(__VA_ARGS__);            \
+    case 44: return FN<MODE, 44>(__VA_ARGS__); case 46: return FN<MODE, 46>(__VA_ARGS__);
+#else
+#define LN_U8_WIDE_CASES(MODE, FN, ...)
+#endif
+
 #ifdef LN_U8_ONLY_NW   // experiment builds (tools/build_variant.py): one instance only
 #define LN_U8_SWITCH(MODE, NW_, FN, ...)                                                             \
   if ((NW_) == LN_U8_ONLY_NW) return FN<MODE, LN_U8_ONLY_NW>(__VA_ARGS__);
@@ -523,6 +545,7 @@ int unroll_u8(int lpu) {
     case 20: return FN<MODE, 20>(__VA_ARGS__); case 24: return FN<MODE, 24>(__VA_ARGS__);            \
     case 28: return FN<MODE, 28>(__VA_ARGS__); case 32: return FN<MODE, 32>(__VA_ARGS__);            \
     case 40: return FN<MODE, 40>(__VA_ARGS__); case 48: return FN<MODE, 48>(__VA_ARGS__);            \
+    LN_U8_WIDE_CASES(MODE, FN, __VA_ARGS__)                                                          \
     default: break;                                                                                  \
   }
 #endif
@@ -538,7 +561,7 @@ int walk_u8_words_mode<LN_BIN_MODE>(int c) {
 #endif
   if (nw < 1) return 0;
   if (nw > 16) nw = (nw + 3) & ~3;
-  if (nw > 32) nw = (nw + 7) & ~7;
+  if (nw > 32) nw = (LN_BIN_MODE != 2 && LN_U8_WIDE_EVEN) ? (nw + 1) & ~1 : (nw + 7) & ~7;
   return nw <= 48 ? nw : 0;
 }
 

@@ -20,7 +20,7 @@ GOLD = os.path.join(ROOT, "tests", "golden")
 def header_functions():
     txt = open(os.path.join(ROOT, "include", "lnorm.h")).read()
     txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
-    return sorted(set(re.findall(r"\b(lnorm_[a-z_]+)\s*\(", txt)))
+    return sorted(set(re.findall(r"\b(lnorm_[a-z0-9_]+)\s*\(", txt)))
 
 
 def test_library_exports_every_header_symbol():

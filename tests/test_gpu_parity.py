@@ -129,6 +129,18 @@ def test_hot_kernel_shapes(lib, d, marg, n, m):
         assert st["launches"] >= 4 and st["steps"] >= 1
 
 
+@pytest.mark.parametrize("marg", [False, True])
+def test_wide_even_word_instances(lib, marg):
+    """Every even word count above 32 (136-184 columns) has its own lane-pair byte instance
+    (no padding to a multiple of 8 words): each one against the oracle, incl. the ragged
+    last word (c not a multiple of 4)."""
+    for c in (135, 143, 151, 167, 175, 183, 136, 144):
+        M = synth.random_matrix(13, c, 40_000 + c + 7 * marg)
+        P = lib.plan(M, with_marginals=marg)
+        assert P["variant_name"] == "bin_u8" and P["lanes_per_unit"] == 2, (c, P)
+        check(lib, M, marg=marg)
+
+
 def test_ties_identity_and_ones(lib):
     for n in (1, 2, 5, 9, 12):
         for d, marg in MODES:
