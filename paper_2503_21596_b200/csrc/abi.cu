@@ -10,6 +10,7 @@
 #include <map>
 #include <memory>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: host ranges per phase (SURVEY.md §5 tracing)
 
 #include <algorithm>
 #include <atomic>
@@ -34,6 +35,16 @@ cudaError_t mapback_launch(int n, int m, int nred, int ld, int32_t* scratch, con
 }  // namespace lnorm
 
 namespace {
+
+// NVTX range for the lifetime of a scope: the host phases of a call (guard statistics,
+// planning, walk enqueue, all-reduce, recovery) show up as named ranges in nsys / ncu's NVTX
+// filter (`ncu --nvtx --nvtx-include "lnorm.walk/"`).  Costs ~100 ns per range without a tool.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // ------------------------------------------------------------------ NCCL --
 // NCCL is resolved at run time (dlopen) so the library loads on hosts without
@@ -724,7 +735,11 @@ int run_device(DevCtx& cx, const int32_t* dIn, const Problem& pr, int rank, int 
   Plan pl;
   // the plan depends only on (M, world): identical on every rank, so a planning error
   // is raised by all ranks alike before any of them reaches the collective
-  int rc = make_plan(pr, std::max(world, vslices), &pl);
+  int rc;
+  {
+    NvtxRange nr("lnorm.plan");
+    rc = make_plan(pr, std::max(world, vslices), &pl);
+  }
   if (rc) return rc;
   cudaStream_t s = cx.cur ? cx.cur : cx.stream;
   const bool collective = comm != nullptr;
@@ -822,7 +837,11 @@ int run_device(DevCtx& cx, const int32_t* dIn, const Problem& pr, int rank, int 
     }
     return LNORM_OK;
   };
-  int pre_rc = pre();
+  int pre_rc;
+  {
+    NvtxRange nr("lnorm.walk");
+    pre_rc = pre();
+  }
   if (pre_rc == -1) return LNORM_OK;           // checkpoint: partial result already written
   cnt = walked;
   if (pre_rc != LNORM_OK) {
@@ -832,6 +851,7 @@ int run_device(DevCtx& cx, const int32_t* dIn, const Problem& pr, int rank, int 
   }
   (void)cudaEventRecord(cx.ev[2], s);
   if (collective) {
+    NvtxRange nr("lnorm.allreduce");
     Nccl& nc = nccl();
     if (!nc.ok) return LNORM_ENCCL;
     if (nc.AllReduce(cx.dCtl + 1, cx.dCtl + 1, 2, ncclUint64, ncclMax, comm, s) != ncclSuccess) return LNORM_ENCCL;
@@ -844,6 +864,7 @@ int run_device(DevCtx& cx, const int32_t* dIn, const Problem& pr, int rank, int 
     ++launches;
   }
   // recovery over the full unit space (same winning unit on every rank)
+  NvtxRange nr_rec("lnorm.recover+sync");
   WalkParams rp = wp;
   rp.unit_begin = 0; rp.unit_count = pl.units;
   walk_params_single(rp);
@@ -904,6 +925,7 @@ struct StreamScope {
 // Guard statistics of a device-resident matrix: one-block kernel on the call's stream,
 // ~0.5 KB copied back (the plan depends on them: the only host round trip before the walk).
 int device_stats(DevCtx& cx, const int32_t* devM, Problem* pr) {
+  NvtxRange nr("lnorm.guard_stats");
   cudaStream_t s = cx.cur;
   guard_stats_kernel<<<1, 256, 0, s>>>(devM, pr->m, pr->transposed ? 1 : 0, pr->r, pr->c,
                                        pr->mode == MODE_MARG ? 1 : 0, cx.dStats);
@@ -920,6 +942,7 @@ int compute_on(int device, const int32_t* hostM, const int32_t* devM, int n, int
                int rank, int world, ncclComm_t comm, cudaStream_t user_stream, int64_t* value, int8_t* argmax,
                int vslices = 1) {
   if (!value || (!hostM && !devM)) return LNORM_EINVAL;
+  NvtxRange nr("lnorm.compute");
   Problem pr;
   DevCtx* cx = nullptr;
   int rc = ctx_get(device, &cx);
@@ -1215,29 +1238,47 @@ int lnorm_compute_checkpointed(const int32_t* M, int32_t n, int32_t m, int32_t d
 int lnorm_compute_batch(const int32_t* M, int32_t batch, int32_t n, int32_t m, int32_t d, int32_t with_marginals,
                         int64_t* values, int8_t* argmax) {
   if (!M || !values || batch < 1) return LNORM_EINVAL;
+  NvtxRange nr("lnorm.compute_batch");
   int dev = 0, rc = current_device(&dev);
   if (rc) return rc;
   const size_t nm = (size_t)n * m;
-  // validate every matrix; the paired batched kernel needs its guard for all of them
+  // validate every matrix; the batched plan must be exact for all of them, so it is made for
+  // the element-wise worst case of their guard statistics (every matrix has the same shape,
+  // orientation and mode): sufW = max over the batch, the 16-bit guards = AND over the batch
   Problem pr;
-  bool all_pair = true;
   for (int b = 0; b < batch; ++b) {
     Problem q;
     if ((rc = validate(M + b * nm, n, m, d, with_marginals, &q))) return rc;
-    if (b == 0) pr = q;
-    all_pair = all_pair && q.fitsPair;
+    if (b == 0) {
+      pr = q;
+      continue;
+    }
+    pr.fits16 = pr.fits16 && q.fits16;
+    pr.fitsPair = pr.fitsPair && q.fitsPair;
+    pr.fitsLdPair = pr.fitsLdPair && q.fitsLdPair;
+    for (int i = 0; i <= kMaxRows; ++i) pr.sufW[i] = std::max(pr.sufW[i], q.sufW[i]);
   }
-  // path: the strategy-paired packed kernel (one launch, units of all matrices), else the
-  // generic warp-per-unit kernel batched the same way for small search spaces (tiny shapes,
-  // any d), else one search per matrix through the hot single-matrix kernels
+  // path: one launch over the units of all matrices through the byte-packed walks (L_1,
+  // L_marg, L_2: walk_u8; L_3, L_4: walk_ldu8 / walk_ldu8w) or the strategy-paired 16-bit
+  // walk, each restaging its per-matrix tables per chunk; else the generic warp-per-unit
+  // kernel batched the same way for small search spaces (tiny shapes, any d); else one
+  // search per matrix through the hot single-matrix kernels
   Plan pl;
   const int64_t target = std::max<int64_t>(1, kNominalLanes * 8 / batch);
-  bool pair = false;
-  if (all_pair && pr.dl == 2 && make_plan(pr, 1, &pl, target, /*allow_u8=*/false) == LNORM_OK && pl.kernel == K_PAIR16)
-    pair = true;
+  int bkern = -1;
+  // batched byte instances exist for the small-matrix regime: <= 32 columns with one lane per
+  // unit (binary), <= 24 columns (d-ary); wider batches take the 16-bit paired walk
+  auto batchable = [&](const Plan& q) {
+    if (q.key_shift != 0) return false;
+    if (q.kernel == K_U8) return pr.c <= 32 && q.u8_lpu == 1;
+    if (q.kernel == K_LDU8) return pr.c <= 24;
+    return q.kernel == K_PAIR16;
+  };
+  if (make_plan(pr, 1, &pl, target) == LNORM_OK && batchable(pl)) bkern = pl.kernel;
+  else if (pr.dl == 2 && make_plan(pr, 1, &pl, target, /*allow_u8=*/false) == LNORM_OK && batchable(pl)) bkern = pl.kernel;
   long double space = 1;
   for (int i = 0; i < pr.r - 1; ++i) space *= pr.dl;
-  if (!pair && space > (long double)(1 << 20)) {
+  if (bkern < 0 && space > (long double)(1 << 20)) {
     for (int b = 0; b < batch; ++b) {
       if ((rc = compute_on(dev, M + b * nm, nullptr, n, m, d, with_marginals, 0, 1, nullptr, nullptr, values + b,
                            argmax ? argmax + (size_t)b * n : nullptr)))
@@ -1250,7 +1291,7 @@ int lnorm_compute_batch(const int32_t* M, int32_t batch, int32_t n, int32_t m, i
   std::lock_guard<std::mutex> g(cx->mu);
   CU(cudaSetDevice(dev));
   cudaStream_t s = cx->stream;
-  if (!pair) {
+  if (bkern < 0) {
     // generic batched plan: the smallest prefix length giving ~64 warps of work per SM
     pl = Plan{};
     pl.kernel = K_GEN;
@@ -1268,7 +1309,12 @@ int lnorm_compute_batch(const int32_t* M, int32_t batch, int32_t n, int32_t m, i
     }
   }
   int64_t tabw = 0, initw = 0;
-  if (pair) walk_pair16_table_sizes(pr.mode, pr.c, pl.k, pl.s, &tabw, &initw);
+  if (bkern == K_PAIR16) walk_pair16_table_sizes(pr.mode, pr.c, pl.k, pl.s, &tabw, &initw);
+  else if (bkern == K_U8) walk_u8_table_sizes(pr.mode, pr.c, pl.k, pl.s, pl.u8_lpu, &tabw, &initw);
+  else if (bkern == K_LDU8) walk_ldu8_table_sizes(pr.dl, pr.c, pl.k, pl.s, &tabw, &initw);
+  // per-matrix records start 16-byte aligned (the kernels read them as int4 / LDS.128 rows)
+  tabw = (tabw + 3) & ~(int64_t)3;
+  initw = (initw + 3) & ~(int64_t)3;
   auto up8 = [](size_t x) { return (x + 7) & ~(size_t)7; };
   const size_t oIn = 0, oM = oIn + up8(batch * nm), oTab = oM + up8(batch * nm), oInit = oTab + up8(batch * (size_t)tabw);
   const size_t oKey = oInit + up8(batch * (size_t)initw);                 // int32 units so far
@@ -1306,17 +1352,32 @@ int lnorm_compute_batch(const int32_t* M, int32_t batch, int32_t n, int32_t m, i
   wp.counter = cx->dCtl; wp.key = keys; wp.unit_max = nullptr;
   wp.unit_begin = 0; wp.unit_count = pl.units * batch;
   wp.batch = batch; wp.units_per = pl.units; wp.m_stride = (int64_t)nm; wp.tab_stride = tabw; wp.init_stride = initw; wp.one = 1;
-  wp.u8_lpu = 1;
+  wp.u8_lpu = bkern == K_U8 ? pl.u8_lpu : 1;
+  wp.key_shift = 0;
   int block = 32, grid = 1;
   CU(cudaEventRecord(cx->ev[1], s));
-  if (pair) {
-    const int occ = std::max(1, walk_pair16_occupancy(pr.mode, pr.c, pl.s, &block));
-    const int64_t P = walk_pair16_units_per_lane(pr.mode, pr.c);
-    const int64_t chunks = (int64_t)batch * ((pl.units + 32 * P - 1) / (32 * P));
-    grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)occ * cx->nsm, chunks));
-    if (walk_pair16_launch(wp, reinterpret_cast<int32_t*>(dTab), dInit, grid, s, &block) != cudaSuccess) {
-      (void)cudaGetLastError(); return LNORM_ECUDA;
+  if (bkern >= 0) {
+    // chunks of 32 lanes x P units (byte binary walk: 32 / lpu lane groups of P units)
+    int occ = 0;
+    int64_t per_chunk = 32;
+    if (bkern == K_PAIR16) {
+      occ = walk_pair16_occupancy(pr.mode, pr.c, pl.s, &block);
+      per_chunk = 32 * (int64_t)walk_pair16_units_per_lane(pr.mode, pr.c);
+    } else if (bkern == K_U8) {
+      occ = walk_u8_occupancy(pr.mode, pr.c, pl.s, pl.u8_lpu, &block);
+      per_chunk = 32 / pl.u8_lpu * (int64_t)walk_u8_units_per_lane(pr.mode, pr.c, pl.u8_lpu);
+    } else {
+      occ = walk_ldu8_occupancy(pr.dl, pr.c, pl.s, &block);
+      per_chunk = 32 * (int64_t)walk_ldu8_units_per_lane(pr.dl, pr.c, pl.s);
     }
+    const int64_t chunks = (int64_t)batch * ((pl.units + per_chunk - 1) / per_chunk);
+    grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)std::max(1, occ) * cx->nsm, chunks));
+    cudaError_t e = cudaErrorInvalidValue;
+    int32_t* tab32 = reinterpret_cast<int32_t*>(dTab);
+    if (bkern == K_PAIR16) e = walk_pair16_launch(wp, tab32, dInit, grid, s, &block);
+    else if (bkern == K_U8) e = walk_u8_launch(wp, tab32, dInit, grid, s, &block);
+    else e = walk_ldu8_launch(wp, tab32, dInit, grid, s, &block);
+    if (e != cudaSuccess) { (void)cudaGetLastError(); return LNORM_ECUDA; }
   } else {
     const int occ = std::max(1, walk_generic_occupancy(pr.dl, pr.c, &block));
     const int64_t want = (wp.unit_count + block / 32 - 1) / (block / 32);
@@ -1356,7 +1417,9 @@ int lnorm_compute_batch(const int32_t* M, int32_t batch, int32_t n, int32_t m, i
   S.d = pr.d == 1 ? 1 : pr.dl; S.units = pl.units * batch; S.units_total = S.units;
   S.steps = (double)S.units * (double)ipow(pr.dl, pl.s);
   S.column_updates = S.steps * pr.c * (pr.mode == MODE_LD && pr.dl >= 3 ? 2 : 1);
-  S.walk_ms = wms; S.total_ms = tms; S.launches = 6; S.variant = pl.kernel; S.block_threads = block; S.grid_blocks = grid;
+  S.walk_ms = wms; S.total_ms = tms; S.launches = bkern >= 0 ? 7 : 6; S.variant = pl.kernel; S.block_threads = block;
+  S.grid_blocks = grid;
+  S.paired_rows = pl.kernel == K_LDU8 ? walk_ldu8_paired_rows(pr.dl, pl.s) : (pl.kernel == K_U8 ? 1 : 0);
   g_stats = S;
   return LNORM_OK;
 }

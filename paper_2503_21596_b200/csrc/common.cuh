@@ -212,6 +212,9 @@ int walk_u8_occupancy(int mode, int c, int s, int lpu, int* block_out);
 cudaError_t walk_u8_launch(const WalkParams& p, int32_t* scratch_tab, int32_t* scratch_init, int grid,
                            cudaStream_t st, int* block_out);
 template <int MODE> int walk_u8_words_mode(int c);
+template <int MODE> void walk_u8_table_sizes_mode(int c, int k, int s, int lpu, int64_t* tab_words, int64_t* init_ints);
+// per-matrix delta-table words and init-record ints of a byte-walk launch (batched strides)
+void walk_u8_table_sizes(int mode, int c, int k, int s, int lpu, int64_t* tab_words, int64_t* init_ints);
 template <int MODE> cudaError_t walk_u8_launch_mode(const WalkParams& p, int32_t* scratch_tab, int32_t* scratch_init,
                                                     int grid, cudaStream_t st);
 template <int MODE> int walk_u8_occupancy_mode(int c, int s, int lpu);
@@ -229,6 +232,8 @@ int walk_ldu8_units_per_lane(int d, int c, int s);
 int walk_ldu8_occupancy(int d, int c, int s, int* block_out);
 cudaError_t walk_ldu8_launch(const WalkParams& p, int32_t* scratch_tab, int32_t* scratch_init, int grid,
                              cudaStream_t st, int* block_out);
+// per-matrix delta-table words and init-record ints of a byte d-ary launch (batched strides)
+void walk_ldu8_table_sizes(int d, int c, int k, int s, int64_t* tab_words, int64_t* init_ints);
 template <int D, int PART> int walk_ldu8_upl_part(int NW, int s);
 template <int D, int PART> int walk_ldu8_occ_part(int NW, int s);
 template <int D, int PART> cudaError_t walk_ldu8_launch_part(const WalkParams& p, const uint32_t* tab, const int32_t* init,

@@ -110,6 +110,12 @@ bool walk_u8_supported(int mode, int c, int s, int lpu) {
   return 2 * s * RW <= 16384;
 }
 
+void walk_u8_table_sizes(int mode, int c, int k, int s, int lpu, int64_t* tab_words, int64_t* init_ints) {
+  if (mode == MODE_L1) walk_u8_table_sizes_mode<MODE_L1>(c, k, s, lpu, tab_words, init_ints);
+  else if (mode == MODE_MARG) walk_u8_table_sizes_mode<MODE_MARG>(c, k, s, lpu, tab_words, init_ints);
+  else walk_u8_table_sizes_mode<MODE_LD>(c, k, s, lpu, tab_words, init_ints);
+}
+
 // largest lanes-per-unit an instance offers for c columns (1 or 2)
 int walk_u8_lanes_per_unit(int mode, int c) {
   if (mode == MODE_L1) return walk_u8_lanes_per_unit_mode<MODE_L1>(c);

@@ -252,7 +252,7 @@ struct LdU8 {
 
 // Init records (global int32, stride CW = 4 NW): prefix rows 0..k, the base (walked
 // rows at label 0), -N_y, then the packed bias words of the NS sets and their K_m.
-template <int D, int NW, int P, int PR>
+template <int D, int NW, int P, int PR, bool BAT = false>
 __global__ void __launch_bounds__(kBlockLU, ((PR == 3 && D == 3 && D * NW * P * PR <= 63) ? LN_LDU8_MINB3 : (D * NW * P * (PR >= 2 ? PR : 1) <= 72 ? LN_LDU8_MINB : 1)))
 walk_ldu8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int32_t* __restrict__ gInit) {
   using WK = LdU8<D, NW, P, PR>;
@@ -260,29 +260,57 @@ walk_ldu8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const in
   extern __shared__ __align__(16) uint32_t sT[];
   const int lane = threadIdx.x & 31;
   const int sw = p.s - PR;                         // walked digits
-  for (int i = lane; i < sw * RD; i += 32) sT[i] = gTab[i];
-  __syncwarp();
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sT);
-  const int32_t* baseRec = gInit + (p.k + 1) * CW;
-  const int32_t* negRec = baseRec + CW;
-  const uint32_t* biasRec = reinterpret_cast<const uint32_t*>(negRec + CW);
   uint32_t Bs[NS * NW], Ks[NS];
-#pragma unroll
-  for (int i = 0; i < NS * NW; ++i) Bs[i] = __ldg(biasRec + i);
-#pragma unroll
-  for (int m = 0; m < NS; ++m) Ks[m] = __ldg(biasRec + NS * NW + m);
   uint32_t nblk = 1;
   for (int i = 1; i < sw; ++i) nblk *= D;
   int32_t best = INT32_MIN;
   uint32_t best_u = 0;
   bool have = false;
-  const int64_t nchunks = (p.unit_count + 32 * P - 1) / (32 * P);
+  // matrix mb's delta table -> shared memory, its bias words and kappas -> registers
+  auto stage = [&](int mb) {
+    __syncwarp();
+    const uint32_t* src = gTab + mb * p.tab_stride;
+    for (int i = lane; i < sw * RD; i += 32) sT[i] = src[i];
+    __syncwarp();
+    const uint32_t* biasRec = reinterpret_cast<const uint32_t*>(gInit + mb * p.init_stride + (p.k + 3) * CW);
+#pragma unroll
+    for (int i = 0; i < NS * NW; ++i) Bs[i] = __ldg(biasRec + i);
+#pragma unroll
+    for (int m = 0; m < NS; ++m) Ks[m] = __ldg(biasRec + NS * NW + m);
+  };
+  // BAT (batched launches, f3): chunk ch -> matrix mb = ch / CPM (units_per units per matrix,
+  // the launch's range unless batched); a warp restages the tables when it moves to the next
+  // matrix.  The single-search instance stages them once.
+  const int64_t CPM = (p.units_per + 32 * P - 1) / (32 * P);
+  const int64_t nchunks = BAT ? CPM * p.batch : CPM;
+  int cur_b = BAT ? -1 : 0;
+  if constexpr (!BAT) stage(0);
   for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    int64_t lc = ch;
+    const int32_t* gI = gInit;
+    if constexpr (BAT) {
+      const int mb = (int)(ch / CPM);
+      lc = ch - (int64_t)mb * CPM;
+      gI = gInit + mb * p.init_stride;
+      if (mb != cur_b) {
+        if (cur_b >= 0) {
+          unsigned long long key = have ? make_key(best, best_u) : 0ull;
+          key = warp_max_u64(key);
+          if (lane == 0 && key) atomicMax(p.key + cur_b, key);
+          best = INT32_MIN; have = false;
+        }
+        stage(mb);
+        cur_b = mb;
+      }
+    }
+    const int32_t* baseRec = gI + (p.k + 1) * CW;
+    const int32_t* negRec = baseRec + CW;
     typename WK::Unit U[P];
 #pragma unroll
     for (int j = 0; j < P; ++j) {
-      const int64_t rel = ch * 32 * P + j * 32 + lane;
-      const int64_t u = p.unit_begin + (rel < p.unit_count ? rel : 0);
+      const int64_t rel = lc * 32 * P + j * 32 + lane;
+      const int64_t u = p.unit_begin + (rel < p.units_per ? rel : 0);
       // prefix labels, pbits per row (the RGS table word; arithmetic prefixes repacked)
       uint64_t lab = 0;
       if (p.prefix_table) lab = p.prefix_table[u - p.unit_begin];
@@ -297,7 +325,7 @@ walk_ldu8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const in
           for (int e = 0; e < 4; ++e) a[g][e] = __ldg(negRec + 4 * q + e) + (g == 0 ? __ldg(baseRec + 4 * q + e) : 0);
         for (int x = 0; x <= p.k; ++x) {
           const int dig = (int)((lab >> (p.pbits * x)) & lmask);
-          const int4 v = __ldg(reinterpret_cast<const int4*>(gInit + x * CW) + q);
+          const int4 v = __ldg(reinterpret_cast<const int4*>(gI + x * CW) + q);
 #pragma unroll
           for (int g = 0; g < D; ++g) {
             const int32_t f = dig == g ? 1 : 0;
@@ -344,8 +372,8 @@ walk_ldu8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const in
     }
 #pragma unroll
     for (int j = 0; j < P; ++j) {
-      const int64_t rel = ch * 32 * P + j * 32 + lane;
-      if (rel < p.unit_count) {
+      const int64_t rel = lc * 32 * P + j * 32 + lane;
+      if (rel < p.units_per) {
         const int32_t ub = U[j].best;
         if (p.unit_max) p.unit_max[rel] = ub;
         if (!have || ub > best) { best = ub; best_u = (uint32_t)(p.unit_begin + rel); have = true; }
@@ -354,11 +382,14 @@ walk_ldu8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const in
   }
   unsigned long long key = have ? make_key(best, best_u) : 0ull;
   key = warp_max_u64(key);
-  if (lane == 0 && key) atomicMax(p.key, key);
+  if (lane == 0 && key) atomicMax(p.key + (BAT && cur_b > 0 ? cur_b : 0), key);
 }
 
 __global__ void build_ldu8_kernel(const int32_t* M, int r, int c, int NW, int k, int s, int pr, uint32_t* tab,
-                                  int32_t* init) {
+                                  int32_t* init, int64_t m_stride, int64_t tab_stride, int64_t init_stride) {
+  M += blockIdx.x * m_stride;              // one block per matrix of a batch
+  tab += blockIdx.x * tab_stride;
+  init += blockIdx.x * init_stride;
   const int RW = lu_pad4(NW), RD = 2 * RW, CW = 4 * NW, sw = s - pr, NS = 1 << pr;
   auto pack = [](const int32_t* v) {
     uint32_t w = 0;
@@ -442,6 +473,15 @@ template <int D, int NW, int PR>
 cudaError_t launch_lu_pr(const WalkParams& p, const uint32_t* tab, const int32_t* init, int grid, cudaStream_t st) {
   constexpr int P = ldu8_units_per_lane<D, NW, PR>();
   const size_t sm = ldu8_smem(NW, p.s);
+  if (p.batch > 1) {                     // batched instances: <= 24 columns (the small-matrix regime)
+    if constexpr (NW <= 6) {
+      cudaError_t e = ensure_dyn_smem((const void*)walk_ldu8_kernel<D, NW, P, PR, true>, sm);
+      if (e != cudaSuccess) return e;
+      walk_ldu8_kernel<D, NW, P, PR, true><<<grid, kBlockLU, sm, st>>>(p, tab, init);
+      return cudaGetLastError();
+    }
+    return cudaErrorInvalidValue;
+  }
   cudaError_t e = ensure_dyn_smem((const void*)walk_ldu8_kernel<D, NW, P, PR>, sm);
   if (e != cudaSuccess) return e;
   walk_ldu8_kernel<D, NW, P, PR><<<grid, kBlockLU, sm, st>>>(p, tab, init);

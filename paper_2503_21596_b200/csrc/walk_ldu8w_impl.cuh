@@ -220,7 +220,7 @@ struct LdW {
 template <int NW, int PR>
 __host__ __device__ constexpr int w_units() { return (NW <= 6) ? LN_LDU8W_P : 1; }
 
-template <int NW, int PR>
+template <int NW, int PR, bool BAT = false>
 __global__ void __launch_bounds__(kBlockW, (w_minb<NW, PR>()))
 walk_ldu8w_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int32_t* __restrict__ gInit) {
   using WK = LdW<NW, PR>;
@@ -229,16 +229,7 @@ walk_ldu8w_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const i
   extern __shared__ __align__(16) uint32_t sT[];
   const int lane = threadIdx.x & 31;
   const int sw = p.s - PR;                         // walked digits
-  const int32_t* baseRec = gInit + (p.k + 1) * CW;
-  const int32_t* negRec = baseRec + CW;
-  const uint32_t* biasRec = reinterpret_cast<const uint32_t*>(negRec + CW);
   uint32_t* sBias = sT + sw * RD;
-  for (int i = lane; i < sw * RD; i += 32) sT[i] = gTab[i];
-  for (int i = lane; i < NS * NW; i += 32) {     // word-major: sBias[q * NS + m]
-    const int q = i / NS, m = i % NS;
-    sBias[i] = biasRec[m * NW + q];
-  }
-  __syncwarp();
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sT);
   const uint32_t sbias = (uint32_t)__cvta_generic_to_shared(sBias);
   // LN_LDU8W_KVEC: XOR with threadIdx.y (always 0 in these one-dimensional blocks, but not
@@ -248,23 +239,61 @@ walk_ldu8w_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const i
 #define LN_LDU8W_KVEC 1
 #endif
   uint32_t Ks[NS];
-#pragma unroll
-  for (int m = 0; m < NS; ++m) Ks[m] = __ldg(biasRec + NS * NW + m) ^ (LN_LDU8W_KVEC ? (uint32_t)threadIdx.y : 0u);
   uint32_t nwords = 1;
   for (int i = 0; i < sw; ++i) nwords *= 3;
   int32_t best_all = INT32_MIN;
   uint32_t best_u = 0;
   bool have = false;
-  const int64_t nchunks = (p.unit_count + 32 * P - 1) / (32 * P);
+  // matrix mb's delta table and word-major bias words -> shared memory, its kappas -> registers
+  auto stage = [&](int mb) {
+    __syncwarp();
+    const int32_t* gM = gInit + mb * p.init_stride;
+    const uint32_t* src = gTab + mb * p.tab_stride;
+    const uint32_t* biasRec = reinterpret_cast<const uint32_t*>(gM + (p.k + 3) * CW);
+    for (int i = lane; i < sw * RD; i += 32) sT[i] = src[i];
+    for (int i = lane; i < NS * NW; i += 32) {     // word-major: sBias[q * NS + m]
+      const int q = i / NS, m = i % NS;
+      sBias[i] = biasRec[m * NW + q];
+    }
+#pragma unroll
+    for (int m = 0; m < NS; ++m) Ks[m] = __ldg(biasRec + NS * NW + m) ^ (LN_LDU8W_KVEC ? (uint32_t)threadIdx.y : 0u);
+    __syncwarp();
+  };
+  // BAT (batched launches, f3): chunk ch -> matrix mb = ch / CPM (units_per units per matrix,
+  // the launch's range unless batched); a warp restages the tables when it moves to the next
+  // matrix.  The single-search instance stages them once.
+  const int64_t CPM = (p.units_per + 32 * P - 1) / (32 * P);
+  const int64_t nchunks = BAT ? CPM * p.batch : CPM;
+  int cur_b = BAT ? -1 : 0;
+  if constexpr (!BAT) stage(0);
   for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    int64_t lc = ch;
+    const int32_t* gI = gInit;
+    if constexpr (BAT) {
+      const int mb = (int)(ch / CPM);
+      lc = ch - (int64_t)mb * CPM;
+      gI = gInit + mb * p.init_stride;
+      if (mb != cur_b) {
+        if (cur_b >= 0) {
+          unsigned long long key = have ? make_key(best_all, best_u) : 0ull;
+          key = warp_max_u64(key);
+          if (lane == 0 && key) atomicMax(p.key + cur_b, key);
+          best_all = INT32_MIN; have = false;
+        }
+        stage(mb);
+        cur_b = mb;
+      }
+    }
+    const int32_t* baseRec = gI + (p.k + 1) * CW;
+    const int32_t* negRec = baseRec + CW;
     uint32_t A[P][3][NW];
     int32_t H[P][NS][3];
     int32_t best[P];
 #pragma unroll
     for (int j = 0; j < P; ++j) {
       // ---- unit init: prefix labels -> the three groups' bytes at the start word (suffix all 0)
-      const int64_t rel = ch * 32 * P + j * 32 + lane;
-      const int64_t u = p.unit_begin + (rel < p.unit_count ? rel : 0);
+      const int64_t rel = lc * 32 * P + j * 32 + lane;
+      const int64_t u = p.unit_begin + (rel < p.units_per ? rel : 0);
       uint64_t lab = 0;
       if (p.prefix_table) lab = p.prefix_table[u - p.unit_begin];
       else for (int x = 0; x <= p.k; ++x) lab |= (uint64_t)prefix_digit(p, u, x) << (p.pbits * x);
@@ -278,7 +307,7 @@ walk_ldu8w_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const i
           for (int e = 0; e < 4; ++e) a[g][e] = __ldg(negRec + 4 * q + e) + (g == 0 ? __ldg(baseRec + 4 * q + e) : 0);
         for (int x = 0; x <= p.k; ++x) {
           const int dig = (int)((lab >> (p.pbits * x)) & lmask);
-          const int4 v = __ldg(reinterpret_cast<const int4*>(gInit + x * CW) + q);
+          const int4 v = __ldg(reinterpret_cast<const int4*>(gI + x * CW) + q);
 #pragma unroll
           for (int g = 0; g < 3; ++g) {
             const int32_t f = dig == g ? 1 : 0;
@@ -326,8 +355,8 @@ walk_ldu8w_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const i
     }
 #pragma unroll
     for (int j = 0; j < P; ++j) {
-      const int64_t rel = ch * 32 * P + j * 32 + lane;
-      if (rel < p.unit_count) {
+      const int64_t rel = lc * 32 * P + j * 32 + lane;
+      if (rel < p.units_per) {
         if (p.unit_max) p.unit_max[rel] = best[j];
         if (!have || best[j] > best_all) { best_all = best[j]; best_u = (uint32_t)(p.unit_begin + rel); have = true; }
       }
@@ -335,7 +364,7 @@ walk_ldu8w_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const i
   }
   unsigned long long key = have ? make_key(best_all, best_u) : 0ull;
   key = warp_max_u64(key);
-  if (lane == 0 && key) atomicMax(p.key, key);
+  if (lane == 0 && key) atomicMax(p.key + (BAT && cur_b > 0 ? cur_b : 0), key);
 }
 
 template <int NW, int PR>
@@ -344,6 +373,15 @@ size_t w_smem(int s) { return sizeof(uint32_t) * (size_t)((s - PR) * 2 * w_pad4(
 template <int NW, int PR>
 cudaError_t launch_w(const WalkParams& p, const uint32_t* tab, const int32_t* init, int grid, cudaStream_t st) {
   const size_t sm = w_smem<NW, PR>(p.s);
+  if (p.batch > 1) {                     // batched instances: <= 24 columns (the small-matrix regime)
+    if constexpr (NW <= 6) {
+      cudaError_t e = ensure_dyn_smem((const void*)walk_ldu8w_kernel<NW, PR, true>, sm);
+      if (e != cudaSuccess) return e;
+      walk_ldu8w_kernel<NW, PR, true><<<grid, kBlockW, sm, st>>>(p, tab, init);
+      return cudaGetLastError();
+    }
+    return cudaErrorInvalidValue;
+  }
   cudaError_t e = ensure_dyn_smem((const void*)walk_ldu8w_kernel<NW, PR>, sm);
   if (e != cudaSuccess) return e;
   walk_ldu8w_kernel<NW, PR><<<grid, kBlockW, sm, st>>>(p, tab, init);

@@ -243,13 +243,17 @@ __host__ __device__ constexpr int u8_min_blocks() {
        : ((u8_foot<MODE, NW, P>() <= 96 && P >= 4) || u8_foot<MODE, NW, P>() <= 54) ? 12 : 1;
 }
 
-template <int MODE, int NW, int P, int LPU>
+// BAT: batched instance (f3, one launch over many matrices: chunk ch -> matrix mb = ch / CPM,
+// local chunk lc; chunks never straddle matrices and a warp restages the delta table when it
+// moves to the next matrix).  The single-search instance (BAT = false) keeps the table staged
+// once and no per-chunk bookkeeping (the batch state costs registers the hot loop needs).
+template <int MODE, int NW, int P, int LPU, bool BAT = false>
 __global__ void __launch_bounds__(kBlockU8, u8_min_blocks<MODE, NW, P, LPU>())
 walk_u8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int32_t* __restrict__ gInit) {
   using LY = U8Layout<MODE, NW>;
   constexpr int G = LY::G, CW = LY::CW;
   constexpr int LG = (P >= 8) ? 3 : (P >= 4) ? 2 : (P == 2 ? 1 : 0);
-  constexpr int NWL = NW / LPU;                    // LPU = lanes per unit                    // words held by one lane
+  constexpr int NWL = NW / LPU;                    // LPU = lanes per unit; words held by one lane
   constexpr int RWL = u8_pad4(NWL);                // its slice of a delta record (16B aligned)
   constexpr int RREC = LPU * RWL;                  // words per delta record
   constexpr int GPW = 32 / LPU;                    // lane groups per warp
@@ -262,23 +266,48 @@ walk_u8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int3
   constexpr int PR = STEP::PR, NS = STEP::NS;
   const int sw = p.s - PR;                         // walked digits (the last PR rows are paired, not walked)
   const int total = 2 * sw * RREC;
-  for (int i = lane; i < total; i += 32) sT[i] = gTab[i];
-  __syncwarp();
+  if constexpr (!BAT) {
+    for (int i = lane; i < total; i += 32) sT[i] = gTab[i];
+    __syncwarp();
+  }
   const uint32_t nblk = 1u << (sw - K);
-  const int32_t* loRec = gInit + (p.k + 1) * CW;
-  const int32_t* tRec = loRec + CW;
-  const int32_t* abRec = tRec + CW;
-  const int32_t* rhoRec = abRec + CW;
   const int kh = p.k - LG;                         // last row of the shared (high) prefix part
   int32_t best_all = INT32_MIN;
   uint32_t best_u = 0;
   bool have = false;
-  const int64_t u_end = p.unit_begin + p.unit_count;
+  // units of one matrix: [unit_begin, unit_begin + units_per) (= the launch's range unless batched)
+  const int64_t u_end = p.unit_begin + p.units_per;
   const int64_t g0 = p.unit_begin / P, g_end = (u_end + P - 1) / P;
-  const int64_t nchunks = (g_end - g0 + GPW - 1) / GPW;
+  const int64_t CPM = (g_end - g0 + GPW - 1) / GPW;
+  const int64_t nchunks = BAT ? CPM * p.batch : CPM;
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sT);
+  int cur_b = BAT ? -1 : 0;
   for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
-    const int64_t g = g0 + ch * GPW + slot;
+    int64_t lc = ch;
+    const int32_t* gI = gInit;
+    if constexpr (BAT) {
+      const int mb = (int)(ch / CPM);
+      lc = ch - (int64_t)mb * CPM;
+      gI = gInit + mb * p.init_stride;
+      if (mb != cur_b) {
+        if (cur_b >= 0) {                          // flush the previous matrix's key
+          unsigned long long key = have ? make_key(best_all, best_u) : 0ull;
+          key = warp_max_u64(key);
+          if (lane == 0 && key) atomicMax(p.key + cur_b, key);
+          best_all = INT32_MIN; have = false;
+        }
+        __syncwarp();
+        const uint32_t* src = gTab + mb * p.tab_stride;
+        for (int i = lane; i < total; i += 32) sT[i] = src[i];
+        __syncwarp();
+        cur_b = mb;
+      }
+    }
+    const int32_t* loRec = gI + (p.k + 1) * CW;
+    const int32_t* tRec = loRec + CW;
+    const int32_t* abRec = tRec + CW;
+    const int32_t* rhoRec = abRec + CW;
+    const int64_t g = g0 + lc * GPW + slot;
     const int64_t uh = min(max(g * P, p.unit_begin), u_end - 1);   // a valid unit of the group
     uint32_t A[P][NWL];
     uint32_t B[NB];
@@ -300,7 +329,7 @@ walk_u8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int3
           // L_1 / L_marg: a_x = +1 (digit 0) or -1; L_2: only rows in group 0 count
           const int dig = (int)((neg >> x) & 1ull);
           const int32_t f = (MODE == MODE_LD) ? 1 - dig : 1 - 2 * dig;
-          const int4 v = __ldg(reinterpret_cast<const int4*>(gInit + x * CW) + q);
+          const int4 v = __ldg(reinterpret_cast<const int4*>(gI + x * CW) + q);
           Pv[0] += f * v.x; Pv[1] += f * v.y; Pv[2] += f * v.z; Pv[3] += f * v.w;
         }
         uint32_t w[NS][2];                         // [paired-row signs][bias set]
@@ -363,7 +392,7 @@ walk_u8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int3
         for (int b = 0; b < LG; ++b) {
           const int dig = lowdig[b];
           const int32_t f = (MODE == MODE_LD) ? 1 - dig : 1 - 2 * dig;
-          const int4 v = __ldg(reinterpret_cast<const int4*>(gInit + (kh + 1 + b) * CW) + q);
+          const int4 v = __ldg(reinterpret_cast<const int4*>(gI + (kh + 1 + b) * CW) + q);
           a[0] += f * v.x; a[1] += f * v.y; a[2] += f * v.z; a[3] += f * v.w;
         }
         A[j][ql] = (uint32_t)(a[0] & 0xFF) | ((uint32_t)(a[1] & 0xFF) << 8) | ((uint32_t)(a[2] & 0xFF) << 16) |
@@ -410,14 +439,17 @@ walk_u8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int3
   }
   unsigned long long key = have ? make_key(best_all, best_u) : 0ull;
   key = warp_max_u64(key);
-  if (lane == 0 && key) atomicMax(p.key, key);
+  if (lane == 0 && key) atomicMax(p.key + (BAT && cur_b > 0 ? cur_b : 0), key);
 }
 
 // Delta table (walked digit b <-> row r-1-b, sign sg = new digit value) and init
 // records; the byte window covers the last s + lg rows (lg = log2 of the lane group).
 template <int MODE>
 __global__ void build_u8_kernel(const int32_t* M, int r, int c, int NW, int k, int s, int lg, int lpu, uint32_t* tab,
-                                int32_t* init) {
+                                int32_t* init, int64_t m_stride, int64_t tab_stride, int64_t init_stride) {
+  M += blockIdx.x * m_stride;              // one block per matrix of a batch
+  tab += blockIdx.x * tab_stride;
+  init += blockIdx.x * init_stride;
   // a record holds lpu slices of pad4(NW / lpu) words (one per lane of a lane pair)
   const int NWL = NW / lpu, RWL = u8_pad4(NWL), RW = lpu * RWL, CW = 4 * NW;
   const int scale = (MODE == MODE_LD) ? 1 : 2;
@@ -462,10 +494,22 @@ __global__ void build_u8_kernel(const int32_t* M, int r, int c, int NW, int k, i
 template <int MODE, int NW, int LPU>
 size_t u8_smem(int s) { return sizeof(uint32_t) * (size_t)(2 * (s - u8_pr<MODE>()) * LPU * u8_pad4(NW / LPU)); }
 
+// batched instances exist for the small-matrix regime only (<= 32 columns, one lane per unit)
+constexpr int kU8BatchMaxNW = 8;
+
 template <int MODE, int NW, int LPU>
 cudaError_t launch_u8_l(const WalkParams& p, const uint32_t* tab, const int32_t* init, int grid, cudaStream_t st) {
   constexpr int P = u8_units_per_lane<MODE, NW, LPU>();
   const size_t sm = u8_smem<MODE, NW, LPU>(p.s);
+  if (p.batch > 1) {
+    if constexpr (NW <= kU8BatchMaxNW && LPU == 1) {
+      cudaError_t e = ensure_dyn_smem((const void*)walk_u8_kernel<MODE, NW, P, LPU, true>, sm);
+      if (e != cudaSuccess) return e;
+      walk_u8_kernel<MODE, NW, P, LPU, true><<<grid, kBlockU8, sm, st>>>(p, tab, init);
+      return cudaGetLastError();
+    }
+    return cudaErrorInvalidValue;
+  }
   cudaError_t e = ensure_dyn_smem((const void*)walk_u8_kernel<MODE, NW, P, LPU>, sm);
   if (e != cudaSuccess) return e;
   walk_u8_kernel<MODE, NW, P, LPU><<<grid, kBlockU8, sm, st>>>(p, tab, init);
@@ -574,12 +618,20 @@ cudaError_t walk_u8_launch_mode<LN_BIN_MODE>(const WalkParams& p, int32_t* scrat
   const int lmax = [&]() -> int { LN_U8_SWITCH(LN_BIN_MODE, NW, lpu_u8) return 1; }();
   const int lpu = (p.u8_lpu == 2 && lmax == 2) ? 2 : 1;
   const int P = [&]() -> int { LN_U8_SWITCH(LN_BIN_MODE, NW, upl_u8, lpu) return 1; }();
-  build_u8_kernel<LN_BIN_MODE><<<1, 256, 0, st>>>(p.M, p.r, p.c, NW, p.k, p.s, P >= 8 ? 3 : P >= 4 ? 2 : (P == 2 ? 1 : 0),
-                                                  lpu, tab, scratch_init);
+  build_u8_kernel<LN_BIN_MODE><<<p.batch, 256, 0, st>>>(p.M, p.r, p.c, NW, p.k, p.s, P >= 8 ? 3 : P >= 4 ? 2 : (P == 2 ? 1 : 0),
+                                                        lpu, tab, scratch_init, p.m_stride, p.tab_stride, p.init_stride);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   LN_U8_SWITCH(LN_BIN_MODE, NW, launch_u8, p, tab, scratch_init, grid, st)
   return cudaErrorInvalidValue;
+}
+
+// per-matrix scratch of a launch (batched launches: the strides): delta records, init records
+template <>
+void walk_u8_table_sizes_mode<LN_BIN_MODE>(int c, int k, int s, int lpu, int64_t* tab_words, int64_t* init_ints) {
+  const int NW = walk_u8_words_mode<LN_BIN_MODE>(c), PR = u8_pr<LN_BIN_MODE>();
+  *tab_words = (int64_t)2 * (s - PR) * lpu * u8_pad4(NW / lpu);
+  *init_ints = (int64_t)(k + 4 + PR) * 4 * NW;
 }
 
 template <>

@@ -6,7 +6,7 @@ compute-sanitizer --tool racecheck python tests/sanitize_cases.py
 Covers the byte kernels (L_1 / L_marg / L_2, aligned and unaligned Algorithm-1 slices, the
 grouped prefix hook; L_3 / L_4 with 1, 2 and 3 paired rows; the all-H L_3 kernel with 3 and 4),
 the 16-bit and int32 families (LNORM_KERNEL), the generic kernel (also batched), the reductions,
-the batched API and the device-input path (guard-statistics kernel, caller stream).  Every value is checked
+the batched API (byte walks, 16-bit paired walk, generic kernel) and the device-input path (guard-statistics kernel, caller stream).  Every value is checked
 against the oracle so a silent corruption also fails.
 """
 import os
@@ -66,6 +66,11 @@ def main():
     Ms = np.stack([synth.random_matrix(10, 10, 540 + i) for i in range(16)])
     vals, _ = L.compute_batch(Ms)
     assert all(int(vals[i]) == oracle.l1(Ms[i])[0] for i in range(16))
+    for d, n, m, b in ((1, 14, 16, 9), (2, 12, 12, 7), (3, 11, 14, 6), (3, 14, 23, 3), (4, 9, 10, 5)):   # batched byte walks
+        Bs = np.stack([synth.random_matrix(n, m, 545 + 13 * i + d) for i in range(b)])
+        vals, _ = L.compute_batch(Bs, d=d)
+        seen.add(L.last_stats()["variant"])
+        assert all(int(vals[i]) == oracle.norm(Bs[i], d=d)[0] for i in range(b))
     Ts = np.stack([synth.random_matrix(4, 3, 550 + i, -1, 1) for i in range(40)])     # generic batched walk
     for d in (1, 3):
         vals, _ = L.compute_batch(Ts, d=d)

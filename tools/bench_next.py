@@ -39,9 +39,13 @@ def timed(fn, reps=3):
 def f3(batch, n, d, marg):
     Ms = np.stack([synth.random_matrix(n, n, 90_000 + i) for i in range(batch)])
     tb, (vb, ab) = timed(lambda: L.compute_batch(Ms, d=d, with_marginals=marg))
-    ts, single = timed(lambda: [L.compute(M, d=d, with_marginals=marg) for M in Ms], reps=1)
-    assert all(int(vb[i]) == single[i][0] for i in range(batch))
-    return {"row": "f3 batched API", "mode": "L_marg" if marg else f"L_{'1' if d == 1 else d}",
+    st = L.last_stats()
+    ts, single = timed(lambda: [L.compute(M, d=d, with_marginals=marg) for M in Ms[:min(batch, 256)]], reps=1)
+    ts *= batch / min(batch, 256)
+    assert all(int(vb[i]) == single[i][0] for i in range(len(single)))
+    return {"variant": L.VARIANTS.get(st["variant"], st["variant"]), "walk_ms": st["walk_ms"], "total_ms": st["total_ms"],
+            "strategies_per_s_walk": st["steps"] / (st["walk_ms"] * 1e-3) if st["walk_ms"] > 0 else None,
+            "row": "f3 batched API", "mode": "L_marg" if marg else f"L_{'1' if d == 1 else d}",
             "matrices": batch, "shape": [n, n], "batched_s": tb, "per_call_s": ts,
             "matrices_per_s_batched": batch / tb, "matrices_per_s_per_call": batch / ts, "speedup": ts / tb}
 
@@ -66,9 +70,12 @@ def f1(n, m, d, seed):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=None)
+    ap.add_argument("--batch-only", action="store_true")
     a = ap.parse_args()
-    rows = [f3(4096, 16, 1, False), f3(4096, 16, 1, True), f3(1024, 20, 1, False), f3(1024, 14, 2, False),
-            f1(36, 40, 1, 7), f1(22, 24, 3, 8)]
+    rows = [f3(4096, 16, 1, False), f3(4096, 16, 1, True), f3(1024, 20, 1, False), f3(1024, 24, 1, False),
+            f3(1024, 14, 2, False), f3(256, 24, 2, False), f3(256, 16, 3, False), f3(64, 18, 3, False), f3(64, 14, 4, False)]
+    if not a.batch_only:
+        rows += [f1(36, 40, 1, 7), f1(22, 24, 3, 8)]
     for r in rows:
         print(json.dumps(r), flush=True)
     if a.out:

@@ -17,15 +17,18 @@ import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
+import bench  # noqa: E402  (the roofline floor model)
 import paper_2503_21596_b200 as L
 from paper_2503_21596_b200 import synth
 
 
-def roofline(col_updates_per_s, variant, nsm=148, mhz=1965.0):
-    # lane-instructions per column update: 2 (int32 add + |.|-accumulate), 1 (s16x2), 1/2 (u8x4)
-    simd = 4 if variant in (7, 8) else (2 if variant in (3, 4, 5, 6) else 1)
-    peak_updates = 128.0 * nsm * mhz * 1e6 * simd / 2
-    return col_updates_per_s / peak_updates
+def roofline(steps_per_s, variant, d, c, s, d_walked, pr, nsm=148, mhz=1965.0):
+    """Fraction of the kernel family's binding-pipe floor (bench.alu_floor):
+    floor instructions per strategy x strategies/s over lanes/clk/SM x SMs x f_max."""
+    per, pipe, lanes = bench.alu_floor(variant, d, c, s, d_walked, pr or None)
+    if per is None:
+        return None, None
+    return per * steps_per_s / (lanes * nsm * mhz * 1e6), pipe
 
 
 def run(n, m, d, seed, budget_s):
@@ -66,10 +69,13 @@ def run(n, m, d, seed, budget_s):
         kind, variant = f"sampled ({count} prefixes of {nfixed} rows)", L.last_stats()["variant"]
     rate = steps / secs
     cu = rate * updates_per_step
+    st = L.last_stats()
+    frac, pipe = roofline(rate, variant, d, plan["cols"], plan["suffix_digits"], st["d"] if d > 1 else 2,
+                          st["paired_rows"])
     return {"config": f"L_{d} {n}x{m}", "n": n, "m": m, "d": d, "seed": seed, "kind": kind, "value": v,
             "kernel_variant": L.VARIANTS.get(variant, variant), "strategies": plan["steps"],
             "steps_per_s": rate, "column_updates_per_s": cu,
-            "roofline_frac": roofline(cu, variant),
+            "roofline_frac": frac, "roofline_pipe": pipe, "lanes_per_unit": plan["lanes_per_unit"],
             "projected_full_search_s": plan["steps"] / rate, "measured_s": secs}
 
 
@@ -77,13 +83,14 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--budget-s", type=float, default=20.0)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--wide-only", action="store_true", help="only the m = 4n L_1 rows")
     a = ap.parse_args()
     rows = []
     for n in range(32, 49, 2):
-        for m in (n, 4 * n):
+        for m in ((4 * n,) if a.wide_only else (n, 4 * n)):
             rows.append(run(n, m, 1, 100 + n, a.budget_s))
             print(json.dumps(rows[-1]), flush=True)
-    for n in range(16, 27, 2):
+    for n in ([] if a.wide_only else range(16, 27, 2)):
         rows.append(run(n, n, 3, 200 + n, a.budget_s))
         print(json.dumps(rows[-1]), flush=True)
     if a.out:
