@@ -336,6 +336,8 @@ int64_t rgs_count(int len, int d) {
   return t > 9e18L ? INT64_MAX : (int64_t)t;
 }
 
+constexpr int kU8MinSuffix = 6;   // shortest byte-walk suffix preferred over a packed 16-bit walk
+
 int make_plan(const Problem& pr, int world, Plan* pl, int64_t target_override = 0, bool allow_u8 = true) {
   const int f = pr.r - 1;
   const int64_t target = target_override > 0 ? target_override : kNominalLanes * 64 * std::max(1, world);
@@ -364,7 +366,12 @@ int make_plan(const Problem& pr, int world, Plan* pl, int64_t target_override = 
           if (u8_fits(pr, s_ + lg) && walk_u8_supported(pr.mode, pr.c, s_, lpu)) su = s_;
         int s_lo = 0;
         for (int s_ = 1; s_ <= su; ++s_) if (walk_u8_supported(pr.mode, pr.c, s_, lpu)) { s_lo = s_; break; }
-        if (su > 0 && s_lo > 0 && f - su <= 31 + kMaxKeyShift) {
+        // wide entries force short suffixes, where the unit init (a prefix-row sum per unit)
+        // outweighs the walk: below 6 suffix rows a packed 16-bit walk is faster whenever its
+        // guard holds (42x42, entries in [-20,20]: byte walk at s = 6 3.88 s, packed 16-bit
+        // 3.89 s; [-25,25] at s = 5: 6.17 s vs ~3.9 s; profiles/r02/envelope_42x42.jsonl)
+        const bool short_u8 = su < kU8MinSuffix && (pr.fitsPair || pr.fits16) && f >= kU8MinSuffix;
+        if (su > 0 && s_lo > 0 && f - su <= 31 + kMaxKeyShift && !short_u8) {
           int k = std::max(lg, f - su);
           while (k < f - s_lo && k < 31 && (1LL << k) < target) ++k;
           // short suffixes spend their time in the lane init: keep s >= 10 while the split
