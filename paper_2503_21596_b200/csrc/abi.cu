@@ -149,7 +149,10 @@ void host_stats(const int32_t* M, const Problem& p, GuardStats* g) {
 // per suffix length a warp max goes to shared memory (no block barrier per row), one barrier
 // at the end combines the eight warps.
 __global__ void __launch_bounds__(256) guard_stats_kernel(const int32_t* M, int m, int transposed, int r, int c,
-                                                          int marg, long long* out) {
+                                                          int marg, long long* out, int64_t m_stride = 0,
+                                                          int out_stride = 0) {
+  M += blockIdx.x * m_stride;              // batched calls: one block per matrix
+  out += blockIdx.x * out_stride;
   constexpr int kW = 8, kPer = kMaxCols / 256;
   __shared__ long long red[kMaxRows][kW];
   __shared__ long long red3[3][kW];
@@ -336,6 +339,7 @@ int64_t rgs_count(int len, int d) {
   return t > 9e18L ? INT64_MAX : (int64_t)t;
 }
 
+constexpr double kLdInitStrategies = 500.0;   // a byte d-ary unit's init, in walked strategies (24 columns)
 constexpr int kU8MinSuffix = 6;   // shortest byte-walk suffix preferred over a packed 16-bit walk
 
 int make_plan(const Problem& pr, int world, Plan* pl, int64_t target_override = 0, bool allow_u8 = true) {
@@ -370,7 +374,9 @@ int make_plan(const Problem& pr, int world, Plan* pl, int64_t target_override = 
         // outweighs the walk: below 6 suffix rows a packed 16-bit walk is faster whenever its
         // guard holds (42x42, entries in [-20,20]: byte walk at s = 6 3.88 s, packed 16-bit
         // 3.89 s; [-25,25] at s = 5: 6.17 s vs ~3.9 s; profiles/r02/envelope_42x42.jsonl)
-        const bool short_u8 = su < kU8MinSuffix && (pr.fitsPair || pr.fits16) && f >= kU8MinSuffix;
+        // (large searches only: below 24 rows the whole search is microseconds either way, and the
+        // byte walk's guard-boundary tests run it at its shortest suffix)
+        const bool short_u8 = su < kU8MinSuffix && (pr.fitsPair || pr.fits16) && f >= 24;
         if (su > 0 && s_lo > 0 && f - su <= 31 + kMaxKeyShift && !short_u8) {
           int k = std::max(lg, f - su);
           while (k < f - s_lo && k < 31 && (1LL << k) < target) ++k;
@@ -417,6 +423,25 @@ int make_plan(const Problem& pr, int world, Plan* pl, int64_t target_override = 
     }
     int k = 0;
     while (k < f - smin && (k + 2) * prefix_bits(d) <= 64 && rgs_count(k + 2, d) <= kTableCap && rgs_count(k + 1, d) < target) ++k;
+    if (kern == K_LDU8 && target_override == 0) {
+      // Small searches (L_3 below ~24 rows): the RGS table caps k, so the split above leaves
+      // 2-5 suffix rows and every unit pays an init (its prefix rows summed into the byte
+      // groups, the bias sums: ~kLdInitStrategies strategies' worth of work) for a walk of a
+      // few hundred strategies.  Pick the prefix length minimising
+      //     ceil(units / resident unit slots) * (init + d^s)
+      // instead (24x24 and larger keep the split above; 20x20 L_3: s 5 -> 7).
+      const double slots = (double)kNominalLanes / 2 * std::max(1, world);   // 16 warps x 32 lanes per SM
+      auto cost = [&](int kk) {
+        return std::ceil((double)rgs_count(kk + 1, d) / slots) * (kLdInitStrategies + std::pow((double)d, f - kk));
+      };
+      int best_k = k;
+      double best_c = cost(k);
+      for (int kk = k - 1; kk >= 0 && f - kk <= 20 && walk_ldu8_supported(d, pr.c, f - kk); --kk) {
+        const double c = cost(kk);
+        if (c < best_c) { best_c = c; best_k = kk; }
+      }
+      k = best_k;
+    }
     p.k = k; p.s = f - k;
     {
       // the RGS prefix list depends only on (k, d): enumerate once per process
@@ -573,6 +598,7 @@ struct DevCtx {
   int64_t* dUnit = nullptr; size_t capUnit = 0;
   int32_t* dRed = nullptr; size_t capRed = 0;      // reduction scratch + reduced matrix + maps
   int64_t* dBatch = nullptr; size_t capBatch = 0;  // batched-call buffers
+  long long* dBStats = nullptr; long long* hBStats = nullptr; size_t capBStats = 0;  // batched guard stats
   int64_t* hRes = nullptr;          // pinned mirror of dRes
   bool ready = false;
 };
@@ -1249,27 +1275,61 @@ int lnorm_compute_batch(const int32_t* M, int32_t batch, int32_t n, int32_t m, i
   int dev = 0, rc = current_device(&dev);
   if (rc) return rc;
   const size_t nm = (size_t)n * m;
-  // validate every matrix; the batched plan must be exact for all of them, so it is made for
-  // the element-wise worst case of their guard statistics (every matrix has the same shape,
-  // orientation and mode): sufW = max over the batch, the 16-bit guards = AND over the batch
   Problem pr;
-  for (int b = 0; b < batch; ++b) {
-    Problem q;
-    if ((rc = validate(M + b * nm, n, m, d, with_marginals, &q))) return rc;
-    if (b == 0) {
-      pr = q;
-      continue;
+  if ((rc = validate_shape(n, m, d, with_marginals, &pr))) return rc;
+  DevCtx* cx = nullptr;
+  if ((rc = ctx_get(dev, &cx))) return rc;
+  std::lock_guard<std::mutex> g(cx->mu);
+  CU(cudaSetDevice(dev));
+  cudaStream_t s = cx->stream;
+  StreamScope scope(cx, nullptr);
+  // every matrix to the device, then its guard statistics there (one block per matrix; the
+  // host loop over thousands of matrices cost more than the whole batched walk)
+  const int sw_ = 3 + pr.r;
+  if ((rc = grow(&cx->dIn, &cx->capIn, (size_t)batch * nm))) return rc;
+  if (cx->capBStats < (size_t)batch * sw_) {
+    cudaFree(cx->dBStats); cudaFreeHost(cx->hBStats);
+    cx->dBStats = nullptr; cx->hBStats = nullptr; cx->capBStats = 0;
+    CU(cudaMalloc(&cx->dBStats, sizeof(long long) * (size_t)batch * sw_));
+    CU(cudaMallocHost(&cx->hBStats, sizeof(long long) * (size_t)batch * sw_));
+    cx->capBStats = (size_t)batch * sw_;
+  }
+  CU(cudaEventRecord(cx->ev[0], s));
+  CU(cudaMemcpyAsync(cx->dIn, M, sizeof(int32_t) * batch * nm, cudaMemcpyHostToDevice, s));
+  guard_stats_kernel<<<batch, 256, 0, s>>>(cx->dIn, m, pr.transposed ? 1 : 0, pr.r, pr.c, pr.mode == MODE_MARG ? 1 : 0,
+                                           cx->dBStats, (int64_t)nm, sw_);
+  CU(cudaGetLastError());
+  CU(cudaMemcpyAsync(cx->hBStats, cx->dBStats, sizeof(long long) * (size_t)batch * sw_, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  // the batched plan must be exact for every matrix, so it is made for the element-wise worst
+  // case of their guard statistics (same shape, orientation and mode): sufW = max over the
+  // batch, the 16-bit guards = AND over the batch; a matrix with sum |M| > 2^31-1 fails the call
+  auto stats_of = [&](int b, Problem* q) {
+    const long long* h = cx->hBStats + (size_t)b * sw_;
+    GuardStats gs;
+    gs.S = h[0]; gs.par[0] = h[1]; gs.par[1] = h[2];
+    for (int x = 1; x <= pr.r; ++x) gs.sufW[x] = h[3 + x - 1];
+    *q = pr;
+    return apply_stats(gs, q);
+  };
+  {
+    Problem all = pr;
+    for (int b = 0; b < batch; ++b) {
+      Problem q;
+      if ((rc = stats_of(b, &q))) return rc;
+      if (b == 0) { all = q; continue; }
+      all.fits16 = all.fits16 && q.fits16;
+      all.fitsPair = all.fitsPair && q.fitsPair;
+      all.fitsLdPair = all.fitsLdPair && q.fitsLdPair;
+      for (int i = 0; i <= kMaxRows; ++i) all.sufW[i] = std::max(all.sufW[i], q.sufW[i]);
     }
-    pr.fits16 = pr.fits16 && q.fits16;
-    pr.fitsPair = pr.fitsPair && q.fitsPair;
-    pr.fitsLdPair = pr.fitsLdPair && q.fitsLdPair;
-    for (int i = 0; i <= kMaxRows; ++i) pr.sufW[i] = std::max(pr.sufW[i], q.sufW[i]);
+    pr = all;
   }
   // path: one launch over the units of all matrices through the byte-packed walks (L_1,
   // L_marg, L_2: walk_u8; L_3, L_4: walk_ldu8 / walk_ldu8w) or the strategy-paired 16-bit
   // walk, each restaging its per-matrix tables per chunk; else the generic warp-per-unit
   // kernel batched the same way for small search spaces (tiny shapes, any d); else one
-  // search per matrix through the hot single-matrix kernels
+  // search per matrix through the hot single-matrix kernels (inputs already on the device)
   Plan pl;
   const int64_t target = std::max<int64_t>(1, kNominalLanes * 8 / batch);
   int bkern = -1;
@@ -1287,17 +1347,17 @@ int lnorm_compute_batch(const int32_t* M, int32_t batch, int32_t n, int32_t m, i
   for (int i = 0; i < pr.r - 1; ++i) space *= pr.dl;
   if (bkern < 0 && space > (long double)(1 << 20)) {
     for (int b = 0; b < batch; ++b) {
-      if ((rc = compute_on(dev, M + b * nm, nullptr, n, m, d, with_marginals, 0, 1, nullptr, nullptr, values + b,
-                           argmax ? argmax + (size_t)b * n : nullptr)))
-        return rc;
+      Problem q;
+      if ((rc = stats_of(b, &q))) return rc;
+      RunOut ro;
+      lnorm_stats st{};
+      if ((rc = run_device(*cx, cx->dIn + (size_t)b * nm, q, 0, 1, nullptr, &ro, &st))) return rc;
+      g_stats = st;
+      values[b] = ro.value;
+      if (argmax) std::memcpy(argmax + (size_t)b * n, ro.argmax.data(), (size_t)n);
     }
     return LNORM_OK;
   }
-  DevCtx* cx = nullptr;
-  if ((rc = ctx_get(dev, &cx))) return rc;
-  std::lock_guard<std::mutex> g(cx->mu);
-  CU(cudaSetDevice(dev));
-  cudaStream_t s = cx->stream;
   if (bkern < 0) {
     // generic batched plan: the smallest prefix length giving ~64 warps of work per SM
     pl = Plan{};
@@ -1323,7 +1383,7 @@ int lnorm_compute_batch(const int32_t* M, int32_t batch, int32_t n, int32_t m, i
   tabw = (tabw + 3) & ~(int64_t)3;
   initw = (initw + 3) & ~(int64_t)3;
   auto up8 = [](size_t x) { return (x + 7) & ~(size_t)7; };
-  const size_t oIn = 0, oM = oIn + up8(batch * nm), oTab = oM + up8(batch * nm), oInit = oTab + up8(batch * (size_t)tabw);
+  const size_t oM = 0, oTab = oM + up8(batch * nm), oInit = oTab + up8(batch * (size_t)tabw);
   const size_t oKey = oInit + up8(batch * (size_t)initw);                 // int32 units so far
   // keys, lex, rmax, values: int64 each per matrix; then argmax bytes
   const size_t words32 = oKey + 8 * (size_t)batch + up8((size_t)batch * n) / 4 + 8;
@@ -1334,7 +1394,7 @@ int lnorm_compute_batch(const int32_t* M, int32_t batch, int32_t n, int32_t m, i
     if ((rc = grow(&cx->dPre, &cx->capPre, ptab.size()))) return rc;
   }
   int32_t* base = reinterpret_cast<int32_t*>(cx->dBatch);
-  int32_t* dIn = base + oIn;
+  int32_t* dIn = cx->dIn;
   int32_t* dMo = base + oM;
   uint32_t* dTab = reinterpret_cast<uint32_t*>(base + oTab);
   int32_t* dInit = base + oInit;
@@ -1343,8 +1403,6 @@ int lnorm_compute_batch(const int32_t* M, int32_t batch, int32_t n, int32_t m, i
   unsigned long long* rmax = lex + batch;
   int64_t* vals = reinterpret_cast<int64_t*>(rmax + batch);
   int8_t* args = reinterpret_cast<int8_t*>(vals + batch);
-  CU(cudaEventRecord(cx->ev[0], s));
-  CU(cudaMemcpyAsync(dIn, M, sizeof(int32_t) * batch * nm, cudaMemcpyHostToDevice, s));
   if (!ptab.empty()) CU(cudaMemcpyAsync(cx->dPre, ptab.data(), sizeof(uint64_t) * ptab.size(), cudaMemcpyHostToDevice, s));
   orient_kernel<<<dim3(std::min(64, (int)((nm + 255) / 256)), std::min(batch, 65535)), 256, 0, s>>>(
       dIn, n, m, pr.transposed ? 1 : 0, dMo, batch);
