@@ -285,7 +285,8 @@ typedef struct {
   int64_t units;
   double steps;                /* strategies walked in total */
   int32_t lanes_per_unit;      /* byte-packed binary walk: 1, or 2 (lane pairs, > 128 columns) */
-  int32_t reserved;
+  int32_t words;               /* byte-packed binary walk: packed words per unit of the instance
+                                  (columns / 4 rounded up to the instance; padding = 4 words - c) */
 } lnorm_plan_info;
 int lnorm_plan(const int32_t* M, int32_t n, int32_t m, int32_t d, int32_t with_marginals, int32_t world,
                lnorm_plan_info* out);

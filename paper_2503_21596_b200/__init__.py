@@ -66,7 +66,7 @@ class PlanInfo(ctypes.Structure):
         ("rows", ctypes.c_int32), ("cols", ctypes.c_int32), ("transposed", ctypes.c_int32),
         ("d_walked", ctypes.c_int32), ("prefix_digits", ctypes.c_int32), ("suffix_digits", ctypes.c_int32),
         ("variant", ctypes.c_int32), ("packed_ok", ctypes.c_int32), ("units", ctypes.c_int64),
-        ("steps", ctypes.c_double), ("lanes_per_unit", ctypes.c_int32), ("reserved", ctypes.c_int32),
+        ("steps", ctypes.c_double), ("lanes_per_unit", ctypes.c_int32), ("words", ctypes.c_int32),
     ]
 
     def as_dict(self):

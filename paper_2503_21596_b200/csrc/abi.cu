@@ -339,6 +339,13 @@ int64_t rgs_count(int len, int d) {
   return t > 9e18L ? INT64_MAX : (int64_t)t;
 }
 
+// shortest byte-walk suffix kept while the split still leaves ~2^21 units (LNORM_U8_SMIN: A/B hook).
+// 13 (round 1: 10): the lane-pair unit init is heavier than the square instances' (34x136:
+// 24.8 -> 20.8 ms, 36x144: 89.7 -> 85.7 ms, squares equal or faster; profiles/r02/ab_u8_smin.log)
+int u8_min_walk() {
+  static const int v = [] { const char* e = getenv("LNORM_U8_SMIN"); return (e && *e) ? atoi(e) : 13; }();
+  return v;
+}
 constexpr double kLdInitStrategies = 500.0;   // a byte d-ary unit's init, in walked strategies (24 columns)
 constexpr int kU8MinSuffix = 6;   // shortest byte-walk suffix preferred over a packed 16-bit walk
 
@@ -380,9 +387,9 @@ int make_plan(const Problem& pr, int world, Plan* pl, int64_t target_override = 
         if (su > 0 && s_lo > 0 && f - su <= 31 + kMaxKeyShift && !short_u8) {
           int k = std::max(lg, f - su);
           while (k < f - s_lo && k < 31 && (1LL << k) < target) ++k;
-          // short suffixes spend their time in the lane init: keep s >= 10 while the split
-          // still leaves ~2^21 units (several chunks per resident warp)
-          while (f - k < 10 && k > std::max(lg, 21) && f - k < su) --k;
+          // short suffixes spend their time in the lane init: keep s >= u8_min_walk() while the
+          // split still leaves ~2^21 units (several chunks per resident warp)
+          while (f - k < u8_min_walk() && k > std::max(lg, 21) && f - k < su) --k;
           p.k = k; p.s = f - k; p.units = 1LL << k;
           p.kernel = K_U8;
           p.u8_lpu = lpu;
@@ -1725,6 +1732,7 @@ int lnorm_plan(const int32_t* M, int32_t n, int32_t m, int32_t d, int32_t with_m
   I.units = pl.units;
   I.steps = (double)pl.units * (double)ipow(pr.dl, pl.s);
   I.lanes_per_unit = pl.kernel == K_U8 ? pl.u8_lpu : 1;
+  I.words = pl.kernel == K_U8 ? walk_u8_words(pr.mode, pr.c) : 0;
   *out = I;
   return LNORM_OK;
 }

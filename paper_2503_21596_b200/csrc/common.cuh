@@ -222,6 +222,8 @@ template <int MODE> int walk_u8_units_per_lane_mode(int c, int lpu);
 template <int MODE> int walk_u8_lanes_per_unit_mode(int c);
 template <int MODE> int walk_u8_paired_rows_mode();
 int walk_u8_lanes_per_unit(int mode, int c);
+// packed words per unit of the byte-walk instance for c columns (0 = none)
+int walk_u8_words(int mode, int c);
 template <int MODE> int walk_u8_unroll_mode(int c, int lpu);
 // Byte-packed d-ary walk, last row paired (L_d, d in {3,4}; guard: every column's
 // sum_x |M_xy| <= 255, checked by the caller).

@@ -116,6 +116,12 @@ void walk_u8_table_sizes(int mode, int c, int k, int s, int lpu, int64_t* tab_wo
   else walk_u8_table_sizes_mode<MODE_LD>(c, k, s, lpu, tab_words, init_ints);
 }
 
+int walk_u8_words(int mode, int c) {
+  if (mode == MODE_L1) return walk_u8_words_mode<MODE_L1>(c);
+  if (mode == MODE_MARG) return walk_u8_words_mode<MODE_MARG>(c);
+  return walk_u8_words_mode<MODE_LD>(c);
+}
+
 // largest lanes-per-unit an instance offers for c columns (1 or 2)
 int walk_u8_lanes_per_unit(int mode, int c) {
   if (mode == MODE_L1) return walk_u8_lanes_per_unit_mode<MODE_L1>(c);

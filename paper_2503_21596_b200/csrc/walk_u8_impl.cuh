@@ -108,7 +108,10 @@ __host__ __device__ constexpr int u8_pr() { return MODE == MODE_LD ? (LN_U8_PAIR
 // lanes per unit an instance can run with (the planner picks 2 where the byte guard allows
 // the extra window row, else 1; both instances are compiled for those NW)
 template <int MODE, int NW>
-__host__ __device__ constexpr int u8_lpu_max() { return (U8Layout<MODE, NW>::G == 1 && NW > 32 && LN_U8_LPU2 && u8_pr<MODE>() >= 1) ? 2 : 1; }
+#ifndef LN_U8_LPU_FROM
+#define LN_U8_LPU_FROM 33                // smallest word count with a lane-pair instance
+#endif
+__host__ __device__ constexpr int u8_lpu_max() { return (U8Layout<MODE, NW>::G == 1 && NW >= LN_U8_LPU_FROM && LN_U8_LPU2 && u8_pr<MODE>() >= 1) ? 2 : 1; }
 template <int MODE, int NW, int LPU = 1>
 __host__ __device__ constexpr int u8_units_per_lane() {
   return LPU == 2 ? (NW / 2 <= 8 ? 4 : 2)
@@ -604,8 +607,8 @@ int walk_u8_words_mode<LN_BIN_MODE>(int c) {
   if (nw != LN_U8_ONLY_NW) return 0;
 #endif
   if (nw < 1) return 0;
-  if (nw > 16) nw = (nw + 3) & ~3;
   if (nw > 32) nw = (LN_BIN_MODE != 2 && LN_U8_WIDE_EVEN) ? (nw + 1) & ~1 : (nw + 7) & ~7;
+  else if (nw > 16) nw = (nw + 3) & ~3;
   return nw <= 48 ? nw : 0;
 }
 

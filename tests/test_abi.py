@@ -207,6 +207,17 @@ def test_plan_lane_pairs_for_wide_rows():
     assert L.plan(synth.random_matrix(42, 42, 2))["lanes_per_unit"] == 1
 
 
+def test_plan_byte_walk_word_counts():
+    """Packed words per unit of the byte instance: exact up to 16 words, multiples of 4 up to 32,
+    every even count above (lane pairs: 136 columns run 34 words, not 36 or 40)."""
+    from paper_2503_21596_b200 import synth
+    for c, words in ((42, 11), (61, 16), (66, 20), (72, 20), (128, 32), (132, 34), (136, 34), (144, 36),
+                     (152, 38), (168, 42), (176, 44), (184, 46), (192, 48)):
+        P = L.plan(synth.random_matrix(14, c, 900 + c))
+        assert P["variant_name"] == "bin_u8" and P["words"] == words, (c, P)
+    assert L.plan(synth.random_matrix(14, 14, 3), d=3)["words"] == 0          # other families: 0
+
+
 def test_plan_large_rows_use_byte_walk_and_reach_63_rows():
     """50-56 rows keep the byte walk (more than 2^31 units: coarse keys, up to 2^39 units);
     up to 63 rows plan with at most 31 suffix digits per unit."""

@@ -138,6 +138,7 @@ def test_wide_even_word_instances(lib, marg):
         M = synth.random_matrix(13, c, 40_000 + c + 7 * marg)
         P = lib.plan(M, with_marginals=marg)
         assert P["variant_name"] == "bin_u8" and P["lanes_per_unit"] == 2, (c, P)
+        assert P["words"] == (c + 3) // 4 + ((c + 3) // 4) % 2, (c, P)      # the even word count itself
         check(lib, M, marg=marg)
 
 
