@@ -64,5 +64,52 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return OUT
 
 
+# Self-check build: the byte binary walk compiled with -G (device debug) and
+# LN_SELFCHECK=1 -- every Gray step of unit 0 of every lane is compared with a from-scratch value
+# (walk_u8_impl.cuh) -- for the 13-16-column instance only (LN_U8_ONLY_NW=4, seconds to build);
+# every other translation unit is the product object.  tests/test_gpu_selfcheck.py loads it.
+SELFCHECK_DIR = os.path.join(HERE, "_selfcheck")
+SELFCHECK_OUT = os.path.join(SELFCHECK_DIR, "liblnorm_selfcheck.so")
+SELFCHECK_TUS = {"abi": ["-O3", "-lineinfo", "-DLN_SELFCHECK=1"],
+                 "walk_u8_l1": ["-G", "-DLN_SELFCHECK=1", "-DLN_U8_ONLY_NW=4"],
+                 "walk_u8_marg": ["-G", "-DLN_SELFCHECK=1", "-DLN_U8_ONLY_NW=4"],
+                 "walk_u8_l2": ["-G", "-DLN_SELFCHECK=1", "-DLN_U8_ONLY_NW=4"]}
+
+
+def build_selfcheck(force: bool = False) -> str:
+    build(force=False)
+    os.makedirs(SELFCHECK_DIR, exist_ok=True)
+    sources = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+    headers = glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(ROOT, "include", "*.h"))
+    objs, jobs = [], []
+    for src in sources:
+        base = os.path.basename(src)[:-3]
+        if base in SELFCHECK_TUS:
+            obj = os.path.join(SELFCHECK_DIR, base + ".o")
+            flags = [f for f in FLAGS if f not in ("-O3", "-lineinfo")] + SELFCHECK_TUS[base]
+            if force or _stale(obj, [src] + headers):
+                jobs.append([NVCC] + ARCH + flags + ["-c", src, "-o", obj])
+            objs.append(obj)
+        else:
+            objs.append(os.path.join(BUILD, base + ".o"))
+
+    def run(cmd):
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc failed:\n{r.stderr}")
+
+    with cf.ThreadPoolExecutor(max_workers=max(1, len(jobs))) as ex:
+        list(ex.map(run, jobs))
+    if force or jobs or not os.path.exists(SELFCHECK_OUT) or os.path.getmtime(OUT) > os.path.getmtime(SELFCHECK_OUT):
+        r = subprocess.run([NVCC] + ARCH + ["-shared", "-o", SELFCHECK_OUT + ".tmp"] + objs + ["-ldl", "-lpthread"],
+                           capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"link failed:\n{r.stderr}")
+        os.replace(SELFCHECK_OUT + ".tmp", SELFCHECK_OUT)
+    return SELFCHECK_OUT
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose=True))
+    if "--selfcheck" in sys.argv:
+        print(build_selfcheck(force="--force" in sys.argv))

@@ -812,6 +812,9 @@ int run_device(DevCtx& cx, const int32_t* dIn, const Problem& pr, int rank, int 
     wp.pbits = prefix_bits(pr.dl);
     wp.key_shift = pl.key_shift;
     wp.counter = cx.dCtl; wp.key = cx.dCtl + 1; wp.unit_max = nullptr;
+#if LN_SELFCHECK
+    if (const char* e = getenv("LNORM_SELFCHECK_INJECT")) wp.selfcheck_delta = atoi(e);
+#endif
     CU(cudaEventRecord(cx.ev[1], s));
     if (ck && ck->path && world == 1 && vslices <= 1 && !collective) {
       // ---- checkpointed walk: chunks of the unit list, state persisted after each
@@ -925,6 +928,9 @@ int run_device(DevCtx& cx, const int32_t* dIn, const Problem& pr, int rank, int 
   CU(cudaEventRecord(cx.ev[3], s));
   CU(cudaStreamSynchronize(s));
   if (cx.hCtl[2]) return LNORM_ENCCL;                 // a peer rank failed before the collective
+#if LN_SELFCHECK
+  if (pl.kernel == K_U8 && cx.hCtl[0]) return LNORM_EINTERNAL;   // a step's value differed from scratch
+#endif
   if (!recovery_consistent(cx.hCtl[1], cx.hCtl[3], cx.hCtl[4])) return LNORM_EINTERNAL;
   out->value = cx.hRes[0];
   out->argmax.assign(reinterpret_cast<int8_t*>(cx.hRes + 1), reinterpret_cast<int8_t*>(cx.hRes + 1) + pr.n);
@@ -1044,7 +1050,9 @@ const char* lnorm_status_string(int status) {
   }
 }
 
-int32_t lnorm_version(void) { return (2 << 16) | 0; }   // 2.0: caller-owned NCCL comm + stream in lnorm_compute_rank, EINTERNAL
+// 2.0: caller-owned NCCL comm + stream in lnorm_compute_rank, EINTERNAL; 2.1: lnorm_imma_l1,
+// lnorm_plan_info.words (the former reserved field)
+int32_t lnorm_version(void) { return (2 << 16) | 1; }
 
 int lnorm_compute(const int32_t* M, int32_t n, int32_t m, int32_t d, int32_t with_marginals,
                   int64_t* value, int8_t* argmax) {

@@ -52,6 +52,9 @@ struct WalkParams {
   // re-walks the whole winning group (lex order = unit order, so the smallest group holding
   // an optimum holds the smallest optimal unit)
   int32_t key_shift;
+  // self-check builds (LN_SELFCHECK): added to every from-scratch value before the comparison
+  // (test hook LNORM_SELFCHECK_INJECT: a nonzero delta must make the call fail)
+  int32_t selfcheck_delta;
 };
 
 // Defaults for a single-matrix launch.

@@ -55,6 +55,37 @@ __device__ __forceinline__ uint32_t sad4(uint32_t a, uint32_t b, uint32_t acc) {
   return d;
 }
 
+// Self-check build (`python -m paper_2503_21596_b200.build --selfcheck`): after
+// every Gray step, unit 0 of every lane recomputes its word's NS strategy values FROM SCRATCH
+// (Eq. 1 / Eq. 2 / Eq. 6 over all r rows of the oriented M, no bytes, no Gray state) and counts
+// any difference in p.counter (unused by this kernel otherwise); the host turns a nonzero count
+// into LNORM_EINTERNAL.  The product build compiles it out (LN_SELFCHECK = 0).
+#ifndef LN_SELFCHECK
+#define LN_SELFCHECK 0
+#endif
+
+template <int MODE>
+__device__ int32_t u8_scratch_value(const WalkParams& p, int64_t u, uint32_t w, int PR, int h) {
+  const uint32_t g = w ^ (w >> 1);
+  int32_t val = 0;
+  for (int y = 0; y < p.c; ++y) {
+    int32_t m0 = 0, m1 = 0;                   // L_1 / L_marg: sum a_x M_xy; L_2: the two groups
+    for (int x = 0; x < p.r; ++x) {
+      int dig;
+      if (x <= p.k) dig = prefix_digit(p, u, x);
+      else if (x < p.r - PR) dig = (int)((g >> (p.r - 1 - PR - x)) & 1u);   // walked digit b <-> row r-1-PR-b
+      else dig = (h >> (p.r - 1 - x)) & 1;                                   // paired row r-1-i <-> bit i of h
+      const int32_t v = p.M[(int64_t)x * p.c + y];
+      if (MODE == MODE_LD) { if (dig) m1 += v; else m0 += v; }
+      else m0 += dig ? -v : v;
+    }
+    if (MODE == MODE_LD) val += abs(m0) + abs(m1);
+    else if (MODE == MODE_MARG && y == 0) val += m0;
+    else val += abs(m0);
+  }
+  return val;
+}
+
 template <int MODE, int NW>
 struct U8Layout {
   static constexpr int G = (MODE == MODE_LD) ? 2 : 1;   // bias sets: |m_0| (and |m_1| for L_2)
@@ -153,9 +184,10 @@ struct U8Step {
   static constexpr int NB = NS * G * NW;        // bias words: set h (paired-row signs h) x group
   // One Gray step: add the packed delta record at sbase + off to every unit's bytes,
   // re-accumulate sum |a - B| (and sum |a - B'| for the paired strategy), keep the max.
+  // vout (self-check builds only, LN_SELFCHECK): receives unit 0's NS strategy values of the word
   static __device__ __forceinline__ void run(uint32_t (&A)[P][NW], const uint32_t (&B)[NB],
                                              const uint32_t (&K)[NS], int32_t (&best)[P], uint32_t sbase, int off,
-                                             uint32_t one) {
+                                             uint32_t one, int32_t* vout = nullptr) {
     uint32_t a0[P], a1[P], hs[P][NS][G];
 #pragma unroll
     for (int v = 0; v < RW / 4; ++v) {
@@ -200,6 +232,7 @@ struct U8Step {
         for (int h = 0; h < NS; ++h) {
           v[h] = (G == 2) ? (int32_t)(hs[j][h][0] + hs[j][h][1]) : (int32_t)hs[j][h][0];
           if (LPU == 2) v[h] += __shfl_xor_sync(0xffffffffu, v[h], 1);   // partner lane: other half of the words
+          if (LN_SELFCHECK && j == 0 && vout) vout[h] = v[h];
         }
 #pragma unroll
         for (int h = 0; h < NS; h += 2) best[j] = __vimax3_s32(best[j], v[h], v[h + 1]);
@@ -418,17 +451,36 @@ walk_u8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int3
     }
     // ---- the walk: 2^s - 1 Gray steps (low K digits unrolled, Table 1's ruler pattern)
     for (uint32_t t = 0; t < nblk; ++t) {
+#if LN_SELFCHECK
+      int32_t vchk[NS];
+      const int64_t u0 = [&] { int64_t u = g * P; return (u < p.unit_begin || u >= u_end) ? uh : u; }();
+      auto check = [&](uint32_t w) {
+        if (BAT) return;                           // (batched instances: not self-checked)
+        for (int h = 0; h < NS; ++h)
+          if (u8_scratch_value<MODE>(p, u0, w, PR, h) + p.selfcheck_delta != vchk[h]) atomicAdd(p.counter, 1ull);
+      };
+#endif
       if (t != 0) {                                    // block start: digit K + ctz(t)
         const int tz = __ffs((int)t) - 1;
         const int b = K + tz;
         const int sg = 1 ^ (int)((t >> (tz + 1)) & 1u);
+#if LN_SELFCHECK
+        STEP::run(A, B, Kc, best, sbase, (2 * b + sg) * RREC + half * RWL, p.one, vchk);
+        check(t << K);
+#else
         STEP::run(A, B, Kc, best, sbase, (2 * b + sg) * RREC + half * RWL, p.one);
+#endif
       }
 #pragma unroll
       for (int jj = 1; jj < (1 << K); ++jj) {
         const int b = u8_cctz(jj);
         const int sg = (b < K - 1) ? (1 ^ ((jj >> (b + 1)) & 1)) : (1 ^ (int)(t & 1u));
+#if LN_SELFCHECK
+        STEP::run(A, B, Kc, best, sbase, (2 * b + sg) * RREC + half * RWL, p.one, vchk);
+        check((t << K) | (uint32_t)jj);
+#else
         STEP::run(A, B, Kc, best, sbase, (2 * b + sg) * RREC + half * RWL, p.one);
+#endif
       }
     }
 #pragma unroll
