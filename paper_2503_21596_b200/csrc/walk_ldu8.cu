@@ -9,17 +9,19 @@ namespace lnorm {
 
 namespace {
 int part_of(int NW) { return NW <= 6 ? 0 : 1; }
+// paired rows of the all-H kernel when the suffix allows (LNORM_LDU8W_PR caps it: A/B)
+constexpr int kLdu8wMaxRows = 5;
 
 // Paired rows of the all-H L_3 kernel (walk_ldu8w_impl.cuh) for a unit of s suffix digits:
-// 4 when at least one walked digit remains, 3 at s = 4, else 0 (the all-E kernel runs).
-// LNORM_LDU8W=0 disables it (A/B); LNORM_LDU8W_PR=3 caps it at three paired rows.
+// 5 when at least two walked digits remain, 4 with one, 3 at s = 4, else 0 (the all-E kernel runs).
+// LNORM_LDU8W=0 disables it (A/B); LNORM_LDU8W_PR=3 or 4 caps the paired rows.
 int ldu8w_rows(int d, int s) {
   if (d != 3) return 0;
   const char* em = getenv("LNORM_LDU8W");
   const char* ec = getenv("LNORM_LDU8W_PR");
-  const int mode = (em && *em) ? atoi(em) : 1, cap = (ec && *ec) ? atoi(ec) : 4;
+  const int mode = (em && *em) ? atoi(em) : 1, cap = (ec && *ec) ? atoi(ec) : kLdu8wMaxRows;
   if (!mode) return 0;
-  const int pr = s >= 5 ? 4 : (s == 4 ? 3 : 0);
+  const int pr = s >= 7 ? 5 : s >= 5 ? 4 : (s == 4 ? 3 : 0);
   return std::min(pr, cap) >= 3 ? std::min(pr, cap) : 0;
 }
 }  // namespace

@@ -43,13 +43,23 @@ namespace lnorm {
 namespace {
 
 constexpr int kBlockW = 32;
+// most paired rows an instance is compiled for (5: 243 labellings per walked word, 2 x 32 bias
+// sums per move; 4: 81, 2 x 16)
+#ifndef LN_LDU8W_MAXPR
+#define LN_LDU8W_MAXPR 5
+#endif
 // resident warps per SM asked of ptxas: 16 (<= 128 registers, four warps per SMSP) where that
 // needs no spills (every instance but NW = 10 and 12 at PR = 4), else 12
 #ifndef LN_LDU8W_MINB
 #define LN_LDU8W_MINB 16
 #endif
 template <int NW, int PR>
-__host__ __device__ constexpr int w_minb() { return (PR == 4 && (NW == 10 || NW == 12)) ? 12 : LN_LDU8W_MINB; }
+#ifndef LN_LDU8W_MINB5
+#define LN_LDU8W_MINB5 12                // five paired rows: 96 H sums per unit, <= 168 registers
+#endif
+__host__ __device__ constexpr int w_minb() {
+  return PR == 5 ? LN_LDU8W_MINB5 : (PR == 4 && (NW == 10 || NW == 12)) ? 12 : LN_LDU8W_MINB;
+}
 constexpr int kTabWordsW = 16384;
 
 __host__ __device__ constexpr int w_pad4(int x) { return (x + 3) & ~3; }
@@ -459,6 +469,9 @@ int occ_w(int s) {
 template <>
 cudaError_t walk_ldu8w_launch_part<LN_LDU8W_PART>(const WalkParams& p, const uint32_t* tab, const int32_t* init, int grid,
                                                    cudaStream_t st, int NW, int pr) {
+#if LN_LDU8W_MAXPR >= 5
+  if (pr == 5) { LN_LDU8W_SWITCH(NW, launch_w, 5, p, tab, init, grid, st) }
+#endif
   if (pr == 4) { LN_LDU8W_SWITCH(NW, launch_w, 4, p, tab, init, grid, st) }
   else if (pr == 3) { LN_LDU8W_SWITCH(NW, launch_w, 3, p, tab, init, grid, st) }
   return cudaErrorInvalidValue;
@@ -469,6 +482,9 @@ int upl_w() { return w_units<NW, PR>(); }
 
 template <>
 int walk_ldu8w_upl_part<LN_LDU8W_PART>(int NW, int pr) {
+#if LN_LDU8W_MAXPR >= 5
+  if (pr == 5) { LN_LDU8W_SWITCH(NW, upl_w, 5) }
+#endif
   if (pr == 4) { LN_LDU8W_SWITCH(NW, upl_w, 4) }
   else if (pr == 3) { LN_LDU8W_SWITCH(NW, upl_w, 3) }
   return 1;
@@ -476,6 +492,9 @@ int walk_ldu8w_upl_part<LN_LDU8W_PART>(int NW, int pr) {
 
 template <>
 int walk_ldu8w_occ_part<LN_LDU8W_PART>(int NW, int pr, int s) {
+#if LN_LDU8W_MAXPR >= 5
+  if (pr == 5) { LN_LDU8W_SWITCH(NW, occ_w, 5, s) }
+#endif
   if (pr == 4) { LN_LDU8W_SWITCH(NW, occ_w, 4, s) }
   else if (pr == 3) { LN_LDU8W_SWITCH(NW, occ_w, 3, s) }
   return 0;
