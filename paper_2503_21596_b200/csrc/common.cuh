@@ -243,12 +243,13 @@ template <int D, int PART> int walk_ldu8_upl_part(int NW, int s);
 template <int D, int PART> int walk_ldu8_occ_part(int NW, int s);
 template <int D, int PART> cudaError_t walk_ldu8_launch_part(const WalkParams& p, const uint32_t* tab, const int32_t* init,
                                                              int grid, cudaStream_t st, int NW);
-// Byte-packed L_3 walk, 3 or 4 paired rows, all-H form, bias words in shared memory
-// (walk_ldu8w_impl.cuh); dispatched by walk_ldu8_launch when d = 3 and the suffix allows.
-template <int PART> cudaError_t walk_ldu8w_launch_part(const WalkParams& p, const uint32_t* tab, const int32_t* init,
-                                                       int grid, cudaStream_t st, int NW, int pr);
-template <int PART> int walk_ldu8w_occ_part(int NW, int pr, int s);
-template <int PART> int walk_ldu8w_upl_part(int NW, int pr);
+// Byte-packed L_3 / L_4 walk, 3-5 paired rows, all-H form, bias words in shared memory
+// (walk_ldu8w_impl.cuh); dispatched by walk_ldu8_launch for L_3 and L_4 when the suffix allows.
+template <int D, int PART> cudaError_t walk_ldu8w_launch_part(const WalkParams& p, const uint32_t* tab,
+                                                              const int32_t* init, int grid, cudaStream_t st, int NW,
+                                                              int pr);
+template <int D, int PART> int walk_ldu8w_occ_part(int NW, int pr, int s);
+template <int D, int PART> int walk_ldu8w_upl_part(int NW, int pr);
 // Generic warp-per-unit walk (any mode, d, c, s).
 bool walk_generic_supported(int d, int c);
 cudaError_t walk_generic_launch(const WalkParams& p, int grid, cudaStream_t st, int* block_out);

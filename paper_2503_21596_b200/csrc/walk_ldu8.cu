@@ -12,16 +12,17 @@ int part_of(int NW) { return NW <= 6 ? 0 : 1; }
 // paired rows of the all-H kernel when the suffix allows (LNORM_LDU8W_PR caps it: A/B)
 constexpr int kLdu8wMaxRows = 5;
 
-// Paired rows of the all-H L_3 kernel (walk_ldu8w_impl.cuh) for a unit of s suffix digits:
-// 5 when at least two walked digits remain, 4 with one, 3 at s = 4, else 0 (the all-E kernel runs).
+// Paired rows of the all-H L_3 / L_4 kernel (walk_ldu8w_impl.cuh) for a unit of s suffix digits:
+// 5 (L_3 only) when at least two walked digits remain, 4 with one, 3 at s = 4, else 0 (the all-E
+// kernel runs).
 // LNORM_LDU8W=0 disables it (A/B); LNORM_LDU8W_PR=3 or 4 caps the paired rows.
 int ldu8w_rows(int d, int s) {
-  if (d != 3) return 0;
+  if (d != 3 && d != 4) return 0;
   const char* em = getenv("LNORM_LDU8W");
   const char* ec = getenv("LNORM_LDU8W_PR");
   const int mode = (em && *em) ? atoi(em) : 1, cap = (ec && *ec) ? atoi(ec) : kLdu8wMaxRows;
   if (!mode) return 0;
-  const int pr = s >= 7 ? 5 : s >= 5 ? 4 : (s == 4 ? 3 : 0);
+  const int pr = (s >= 7 && d == 3) ? 5 : s >= 5 ? 4 : (s == 4 ? 3 : 0);
   return std::min(pr, cap) >= 3 ? std::min(pr, cap) : 0;
 }
 }  // namespace
@@ -46,7 +47,10 @@ void walk_ldu8_table_sizes(int d, int c, int k, int s, int64_t* tab_words, int64
 
 int walk_ldu8_units_per_lane(int d, int c, int s) {
   const int NW = words_of(c), pt = part_of(NW);
-  if (const int wr = ldu8w_rows(d, s)) return pt ? walk_ldu8w_upl_part<1>(NW, wr) : walk_ldu8w_upl_part<0>(NW, wr);
+  if (const int wr = ldu8w_rows(d, s)) {
+    if (d == 4) return pt ? walk_ldu8w_upl_part<4, 1>(NW, wr) : walk_ldu8w_upl_part<4, 0>(NW, wr);
+    return pt ? walk_ldu8w_upl_part<3, 1>(NW, wr) : walk_ldu8w_upl_part<3, 0>(NW, wr);
+  }
   if (d == 3) return pt ? walk_ldu8_upl_part<3, 1>(NW, s) : walk_ldu8_upl_part<3, 0>(NW, s);
   if (d == 4) return pt ? walk_ldu8_upl_part<4, 1>(NW, s) : walk_ldu8_upl_part<4, 0>(NW, s);
   return 1;
@@ -55,7 +59,10 @@ int walk_ldu8_units_per_lane(int d, int c, int s) {
 int walk_ldu8_occupancy(int d, int c, int s, int* block_out) {
   *block_out = kBlockLU;
   const int NW = words_of(c), pt = part_of(NW);
-  if (const int wr = ldu8w_rows(d, s)) return pt ? walk_ldu8w_occ_part<1>(NW, wr, s) : walk_ldu8w_occ_part<0>(NW, wr, s);
+  if (const int wr = ldu8w_rows(d, s)) {
+    if (d == 4) return pt ? walk_ldu8w_occ_part<4, 1>(NW, wr, s) : walk_ldu8w_occ_part<4, 0>(NW, wr, s);
+    return pt ? walk_ldu8w_occ_part<3, 1>(NW, wr, s) : walk_ldu8w_occ_part<3, 0>(NW, wr, s);
+  }
   if (d == 3) return pt ? walk_ldu8_occ_part<3, 1>(NW, s) : walk_ldu8_occ_part<3, 0>(NW, s);
   if (d == 4) return pt ? walk_ldu8_occ_part<4, 1>(NW, s) : walk_ldu8_occ_part<4, 0>(NW, s);
   return 0;
@@ -73,8 +80,10 @@ cudaError_t walk_ldu8_launch(const WalkParams& p, int32_t* scratch_tab, int32_t*
                                              p.tab_stride, p.init_stride);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  if (wr) return pt ? walk_ldu8w_launch_part<1>(p, tab, scratch_init, grid, st, NW, wr)
-                    : walk_ldu8w_launch_part<0>(p, tab, scratch_init, grid, st, NW, wr);
+  if (wr && p.d == 4) return pt ? walk_ldu8w_launch_part<4, 1>(p, tab, scratch_init, grid, st, NW, wr)
+                                : walk_ldu8w_launch_part<4, 0>(p, tab, scratch_init, grid, st, NW, wr);
+  if (wr) return pt ? walk_ldu8w_launch_part<3, 1>(p, tab, scratch_init, grid, st, NW, wr)
+                    : walk_ldu8w_launch_part<3, 0>(p, tab, scratch_init, grid, st, NW, wr);
   if (p.d == 3) return pt ? walk_ldu8_launch_part<3, 1>(p, tab, scratch_init, grid, st, NW)
                           : walk_ldu8_launch_part<3, 0>(p, tab, scratch_init, grid, st, NW);
   if (p.d == 4) return pt ? walk_ldu8_launch_part<4, 1>(p, tab, scratch_init, grid, st, NW)

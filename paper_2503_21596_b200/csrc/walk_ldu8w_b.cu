@@ -1,3 +1,4 @@
-// Byte-packed L_3 walk with 3-4 paired rows in the all-H form, 7-12 packed words (walk_ldu8w_impl.cuh).
+// Byte-packed L_3 walk with 3-5 paired rows in the all-H form, 7-12 packed words (walk_ldu8w_impl.cuh).
+#define LN_LDU8W_D 3
 #define LN_LDU8W_PART 1
 #include "walk_ldu8w_impl.cuh"

@@ -49,29 +49,30 @@ constexpr int kBlockW = 32;
 #define LN_LDU8W_MAXPR 5
 #endif
 // resident warps per SM asked of ptxas: 16 (<= 128 registers, four warps per SMSP) where that
-// needs no spills (every instance but NW = 10 and 12 at PR = 4), else 12
+// needs no spills (L_3 up to four paired rows except NW = 10 and 12), else 12 (<= 168 registers:
+// L_3 with five paired rows, 96 H sums per unit; L_4 with four, 64 H sums + the convolution levels)
 #ifndef LN_LDU8W_MINB
 #define LN_LDU8W_MINB 16
 #endif
-template <int NW, int PR>
 #ifndef LN_LDU8W_MINB5
-#define LN_LDU8W_MINB5 12                // five paired rows: 96 H sums per unit, <= 168 registers
+#define LN_LDU8W_MINB5 12
 #endif
+template <int D, int NW, int PR>
 __host__ __device__ constexpr int w_minb() {
-  return PR == 5 ? LN_LDU8W_MINB5 : (PR == 4 && (NW == 10 || NW == 12)) ? 12 : LN_LDU8W_MINB;
+  return (PR == 5 || (D == 4 && PR >= 4)) ? LN_LDU8W_MINB5 : (PR == 4 && (NW == 10 || NW == 12)) ? 12 : LN_LDU8W_MINB;
 }
 constexpr int kTabWordsW = 16384;
 
 __host__ __device__ constexpr int w_pad4(int x) { return (x + 3) & ~3; }
-__host__ __device__ constexpr int w_pow3(int e) { return e == 0 ? 1 : 3 * w_pow3(e - 1); }
+__host__ __device__ constexpr int w_pow(int d, int e) { return e == 0 ? 1 : d * w_pow(d, e - 1); }
 __host__ __device__ constexpr int w_popc(int x) { return x == 0 ? 0 : (x & 1) + w_popc(x >> 1); }
 // the i-th submask of U in increasing order (i < 2^popc(U)): bit j of i -> j-th set bit of U
 __host__ __device__ constexpr int w_submask(int U, int i) {
   return U == 0 ? 0 : ((U & 1) ? ((i & 1) | (w_submask(U >> 1, i >> 1) << 1)) : (w_submask(U >> 1, i) << 1));
 }
-// bitmask of the paired rows labelled g in labelling L (base-3 digits of L, paired row b = digit b)
-__host__ __device__ constexpr int w_mask(int L, int g, int PR) {
-  return PR == 0 ? 0 : ((L % 3 == g) ? 1 : 0) | (w_mask(L / 3, g, PR - 1) << 1);
+// bitmask of the paired rows labelled g in labelling L (base-D digits of L, paired row b = digit b)
+__host__ __device__ constexpr int w_mask(int L, int g, int PR, int D) {
+  return PR == 0 ? 0 : ((L % D == g) ? 1 : 0) | (w_mask(L / D, g, PR - 1, D) << 1);
 }
 
 __device__ __forceinline__ uint32_t w_sad4(uint32_t a, uint32_t b, uint32_t acc) {
@@ -141,65 +142,77 @@ __device__ __forceinline__ int32_t w_max_tree(const int32_t (&v)[N]) {
   }
 }
 
-template <int NW, int PR>
+template <int D, int NW, int PR>
 struct LdW {
   static constexpr int RW = w_pad4(NW);
   static constexpr int RD = 2 * RW;          // delta record: +row at [0, NW), -row at [RW, RW + NW)
   static constexpr int NS = 1 << PR;         // bias sets (subsets of the paired rows)
-  static constexpr int NL = w_pow3(PR);      // labellings of the paired rows
+  static constexpr int NL = w_pow(D, PR);    // labellings of the paired rows
 
-  // the value of labelling L: H[T_0][0] + H[T_1][1] + H[T_2][2] (masks forced to compile time)
+  // Direct form (LN_LDU8W_CONV = 0, L_3 only): the value of labelling L is
+  // sum_g H[T_g][g] (masks forced to compile time), D - 1 FADD per labelling.
   template <int L>
-  static __device__ __forceinline__ int32_t cand(const int32_t (&H)[NS][3], uint32_t one) {
-    constexpr int m0 = std::integral_constant<int, w_mask(L, 0, PR)>::value;
-    constexpr int m1 = std::integral_constant<int, w_mask(L, 1, PR)>::value;
-    constexpr int m2 = std::integral_constant<int, w_mask(L, 2, PR)>::value;
+  static __device__ __forceinline__ int32_t cand(const int32_t (&H)[NS][D], uint32_t one) {
+    constexpr int m0 = std::integral_constant<int, w_mask(L, 0, PR, D)>::value;
+    constexpr int m1 = std::integral_constant<int, w_mask(L, 1, PR, D)>::value;
+    constexpr int m2 = std::integral_constant<int, w_mask(L, 2, PR, D)>::value;
     return w_fadd(w_fadd(H[m0][0], H[m1][1], one), H[m2][2], one);
   }
   template <int... Ls>
-  static __device__ __forceinline__ int32_t best_seq(const int32_t (&H)[NS][3], int32_t best, uint32_t one,
+  static __device__ __forceinline__ int32_t best_seq(const int32_t (&H)[NS][D], int32_t best, uint32_t one,
                                                      std::integer_sequence<int, Ls...>) {
     int32_t v[NL + 1] = {cand<Ls>(H, one)..., best};
     return w_max_tree<NL + 1>(v);
   }
-  // Max-plus subset convolution form of the same maximum (LN_LDU8W_CONV = 1): with
-  //     F(U) = max over T0 subset of U of  H[T0][0] + H[U \ T0][1]
-  // the best labelling is  max over T2 of  H[T2][2] + F(complement of T2)  -- the 3^PR
-  // labellings split by their label-2 set T2.  Additions: sum_U 2^|U| = 3^PR for the F(U) plus
-  // 2^PR for the last step (97 FADD at PR = 4 instead of 2 * 81 = 162), the maxes about the same
-  // (the kernel is issue-bound, so the 65 saved FMA-pipe instructions per move are time).
-  template <int U, int I>
-  static __device__ __forceinline__ int32_t conv_term(const int32_t (&H)[NS][3], uint32_t one) {
-    constexpr int T0 = std::integral_constant<int, w_submask(U, I)>::value;
-    return w_fadd(H[T0][0], H[U ^ T0][1], one);
+  // Max-plus subset convolution form of the same maximum (LN_LDU8W_CONV = 1).  A labelling of the
+  // paired rows is a partition (T_0, .., T_{D-1}) of them by label, valued sum_g H[T_g][g]; with
+  //     G_1(U) = H[U][0],   G_{g+1}(U) = max over T subset of U of  H[T][g] + G_g(U \ T)
+  // the best labelling is G_D(all paired rows).  Additions: 3^PR per intermediate level (sum over
+  // U of 2^|U|) plus 2^PR for the last one -- L_3, PR = 4: 97 FADD instead of 2 * 81 = 162; L_4,
+  // PR = 4: 178 instead of 3 * 256 = 768 -- with about as many maxes as the direct form.
+  template <int G, int U, int I>
+  static __device__ __forceinline__ int32_t lvl_term(const int32_t (&H)[NS][D], const int32_t (&Gp)[NS], uint32_t one) {
+    constexpr int T = std::integral_constant<int, w_submask(U, I)>::value;
+    return w_fadd(H[T][G], Gp[U ^ T], one);
   }
-  template <int U, int... Is>
-  static __device__ __forceinline__ int32_t conv_F(const int32_t (&H)[NS][3], uint32_t one,
-                                                   std::integer_sequence<int, Is...>) {
-    int32_t v[sizeof...(Is)] = {conv_term<U, Is>(H, one)...};
+  template <int G, int U, int... Is>
+  static __device__ __forceinline__ int32_t lvl_U(const int32_t (&H)[NS][D], const int32_t (&Gp)[NS], uint32_t one,
+                                                  std::integer_sequence<int, Is...>) {
+    int32_t v[sizeof...(Is)] = {lvl_term<G, U, Is>(H, Gp, one)...};
     return w_max_tree<(int)sizeof...(Is)>(v);
   }
-  template <int T2>
-  static __device__ __forceinline__ int32_t conv_last(const int32_t (&H)[NS][3], uint32_t one) {
-    constexpr int U = (NS - 1) ^ T2;
-    return w_fadd(H[T2][2], conv_F<U>(H, one, std::make_integer_sequence<int, (1 << w_popc(U))>{}), one);
+  template <int G, int... Us>
+  static __device__ __forceinline__ void lvl_all(const int32_t (&H)[NS][D], const int32_t (&Gp)[NS], int32_t (&Gn)[NS],
+                                                 uint32_t one, std::integer_sequence<int, Us...>) {
+    ((Gn[Us] = lvl_U<G, Us>(H, Gp, one, std::make_integer_sequence<int, (1 << w_popc(Us))>{})), ...);
   }
-  template <int... T2s>
-  static __device__ __forceinline__ int32_t conv_best(const int32_t (&H)[NS][3], int32_t best, uint32_t one,
-                                                      std::integer_sequence<int, T2s...>) {
-    int32_t v[NS + 1] = {conv_last<T2s>(H, one)..., best};
-    return w_max_tree<NS + 1>(v);
+  template <int G, int... Is>
+  static __device__ __forceinline__ int32_t lvl_last(const int32_t (&H)[NS][D], const int32_t (&Gp)[NS], int32_t best,
+                                                     uint32_t one, std::integer_sequence<int, Is...>) {
+    int32_t v[sizeof...(Is) + 1] = {lvl_term<G, NS - 1, Is>(H, Gp, one)..., best};   // U = all paired rows
+    return w_max_tree<(int)sizeof...(Is) + 1>(v);
+  }
+  static __device__ __forceinline__ int32_t conv_best(const int32_t (&H)[NS][D], int32_t best, uint32_t one) {
+    int32_t G1[NS], G2[NS];
+#pragma unroll
+    for (int m = 0; m < NS; ++m) G1[m] = H[m][0];
+    lvl_all<1>(H, G1, G2, one, std::make_integer_sequence<int, NS>{});
+    if constexpr (D == 3) {
+      return lvl_last<2>(H, G2, best, one, std::make_integer_sequence<int, NS>{});
+    } else {
+      int32_t G3[NS];
+      lvl_all<2>(H, G2, G3, one, std::make_integer_sequence<int, NS>{});
+      return lvl_last<3>(H, G3, best, one, std::make_integer_sequence<int, NS>{});
+    }
   }
   // max(best, every labelling's value of the current word)
-  static __device__ __forceinline__ int32_t best_of(const int32_t (&H)[NS][3], int32_t best, uint32_t one) {
+  static __device__ __forceinline__ int32_t best_of(const int32_t (&H)[NS][D], int32_t best, uint32_t one) {
 #ifndef LN_LDU8W_CONV
 #define LN_LDU8W_CONV 1
 #endif
-#if LN_LDU8W_CONV
-    return conv_best(H, best, one, std::make_integer_sequence<int, NS>{});
-#else
-    return best_seq(H, best, one, std::make_integer_sequence<int, NL>{});
-#endif
+    static_assert(D == 3 || D == 4, "L_3 and L_4");
+    if constexpr (LN_LDU8W_CONV || D != 3) return conv_best(H, best, one);
+    else return best_seq(H, best, one, std::make_integer_sequence<int, NL>{});
   }
 
   // A move between groups GA < GB (either direction): the lower group adds the packed row at
@@ -212,7 +225,7 @@ struct LdW {
   // operand A[g][i] (operand reuse cache), so each reads two registers (bias word, accumulator)
   // instead of three; the register-file read ports, not the ALU pipe, bound a 3-source mix.
   template <int GA, int GB, int P>
-  static __device__ __forceinline__ void sums(uint32_t (&A)[P][3][NW], int32_t (&H)[P][NS][3], const uint32_t (&Ks)[NS],
+  static __device__ __forceinline__ void sums(uint32_t (&A)[P][D][NW], int32_t (&H)[P][NS][D], const uint32_t (&Ks)[NS],
                                               uint32_t rowA, uint32_t rowB, uint32_t sbias) {
 #ifndef LN_LDU8W_HB
 #define LN_LDU8W_HB 8
@@ -270,10 +283,10 @@ struct LdW {
 template <int NW, int PR>
 __host__ __device__ constexpr int w_units() { return (NW <= 6) ? LN_LDU8W_P : 1; }
 
-template <int NW, int PR, bool BAT = false>
-__global__ void __launch_bounds__(kBlockW, (w_minb<NW, PR>()))
+template <int D, int NW, int PR, bool BAT = false>
+__global__ void __launch_bounds__(kBlockW, (w_minb<D, NW, PR>()))
 walk_ldu8w_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int32_t* __restrict__ gInit) {
-  using WK = LdW<NW, PR>;
+  using WK = LdW<D, NW, PR>;
   constexpr int P = w_units<NW, PR>();
   constexpr int RD = WK::RD, RW = WK::RW, CW = 4 * NW, NS = WK::NS;
   extern __shared__ __align__(16) uint32_t sT[];
@@ -290,7 +303,7 @@ walk_ldu8w_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const i
 #endif
   uint32_t Ks[NS];
   uint32_t nwords = 1;
-  for (int i = 0; i < sw; ++i) nwords *= 3;
+  for (int i = 0; i < sw; ++i) nwords *= D;
   int32_t best_all = INT32_MIN;
   uint32_t best_u = 0;
   bool have = false;
@@ -336,12 +349,12 @@ walk_ldu8w_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const i
     }
     const int32_t* baseRec = gI + (p.k + 1) * CW;
     const int32_t* negRec = baseRec + CW;
-    uint32_t A[P][3][NW];
-    int32_t H[P][NS][3];
+    uint32_t A[P][D][NW];
+    int32_t H[P][NS][D];
     int32_t best[P];
 #pragma unroll
     for (int j = 0; j < P; ++j) {
-      // ---- unit init: prefix labels -> the three groups' bytes at the start word (suffix all 0)
+      // ---- unit init: prefix labels -> the D groups' bytes at the start word (suffix all 0)
       const int64_t rel = lc * 32 * P + j * 32 + lane;
       const int64_t u = p.unit_begin + (rel < p.units_per ? rel : 0);
       uint64_t lab = 0;
@@ -350,27 +363,27 @@ walk_ldu8w_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const i
       const uint64_t lmask = (1ull << p.pbits) - 1ull;
 #pragma unroll
       for (int q = 0; q < NW; ++q) {
-        int32_t a[3][4];
+        int32_t a[D][4];
 #pragma unroll
-        for (int g = 0; g < 3; ++g)
+        for (int g = 0; g < D; ++g)
 #pragma unroll
           for (int e = 0; e < 4; ++e) a[g][e] = __ldg(negRec + 4 * q + e) + (g == 0 ? __ldg(baseRec + 4 * q + e) : 0);
         for (int x = 0; x <= p.k; ++x) {
           const int dig = (int)((lab >> (p.pbits * x)) & lmask);
           const int4 v = __ldg(reinterpret_cast<const int4*>(gI + x * CW) + q);
 #pragma unroll
-          for (int g = 0; g < 3; ++g) {
+          for (int g = 0; g < D; ++g) {
             const int32_t f = dig == g ? 1 : 0;
             a[g][0] += f * v.x; a[g][1] += f * v.y; a[g][2] += f * v.z; a[g][3] += f * v.w;
           }
         }
 #pragma unroll
-        for (int g = 0; g < 3; ++g)
+        for (int g = 0; g < D; ++g)
           A[j][g][q] = (uint32_t)(a[g][0] & 0xFF) | ((uint32_t)(a[g][1] & 0xFF) << 8) |
                        ((uint32_t)(a[g][2] & 0xFF) << 16) | ((uint32_t)(a[g][3] & 0xFF) << 24);
       }
 #pragma unroll
-      for (int g = 0; g < 3; ++g)
+      for (int g = 0; g < D; ++g)
 #pragma unroll
         for (int m = 0; m < NS; ++m) {
           uint32_t h = Ks[m];
@@ -380,26 +393,28 @@ walk_ldu8w_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const i
         }
       best[j] = WK::best_of(H[j], 0, p.one);          // every value is >= 0 (a sum of |.|)
     }
-    // ---- the walk: words 1 .. 3^sw - 1, one dispatch site for the four move cases
+    // ---- the walk: words 1 .. D^sw - 1, one dispatch site per pair of adjacent labels
     uint32_t t = 0, jj = 0;
     for (uint32_t w = 1; w < nwords; ++w) {
       uint32_t i, from, to;
-      if (++jj == 3) { jj = 0; ++t; }
+      if (++jj == D) { jj = 0; ++t; }
       if (jj == 0) {
-        dary_block_start<3>(t, &i, &from, &to);
-      } else {
+        dary_block_start<D>(t, &i, &from, &to);
+      } else {                                       // low digit: 0 -> D-1 (even block) or back (odd)
         i = 0;
         const bool odd = (t & 1u) != 0;
-        from = odd ? 3 - jj : jj - 1;
-        to = odd ? 2 - jj : jj;
+        from = odd ? D - jj : jj - 1;
+        to = odd ? D - 1 - jj : jj;
       }
       // walked digit i's delta record: +row at srow, -row at srow + 4 RW bytes; the group the
       // row leaves (from) adds the -row, the group it joins (to) the +row
       const uint32_t srow = sbase + 4u * i * (uint32_t)RD;
       const uint32_t rlo = from < to ? srow + 4u * (uint32_t)RW : srow;   // row for the lower group
       const uint32_t rhi = from < to ? srow : srow + 4u * (uint32_t)RW;   // row for the higher group
-      if (from + to == 1) WK::template sums<0, 1, P>(A, H, Ks, rlo, rhi, sbias);
-      else WK::template sums<1, 2, P>(A, H, Ks, rlo, rhi, sbias);
+      const uint32_t lo = from < to ? from : to;       // the move is between labels lo and lo + 1
+      if (lo == 0) WK::template sums<0, 1, P>(A, H, Ks, rlo, rhi, sbias);
+      else if (D == 3 || lo == 1) WK::template sums<1, 2, P>(A, H, Ks, rlo, rhi, sbias);
+      else if constexpr (D >= 4) WK::template sums<2, 3, P>(A, H, Ks, rlo, rhi, sbias);
 #pragma unroll
       for (int j = 0; j < P; ++j) best[j] = WK::best_of(H[j], best[j], p.one);
     }
@@ -420,83 +435,84 @@ walk_ldu8w_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const i
 template <int NW, int PR>
 size_t w_smem(int s) { return sizeof(uint32_t) * (size_t)((s - PR) * 2 * w_pad4(NW) + (1 << PR) * NW); }
 
-template <int NW, int PR>
+template <int D, int NW, int PR>
 cudaError_t launch_w(const WalkParams& p, const uint32_t* tab, const int32_t* init, int grid, cudaStream_t st) {
   const size_t sm = w_smem<NW, PR>(p.s);
   if (p.batch > 1) {                     // batched instances: <= 24 columns (the small-matrix regime)
     if constexpr (NW <= 6) {
-      cudaError_t e = ensure_dyn_smem((const void*)walk_ldu8w_kernel<NW, PR, true>, sm);
+      cudaError_t e = ensure_dyn_smem((const void*)walk_ldu8w_kernel<D, NW, PR, true>, sm);
       if (e != cudaSuccess) return e;
-      walk_ldu8w_kernel<NW, PR, true><<<grid, kBlockW, sm, st>>>(p, tab, init);
+      walk_ldu8w_kernel<D, NW, PR, true><<<grid, kBlockW, sm, st>>>(p, tab, init);
       return cudaGetLastError();
     }
     return cudaErrorInvalidValue;
   }
-  cudaError_t e = ensure_dyn_smem((const void*)walk_ldu8w_kernel<NW, PR>, sm);
+  cudaError_t e = ensure_dyn_smem((const void*)walk_ldu8w_kernel<D, NW, PR>, sm);
   if (e != cudaSuccess) return e;
-  walk_ldu8w_kernel<NW, PR><<<grid, kBlockW, sm, st>>>(p, tab, init);
+  walk_ldu8w_kernel<D, NW, PR><<<grid, kBlockW, sm, st>>>(p, tab, init);
   return cudaGetLastError();
 }
 
-template <int NW, int PR>
+template <int D, int NW, int PR>
 int occ_w(int s) {
   const size_t sm = w_smem<NW, PR>(s);
-  const int nb = occupancy_cached((const void*)walk_ldu8w_kernel<NW, PR>, kBlockW, sm);
+  const int nb = occupancy_cached((const void*)walk_ldu8w_kernel<D, NW, PR>, kBlockW, sm);
   return nb;
 }
+
+template <int D, int NW, int PR>
+int upl_w() { return w_units<NW, PR>(); }
 
 }  // namespace
 
 #ifdef LN_LDU8W_PART
-// part 0: 1-6 packed words (<= 24 columns), part 1: 7-12
+// One translation unit per label count (LN_LDU8W_D) and half of the column range
+// (LN_LDU8W_PART 0: 1-6 packed words, <= 24 columns; 1: 7-12), compiled in parallel.
 #define LN_LDU8W_SWITCH(NW_, FN, PR, ...)                                                          \
   if constexpr (LN_LDU8W_PART == 0) {                                                              \
     switch (NW_) {                                                                                 \
-      case 1: return FN<1, PR>(__VA_ARGS__); case 2: return FN<2, PR>(__VA_ARGS__);                \
-      case 3: return FN<3, PR>(__VA_ARGS__); case 4: return FN<4, PR>(__VA_ARGS__);                \
-      case 5: return FN<5, PR>(__VA_ARGS__); case 6: return FN<6, PR>(__VA_ARGS__);                \
+      case 1: return FN<LN_LDU8W_D, 1, PR>(__VA_ARGS__); case 2: return FN<LN_LDU8W_D, 2, PR>(__VA_ARGS__); \
+      case 3: return FN<LN_LDU8W_D, 3, PR>(__VA_ARGS__); case 4: return FN<LN_LDU8W_D, 4, PR>(__VA_ARGS__); \
+      case 5: return FN<LN_LDU8W_D, 5, PR>(__VA_ARGS__); case 6: return FN<LN_LDU8W_D, 6, PR>(__VA_ARGS__); \
       default: break;                                                                              \
     }                                                                                              \
   } else {                                                                                         \
     switch (NW_) {                                                                                 \
-      case 7: return FN<7, PR>(__VA_ARGS__);   case 8: return FN<8, PR>(__VA_ARGS__);              \
-      case 9: return FN<9, PR>(__VA_ARGS__);   case 10: return FN<10, PR>(__VA_ARGS__);            \
-      case 11: return FN<11, PR>(__VA_ARGS__); case 12: return FN<12, PR>(__VA_ARGS__);            \
+      case 7: return FN<LN_LDU8W_D, 7, PR>(__VA_ARGS__);   case 8: return FN<LN_LDU8W_D, 8, PR>(__VA_ARGS__);   \
+      case 9: return FN<LN_LDU8W_D, 9, PR>(__VA_ARGS__);   case 10: return FN<LN_LDU8W_D, 10, PR>(__VA_ARGS__); \
+      case 11: return FN<LN_LDU8W_D, 11, PR>(__VA_ARGS__); case 12: return FN<LN_LDU8W_D, 12, PR>(__VA_ARGS__); \
       default: break;                                                                              \
     }                                                                                              \
   }
+// paired rows compiled per label count: L_3 3-5, L_4 3-4 (64 H sums per unit at four)
+#if LN_LDU8W_D == 3 && LN_LDU8W_MAXPR >= 5
+#define LN_LDU8W_PRS(FN, ...)                                                                      \
+  if (pr == 5) { LN_LDU8W_SWITCH(NW, FN, 5, __VA_ARGS__) }                                         \
+  else if (pr == 4) { LN_LDU8W_SWITCH(NW, FN, 4, __VA_ARGS__) }                                    \
+  else if (pr == 3) { LN_LDU8W_SWITCH(NW, FN, 3, __VA_ARGS__) }
+#else
+#define LN_LDU8W_PRS(FN, ...)                                                                      \
+  if (pr == 4) { LN_LDU8W_SWITCH(NW, FN, 4, __VA_ARGS__) }                                         \
+  else if (pr == 3) { LN_LDU8W_SWITCH(NW, FN, 3, __VA_ARGS__) }
+#endif
 
 template <>
-cudaError_t walk_ldu8w_launch_part<LN_LDU8W_PART>(const WalkParams& p, const uint32_t* tab, const int32_t* init, int grid,
-                                                   cudaStream_t st, int NW, int pr) {
-#if LN_LDU8W_MAXPR >= 5
-  if (pr == 5) { LN_LDU8W_SWITCH(NW, launch_w, 5, p, tab, init, grid, st) }
-#endif
-  if (pr == 4) { LN_LDU8W_SWITCH(NW, launch_w, 4, p, tab, init, grid, st) }
-  else if (pr == 3) { LN_LDU8W_SWITCH(NW, launch_w, 3, p, tab, init, grid, st) }
+cudaError_t walk_ldu8w_launch_part<LN_LDU8W_D, LN_LDU8W_PART>(const WalkParams& p, const uint32_t* tab,
+                                                               const int32_t* init, int grid, cudaStream_t st, int NW,
+                                                               int pr) {
+  LN_LDU8W_PRS(launch_w, p, tab, init, grid, st)
   return cudaErrorInvalidValue;
 }
 
-template <int NW, int PR>
-int upl_w() { return w_units<NW, PR>(); }
-
 template <>
-int walk_ldu8w_upl_part<LN_LDU8W_PART>(int NW, int pr) {
-#if LN_LDU8W_MAXPR >= 5
-  if (pr == 5) { LN_LDU8W_SWITCH(NW, upl_w, 5) }
-#endif
-  if (pr == 4) { LN_LDU8W_SWITCH(NW, upl_w, 4) }
-  else if (pr == 3) { LN_LDU8W_SWITCH(NW, upl_w, 3) }
+int walk_ldu8w_upl_part<LN_LDU8W_D, LN_LDU8W_PART>(int NW, int pr) {
+  LN_LDU8W_PRS(upl_w)
   return 1;
 }
 
 template <>
-int walk_ldu8w_occ_part<LN_LDU8W_PART>(int NW, int pr, int s) {
-#if LN_LDU8W_MAXPR >= 5
-  if (pr == 5) { LN_LDU8W_SWITCH(NW, occ_w, 5, s) }
-#endif
-  if (pr == 4) { LN_LDU8W_SWITCH(NW, occ_w, 4, s) }
-  else if (pr == 3) { LN_LDU8W_SWITCH(NW, occ_w, 3, s) }
+int walk_ldu8w_occ_part<LN_LDU8W_D, LN_LDU8W_PART>(int NW, int pr, int s) {
+  LN_LDU8W_PRS(occ_w, s)
   return 0;
 }
 #endif
