@@ -167,43 +167,60 @@ struct LdW {
   // Max-plus subset convolution form of the same maximum (LN_LDU8W_CONV = 1).  A labelling of the
   // paired rows is a partition (T_0, .., T_{D-1}) of them by label, valued sum_g H[T_g][g]; with
   //     G_1(U) = H[U][0],   G_{g+1}(U) = max over T subset of U of  H[T][g] + G_g(U \ T)
-  // the best labelling is G_D(all paired rows).  Additions: 3^PR per intermediate level (sum over
+  // the best labelling is G_D(all paired rows) = max over T of H[T][D-1] + G_{D-1}(rest).  Additions: 3^PR per intermediate level (sum over
   // U of 2^|U|) plus 2^PR for the last one -- L_3, PR = 4: 97 FADD instead of 2 * 81 = 162; L_4,
   // PR = 4: 178 instead of 3 * 256 = 768 -- with about as many maxes as the direct form.
-  template <int G, int U, int I>
-  static __device__ __forceinline__ int32_t lvl_term(const int32_t (&H)[NS][D], const int32_t (&Gp)[NS], uint32_t one) {
+  // L_01(U) = max over T subset of U of H[T][1] + H[U \ T][0]  (= G_2(U), streamed)
+  template <int U, int I>
+  static __device__ __forceinline__ int32_t term01(const int32_t (&H)[NS][D], uint32_t one) {
     constexpr int T = std::integral_constant<int, w_submask(U, I)>::value;
-    return w_fadd(H[T][G], Gp[U ^ T], one);
+    return w_fadd(H[T][1], H[U ^ T][0], one);
   }
-  template <int G, int U, int... Is>
-  static __device__ __forceinline__ int32_t lvl_U(const int32_t (&H)[NS][D], const int32_t (&Gp)[NS], uint32_t one,
-                                                  std::integer_sequence<int, Is...>) {
-    int32_t v[sizeof...(Is)] = {lvl_term<G, U, Is>(H, Gp, one)...};
+  template <int U, int... Is>
+  static __device__ __forceinline__ int32_t L01(const int32_t (&H)[NS][D], uint32_t one, std::integer_sequence<int, Is...>) {
+    int32_t v[sizeof...(Is)] = {term01<U, Is>(H, one)...};
     return w_max_tree<(int)sizeof...(Is)>(v);
   }
-  template <int G, int... Us>
-  static __device__ __forceinline__ void lvl_all(const int32_t (&H)[NS][D], const int32_t (&Gp)[NS], int32_t (&Gn)[NS],
-                                                 uint32_t one, std::integer_sequence<int, Us...>) {
-    ((Gn[Us] = lvl_U<G, Us>(H, Gp, one, std::make_integer_sequence<int, (1 << w_popc(Us))>{})), ...);
+  template <int U>
+  static __device__ __forceinline__ int32_t G2(const int32_t (&H)[NS][D], uint32_t one) {
+    return L01<U>(H, one, std::make_integer_sequence<int, (1 << w_popc(U))>{});
   }
-  template <int G, int... Is>
-  static __device__ __forceinline__ int32_t lvl_last(const int32_t (&H)[NS][D], const int32_t (&Gp)[NS], int32_t best,
-                                                     uint32_t one, std::integer_sequence<int, Is...>) {
-    int32_t v[sizeof...(Is) + 1] = {lvl_term<G, NS - 1, Is>(H, Gp, one)..., best};   // U = all paired rows
-    return w_max_tree<(int)sizeof...(Is) + 1>(v);
+  // L_4's middle level from the stored G_2 values: G_3(U) = max over T subset of U of H[T][2] + G_2(U \ T)
+  template <int U, int I>
+  static __device__ __forceinline__ int32_t term2(const int32_t (&H)[NS][D], const int32_t (&g2)[NS], uint32_t one) {
+    constexpr int T = std::integral_constant<int, w_submask(U, I)>::value;
+    return w_fadd(H[T][2], g2[U ^ T], one);
+  }
+  template <int U, int... Is>
+  static __device__ __forceinline__ int32_t L2(const int32_t (&H)[NS][D], const int32_t (&g2)[NS], uint32_t one,
+                                               std::integer_sequence<int, Is...>) {
+    int32_t v[sizeof...(Is)] = {term2<U, Is>(H, g2, one)...};
+    return w_max_tree<(int)sizeof...(Is)>(v);
+  }
+  // last level, one term per label-(D-1) set T (the complement is the rest of the paired rows);
+  // the intermediate level is streamed (L_3) or read from the stored G_2 (L_4), so at most NS
+  // intermediate values are live next to the H sums
+  template <int T>
+  static __device__ __forceinline__ int32_t last(const int32_t (&H)[NS][D], const int32_t (&g2)[NS], uint32_t one) {
+    constexpr int U = (NS - 1) ^ T;
+    if constexpr (D == 3) return w_fadd(H[T][2], G2<U>(H, one), one);
+    else return w_fadd(H[T][3], L2<U>(H, g2, one, std::make_integer_sequence<int, (1 << w_popc(U))>{}), one);
+  }
+  template <int... Us>
+  static __device__ __forceinline__ void fill_g2(const int32_t (&H)[NS][D], int32_t (&g2)[NS], uint32_t one,
+                                                 std::integer_sequence<int, Us...>) {
+    ((g2[Us] = G2<Us>(H, one)), ...);
+  }
+  template <int... Ts>
+  static __device__ __forceinline__ int32_t conv_seq(const int32_t (&H)[NS][D], const int32_t (&g2)[NS], int32_t best,
+                                                     uint32_t one, std::integer_sequence<int, Ts...>) {
+    int32_t v[NS + 1] = {last<Ts>(H, g2, one)..., best};
+    return w_max_tree<NS + 1>(v);
   }
   static __device__ __forceinline__ int32_t conv_best(const int32_t (&H)[NS][D], int32_t best, uint32_t one) {
-    int32_t G1[NS], G2[NS];
-#pragma unroll
-    for (int m = 0; m < NS; ++m) G1[m] = H[m][0];
-    lvl_all<1>(H, G1, G2, one, std::make_integer_sequence<int, NS>{});
-    if constexpr (D == 3) {
-      return lvl_last<2>(H, G2, best, one, std::make_integer_sequence<int, NS>{});
-    } else {
-      int32_t G3[NS];
-      lvl_all<2>(H, G2, G3, one, std::make_integer_sequence<int, NS>{});
-      return lvl_last<3>(H, G3, best, one, std::make_integer_sequence<int, NS>{});
-    }
+    int32_t g2[NS];
+    if constexpr (D == 4) fill_g2(H, g2, one, std::make_integer_sequence<int, NS>{});
+    return conv_seq(H, g2, best, one, std::make_integer_sequence<int, NS>{});
   }
   // max(best, every labelling's value of the current word)
   static __device__ __forceinline__ int32_t best_of(const int32_t (&H)[NS][D], int32_t best, uint32_t one) {
