@@ -46,6 +46,14 @@ CONFIGS = {
 }
 
 
+def conv_max_ops(d, pr):
+    """ALU max instructions per walked word of the all-H kernel's subset convolution
+    (walk_ldu8w_impl.cuh: w_max_tree over every subset's candidates, D - 2 levels, last step)."""
+    from math import comb
+    level = sum(comb(pr, k) * ((2 ** k - 1 + 1) // 2) for k in range(pr + 1))   # sum_U ceil((2^|U|-1)/2)
+    return (d - 2) * level + (2 ** pr + 1) // 2
+
+
 def alu_floor(variant, d, c, s, d_walked, pr=None):
     """Binding-pipe instruction floor per strategy of the kernel family's own algorithm
     (DESIGN.md "Roofline"): (instructions per strategy, pipe, lane-instructions/clk/SM of that pipe).
@@ -53,10 +61,13 @@ def alu_floor(variant, d, c, s, d_walked, pr=None):
     7 byte walk (L_1/L_marg/L_2): per walked word, per unit, G*c/4 VABSDIFF4 per bias set (two
       sets: the paired last row's two signs) + one VIMNMX3 per two strategies
       -> G*c/4 + 1/2 per strategy on the ALU pipe (G = 2 for L_2's two groups).
-    8 byte d-ary walk (L_3/L_4), PR paired rows (lnorm_stats.paired_rows; L_3: 4 if s >= 5): a move
-      recomputes 2^PR bias sums of the two changed groups: 2*2^PR*c/4 VABSDIFF4, then the max of
-      the T = d^PR labellings (ceil((T-1)/2) VIMNMX3) and one VIADDMNMX for the running best,
-      shared by T strategies, on the ALU pipe.
+    8 byte d-ary walk (L_3/L_4), PR paired rows (lnorm_stats.paired_rows): a move recomputes the
+      2^PR bias sums of the two changed groups: 2*2^PR*c/4 VABSDIFF4.  PR >= 3 is the all-H kernel
+      (walk_ldu8w_impl.cuh), whose best labelling is a max-plus subset convolution: per level a
+      max tree over the 2^|U| candidates of every subset U (ceil((2^|U|-1)/2) three-input maxes),
+      D - 2 levels, then ceil(2^PR/2) for the last step with the running best (conv_max_ops);
+      PR <= 2 is the all-E kernel: the max of the T = d^PR labellings (ceil((T-1)/2)) + 1.
+      Shared by the d^PR strategies of the word, on the ALU pipe.
     16-bit / int32 families: issue-bound (both integer pipes), instructions per strategy."""
     if variant == 7:
         G = 2 if d == 2 else 1
@@ -65,7 +76,8 @@ def alu_floor(variant, d, c, s, d_walked, pr=None):
         if not pr:
             pr = 3 if s >= 4 else (2 if s == 3 else 1)
         T = d_walked ** pr
-        per_word = 2 * (2 ** pr) * c / 4.0 + (T - 1 + 1) // 2 + 1   # ceil((T-1)/2) = T // 2
+        maxes = conv_max_ops(d_walked, pr) if pr >= 3 else T // 2 + 1   # all-H vs all-E epilogue
+        per_word = 2 * (2 ** pr) * c / 4.0 + maxes
         return per_word / T, "alu", 64.0
     if variant in (3, 5):
         return float(c), "issue", 128.0
