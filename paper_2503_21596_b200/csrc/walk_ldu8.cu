@@ -42,7 +42,7 @@ bool walk_ldu8_supported(int d, int c, int s) {
 void walk_ldu8_table_sizes(int d, int c, int k, int s, int64_t* tab_words, int64_t* init_ints) {
   const int NW = words_of(c), pr = walk_ldu8_paired_rows(d, s);
   *tab_words = (int64_t)(s - pr) * 2 * lu_pad4(NW);
-  *init_ints = (int64_t)(k + 3) * 4 * NW + (int64_t)NW * (1 << pr) + (1 << pr);
+  *init_ints = (int64_t)(k + 3) * 4 * NW + (int64_t)NW * (1 << pr) + (1 << pr) + (int64_t)(k + 3) * NW;
 }
 
 int walk_ldu8_units_per_lane(int d, int c, int s) {
@@ -74,7 +74,8 @@ cudaError_t walk_ldu8_launch(const WalkParams& p, int32_t* scratch_tab, int32_t*
   const int NW = words_of(p.c), pt = part_of(NW);
   const int wr = ldu8w_rows(p.d, p.s);
   const int pr = wr ? wr : ldu8_rows(p.s);
-  if ((p.s - pr) * 2 * lu_pad4(NW) > kTabWordsLU || (p.k + 3) * 4 * NW + (NW + 1) * (1 << pr) > 16384) return cudaErrorInvalidValue;
+  if ((p.s - pr) * 2 * lu_pad4(NW) > kTabWordsLU || (p.k + 3) * 5 * NW + (NW + 1) * (1 << pr) > 16384)
+    return cudaErrorInvalidValue;
   uint32_t* tab = reinterpret_cast<uint32_t*>(scratch_tab);
   build_ldu8_kernel<<<p.batch, 128, 0, st>>>(p.M, p.r, p.c, NW, p.k, p.s, pr, tab, scratch_init, p.m_stride,
                                              p.tab_stride, p.init_stride);

@@ -448,6 +448,27 @@ __global__ void build_ldu8_kernel(const int32_t* M, int r, int c, int NW, int k,
     }
     bias[NS * NW + m] = (uint32_t)kap;
   }
+  // packed prefix rows (signed deltas, sum_e 256^e M_xy mod 2^32) and the packed start bytes of
+  // group 0 (base - N) and of the other groups (-N): the all-H kernel's unit init adds whole
+  // packed rows to its groups (every partial sum is a subset sum of the column, so no byte
+  // leaves [0, 255]) instead of summing int32 columns
+  uint32_t* pk = reinterpret_cast<uint32_t*>(init + (k + 3) * CW) + NS * NW + NS;
+  for (int i = threadIdx.x; i < (k + 1) * NW; i += blockDim.x) {
+    const int x = i / NW, q = i % NW;
+    int32_t v[4];
+    for (int e = 0; e < 4; ++e) v[e] = (4 * q + e < c) ? M[(int64_t)x * c + 4 * q + e] : 0;
+    pk[i] = pack(v);
+  }
+  __syncthreads();                             // the base / -N records above are read back here
+  for (int q = threadIdx.x; q < NW; q += blockDim.x) {
+    int32_t v0[4], vg[4];
+    for (int e = 0; e < 4; ++e) {
+      vg[e] = init[(k + 2) * CW + 4 * q + e];                  // -N
+      v0[e] = vg[e] + init[(k + 1) * CW + 4 * q + e];          // base - N
+    }
+    pk[(k + 1) * NW + q] = pack(v0);
+    pk[(k + 2) * NW + q] = pack(vg);
+  }
 }
 
 #ifndef LN_LDU8_PMAX

@@ -364,8 +364,6 @@ walk_ldu8w_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const i
         cur_b = mb;
       }
     }
-    const int32_t* baseRec = gI + (p.k + 1) * CW;
-    const int32_t* negRec = baseRec + CW;
     uint32_t A[P][D][NW];
     int32_t H[P][NS][D];
     int32_t best[P];
@@ -378,26 +376,25 @@ walk_ldu8w_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const i
       if (p.prefix_table) lab = p.prefix_table[u - p.unit_begin];
       else for (int x = 0; x <= p.k; ++x) lab |= (uint64_t)prefix_digit(p, u, x) << (p.pbits * x);
       const uint64_t lmask = (1ull << p.pbits) - 1ull;
+      // packed start bytes, then every prefix row's packed word added to the group of its label
+      // (build_ldu8_kernel's packed records: 2 instructions per row, word and group)
+      const uint32_t* pkRec = reinterpret_cast<const uint32_t*>(gI + (p.k + 3) * CW) + NS * NW + NS;
+      const uint32_t* stRec = pkRec + (p.k + 1) * NW;
 #pragma unroll
       for (int q = 0; q < NW; ++q) {
-        int32_t a[D][4];
+        A[j][0][q] = __ldg(stRec + q);
+        const uint32_t sg = __ldg(stRec + NW + q);
 #pragma unroll
-        for (int g = 0; g < D; ++g)
+        for (int g = 1; g < D; ++g) A[j][g][q] = sg;
+      }
+      for (int x = 0; x <= p.k; ++x) {
+        const int dig = (int)((lab >> (p.pbits * x)) & lmask);
 #pragma unroll
-          for (int e = 0; e < 4; ++e) a[g][e] = __ldg(negRec + 4 * q + e) + (g == 0 ? __ldg(baseRec + 4 * q + e) : 0);
-        for (int x = 0; x <= p.k; ++x) {
-          const int dig = (int)((lab >> (p.pbits * x)) & lmask);
-          const int4 v = __ldg(reinterpret_cast<const int4*>(gI + x * CW) + q);
+        for (int q = 0; q < NW; ++q) {
+          const uint32_t w = __ldg(pkRec + x * NW + q);
 #pragma unroll
-          for (int g = 0; g < D; ++g) {
-            const int32_t f = dig == g ? 1 : 0;
-            a[g][0] += f * v.x; a[g][1] += f * v.y; a[g][2] += f * v.z; a[g][3] += f * v.w;
-          }
+          for (int g = 0; g < D; ++g) A[j][g][q] += (dig == g) ? w : 0u;
         }
-#pragma unroll
-        for (int g = 0; g < D; ++g)
-          A[j][g][q] = (uint32_t)(a[g][0] & 0xFF) | ((uint32_t)(a[g][1] & 0xFF) << 8) |
-                       ((uint32_t)(a[g][2] & 0xFF) << 16) | ((uint32_t)(a[g][3] & 0xFF) << 24);
       }
 #pragma unroll
       for (int g = 0; g < D; ++g)
