@@ -246,11 +246,14 @@ cudaError_t recover_launch(const WalkParams& p, unsigned long long* lex_out, uns
   const int nsm = device_sms();
   cudaError_t e = ensure_dyn_smem((const void*)recover_kernel, std::max<size_t>(sm, 96 * 1024));
   if (e != cudaSuccess) return e;
-  // blocks per matrix: enough warps for ~16-word chunks (the recovery is latency-bound: a
-  // d-ary step of this generic walk is a few hundred cycles), at most 4 per SM
+  // blocks per matrix: enough warps for ~2-word chunks, at most 4 blocks per SM.  The recovery is
+  // latency-bound (one warp per chunk, a d-ary step of this generic walk is a few hundred cycles
+  // of dependent work, the chunk's init ~1-2k): a 20x20 search's 32-word unit took 21 us with
+  // 8-word chunks on one block (ncu: 4 warps, 9 cycles per instruction), several us with 2-word
+  // chunks; large units still fill 4 blocks per SM
   uint64_t words = 1;
   for (int i = 0; i < p.s; ++i) words *= (uint64_t)(p.mode == MODE_LD ? p.d : 2);
-  int gx = (int)std::min<uint64_t>((uint64_t)nsm * 4, std::max<uint64_t>(1, words / (16ull * kGenWarps)));
+  int gx = (int)std::min<uint64_t>((uint64_t)nsm * 4, std::max<uint64_t>(1, words / (2ull * kGenWarps)));
   if (p.batch > 1) gx = std::max(1, std::min(gx, (nsm * 8 + p.batch - 1) / p.batch));
   const int gy = std::max(1, std::min(p.batch > 0 ? p.batch : 1, 65535));
   recover_kernel<<<dim3(gx, gy), 32 * kGenWarps, sm, st>>>(p, lex_out, rmax_out, stage);
