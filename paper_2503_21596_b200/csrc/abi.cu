@@ -101,6 +101,7 @@ struct Problem {
   bool fits16 = false;  // packed 16-bit column-pair path is exact
   bool fitsPair = false;  // strategy-paired path is exact: sum |M| <= 16383
   bool fitsLdPair = false;  // last-row-paired d-ary path is exact: sum |M| <= 32767
+  bool fitsU16 = false;     // every strategy value fits 16 unsigned bits: sum |M| <= 65535 (packed maxima)
   // u8 guard: sufW[s] = max over columns y of sum_{x = r-s}^{r-1} |M_xy| (the last s rows)
   int64_t sufW[kMaxRows + 1] = {};
 };
@@ -258,6 +259,7 @@ int apply_stats(const GuardStats& g, Problem* p) {
   for (int s = 0; s <= kMaxRows; ++s) p->sufW[s] = g.sufW[s];
   p->fitsPair = g.S <= 16383;
   p->fitsLdPair = g.S <= 32767;
+  p->fitsU16 = g.S <= 65535;
   return LNORM_OK;
 }
 
@@ -689,6 +691,7 @@ int launch_walk(DevCtx& cx, const Problem& pr, const Plan& pl, WalkParams& wp, i
   if (pl.kernel == K_PAIR16) per_block *= walk_pair16_units_per_lane(pr.mode, pr.c);
   if (pl.kernel == K_U8) per_block = per_block * walk_u8_units_per_lane(pr.mode, pr.c, pl.u8_lpu) / pl.u8_lpu;
   wp.u8_lpu = pl.u8_lpu;
+  wp.u8_pack_max = pr.fitsU16 ? 1 : 0;
   if (pl.kernel == K_LDPAIR16) per_block *= walk_ldpair16_units_per_lane(pr.dl, pr.c);
   if (pl.kernel == K_LDU8) per_block *= walk_ldu8_units_per_lane(pr.dl, pr.c, pl.s);
   int64_t want = (wp.unit_count + per_block - 1) / per_block;

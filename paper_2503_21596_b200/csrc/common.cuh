@@ -55,6 +55,9 @@ struct WalkParams {
   // self-check builds (LN_SELFCHECK): added to every from-scratch value before the comparison
   // (test hook LNORM_SELFCHECK_INJECT: a nonzero delta must make the call fail)
   int32_t selfcheck_delta;
+  // byte binary walk (L_1 / L_2): every strategy value <= 65535 (sum |M|), so two units' running
+  // maxima may share a register as 16-bit halves (set by the host planner)
+  int32_t u8_pack_max;
 };
 
 // Defaults for a single-matrix launch.

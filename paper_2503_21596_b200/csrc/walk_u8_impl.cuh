@@ -175,7 +175,11 @@ __host__ __device__ constexpr int u8_unroll() {
        : u8_step_instr<MODE, NW, P>() * 4 <= LN_U8_BUDGET ? 2 : 1;
 }
 
-template <int MODE, int NW, int P, int LPU = 1>
+// PK: the running maxima of two units share one register as unsigned 16-bit halves (every value
+// is a non-negative integer <= sum |M| <= 65535: L_1 and L_2, host-checked), so ONE VIMNMX3.U16x2
+// serves the four strategies (two units x the paired row's two signs) of a walked word; the two
+// values are packed by an IMAD (FMA-heavy pipe) -- half the epilogue's ALU instructions.
+template <int MODE, int NW, int P, int LPU = 1, bool PK = false>
 struct U8Step {
   // NW here = the words THIS lane holds (half of the unit's words when LPU = 2)
   static constexpr int PR = u8_pr<MODE>(), NS = 1 << PR;   // paired rows, bias sets
@@ -224,7 +228,22 @@ struct U8Step {
         }
       }
     }
-    if (PR >= 1) {
+    if (PK) {
+      static_assert(!PK || (PR == 1 && LPU == 1 && P % 2 == 0 && MODE != MODE_MARG), "packed maxima");
+      const uint32_t k16 = one << 16;                 // 65536 from a kernel parameter: IMAD, not LEA
+#pragma unroll
+      for (int j = 0; j < P; j += 2) {
+        uint32_t w[NS];
+#pragma unroll
+        for (int h = 0; h < NS; ++h) {
+          const uint32_t lo = (G == 2) ? hs[j][h][0] + hs[j][h][1] : hs[j][h][0];
+          const uint32_t hi = (G == 2) ? hs[j + 1][h][0] + hs[j + 1][h][1] : hs[j + 1][h][0];
+          if (LN_SELFCHECK && j == 0 && vout) vout[h] = (int32_t)lo;
+          asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(w[h]) : "r"(hi), "r"(k16), "r"(lo));
+        }
+        best[j / 2] = (int32_t)__vimax3_u16x2((uint32_t)best[j / 2], w[0], w[1]);
+      }
+    } else if (PR >= 1) {
 #pragma unroll
       for (int j = 0; j < P; ++j) {
         int32_t v[NS];
@@ -283,7 +302,7 @@ __host__ __device__ constexpr int u8_min_blocks() {
 // local chunk lc; chunks never straddle matrices and a warp restages the delta table when it
 // moves to the next matrix).  The single-search instance (BAT = false) keeps the table staged
 // once and no per-chunk bookkeeping (the batch state costs registers the hot loop needs).
-template <int MODE, int NW, int P, int LPU, bool BAT = false>
+template <int MODE, int NW, int P, int LPU, bool BAT = false, bool PK = false>
 __global__ void __launch_bounds__(kBlockU8, u8_min_blocks<MODE, NW, P, LPU>())
 walk_u8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int32_t* __restrict__ gInit) {
   using LY = U8Layout<MODE, NW>;
@@ -294,7 +313,7 @@ walk_u8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int3
   constexpr int RREC = LPU * RWL;                  // words per delta record
   constexpr int GPW = 32 / LPU;                    // lane groups per warp
   constexpr int K = u8_unroll<MODE, NWL, P>();
-  using STEP = U8Step<MODE, NWL, P, LPU>;
+  using STEP = U8Step<MODE, NWL, P, LPU, PK>;
   constexpr int NB = STEP::NB;
   extern __shared__ __align__(16) uint32_t sT[];
   const int lane = threadIdx.x & 31;
@@ -449,6 +468,10 @@ walk_u8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int3
       }
       best[j] = v0;
     }
+    if constexpr (PK) {                                // two units' maxima per register (lo: unit 2i)
+#pragma unroll
+      for (int i = 0; i < P / 2; ++i) best[i] = (int32_t)(((uint32_t)best[2 * i + 1] << 16) | (uint32_t)best[2 * i]);
+    }
     // ---- the walk: 2^s - 1 Gray steps (low K digits unrolled, Table 1's ruler pattern)
     for (uint32_t t = 0; t < nblk; ++t) {
 #if LN_SELFCHECK
@@ -481,6 +504,14 @@ walk_u8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int3
 #else
         STEP::run(A, B, Kc, best, sbase, (2 * b + sg) * RREC + half * RWL, p.one);
 #endif
+      }
+    }
+    if constexpr (PK) {                                // unpack (back to front: slot i holds units 2i, 2i+1)
+#pragma unroll
+      for (int i = P / 2 - 1; i >= 0; --i) {
+        const uint32_t w = (uint32_t)best[i];
+        best[2 * i + 1] = (int32_t)(w >> 16);
+        best[2 * i] = (int32_t)(w & 0xFFFFu);
       }
     }
 #pragma unroll
@@ -551,6 +582,13 @@ size_t u8_smem(int s) { return sizeof(uint32_t) * (size_t)(2 * (s - u8_pr<MODE>(
 
 // batched instances exist for the small-matrix regime only (<= 32 columns, one lane per unit)
 constexpr int kU8BatchMaxNW = 8;
+// packed-maxima instances (LN_U8_PACKMAX, U8Step PK) for up to 64 columns (four units per lane).
+// Off: measured 5.6 % SLOWER on 42x42 L_1 (1583 vs 1499 ms, profiles/r02/ab_u8_packmax.jsonl) --
+// the halved VIMNMX3 count does not pay for the packing IMADs and the longer dependency chain
+#ifndef LN_U8_PACKMAX
+#define LN_U8_PACKMAX 0
+#endif
+constexpr int kU8PackMaxNW = LN_U8_PACKMAX ? 16 : 0;
 
 template <int MODE, int NW, int LPU>
 cudaError_t launch_u8_l(const WalkParams& p, const uint32_t* tab, const int32_t* init, int grid, cudaStream_t st) {
@@ -564,6 +602,14 @@ cudaError_t launch_u8_l(const WalkParams& p, const uint32_t* tab, const int32_t*
       return cudaGetLastError();
     }
     return cudaErrorInvalidValue;
+  }
+  if constexpr (MODE != MODE_MARG && LPU == 1 && P % 2 == 0 && NW <= kU8PackMaxNW && u8_pr<MODE>() == 1) {
+    if (p.u8_pack_max) {                 // every value <= sum |M| <= 65535 (host): packed maxima
+      cudaError_t e = ensure_dyn_smem((const void*)walk_u8_kernel<MODE, NW, P, LPU, false, true>, sm);
+      if (e != cudaSuccess) return e;
+      walk_u8_kernel<MODE, NW, P, LPU, false, true><<<grid, kBlockU8, sm, st>>>(p, tab, init);
+      return cudaGetLastError();
+    }
   }
   cudaError_t e = ensure_dyn_smem((const void*)walk_u8_kernel<MODE, NW, P, LPU>, sm);
   if (e != cudaSuccess) return e;
