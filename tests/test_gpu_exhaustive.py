@@ -70,3 +70,22 @@ def test_r6_rule_is_the_single_call_rule_too(lib):
             v, arg = lib.compute(M, with_marginals=marg)
             ev, earg = expected(M, 1, marg)
             assert v == ev and list(arg) == list(earg), (seed, marg)
+
+
+@pytest.mark.parametrize("d,marg", MODES + [(4, False)], ids=["L1", "marg", "L2", "L3", "L4"])
+def test_spec_1000_random_small_matrices(lib, d, marg):
+    """SPEC.md acceptance criterion: 1000 seeded random matrices with n, m <= 6 and entries
+    in [-9, 9]; grouped by shape into batched calls; value and argmax against the oracle."""
+    from paper_2503_21596_b200 import synth
+    g = synth.SplitMix64(423 + 10 * d + marg)
+    by_shape = {}
+    for i in range(1000):
+        n, m = 1 + g.next() % 6, 1 + g.next() % 6
+        by_shape.setdefault((n, m), []).append(synth.random_matrix(n, m, 42_300 + i, -9, 9))
+    assert sum(len(v) for v in by_shape.values()) == 1000
+    for (n, m), mats in sorted(by_shape.items()):
+        Ms = np.stack(mats)
+        vals, args = lib.compute_batch(Ms, d=d, with_marginals=marg)
+        for i, M in enumerate(Ms):
+            ev, earg = expected(M, d, marg)
+            assert vals[i] == ev and list(args[i]) == list(earg), ((n, m), M.tolist())
