@@ -57,6 +57,10 @@ constexpr int kBlockW = 32;
 #ifndef LN_LDU8W_MINB5
 #define LN_LDU8W_MINB5 12
 #endif
+// paired rows from which the kappa sums live in shared memory instead of registers (LdW::KS)
+#ifndef LN_LDU8W_KSMEM_PR
+#define LN_LDU8W_KSMEM_PR 5
+#endif
 template <int D, int NW, int PR>
 __host__ __device__ constexpr int w_minb() {
   return (PR == 5 || (D == 4 && PR >= 4)) ? LN_LDU8W_MINB5 : (PR == 4 && (NW == 10 || NW == 12)) ? 12 : LN_LDU8W_MINB;
@@ -241,6 +245,12 @@ struct LdW {
   // half of the bias sets, all VABSDIFF4 of one group back to back -- they share the byte
   // operand A[g][i] (operand reuse cache), so each reads two registers (bias word, accumulator)
   // instead of three; the register-file read ports, not the ALU pipe, bound a 3-source mix.
+  // KS: the kappa sums (accumulator starts) are read from shared memory (after the bias words)
+  // instead of living in NS registers -- frees 32 registers at five paired rows, where every
+  // instance but 24 columns otherwise spills 30-430 bytes (26x26 L_3: 79.0 -> 75.5 ms; 24x24,
+  // spill-free either way: 7.89 vs 7.96 ms, so it keeps its kappas in registers;
+  // profiles/r02/ab_l3_ksmem.jsonl)
+  static constexpr bool KS = PR >= LN_LDU8W_KSMEM_PR && NW != 6;
   template <int GA, int GB, int P>
   static __device__ __forceinline__ void sums(uint32_t (&A)[P][D][NW], int32_t (&H)[P][NS][D], const uint32_t (&Ks)[NS],
                                               uint32_t rowA, uint32_t rowB, uint32_t sbias) {
@@ -270,16 +280,26 @@ struct LdW {
               const uint4 bq = lds128(sbias + 4u * (uint32_t)(i * NS + h * HB + 4 * q));
               bb[4 * q] = bq.x; bb[4 * q + 1] = bq.y; bb[4 * q + 2] = bq.z; bb[4 * q + 3] = bq.w;
             }
+            uint32_t kk[HB];                           // accumulator starts of this batch of bias sets
+#pragma unroll
+            for (int m = 0; m < HB; ++m) kk[m] = KS ? 0u : Ks[h * HB + m];
+            if (KS && i == 0) {
+#pragma unroll
+              for (int q = 0; q < HB / 4; ++q) {
+                const uint4 kq = lds128(sbias + 4u * (uint32_t)(NW * NS + h * HB + 4 * q));
+                kk[4 * q] = kq.x; kk[4 * q + 1] = kq.y; kk[4 * q + 2] = kq.z; kk[4 * q + 3] = kq.w;
+              }
+            }
 #pragma unroll
             for (int j = 0; j < P; ++j) {
 #pragma unroll
               for (int m = 0; m < HB; ++m)
                 H[j][h * HB + m][GA] =
-                    (int32_t)w_sad4(A[j][GA][i], bb[m], i == 0 ? Ks[h * HB + m] : (uint32_t)H[j][h * HB + m][GA]);
+                    (int32_t)w_sad4(A[j][GA][i], bb[m], i == 0 ? kk[m] : (uint32_t)H[j][h * HB + m][GA]);
 #pragma unroll
               for (int m = 0; m < HB; ++m)
                 H[j][h * HB + m][GB] =
-                    (int32_t)w_sad4(A[j][GB][i], bb[m], i == 0 ? Ks[h * HB + m] : (uint32_t)H[j][h * HB + m][GB]);
+                    (int32_t)w_sad4(A[j][GB][i], bb[m], i == 0 ? kk[m] : (uint32_t)H[j][h * HB + m][GB]);
             }
           }
         }
@@ -335,8 +355,11 @@ walk_ldu8w_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const i
       const int q = i / NS, m = i % NS;
       sBias[i] = biasRec[m * NW + q];
     }
+    for (int m = lane; m < NS; m += 32) sBias[NS * NW + m] = biasRec[NS * NW + m];   // kappas (WK::KS)
+    if constexpr (!WK::KS) {
 #pragma unroll
-    for (int m = 0; m < NS; ++m) Ks[m] = __ldg(biasRec + NS * NW + m) ^ (LN_LDU8W_KVEC ? (uint32_t)threadIdx.y : 0u);
+      for (int m = 0; m < NS; ++m) Ks[m] = __ldg(biasRec + NS * NW + m) ^ (LN_LDU8W_KVEC ? (uint32_t)threadIdx.y : 0u);
+    }
     __syncwarp();
   };
   // BAT (batched launches, f3): chunk ch -> matrix mb = ch / CPM (units_per units per matrix,
@@ -400,7 +423,7 @@ walk_ldu8w_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const i
       for (int g = 0; g < D; ++g)
 #pragma unroll
         for (int m = 0; m < NS; ++m) {
-          uint32_t h = Ks[m];
+          uint32_t h = WK::KS ? sBias[NS * NW + m] : Ks[m];
 #pragma unroll
           for (int q = 0; q < NW; ++q) h = w_sad4(A[j][g][q], sBias[q * NS + m], h);
           H[j][m][g] = (int32_t)h;
@@ -447,7 +470,7 @@ walk_ldu8w_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const i
 }
 
 template <int NW, int PR>
-size_t w_smem(int s) { return sizeof(uint32_t) * (size_t)((s - PR) * 2 * w_pad4(NW) + (1 << PR) * NW); }
+size_t w_smem(int s) { return sizeof(uint32_t) * (size_t)((s - PR) * 2 * w_pad4(NW) + (1 << PR) * (NW + 1)); }
 
 template <int D, int NW, int PR>
 cudaError_t launch_w(const WalkParams& p, const uint32_t* tab, const int32_t* init, int grid, cudaStream_t st) {
