@@ -1231,7 +1231,7 @@ int lnorm_compute_reduced(const int32_t* M, int32_t n, int32_t m, int32_t d, int
   CU(cudaMemcpyAsync(cx->dIn, M, sizeof(int32_t) * nm, cudaMemcpyHostToDevice, s));
   const int mode = with_marginals ? MODE_MARG : (d == 1 ? MODE_L1 : MODE_LD);
   if (reduce_launch(cx->dIn, n, m, mode, scratch, R, rowsel, info, s) != cudaSuccess) { (void)cudaGetLastError(); return LNORM_ECUDA; }
-  int32_t hinfo[4] = {0, 0, 0, 0};
+  int32_t hinfo[3] = {0, 0, 0};                              // reduced rows, columns, mode (reduce_kernel)
   CU(cudaMemcpyAsync(hinfo, info, sizeof(hinfo), cudaMemcpyDeviceToHost, s));
   CU(cudaStreamSynchronize(s));
   const int nr = hinfo[0], mr = hinfo[1], mode2 = hinfo[2];
@@ -1240,7 +1240,8 @@ int lnorm_compute_reduced(const int32_t* M, int32_t n, int32_t m, int32_t d, int
   lnorm_stats st{};
   if (nr > 0 && mr > 0) {
     std::vector<int32_t> hR((size_t)nr * mr);
-    CU(cudaMemcpy(hR.data(), R, sizeof(int32_t) * hR.size(), cudaMemcpyDeviceToHost));
+    CU(cudaMemcpyAsync(hR.data(), R, sizeof(int32_t) * hR.size(), cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
     Problem pr;
     const int marg2 = mode2 == MODE_MARG ? 1 : 0;
     if ((rc = validate(hR.data(), nr, mr, d, marg2, &pr))) return rc;
