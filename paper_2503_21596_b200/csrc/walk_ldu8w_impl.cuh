@@ -1,9 +1,9 @@
-// Hot d-ary Gray walk for L_3, column sums packed four per register as offset bytes,
-// the LAST PR (3 or 4) rows evaluated for all 3^PR labellings at every walked word, with
-// every group's 2^PR bias sums kept as plain |.|-sums ("all-H" form) and the bias words
+// Hot d-ary Gray walk for L_3 and L_4, column sums packed four per register as offset bytes,
+// the LAST PR rows (L_3: 3-5, L_4: 3-4) evaluated for all D^PR labellings at every walked word,
+// with every group's 2^PR bias sums kept as plain |.|-sums ("all-H" form) and the bias words
 // staged in shared memory.
 //
-// Same units, restricted-growth prefixes, warp-uniform reflected ternary walk (PAPER.md
+// Same units, restricted-growth prefixes, warp-uniform reflected D-ary walk (PAPER.md
 // Eqs. 13-17) and byte encoding as walk_ldu8_impl.cuh (read its header first): group g's
 // column sum m_g,y lives in [N_y, N_y + W_y], a_g,y = m_g,y - N_y is one unsigned byte
 // when every W_y <= 255, one 32-bit add of a packed row moves a row between two groups
@@ -12,27 +12,28 @@
 // What differs.  For a subset T of the paired rows let
 //     H[T][g] = sum_y |m_g,y + sum_{i in T} rho_i,y|        (T = {} is the plain ||m_g||_1)
 // = sum_y |a_g,y - B_T,y| + kappa_T  with B_T = clamp(-N - sum_{i in T} rho_i, 0, 255).  A
-// labelling of the paired rows is the partition (T_0, T_1, T_2) of them by label, and by
+// labelling of the paired rows is the partition (T_0, .., T_{D-1}) of them by label, and by
 // Eq. (6) the strategy's value is exactly
-//     L*(walked word, labelling) = H[T_0][0] + H[T_1][1] + H[T_2][2]
-// -- three non-negative terms, no running S or differences to maintain.  A move p -> q
-// re-accumulates the 2^PR sums of the two changed groups (2 * 2^PR * NW VABSDIFF4 on the
-// ALU pipe), the 3^PR candidate values are two IMADs each (FMA-heavy pipe) and one max
-// tree over them and the running best (ceil(3^PR / 2) VIMNMX3, ALU).  Per strategy that is
-// (2 * 2^PR * c/4 + 3^PR / 2) / 3^PR ALU instructions: 4.07 at PR = 3, 2.88 at PR = 4 for
-// 24 columns (the all-E form of walk_ldu8_impl.cuh at PR = 3 needs the same 4.07).
+//     L*(walked word, labelling) = sum_g H[T_g][g]
+// -- D non-negative terms, no running S or differences to maintain.  A move p -> q
+// re-accumulates the 2^PR sums of the two changed groups (2 * 2^PR * NW VABSDIFF4 on the ALU
+// pipe); the best labelling of the word is a max-plus subset convolution over the H (LdW::
+// conv_best: G_2(U) = max_{T subset U} H[T][1] + H[U \ T][0], for L_4 G_3(U) likewise from
+// G_2, then the last label's term), 3^PR (+ 3^PR for L_4) + 2^PR additions as subnormal-float
+// FADDs (FMA pipes) and about D^PR / 2 three-input maxes (ALU).  At 24 columns that is 2.96
+// ALU instructions per strategy at PR = 4 and 2.14 at PR = 5 (round 1's all-E walk: 4.07).
 //
-// The 2^PR * NW bias words do not fit the register file next to 48 H sums at PR = 4, so they
-// are read per move from shared memory with warp-uniform LDS.128 broadcasts (four bias sets of
-// one word each, shared by the two moved groups); the K_T constants stay in registers.
+// The 2^PR * NW bias words do not fit the register file next to the H sums, so they are read per
+// move from shared memory with warp-uniform LDS.128 broadcasts (four bias sets of one word each,
+// shared by the two moved groups); the kappa sums stay in registers, or at five paired rows in
+// shared memory as well (LdW::KS).
 //
-// Control: a move of the reflected ternary walk is 0->1, 1->2, 2->1 or 1->0; the kernel holds
-// TWO sum bodies (groups {0,1} and {1,2}; the direction only picks which of the delta
-// record's +row / -row each group adds, a uniform shared-memory offset) and ONE copy of the
-// max tree, so the hot code stays small for the instruction cache.  The changed digit, old
-// and new label come from the uniform word counter: inside a block of three
-// words the low digit moves 0->1->2 (even block) or 2->1->0 (odd block: label complement),
-// the block start is dary_block_start (Eq. 17).
+// Control: a move of the reflected D-ary walk is between adjacent labels lo and lo + 1; the
+// kernel holds D - 1 sum bodies (the direction only picks which of the delta record's +row /
+// -row each group adds, a uniform shared-memory offset) and ONE copy of the convolution, so the
+// hot code stays small for the instruction cache.  The changed digit, old and new label come
+// from the uniform word counter: inside a block of D words the low digit moves 0 -> D-1 (even
+// block) or back (odd block), the block start is dary_block_start (Eq. 17).
 #include <type_traits>
 #include <utility>
 
