@@ -1624,6 +1624,7 @@ int lnorm_prefix_maxima(const int32_t* M, int32_t n, int32_t m, int32_t d, int32
   S.column_updates = S.steps * pr.c * (pr.mode == MODE_LD && base >= 3 ? 2 : 1);
   S.walk_ms = wms; S.total_ms = wms; S.launches = pl.kernel == K_GEN ? 1 : 2; S.variant = pl.kernel;
   S.block_threads = block; S.grid_blocks = grid;
+  S.paired_rows = pl.kernel == K_LDU8 ? walk_ldu8_paired_rows(pr.dl, pl.s) : (pl.kernel == K_U8 ? 1 : 0);
   g_stats = S;
   return LNORM_OK;
 }

@@ -338,6 +338,30 @@ def test_ldu8_paired_rows_every_suffix_length(lib, d, s, allh, monkeypatch):
     check(lib, M, d=d)
 
 
+@pytest.mark.parametrize("d,cap", [(3, 3), (3, 4), (3, 5), (4, 3), (4, 4)])
+def test_allh_instances_every_width(lib, d, cap, monkeypatch):
+    """The all-H byte d-ary walk (walk_ldu8w) at every paired-row count it compiles (L_3: 3-5,
+    L_4: 3-4, capped with LNORM_LDU8W_PR) over column counts that hit both translation-unit
+    halves, ragged last words, the five-row instances with kappas in shared memory (all but
+    24 columns) and registers (24): per-prefix maxima of random RGS-free prefixes against the
+    oracle, through the prefix hook with an 8-row suffix."""
+    monkeypatch.setenv("LNORM_LDU8W_PR", str(cap))
+    n = 13 if d == 3 else 11
+    for c in (5, 13, 24, 27, 33, 47):
+        M = synth.random_matrix(n, c, 65_000 + 100 * d + 10 * cap + c, -5, 5)
+        nfixed = n - 8
+        g = synth.SplitMix64(650 + c + d)
+        P = np.zeros((24, nfixed), dtype=np.int8)
+        for i in range(24):
+            for x in range(1, nfixed):
+                P[i, x] = g.next() % d
+        got = lib.prefix_maxima(M, P, d=d)
+        st = lib.last_stats()
+        assert st["variant"] == 8 and st["paired_rows"] == cap, (c, st["paired_rows"])
+        for i in range(24):
+            assert got[i] == oracle.prefix_max(M, P[i], d=d)[0], (c, i, list(P[i]))
+
+
 def test_bench_configs_plan_the_byte_kernel(lib):
     """The 42x42 L_1 and 40x40 L_marg bench workloads run the byte-packed kernel."""
     assert lib.plan(synth.random_matrix(42, 42, 2))["variant_name"] == "bin_u8"
