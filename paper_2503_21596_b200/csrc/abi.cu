@@ -494,7 +494,7 @@ int make_plan(const Problem& pr, int world, Plan* pl, int64_t target_override = 
 __global__ void orient_kernel(const int32_t* in, int n, int m, int transpose, int32_t* out, int batch = 1,
                               unsigned long long* ctl = nullptr) {
   if (ctl && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
-    ctl[0] = 0ull; ctl[1] = 0ull; ctl[2] = 0ull; ctl[3] = ~0ull; ctl[4] = 0ull;
+    ctl[0] = 0ull; ctl[1] = 0ull; ctl[2] = 0ull; ctl[3] = ~0ull; ctl[4] = 0ull; ctl[5] = 0ull;
   }
   const int64_t total = (int64_t)n * m;
   for (int b = blockIdx.y; b < batch; b += gridDim.y) {
@@ -510,15 +510,17 @@ __global__ void orient_kernel(const int32_t* in, int n, int m, int transpose, in
 // Control block of one search (device):
 //   [0] work counter (generic kernel)   [1] max reduction key   [2] error flag
 //   [3] min lexicographic suffix key (recovery)   [4] max value the recovery re-walk
-//   saw, biased like the key (self-check).  [1] and [2] are adjacent: the multi-rank
+//   saw, biased like the key (self-check).  [5] the byte walks' dynamic chunk counter (zeroed by
+//   their table-build kernel before every walk launch).  [1] and [2] are adjacent: the multi-rank
 //   all-reduce(max) combines the key and the "some rank failed" flag in ONE call.
-constexpr int kCtlWords = 5;
+constexpr int kCtlWords = 6;
 __global__ void init_ctl_kernel(unsigned long long* ctl) {
   ctl[0] = 0ull;
   ctl[1] = 0ull;
   ctl[2] = 0ull;
   ctl[3] = ~0ull;
   ctl[4] = 0ull;
+  ctl[5] = 0ull;
 }
 
 // Test hook (LNORM_TEST_CORRUPT_KEY=delta): shift the reduced key's value by delta so
@@ -814,7 +816,7 @@ int run_device(DevCtx& cx, const int32_t* dIn, const Problem& pr, int rank, int 
     wp.M = cx.dM; wp.r = pr.r; wp.c = pr.c; wp.mode = pr.mode; wp.d = pr.dl; wp.k = pl.k; wp.s = pl.s;
     wp.pbits = prefix_bits(pr.dl);
     wp.key_shift = pl.key_shift;
-    wp.counter = cx.dCtl; wp.key = cx.dCtl + 1; wp.unit_max = nullptr;
+    wp.counter = cx.dCtl; wp.key = cx.dCtl + 1; wp.unit_max = nullptr; wp.chunk_ctr = cx.dCtl + 5;
 #if LN_SELFCHECK
     if (const char* e = getenv("LNORM_SELFCHECK_INJECT")) wp.selfcheck_delta = atoi(e);
 #endif
@@ -1433,7 +1435,7 @@ int lnorm_compute_batch(const int32_t* M, int32_t batch, int32_t n, int32_t m, i
   WalkParams wp{};
   wp.M = dMo; wp.r = pr.r; wp.c = pr.c; wp.mode = pr.mode; wp.d = pr.dl; wp.k = pl.k; wp.s = pl.s;
   wp.pbits = prefix_bits(pr.dl); wp.prefix_table = ptab.empty() ? nullptr : cx->dPre;
-  wp.counter = cx->dCtl; wp.key = keys; wp.unit_max = nullptr;
+  wp.counter = cx->dCtl; wp.key = keys; wp.unit_max = nullptr; wp.chunk_ctr = cx->dCtl + 5;
   wp.unit_begin = 0; wp.unit_count = pl.units * batch;
   wp.batch = batch; wp.units_per = pl.units; wp.m_stride = (int64_t)nm; wp.tab_stride = tabw; wp.init_stride = initw; wp.one = 1;
   wp.u8_lpu = bkern == K_U8 ? pl.u8_lpu : 1;
@@ -1608,7 +1610,7 @@ int lnorm_prefix_maxima(const int32_t* M, int32_t n, int32_t m, int32_t d, int32
   wp.M = cx->dM; wp.r = n; wp.c = m; wp.mode = pr.mode; wp.d = base; wp.k = pl.k; wp.s = pl.s;
   wp.unit_begin = 0; wp.unit_count = count; wp.prefix_table = cx->dPre; wp.pbits = pb;
   walk_params_single(wp);
-  wp.counter = cx->dCtl; wp.key = cx->dCtl + 1; wp.unit_max = cx->dUnit;
+  wp.counter = cx->dCtl; wp.key = cx->dCtl + 1; wp.unit_max = cx->dUnit; wp.chunk_ctr = cx->dCtl + 5;
   int grid = 0, block = 0;
   CU(cudaEventRecord(cx->ev[1], s));
   if ((rc = launch_walk(*cx, pr, pl, wp, &grid, &block))) return rc;

@@ -36,6 +36,10 @@ struct WalkParams {
   const uint64_t* prefix_table;  // packed prefix digits (pbits per row 0..k) or nullptr:
                                  //   binary arithmetic prefix, digit of row x = bit (k-x) of u
   unsigned long long* counter;   // work counter (zeroed before launch)
+  // dynamic chunk schedule of the byte walks (LN_DYN_CHUNKS): chunks beyond the first wave are
+  // handed out by an atomicAdd on this word, zeroed by the table-build kernel that precedes every
+  // walk launch; nullptr = static round-robin chunks
+  unsigned long long* chunk_ctr;
   unsigned long long* key;       // global max key (zeroed before launch)
   int64_t* unit_max;             // optional per-unit maxima (index u - unit_begin)
   // batched launches (walk_pair16 only; every other kernel uses batch == 1):
@@ -97,6 +101,26 @@ __device__ __forceinline__ uint4 lds128(uint32_t saddr) {
   asm volatile("ld.volatile.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
                : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(saddr));
   return v;
+}
+
+// Dynamic chunk schedule (byte walks).  A warp's first chunk is blockIdx.x; every later one is
+// gridDim.x + an atomicAdd on p.chunk_ctr by lane 0 when the warp finishes its current chunk
+// (fetched at the end, not prefetched: a prefetched index would stay live across the walk and
+// push the 168-register L_3 instances into stack spills).  Warps that the schedulers favour take
+// more chunks, so every warp of the grid stays resident until the work runs out (static
+// round-robin chunks left ~20 % of the resident warps idle at the end of L_3 searches: ncu
+// sm__warps_active 9.5 of 12).  The reduction key orders by value and unit only, so the result
+// does not depend on which warp walked a chunk.
+#ifndef LN_DYN_CHUNKS
+#define LN_DYN_CHUNKS 1
+#endif
+__device__ __forceinline__ int64_t next_chunk(int64_t ch, unsigned long long* ctr, int lane) {
+  if (LN_DYN_CHUNKS && ctr) {
+    unsigned long long nx = 0;
+    if (lane == 0) nx = atomicAdd(ctr, 1ull);
+    return (int64_t)gridDim.x + (int64_t)__shfl_sync(0xffffffffu, nx, 0);
+  }
+  return ch + gridDim.x;
 }
 
 __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {

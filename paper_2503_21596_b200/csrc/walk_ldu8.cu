@@ -78,7 +78,7 @@ cudaError_t walk_ldu8_launch(const WalkParams& p, int32_t* scratch_tab, int32_t*
     return cudaErrorInvalidValue;
   uint32_t* tab = reinterpret_cast<uint32_t*>(scratch_tab);
   build_ldu8_kernel<<<p.batch, 128, 0, st>>>(p.M, p.r, p.c, NW, p.k, p.s, pr, tab, scratch_init, p.m_stride,
-                                             p.tab_stride, p.init_stride);
+                                             p.tab_stride, p.init_stride, p.chunk_ctr);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   if (wr && p.d == 4) return pt ? walk_ldu8w_launch_part<4, 1>(p, tab, scratch_init, grid, st, NW, wr)

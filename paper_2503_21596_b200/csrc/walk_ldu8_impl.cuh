@@ -286,7 +286,7 @@ walk_ldu8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const in
   const int64_t nchunks = BAT ? CPM * p.batch : CPM;
   int cur_b = BAT ? -1 : 0;
   if constexpr (!BAT) stage(0);
-  for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+  for (int64_t ch = blockIdx.x; ch < nchunks; ch = next_chunk(ch, p.chunk_ctr, lane)) {
     int64_t lc = ch;
     const int32_t* gI = gInit;
     if constexpr (BAT) {
@@ -386,7 +386,9 @@ walk_ldu8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const in
 }
 
 __global__ void build_ldu8_kernel(const int32_t* M, int r, int c, int NW, int k, int s, int pr, uint32_t* tab,
-                                  int32_t* init, int64_t m_stride, int64_t tab_stride, int64_t init_stride) {
+                                  int32_t* init, int64_t m_stride, int64_t tab_stride, int64_t init_stride,
+                                  unsigned long long* chunk_ctr) {
+  if (chunk_ctr && blockIdx.x == 0 && threadIdx.x == 0) *chunk_ctr = 0ull;   // the next walk's chunk schedule
   M += blockIdx.x * m_stride;              // one block per matrix of a batch
   tab += blockIdx.x * tab_stride;
   init += blockIdx.x * init_stride;

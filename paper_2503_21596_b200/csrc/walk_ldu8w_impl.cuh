@@ -370,7 +370,7 @@ walk_ldu8w_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const i
   const int64_t nchunks = BAT ? CPM * p.batch : CPM;
   int cur_b = BAT ? -1 : 0;
   if constexpr (!BAT) stage(0);
-  for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+  for (int64_t ch = blockIdx.x; ch < nchunks; ch = next_chunk(ch, p.chunk_ctr, lane)) {
     int64_t lc = ch;
     const int32_t* gI = gInit;
     if constexpr (BAT) {

@@ -337,7 +337,7 @@ walk_u8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int3
   const int64_t nchunks = BAT ? CPM * p.batch : CPM;
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sT);
   int cur_b = BAT ? -1 : 0;
-  for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+  for (int64_t ch = blockIdx.x; ch < nchunks; ch = next_chunk(ch, p.chunk_ctr, lane)) {
     int64_t lc = ch;
     const int32_t* gI = gInit;
     if constexpr (BAT) {
@@ -532,7 +532,9 @@ walk_u8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int3
 // records; the byte window covers the last s + lg rows (lg = log2 of the lane group).
 template <int MODE>
 __global__ void build_u8_kernel(const int32_t* M, int r, int c, int NW, int k, int s, int lg, int lpu, uint32_t* tab,
-                                int32_t* init, int64_t m_stride, int64_t tab_stride, int64_t init_stride) {
+                                int32_t* init, int64_t m_stride, int64_t tab_stride, int64_t init_stride,
+                                unsigned long long* chunk_ctr) {
+  if (chunk_ctr && blockIdx.x == 0 && threadIdx.x == 0) *chunk_ctr = 0ull;   // the next walk's chunk schedule
   M += blockIdx.x * m_stride;              // one block per matrix of a batch
   tab += blockIdx.x * tab_stride;
   init += blockIdx.x * init_stride;
@@ -720,7 +722,8 @@ cudaError_t walk_u8_launch_mode<LN_BIN_MODE>(const WalkParams& p, int32_t* scrat
   const int lpu = (p.u8_lpu == 2 && lmax == 2) ? 2 : 1;
   const int P = [&]() -> int { LN_U8_SWITCH(LN_BIN_MODE, NW, upl_u8, lpu) return 1; }();
   build_u8_kernel<LN_BIN_MODE><<<p.batch, 256, 0, st>>>(p.M, p.r, p.c, NW, p.k, p.s, P >= 8 ? 3 : P >= 4 ? 2 : (P == 2 ? 1 : 0),
-                                                        lpu, tab, scratch_init, p.m_stride, p.tab_stride, p.init_stride);
+                                                        lpu, tab, scratch_init, p.m_stride, p.tab_stride, p.init_stride,
+                                                        p.chunk_ctr);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   LN_U8_SWITCH(LN_BIN_MODE, NW, launch_u8, p, tab, scratch_init, grid, st)
