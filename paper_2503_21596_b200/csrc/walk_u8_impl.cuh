@@ -55,6 +55,31 @@ __device__ __forceinline__ uint32_t sad4(uint32_t a, uint32_t b, uint32_t acc) {
   return d;
 }
 
+// Per-byte |a_b - b_b| (no accumulate): VABSDIFF4.U8 with the full byte mask
+__device__ __forceinline__ uint32_t absdiff4_bytes(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("vabsdiff4.u32.u32.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(0u));
+  return d;
+}
+// acc + sum_b x_b * w_b over unsigned bytes: IDP.4A (FMA-heavy pipe), used with a 0/1 byte mask w
+__device__ __forceinline__ uint32_t dp4a_u(uint32_t x, uint32_t w, uint32_t acc) {
+  uint32_t d;
+  asm("dp4a.u32.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(x), "r"(w), "r"(acc));
+  return d;
+}
+
+// Merged last word (MRG, LN_U8_MERGE): when the last packed word holds only one or two live
+// columns (c mod 4 = 1 or 2 -- e.g. 42 columns = 10 full words + 2), units 2i and 2i+1 of a lane
+// group keep those columns in ONE register (unit 2i in bytes 0-1, unit 2i+1 in bytes 2-3; their
+// bias bytes are shared, the delta record's last word is duplicated into bytes 2-3).  One
+// per-byte VABSDIFF4 (ALU) then serves both units, and two IDP.4A with the byte masks 0x0101 /
+// 0x01010000 (FMA-heavy pipe) add each unit's two bytes to its own sum -- the ALU pipe, which
+// binds, does 21 instead of 22 VABSDIFF4 per unit and word at 42 columns.  Measured 3.4 % SLOWER
+// on 42x42 L_1 (1490 vs 1441 ms, profiles/r02/ab_u8_merge.log): off by default (no instances).
+#ifndef LN_U8_MERGE
+#define LN_U8_MERGE 0
+#endif
+
 // Self-check build (`python -m paper_2503_21596_b200.build --selfcheck`): after
 // every Gray step, unit 0 of every lane recomputes its word's NS strategy values FROM SCRATCH
 // (Eq. 1 / Eq. 2 / Eq. 6 over all r rows of the oriented M, no bytes, no Gray state) and counts
@@ -179,13 +204,14 @@ __host__ __device__ constexpr int u8_unroll() {
 // is a non-negative integer <= sum |M| <= 65535: L_1 and L_2, host-checked), so ONE VIMNMX3.U16x2
 // serves the four strategies (two units x the paired row's two signs) of a walked word; the two
 // values are packed by an IMAD (FMA-heavy pipe) -- half the epilogue's ALU instructions.
-template <int MODE, int NW, int P, int LPU = 1, bool PK = false>
+template <int MODE, int NW, int P, int LPU = 1, bool PK = false, bool MRG = false>
 struct U8Step {
   // NW here = the words THIS lane holds (half of the unit's words when LPU = 2)
   static constexpr int PR = u8_pr<MODE>(), NS = 1 << PR;   // paired rows, bias sets
   static_assert(LPU == 1 || PR >= 1, "lane pairs need the paired epilogue");
   static constexpr int G = U8Layout<MODE, NW>::G, RW = U8Layout<MODE, NW>::RW;
   static constexpr int NB = NS * G * NW;        // bias words: set h (paired-row signs h) x group
+  static_assert(!MRG || (G == 1 && LPU == 1 && PR >= 1 && P % 2 == 0 && NW >= 2 && !PK), "merged last word");
   // One Gray step: add the packed delta record at sbase + off to every unit's bytes,
   // re-accumulate sum |a - B| (and sum |a - B'| for the paired strategy), keep the max.
   // vout (self-check builds only, LN_SELFCHECK): receives unit 0's NS strategy values of the word
@@ -200,7 +226,18 @@ struct U8Step {
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int i = 4 * v + e;
-        if (i < NW) {
+        if (MRG && i == NW - 1) {                  // the merged last word of unit pairs (2i, 2i+1)
+#pragma unroll
+          for (int j = 0; j < P; j += 2) {
+            A[j][i] = u8_add(A[j][i], rq[e], one);
+#pragma unroll
+            for (int h = 0; h < NS; ++h) {
+              const uint32_t x = absdiff4_bytes(A[j][i], B[h * NW + i]);
+              hs[j][h][0] = dp4a_u(x, 0x00000101u, hs[j][h][0]);
+              hs[j + 1][h][0] = dp4a_u(x, 0x01010000u, hs[j + 1][h][0]);
+            }
+          }
+        } else if (i < NW) {
 #pragma unroll
           for (int j = 0; j < P; ++j) {
             A[j][i] = u8_add(A[j][i], rq[e], one);
@@ -302,7 +339,7 @@ __host__ __device__ constexpr int u8_min_blocks() {
 // local chunk lc; chunks never straddle matrices and a warp restages the delta table when it
 // moves to the next matrix).  The single-search instance (BAT = false) keeps the table staged
 // once and no per-chunk bookkeeping (the batch state costs registers the hot loop needs).
-template <int MODE, int NW, int P, int LPU, bool BAT = false, bool PK = false>
+template <int MODE, int NW, int P, int LPU, bool BAT = false, bool PK = false, bool MRG = false>
 __global__ void __launch_bounds__(kBlockU8, u8_min_blocks<MODE, NW, P, LPU>())
 walk_u8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int32_t* __restrict__ gInit) {
   using LY = U8Layout<MODE, NW>;
@@ -313,7 +350,7 @@ walk_u8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int3
   constexpr int RREC = LPU * RWL;                  // words per delta record
   constexpr int GPW = 32 / LPU;                    // lane groups per warp
   constexpr int K = u8_unroll<MODE, NWL, P>();
-  using STEP = U8Step<MODE, NWL, P, LPU, PK>;
+  using STEP = U8Step<MODE, NWL, P, LPU, PK, MRG>;
   constexpr int NB = STEP::NB;
   extern __shared__ __align__(16) uint32_t sT[];
   const int lane = threadIdx.x & 31;
@@ -468,6 +505,15 @@ walk_u8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int3
       }
       best[j] = v0;
     }
+    if constexpr (MRG) {                               // merge the last words: unit 2i+1's bytes 0-1 -> 2i's bytes 2-3
+#pragma unroll
+      for (int h = 0; h < NS; ++h) {
+        const uint32_t b = B[h * NWL + NWL - 1] & 0xFFFFu;
+        B[h * NWL + NWL - 1] = b | (b << 16);
+      }
+#pragma unroll
+      for (int j = 0; j < P; j += 2) A[j][NWL - 1] = (A[j][NWL - 1] & 0xFFFFu) | (A[j + 1][NWL - 1] << 16);
+    }
     if constexpr (PK) {                                // two units' maxima per register (lo: unit 2i)
 #pragma unroll
       for (int i = 0; i < P / 2; ++i) best[i] = (int32_t)(((uint32_t)best[2 * i + 1] << 16) | (uint32_t)best[2 * i]);
@@ -533,7 +579,7 @@ walk_u8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int3
 template <int MODE>
 __global__ void build_u8_kernel(const int32_t* M, int r, int c, int NW, int k, int s, int lg, int lpu, uint32_t* tab,
                                 int32_t* init, int64_t m_stride, int64_t tab_stride, int64_t init_stride,
-                                unsigned long long* chunk_ctr) {
+                                unsigned long long* chunk_ctr, int mrg) {
   if (chunk_ctr && blockIdx.x == 0 && threadIdx.x == 0) *chunk_ctr = 0ull;   // the next walk's chunk schedule
   M += blockIdx.x * m_stride;              // one block per matrix of a batch
   tab += blockIdx.x * tab_stride;
@@ -556,6 +602,7 @@ __global__ void build_u8_kernel(const int32_t* M, int r, int c, int NW, int k, i
         const int32_t v = (ql < NWL && y < c) ? f * row[y] : 0;
         w += (uint32_t)v << (8 * e);       // packed signed delta sum_e 256^e delta_e (mod 2^32)
       }
+      if (mrg && q == NW - 1) w *= 65537u;   // merged last word: the same delta for bytes 2-3 (D + 2^16 D)
       tab[rec * RW + i] = w;
     }
   }
@@ -592,10 +639,26 @@ constexpr int kU8BatchMaxNW = 8;
 #endif
 constexpr int kU8PackMaxNW = LN_U8_PACKMAX ? 16 : 0;
 
+// merged-last-word instances (MRG): 33-48 columns (the m = n sweep and the 42x42 headline)
+template <int MODE, int NW, int LPU>
+__host__ __device__ constexpr bool u8_has_mrg() {
+  return LN_U8_MERGE && LPU == 1 && MODE != MODE_LD && NW >= 9 && NW <= 12 && u8_units_per_lane<MODE, NW, LPU>() % 2 == 0 &&
+         u8_pr<MODE>() >= 1;
+}
+inline bool u8_mrg_cols(int c) { return (c & 3) == 1 || (c & 3) == 2; }
+
 template <int MODE, int NW, int LPU>
 cudaError_t launch_u8_l(const WalkParams& p, const uint32_t* tab, const int32_t* init, int grid, cudaStream_t st) {
   constexpr int P = u8_units_per_lane<MODE, NW, LPU>();
   const size_t sm = u8_smem<MODE, NW, LPU>(p.s);
+  if constexpr (u8_has_mrg<MODE, NW, LPU>()) {
+    if (p.batch == 1 && u8_mrg_cols(p.c)) {
+      cudaError_t e = ensure_dyn_smem((const void*)walk_u8_kernel<MODE, NW, P, LPU, false, false, true>, sm);
+      if (e != cudaSuccess) return e;
+      walk_u8_kernel<MODE, NW, P, LPU, false, false, true><<<grid, kBlockU8, sm, st>>>(p, tab, init);
+      return cudaGetLastError();
+    }
+  }
   if (p.batch > 1) {
     if constexpr (NW <= kU8BatchMaxNW && LPU == 1) {
       cudaError_t e = ensure_dyn_smem((const void*)walk_u8_kernel<MODE, NW, P, LPU, true>, sm);
@@ -653,6 +716,9 @@ int upl_u8(int lpu) {
 
 template <int MODE, int NW>
 int lpu_u8() { return u8_lpu_max<MODE, NW>(); }
+
+template <int MODE, int NW>
+int mrg_u8(int lpu) { return lpu == 1 && u8_has_mrg<MODE, NW, 1>() ? 1 : 0; }
 
 template <int MODE, int NW>
 int unroll_u8(int lpu) {
@@ -721,9 +787,10 @@ cudaError_t walk_u8_launch_mode<LN_BIN_MODE>(const WalkParams& p, int32_t* scrat
   const int lmax = [&]() -> int { LN_U8_SWITCH(LN_BIN_MODE, NW, lpu_u8) return 1; }();
   const int lpu = (p.u8_lpu == 2 && lmax == 2) ? 2 : 1;
   const int P = [&]() -> int { LN_U8_SWITCH(LN_BIN_MODE, NW, upl_u8, lpu) return 1; }();
+  const int mrg = [&]() -> int { LN_U8_SWITCH(LN_BIN_MODE, NW, mrg_u8, lpu) return 0; }() && p.batch == 1 && u8_mrg_cols(p.c);
   build_u8_kernel<LN_BIN_MODE><<<p.batch, 256, 0, st>>>(p.M, p.r, p.c, NW, p.k, p.s, P >= 8 ? 3 : P >= 4 ? 2 : (P == 2 ? 1 : 0),
                                                         lpu, tab, scratch_init, p.m_stride, p.tab_stride, p.init_stride,
-                                                        p.chunk_ctr);
+                                                        p.chunk_ctr, mrg);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   LN_U8_SWITCH(LN_BIN_MODE, NW, launch_u8, p, tab, scratch_init, grid, st)

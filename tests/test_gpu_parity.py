@@ -530,3 +530,21 @@ def test_sliced_ranks_42x42_planted(lib):
     expect = sum(oracle.l1(B)[0] for B in blocks)
     v, arg = lib.compute_sliced(M, 8)
     assert v == expect and oracle.value(M, arg) == v
+
+
+@pytest.mark.parametrize("marg", [False, True], ids=["L1", "marg"])
+@pytest.mark.parametrize("c", [33, 34, 37, 38, 41, 42, 45, 46])
+def test_u8_merged_last_word(lib, c, marg):
+    """Byte walk with c mod 4 in {1, 2} (a partly padded last word; with LN_U8_MERGE=1 the merged
+    last-word instances of walk_u8_impl.cuh): the full search and EVERY unit's maximum (all four
+    units of each lane group) equal the oracle's."""
+    n = 14
+    M = synth.random_matrix(n, c, 1300 + c + 50 * marg)
+    check(lib, M, d=1, marg=marg)
+    assert lib.last_stats()["variant"] == 7
+    k = 8
+    units = np.arange(1 << k, dtype=np.uint64)
+    got = lib.unit_maxima(M, k, units, with_marginals=marg)
+    for u, gv in zip(units.tolist(), got):
+        pre = [0] + [(u >> (k - x)) & 1 for x in range(1, k + 1)]
+        assert gv == oracle.prefix_max(M, pre, with_marginals=marg)[0], (u, c, marg)
