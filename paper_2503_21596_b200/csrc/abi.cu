@@ -349,7 +349,11 @@ int u8_min_walk() {
   return v;
 }
 constexpr double kLdInitStrategies = 500.0;   // a byte d-ary unit's init, in walked strategies (24 columns)
-constexpr int kU8MinSuffix = 6;   // shortest byte-walk suffix preferred over a packed 16-bit walk
+constexpr int kU8MinSuffix = 6;
+constexpr double kU8InitWords = 8.0;
+#ifndef LN_U8_SMALL_PLAN
+#define LN_U8_SMALL_PLAN 1
+#endif   // a byte binary unit's init, in walked words (its prefix rows summed per word)   // shortest byte-walk suffix preferred over a packed 16-bit walk
 
 int make_plan(const Problem& pr, int world, Plan* pl, int64_t target_override = 0, bool allow_u8 = true) {
   const int f = pr.r - 1;
@@ -392,6 +396,27 @@ int make_plan(const Problem& pr, int world, Plan* pl, int64_t target_override = 
           // short suffixes spend their time in the lane init: keep s >= u8_min_walk() while the
           // split still leaves ~2^21 units (several chunks per resident warp)
           while (f - k < u8_min_walk() && k > std::max(lg, 21) && f - k < su) --k;
+          if (LN_U8_SMALL_PLAN && (1LL << k) < target && target_override == 0) {
+            // Small searches (below ~2^23 units: 24x24 L_2, 20-30 rows): the split above takes
+            // the shortest suffix the instance allows, which can leave slightly more units than
+            // one wave of resident unit slots, each paying an init for a walk of a few words.
+            // Pick the prefix length minimising ceil(units / slots) * (init + walked words),
+            // as the d-ary planner does (kU8InitWords: a unit's init in walked words).
+            const double slots = (double)kNominalLanes / 2 * std::max(1, world) *
+                                 walk_u8_units_per_lane(pr.mode, pr.c, lpu) / lpu;
+            const int pr1 = pr.mode == MODE_L1 ? walk_u8_paired_rows_mode<MODE_L1>()
+                          : pr.mode == MODE_MARG ? walk_u8_paired_rows_mode<MODE_MARG>() : walk_u8_paired_rows_mode<MODE_LD>();
+            auto cost = [&](int kk) {
+              return std::ceil(std::ldexp(1.0, kk) / slots) * (kU8InitWords + std::ldexp(1.0, f - kk - pr1));
+            };
+            int best_k = k;
+            double best_c = cost(k);
+            for (int kk = k - 1; kk >= std::max(lg, f - su); --kk) {
+              const double c = cost(kk);
+              if (c < best_c) { best_c = c; best_k = kk; }
+            }
+            k = best_k;
+          }
           p.k = k; p.s = f - k; p.units = 1LL << k;
           p.kernel = K_U8;
           p.u8_lpu = lpu;
