@@ -147,7 +147,62 @@ __device__ __forceinline__ int32_t w_max_tree(const int32_t (&v)[N]) {
   }
 }
 
-template <int D, int NW, int PR>
+// PK (two units per lane, every H / convolution value of the two units packed as unsigned 16-bit
+// halves): VIADD.16x2 (FMA pipe) adds both units' candidates in one instruction and VIMNMX3.U16x2
+// (ALU) takes the max of three pairs -- half the convolution's max instructions per unit.  Exact:
+// every H, convolution value and strategy value is a partial sum of one labelling's value, which
+// is <= sum |M| <= 255 * 48 < 2^16 under the byte guard (every column's sum_x |M_xy| <= 255).
+// LN_LDU8W_PK_IMAD: the packed add as a 32-bit IMAD a * one + b (no half ever carries: both halves
+// stay below 2^16), which ptxas cannot fuse with the following max into an ALU-pipe VIADDMNMX
+// the way it fuses VIADD.16x2 -- the adds stay on the FMA-heavy pipe, the ALU does only maxima
+#ifndef LN_LDU8W_PK_IMAD
+#define LN_LDU8W_PK_IMAD 1
+#endif
+template <bool PK>
+__device__ __forceinline__ int32_t op_add(int32_t a, int32_t b, uint32_t one) {
+  if constexpr (PK) {
+#if LN_LDU8W_PK_IMAD
+    uint32_t r;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"((uint32_t)a), "r"(one), "r"((uint32_t)b));
+    return (int32_t)r;
+#else
+    (void)one;
+    return (int32_t)__vadd2((uint32_t)a, (uint32_t)b);
+#endif
+  } else {
+    return w_fadd(a, b, one);
+  }
+}
+template <bool PK>
+__device__ __forceinline__ int32_t op_max3(int32_t a, int32_t b, int32_t c) {
+  if constexpr (PK) return (int32_t)__vimax3_u16x2((uint32_t)a, (uint32_t)b, (uint32_t)c);
+  else return w_max3(a, b, c);
+}
+template <bool PK>
+__device__ __forceinline__ int32_t op_max2(int32_t a, int32_t b) {
+  if constexpr (PK) return (int32_t)__vmaxu2((uint32_t)a, (uint32_t)b);
+  else return w_max2(a, b);
+}
+template <bool PK, int N>
+__device__ __forceinline__ int32_t op_max_tree(const int32_t (&v)[N]) {
+  if constexpr (N == 1) {
+    return v[0];
+  } else if constexpr (N == 2) {
+    return op_max2<PK>(v[0], v[1]);
+  } else {
+    constexpr int M = (N + 2) / 3;
+    int32_t w[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+      if (3 * i + 2 < N) w[i] = op_max3<PK>(v[3 * i], v[3 * i + 1], v[3 * i + 2]);
+      else if (3 * i + 1 < N) w[i] = op_max2<PK>(v[3 * i], v[3 * i + 1]);
+      else w[i] = v[3 * i];
+    }
+    return op_max_tree<PK, M>(w);
+  }
+}
+
+template <int D, int NW, int PR, bool PK = false>
 struct LdW {
   static constexpr int RW = w_pad4(NW);
   static constexpr int RD = 2 * RW;          // delta record: +row at [0, NW), -row at [RW, RW + NW)
@@ -161,13 +216,13 @@ struct LdW {
     constexpr int m0 = std::integral_constant<int, w_mask(L, 0, PR, D)>::value;
     constexpr int m1 = std::integral_constant<int, w_mask(L, 1, PR, D)>::value;
     constexpr int m2 = std::integral_constant<int, w_mask(L, 2, PR, D)>::value;
-    return w_fadd(w_fadd(H[m0][0], H[m1][1], one), H[m2][2], one);
+    return op_add<PK>(op_add<PK>(H[m0][0], H[m1][1], one), H[m2][2], one);
   }
   template <int... Ls>
   static __device__ __forceinline__ int32_t best_seq(const int32_t (&H)[NS][D], int32_t best, uint32_t one,
                                                      std::integer_sequence<int, Ls...>) {
     int32_t v[NL + 1] = {cand<Ls>(H, one)..., best};
-    return w_max_tree<NL + 1>(v);
+    return op_max_tree<PK, NL + 1>(v);
   }
   // Max-plus subset convolution form of the same maximum (LN_LDU8W_CONV = 1).  A labelling of the
   // paired rows is a partition (T_0, .., T_{D-1}) of them by label, valued sum_g H[T_g][g]; with
@@ -179,12 +234,12 @@ struct LdW {
   template <int U, int I>
   static __device__ __forceinline__ int32_t term01(const int32_t (&H)[NS][D], uint32_t one) {
     constexpr int T = std::integral_constant<int, w_submask(U, I)>::value;
-    return w_fadd(H[T][1], H[U ^ T][0], one);
+    return op_add<PK>(H[T][1], H[U ^ T][0], one);
   }
   template <int U, int... Is>
   static __device__ __forceinline__ int32_t L01(const int32_t (&H)[NS][D], uint32_t one, std::integer_sequence<int, Is...>) {
     int32_t v[sizeof...(Is)] = {term01<U, Is>(H, one)...};
-    return w_max_tree<(int)sizeof...(Is)>(v);
+    return op_max_tree<PK, (int)sizeof...(Is)>(v);
   }
   template <int U>
   static __device__ __forceinline__ int32_t G2(const int32_t (&H)[NS][D], uint32_t one) {
@@ -194,13 +249,13 @@ struct LdW {
   template <int U, int I>
   static __device__ __forceinline__ int32_t term2(const int32_t (&H)[NS][D], const int32_t (&g2)[NS], uint32_t one) {
     constexpr int T = std::integral_constant<int, w_submask(U, I)>::value;
-    return w_fadd(H[T][2], g2[U ^ T], one);
+    return op_add<PK>(H[T][2], g2[U ^ T], one);
   }
   template <int U, int... Is>
   static __device__ __forceinline__ int32_t L2(const int32_t (&H)[NS][D], const int32_t (&g2)[NS], uint32_t one,
                                                std::integer_sequence<int, Is...>) {
     int32_t v[sizeof...(Is)] = {term2<U, Is>(H, g2, one)...};
-    return w_max_tree<(int)sizeof...(Is)>(v);
+    return op_max_tree<PK, (int)sizeof...(Is)>(v);
   }
   // last level, one term per label-(D-1) set T (the complement is the rest of the paired rows);
   // the intermediate level is streamed (L_3) or read from the stored G_2 (L_4), so at most NS
@@ -208,8 +263,8 @@ struct LdW {
   template <int T>
   static __device__ __forceinline__ int32_t last(const int32_t (&H)[NS][D], const int32_t (&g2)[NS], uint32_t one) {
     constexpr int U = (NS - 1) ^ T;
-    if constexpr (D == 3) return w_fadd(H[T][2], G2<U>(H, one), one);
-    else return w_fadd(H[T][3], L2<U>(H, g2, one, std::make_integer_sequence<int, (1 << w_popc(U))>{}), one);
+    if constexpr (D == 3) return op_add<PK>(H[T][2], G2<U>(H, one), one);
+    else return op_add<PK>(H[T][3], L2<U>(H, g2, one, std::make_integer_sequence<int, (1 << w_popc(U))>{}), one);
   }
   template <int... Us>
   static __device__ __forceinline__ void fill_g2(const int32_t (&H)[NS][D], int32_t (&g2)[NS], uint32_t one,
@@ -220,7 +275,7 @@ struct LdW {
   static __device__ __forceinline__ int32_t conv_seq(const int32_t (&H)[NS][D], const int32_t (&g2)[NS], int32_t best,
                                                      uint32_t one, std::integer_sequence<int, Ts...>) {
     int32_t v[NS + 1] = {last<Ts>(H, g2, one)..., best};
-    return w_max_tree<NS + 1>(v);
+    return op_max_tree<PK, NS + 1>(v);
   }
   static __device__ __forceinline__ int32_t conv_best(const int32_t (&H)[NS][D], int32_t best, uint32_t one) {
     int32_t g2[NS];
@@ -308,6 +363,58 @@ struct LdW {
     }
   }
 };
+
+// Packed variant (PK instances): the two units of a lane move the same rows; their bias sums are
+// accumulated in 32 bits (four independent VABSDIFF4 chains per bias set: two units x two groups,
+// all reading the same bias word from the operand-reuse cache) and packed by one IMAD each.  Bias
+// words set-major in shared memory (sbias + 4 (m RW + i)), kappa sums after them (sbias + 4 (NS RW + m)).
+template <int D, int NW, int PR, int GA, int GB>
+__device__ __forceinline__ void sums_pk(uint32_t (&A)[2][D][NW], int32_t (&H)[1 << PR][D], uint32_t rowA,
+                                        uint32_t rowB, uint32_t sbias, uint32_t k16) {
+  constexpr int RW = w_pad4(NW), NS = 1 << PR;
+#pragma unroll
+  for (int v = 0; v < RW / 4; ++v) {
+    const uint4 xa = lds128(rowA + 16u * (uint32_t)v);
+    const uint4 xb = lds128(rowB + 16u * (uint32_t)v);
+    const uint32_t ra[4] = {xa.x, xa.y, xa.z, xa.w}, rb[4] = {xb.x, xb.y, xb.z, xb.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int i = 4 * v + e;
+      if (i < NW) {
+        A[0][GA][i] += ra[e]; A[1][GA][i] += ra[e];
+        A[0][GB][i] += rb[e]; A[1][GB][i] += rb[e];
+      }
+    }
+  }
+#pragma unroll
+  for (int m4 = 0; m4 < NS; m4 += 4) {
+    const uint4 kq = lds128(sbias + 4u * (uint32_t)(NS * RW + m4));
+    const uint32_t kk[4] = {kq.x, kq.y, kq.z, kq.w};
+#pragma unroll
+    for (int mm = 0; mm < 4; ++mm) {
+      const int m = m4 + mm;
+      uint32_t b[RW];
+#pragma unroll
+      for (int v = 0; v < RW / 4; ++v) {
+        const uint4 q = lds128(sbias + 4u * (uint32_t)(m * RW + 4 * v));
+        b[4 * v] = q.x; b[4 * v + 1] = q.y; b[4 * v + 2] = q.z; b[4 * v + 3] = q.w;
+      }
+      uint32_t a0 = kk[mm], a1 = kk[mm], c0 = kk[mm], c1 = kk[mm];
+#pragma unroll
+      for (int i = 0; i < NW; ++i) {
+        a0 = w_sad4(A[0][GA][i], b[i], a0);
+        a1 = w_sad4(A[1][GA][i], b[i], a1);
+        c0 = w_sad4(A[0][GB][i], b[i], c0);
+        c1 = w_sad4(A[1][GB][i], b[i], c1);
+      }
+      uint32_t pa, pc;
+      asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(pa) : "r"(a1), "r"(k16), "r"(a0));
+      asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(pc) : "r"(c1), "r"(k16), "r"(c0));
+      H[m][GA] = (int32_t)pa;
+      H[m][GB] = (int32_t)pc;
+    }
+  }
+}
 
 // Init records: as build_ldu8_kernel writes them (prefix rows 0..k, the walked base, -N,
 // then NS * NW bias words and the NS kappa sums), stride CW = 4 NW.
@@ -470,8 +577,126 @@ walk_ldu8w_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const i
   if (lane == 0 && key) atomicMax(p.key + (BAT && cur_b > 0 ? cur_b : 0), key);
 }
 
+// Packed two-unit instances (single searches; LN_LDU8W_PK): L_3 with five paired rows and L_4 with
+// four, up to 24 columns.
+#ifndef LN_LDU8W_PK
+#define LN_LDU8W_PK 1
+#endif
+template <int D, int NW, int PR>
+__host__ __device__ constexpr bool w_has_pk() {
+  return LN_LDU8W_PK && NW <= 6 && ((D == 3 && PR == 5) || (D == 4 && PR == 4));
+}
+
+// The walk with two units per lane and packed H (see sums_pk / op_add): same units, chunks, Gray
+// control and reduction key as walk_ldu8w_kernel; a chunk is 64 consecutive units (unit j of lane l
+// = chunk base + 32 j + l).
+template <int D, int NW, int PR>
+__global__ void __launch_bounds__(kBlockW, (w_minb<D, NW, PR>()))
+walk_ldu8w_pk_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int32_t* __restrict__ gInit) {
+  using WK = LdW<D, NW, PR, true>;
+  constexpr int P = 2;
+  constexpr int RD = WK::RD, RW = WK::RW, CW = 4 * NW, NS = WK::NS;
+  extern __shared__ __align__(16) uint32_t sT[];
+  const int lane = threadIdx.x & 31;
+  const int sw = p.s - PR;
+  uint32_t* sBias = sT + sw * RD;                 // set-major: sBias[m * RW + q], kappas at NS * RW
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sT);
+  const uint32_t sbias = (uint32_t)__cvta_generic_to_shared(sBias);
+  const uint32_t k16 = p.one << 16;
+  uint32_t nwords = 1;
+  for (int i = 0; i < sw; ++i) nwords *= D;
+  {
+    const uint32_t* biasRec = reinterpret_cast<const uint32_t*>(gInit + (p.k + 3) * CW);
+    for (int i = lane; i < sw * RD; i += 32) sT[i] = gTab[i];
+    for (int i = lane; i < NS * RW; i += 32) {
+      const int m = i / RW, q = i % RW;
+      sBias[i] = q < NW ? biasRec[m * NW + q] : 0u;
+    }
+    for (int m = lane; m < NS; m += 32) sBias[NS * RW + m] = biasRec[NS * NW + m];
+    __syncwarp();
+  }
+  int32_t best_all = INT32_MIN;
+  uint32_t best_u = 0;
+  bool have = false;
+  const int64_t nchunks = (p.units_per + 32 * P - 1) / (32 * P);
+  for (int64_t ch = blockIdx.x; ch < nchunks; ch = next_chunk(ch, p.chunk_ctr, lane)) {
+    uint32_t A[P][D][NW];
+    int32_t H[NS][D];
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
+      const int64_t rel = ch * 32 * P + j * 32 + lane;
+      const int64_t u = p.unit_begin + (rel < p.units_per ? rel : 0);
+      uint64_t lab = 0;
+      if (p.prefix_table) lab = p.prefix_table[u - p.unit_begin];
+      else for (int x = 0; x <= p.k; ++x) lab |= (uint64_t)prefix_digit(p, u, x) << (p.pbits * x);
+      const uint64_t lmask = (1ull << p.pbits) - 1ull;
+      const uint32_t* pkRec = reinterpret_cast<const uint32_t*>(gInit + (p.k + 3) * CW) + NS * NW + NS;
+      const uint32_t* stRec = pkRec + (p.k + 1) * NW;
+#pragma unroll
+      for (int q = 0; q < NW; ++q) {
+        A[j][0][q] = __ldg(stRec + q);
+        const uint32_t sg = __ldg(stRec + NW + q);
+#pragma unroll
+        for (int g = 1; g < D; ++g) A[j][g][q] = sg;
+      }
+      for (int x = 0; x <= p.k; ++x) {
+        const int dig = (int)((lab >> (p.pbits * x)) & lmask);
+#pragma unroll
+        for (int q = 0; q < NW; ++q) {
+          const uint32_t w = __ldg(pkRec + x * NW + q);
+#pragma unroll
+          for (int g = 0; g < D; ++g) A[j][g][q] += (dig == g) ? w : 0u;
+        }
+      }
+#pragma unroll
+      for (int g = 0; g < D; ++g)
+#pragma unroll
+        for (int m = 0; m < NS; ++m) {
+          uint32_t h = sBias[NS * RW + m];
+#pragma unroll
+          for (int q = 0; q < NW; ++q) h = w_sad4(A[j][g][q], sBias[m * RW + q], h);
+          H[m][g] = j == 0 ? (int32_t)h : (int32_t)((uint32_t)H[m][g] | (h << 16));   // unit j in half j
+        }
+    }
+    int32_t best = WK::best_of(H, 0, p.one);       // both units' start words (every value >= 0)
+    uint32_t t = 0, jj = 0;
+    for (uint32_t w = 1; w < nwords; ++w) {
+      uint32_t i, from, to;
+      if (++jj == D) { jj = 0; ++t; }
+      if (jj == 0) {
+        dary_block_start<D>(t, &i, &from, &to);
+      } else {
+        i = 0;
+        const bool odd = (t & 1u) != 0;
+        from = odd ? D - jj : jj - 1;
+        to = odd ? D - 1 - jj : jj;
+      }
+      const uint32_t srow = sbase + 4u * i * (uint32_t)RD;
+      const uint32_t rlo = from < to ? srow + 4u * (uint32_t)RW : srow;
+      const uint32_t rhi = from < to ? srow : srow + 4u * (uint32_t)RW;
+      const uint32_t lo = from < to ? from : to;
+      if (lo == 0) sums_pk<D, NW, PR, 0, 1>(A, H, rlo, rhi, sbias, k16);
+      else if (D == 3 || lo == 1) sums_pk<D, NW, PR, 1, 2>(A, H, rlo, rhi, sbias, k16);
+      else if constexpr (D >= 4) sums_pk<D, NW, PR, 2, 3>(A, H, rlo, rhi, sbias, k16);
+      best = WK::best_of(H, best, p.one);
+    }
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
+      const int64_t rel = ch * 32 * P + j * 32 + lane;
+      const int32_t bj = (int32_t)(j == 0 ? ((uint32_t)best & 0xFFFFu) : ((uint32_t)best >> 16));
+      if (rel < p.units_per) {
+        if (p.unit_max) p.unit_max[rel] = bj;
+        if (!have || bj > best_all) { best_all = bj; best_u = (uint32_t)(p.unit_begin + rel); have = true; }
+      }
+    }
+  }
+  unsigned long long key = have ? make_key(best_all, best_u) : 0ull;
+  key = warp_max_u64(key);
+  if (lane == 0 && key) atomicMax(p.key, key);
+}
+
 template <int NW, int PR>
-size_t w_smem(int s) { return sizeof(uint32_t) * (size_t)((s - PR) * 2 * w_pad4(NW) + (1 << PR) * (NW + 1)); }
+size_t w_smem(int s) { return sizeof(uint32_t) * (size_t)((s - PR) * 2 * w_pad4(NW) + (1 << PR) * (w_pad4(NW) + 1)); }
 
 template <int D, int NW, int PR>
 cudaError_t launch_w(const WalkParams& p, const uint32_t* tab, const int32_t* init, int grid, cudaStream_t st) {
@@ -484,6 +709,12 @@ cudaError_t launch_w(const WalkParams& p, const uint32_t* tab, const int32_t* in
       return cudaGetLastError();
     }
     return cudaErrorInvalidValue;
+  }
+  if constexpr (w_has_pk<D, NW, PR>()) {
+    cudaError_t e = ensure_dyn_smem((const void*)walk_ldu8w_pk_kernel<D, NW, PR>, sm);
+    if (e != cudaSuccess) return e;
+    walk_ldu8w_pk_kernel<D, NW, PR><<<grid, kBlockW, sm, st>>>(p, tab, init);
+    return cudaGetLastError();
   }
   cudaError_t e = ensure_dyn_smem((const void*)walk_ldu8w_kernel<D, NW, PR>, sm);
   if (e != cudaSuccess) return e;
