@@ -54,7 +54,7 @@ def conv_max_ops(d, pr):
     return (d - 2) * level + (2 ** pr + 1) // 2
 
 
-def alu_floor(variant, d, c, s, d_walked, pr=None):
+def alu_floor(variant, d, c, s, d_walked, pr=None, packed=0):
     """Binding-pipe instruction floor per strategy of the kernel family's own algorithm
     (DESIGN.md "Roofline"): (instructions per strategy, pipe, lane-instructions/clk/SM of that pipe).
 
@@ -67,7 +67,9 @@ def alu_floor(variant, d, c, s, d_walked, pr=None):
       max tree over the 2^|U| candidates of every subset U (ceil((2^|U|-1)/2) three-input maxes),
       D - 2 levels, then ceil(2^PR/2) for the last step with the running best (conv_max_ops);
       PR <= 2 is the all-E kernel: the max of the T = d^PR labellings (ceil((T-1)/2)) + 1.
-      Shared by the d^PR strategies of the word, on the ALU pipe.
+      Shared by the d^PR strategies of the word, on the ALU pipe.  Packed two-unit instances
+      (lnorm_stats.packed_units = 2: both units' values as u16 halves) take each max once for
+      the two units: half the max instructions per strategy.
     16-bit / int32 families: issue-bound (both integer pipes), instructions per strategy."""
     if variant == 7:
         G = 2 if d == 2 else 1
@@ -77,6 +79,8 @@ def alu_floor(variant, d, c, s, d_walked, pr=None):
             pr = 3 if s >= 4 else (2 if s == 3 else 1)
         T = d_walked ** pr
         maxes = conv_max_ops(d_walked, pr) if pr >= 3 else T // 2 + 1   # all-H vs all-E epilogue
+        if packed == 2:
+            maxes = maxes / 2.0                                              # u16x2 maxima serve two units
         per_word = 2 * (2 ** pr) * c / 4.0 + maxes
         return per_word / T, "alu", 64.0
     if variant in (3, 5):
@@ -169,7 +173,8 @@ VARIANT_NAMES = {0: "bin_int32", 1: "ld_int32", 2: "generic", 3: "bin_packed16",
                  6: "ld_pair16", 7: "bin_u8", 8: "ld_u8"}
 ALU_FLOOR_NOTE = {
     7: "per strategy: G*c/4 VABSDIFF4 (four |.|-accumulates each) + 1/2 VIMNMX3, ALU pipe (c columns, G = 1; L_2: 2)",
-    8: "per walked word: 2*2^PR*c/4 VABSDIFF4 + ceil((d^PR-1)/2) VIMNMX3 + 1 VIADDMNMX for d^PR strategies, ALU pipe",
+    8: ("per walked word: 2*2^PR*c/4 VABSDIFF4 + the subset convolution's three-input maxes (PR >= 3; all-E: "
+        "ceil((d^PR-1)/2) + 1) for d^PR strategies, ALU pipe; packed two-unit instances: half the maxes"),
 }
 
 
@@ -345,7 +350,7 @@ def main():
         peak_mhz = load_peak_clock()
         variant = st["variant"]
         per_strat, pipe, lanes = alu_floor(variant, d, cols, st["suffix_digits"], st["d"] if d > 1 else 2,
-                                           st.get("paired_rows"))
+                                           st.get("paired_rows"), st.get("packed_units", 0))
         dtype = {7: "u8x4", 8: "u8x4", 3: "int16x2", 4: "int16x2", 5: "int16x2", 6: "int16x2"}.get(variant, "int32")
         rank_steps = per_rank[0][3]
         roof = {"bound": "alu", "achieved": None, "peak": None, "unit": None, "frac": None, "traffic": None}

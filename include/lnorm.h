@@ -330,7 +330,7 @@ typedef struct {
   int32_t variant;             /* kernel variant id */
   int32_t block_threads, grid_blocks;
   int32_t paired_rows;         /* packed kernels: last rows evaluated for all labels per walked word (0: none) */
-  int32_t reserved;
+  int32_t packed_units;        /* L_3 / L_4 byte walk: 2 if two units per lane share 16-bit packed sums, else 0 */
 } lnorm_stats;
 int lnorm_last_stats(lnorm_stats* out);
 

@@ -54,7 +54,7 @@ class Stats(ctypes.Structure):
         ("units", ctypes.c_int64), ("units_total", ctypes.c_int64), ("steps", ctypes.c_double),
         ("column_updates", ctypes.c_double), ("walk_ms", ctypes.c_double), ("total_ms", ctypes.c_double),
         ("launches", ctypes.c_int32), ("variant", ctypes.c_int32), ("block_threads", ctypes.c_int32),
-        ("grid_blocks", ctypes.c_int32), ("paired_rows", ctypes.c_int32), ("reserved", ctypes.c_int32),
+        ("grid_blocks", ctypes.c_int32), ("paired_rows", ctypes.c_int32), ("packed_units", ctypes.c_int32),
     ]
 
     def as_dict(self):

@@ -720,7 +720,7 @@ int launch_walk(DevCtx& cx, const Problem& pr, const Plan& pl, WalkParams& wp, i
   wp.u8_lpu = pl.u8_lpu;
   wp.u8_pack_max = pr.fitsU16 ? 1 : 0;
   if (pl.kernel == K_LDPAIR16) per_block *= walk_ldpair16_units_per_lane(pr.dl, pr.c);
-  if (pl.kernel == K_LDU8) per_block *= walk_ldu8_units_per_lane(pr.dl, pr.c, pl.s);
+  if (pl.kernel == K_LDU8) per_block *= walk_ldu8_packed(pr.dl, pr.c, pl.s) ? 2 : walk_ldu8_units_per_lane(pr.dl, pr.c, pl.s);
   int64_t want = (wp.unit_count + per_block - 1) / per_block;
   int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)occ * cx.nsm, want));
   cudaError_t e;
@@ -975,6 +975,7 @@ int run_device(DevCtx& cx, const int32_t* dIn, const Problem& pr, int rank, int 
   S.walk_ms = wms; S.total_ms = tms; S.launches = launches; S.variant = pl.kernel;
   S.block_threads = block; S.grid_blocks = grid;
   S.paired_rows = pl.kernel == K_LDU8 ? walk_ldu8_paired_rows(pr.dl, pl.s) : (pl.kernel == K_U8 ? 1 : 0);
+  S.packed_units = pl.kernel == K_LDU8 && walk_ldu8_packed(pr.dl, pr.c, pl.s) ? 2 : 0;
   *st = S;
   return LNORM_OK;
 }
@@ -1652,6 +1653,7 @@ int lnorm_prefix_maxima(const int32_t* M, int32_t n, int32_t m, int32_t d, int32
   S.walk_ms = wms; S.total_ms = wms; S.launches = pl.kernel == K_GEN ? 1 : 2; S.variant = pl.kernel;
   S.block_threads = block; S.grid_blocks = grid;
   S.paired_rows = pl.kernel == K_LDU8 ? walk_ldu8_paired_rows(pr.dl, pl.s) : (pl.kernel == K_U8 ? 1 : 0);
+  S.packed_units = pl.kernel == K_LDU8 && walk_ldu8_packed(pr.dl, pr.c, pl.s) ? 2 : 0;
   g_stats = S;
   return LNORM_OK;
 }

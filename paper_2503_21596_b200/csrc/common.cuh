@@ -277,6 +277,9 @@ template <int D, int PART> cudaError_t walk_ldu8w_launch_part(const WalkParams& 
                                                               int pr);
 template <int D, int PART> int walk_ldu8w_occ_part(int NW, int pr, int s);
 template <int D, int PART> int walk_ldu8w_upl_part(int NW, int pr);
+template <int D, int PART> int walk_ldu8w_pk_part(int NW, int pr);
+// single-search L_3 / L_4 byte walks: 1 if the instance keeps two units per lane with packed sums
+int walk_ldu8_packed(int d, int c, int s);
 // Generic warp-per-unit walk (any mode, d, c, s).
 bool walk_generic_supported(int d, int c);
 cudaError_t walk_generic_launch(const WalkParams& p, int grid, cudaStream_t st, int* block_out);

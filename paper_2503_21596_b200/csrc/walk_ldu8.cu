@@ -45,6 +45,15 @@ void walk_ldu8_table_sizes(int d, int c, int k, int s, int64_t* tab_words, int64
   *init_ints = (int64_t)(k + 3) * 4 * NW + (int64_t)NW * (1 << pr) + (1 << pr) + (int64_t)(k + 3) * NW;
 }
 
+int walk_ldu8_packed(int d, int c, int s) {
+  const int NW = words_of(c), pt = part_of(NW);
+  if (const int wr = ldu8w_rows(d, s)) {
+    if (d == 4) return pt ? walk_ldu8w_pk_part<4, 1>(NW, wr) : walk_ldu8w_pk_part<4, 0>(NW, wr);
+    return pt ? walk_ldu8w_pk_part<3, 1>(NW, wr) : walk_ldu8w_pk_part<3, 0>(NW, wr);
+  }
+  return 0;
+}
+
 int walk_ldu8_units_per_lane(int d, int c, int s) {
   const int NW = words_of(c), pt = part_of(NW);
   if (const int wr = ldu8w_rows(d, s)) {

@@ -153,10 +153,11 @@ __device__ __forceinline__ int32_t w_max_tree(const int32_t (&v)[N]) {
 // every H, convolution value and strategy value is a partial sum of one labelling's value, which
 // is <= sum |M| <= 255 * 48 < 2^16 under the byte guard (every column's sum_x |M_xy| <= 255).
 // LN_LDU8W_PK_IMAD: the packed add as a 32-bit IMAD a * one + b (no half ever carries: both halves
-// stay below 2^16), which ptxas cannot fuse with the following max into an ALU-pipe VIADDMNMX
-// the way it fuses VIADD.16x2 -- the adds stay on the FMA-heavy pipe, the ALU does only maxima
+// stay below 2^16), which ptxas cannot fuse with the following max into an ALU-pipe VIADDMNMX.U16x2
+// the way it fuses VIADD.16x2.  Measured 2.5 % slower (24x24 L_3 5.90 vs 5.75 ms, 26x26 58.1 vs
+// 57.5 ms; profiles/r02/ab_l3_pk_imad.log): the fused form needs fewer issue slots, off by default
 #ifndef LN_LDU8W_PK_IMAD
-#define LN_LDU8W_PK_IMAD 1
+#define LN_LDU8W_PK_IMAD 0
 #endif
 template <bool PK>
 __device__ __forceinline__ int32_t op_add(int32_t a, int32_t b, uint32_t one) {
@@ -582,9 +583,12 @@ walk_ldu8w_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const i
 #ifndef LN_LDU8W_PK
 #define LN_LDU8W_PK 1
 #endif
+#ifndef LN_LDU8W_PK_MAXNW
+#define LN_LDU8W_PK_MAXNW 8
+#endif
 template <int D, int NW, int PR>
 __host__ __device__ constexpr bool w_has_pk() {
-  return LN_LDU8W_PK && NW <= 6 && ((D == 3 && PR == 5) || (D == 4 && PR == 4));
+  return LN_LDU8W_PK && NW <= LN_LDU8W_PK_MAXNW && ((D == 3 && PR == 5) || (D == 4 && PR == 4));
 }
 
 // The walk with two units per lane and packed H (see sums_pk / op_add): same units, chunks, Gray
@@ -732,6 +736,9 @@ int occ_w(int s) {
 template <int D, int NW, int PR>
 int upl_w() { return w_units<NW, PR>(); }
 
+template <int D, int NW, int PR>
+int pk_w() { return w_has_pk<D, NW, PR>() ? 1 : 0; }
+
 }  // namespace
 
 #ifdef LN_LDU8W_PART
@@ -777,6 +784,12 @@ template <>
 int walk_ldu8w_upl_part<LN_LDU8W_D, LN_LDU8W_PART>(int NW, int pr) {
   LN_LDU8W_PRS(upl_w)
   return 1;
+}
+
+template <>
+int walk_ldu8w_pk_part<LN_LDU8W_D, LN_LDU8W_PART>(int NW, int pr) {
+  LN_LDU8W_PRS(pk_w)
+  return 0;
 }
 
 template <>

@@ -22,10 +22,10 @@ import paper_2503_21596_b200 as L
 from paper_2503_21596_b200 import synth
 
 
-def roofline(steps_per_s, variant, d, c, s, d_walked, pr, nsm=148, mhz=1965.0):
+def roofline(steps_per_s, variant, d, c, s, d_walked, pr, packed=0, nsm=148, mhz=1965.0):
     """Fraction of the kernel family's binding-pipe floor (bench.alu_floor):
     floor instructions per strategy x strategies/s over lanes/clk/SM x SMs x f_max."""
-    per, pipe, lanes = bench.alu_floor(variant, d, c, s, d_walked, pr or None)
+    per, pipe, lanes = bench.alu_floor(variant, d, c, s, d_walked, pr or None, packed)
     if per is None:
         return None, None
     return per * steps_per_s / (lanes * nsm * mhz * 1e6), pipe
@@ -71,7 +71,7 @@ def run(n, m, d, seed, budget_s):
     cu = rate * updates_per_step
     st = L.last_stats()
     frac, pipe = roofline(rate, variant, d, plan["cols"], plan["suffix_digits"], st["d"] if d > 1 else 2,
-                          st["paired_rows"])
+                          st["paired_rows"], st.get("packed_units", 0))
     return {"config": f"L_{d} {n}x{m}", "n": n, "m": m, "d": d, "seed": seed, "kind": kind, "value": v,
             "kernel_variant": L.VARIANTS.get(variant, variant), "strategies": plan["steps"],
             "steps_per_s": rate, "column_updates_per_s": cu,
