@@ -548,3 +548,35 @@ def test_u8_merged_last_word(lib, c, marg):
     for u, gv in zip(units.tolist(), got):
         pre = [0] + [(u >> (k - x)) & 1 for x in range(1, k + 1)]
         assert gv == oracle.prefix_max(M, pre, with_marginals=marg)[0], (u, c, marg)
+
+
+def _rgs(length, d):
+    """Restricted-growth labellings of the given length in lexicographic order (independent of the library)."""
+    out = []
+
+    def rec(pre, mx):
+        if len(pre) == length:
+            out.append(list(pre))
+            return
+        for a in range(min(mx + 2, d)):
+            rec(pre + [a], max(mx, a))
+    rec([0], 0)
+    return out
+
+
+@pytest.mark.parametrize("d,n", [(3, 14), (4, 12)], ids=["L3", "L4"])
+@pytest.mark.parametrize("c", [4, 20, 24, 26, 32])
+def test_packed_two_unit_walk_every_unit(lib, d, n, c):
+    """The packed two-unit all-H walk (walk_ldu8w_impl.cuh, walk_ldu8w_pk_kernel: L_3 with five
+    paired rows, L_4 with four, up to 32 columns): both units of every lane -- the low and the high
+    16-bit half of every packed sum -- give the oracle's maximum for EVERY unit of the search."""
+    M = synth.random_matrix(n, c, 1700 + 10 * d + c)
+    k = 5
+    lst = _rgs(k + 1, d)
+    units = np.arange(len(lst), dtype=np.uint64)
+    got = lib.unit_maxima(M, k, units, d=d)
+    st = lib.last_stats()
+    assert st["variant"] == 8 and st["paired_rows"] == (5 if d == 3 else 4)
+    assert st["packed_units"] == 2
+    for i, gv in enumerate(got):
+        assert gv == oracle.prefix_max(M, lst[i], d=d)[0], (i, lst[i])

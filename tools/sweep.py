@@ -84,9 +84,10 @@ def main():
     ap.add_argument("--budget-s", type=float, default=20.0)
     ap.add_argument("--out", default=None)
     ap.add_argument("--wide-only", action="store_true", help="only the m = 4n L_1 rows")
+    ap.add_argument("--l3-only", action="store_true", help="only the L_3 rows (config 5b)")
     a = ap.parse_args()
     rows = []
-    for n in range(32, 49, 2):
+    for n in ([] if a.l3_only else range(32, 49, 2)):
         for m in ((4 * n,) if a.wide_only else (n, 4 * n)):
             rows.append(run(n, m, 1, 100 + n, a.budget_s))
             print(json.dumps(rows[-1]), flush=True)
