@@ -583,12 +583,16 @@ walk_ldu8w_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const i
 #ifndef LN_LDU8W_PK
 #define LN_LDU8W_PK 1
 #endif
+#ifndef LN_LDU8W_PK_PR4
+#define LN_LDU8W_PK_PR4 0            // L_3 with four paired rows (short suffixes: small searches)
+#endif
 #ifndef LN_LDU8W_PK_MAXNW
 #define LN_LDU8W_PK_MAXNW 8
 #endif
 template <int D, int NW, int PR>
 __host__ __device__ constexpr bool w_has_pk() {
-  return LN_LDU8W_PK && NW <= LN_LDU8W_PK_MAXNW && ((D == 3 && PR == 5) || (D == 4 && PR == 4));
+  return LN_LDU8W_PK && NW <= LN_LDU8W_PK_MAXNW &&
+         ((D == 3 && PR == 5) || (D == 4 && PR == 4) || (LN_LDU8W_PK_PR4 && D == 3 && PR == 4));
 }
 
 // The walk with two units per lane and packed H (see sums_pk / op_add): same units, chunks, Gray
