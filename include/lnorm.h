@@ -267,6 +267,19 @@ int lnorm_gray_change(int32_t d, uint64_t j, int32_t* digit, int32_t* from, int3
 int lnorm_partition(uint64_t C, int64_t T, int64_t t, int64_t* j_min, int64_t* j_max);
 
 /*
+ * The 8-byte reduction key every walk kernel, the grid-wide atomicMax and the
+ * multi-rank ncclAllReduce(max) combine (the same __host__ __device__ code as
+ * the kernels): high word = value with its sign bit flipped (unsigned order =
+ * signed order, negative L_marg values included), low word = 0xFFFFFFFF - unit,
+ * so the max over keys is the maximal value and, among equal values, the
+ * SMALLEST unit -- the one holding the lexicographically smallest optimum
+ * ("thread-wise maximal values are compared"; R2).
+ * lnorm_key_decode inverts it.  Host-only, no device needed.
+ */
+uint64_t lnorm_reduction_key(int32_t value, uint32_t unit);
+int lnorm_key_decode(uint64_t key, int32_t* value, uint32_t* unit);
+
+/*
  * Host-only planning (no device needed): the orientation, unit split and
  * kernel family lnorm_compute would use for this input on `world` ranks.
  * variant: 0 int32 binary walk, 1 int32 d-ary walk, 2 generic warp-per-unit,

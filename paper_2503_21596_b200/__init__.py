@@ -20,7 +20,7 @@ import numpy as np
 __all__ = [
     "LNormError", "load", "compute", "compute_device", "compute_reduced", "compute_batch", "compute_multi", "Comm",
     "compute_rank", "compute_rank_device", "torch_nccl_comm", "prefix_maxima", "unit_maxima",
-    "walk_trace", "imma_l1", "gray_digit", "gray_change", "partition", "last_stats", "status_string", "SYMBOLS", "plan",
+    "walk_trace", "imma_l1", "gray_digit", "gray_change", "partition", "reduction_key", "key_decode", "last_stats", "status_string", "SYMBOLS", "plan",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -32,6 +32,7 @@ SYMBOLS = [
     "lnorm_comm_unique_id", "lnorm_comm_create", "lnorm_comm_nccl", "lnorm_comm_destroy", "lnorm_compute_rank",
     "lnorm_compute_rank_device",
     "lnorm_prefix_maxima", "lnorm_unit_maxima", "lnorm_walk_trace", "lnorm_gray_digit", "lnorm_gray_change", "lnorm_partition",
+    "lnorm_reduction_key", "lnorm_key_decode",
     "lnorm_last_stats", "lnorm_plan", "lnorm_compute_sliced", "lnorm_compute_reduced", "lnorm_compute_batch",
     "lnorm_compute_checkpointed", "lnorm_imma_l1",
 ]
@@ -111,6 +112,8 @@ def load():
             "lnorm_gray_digit": ([i32, i32, u64], i32),
             "lnorm_gray_change": ([i32, u64, i32p, i32p, i32p], ctypes.c_int),
             "lnorm_partition": ([u64, i64, i64, i64p, i64p], ctypes.c_int),
+            "lnorm_reduction_key": ([i32, ctypes.c_uint32], u64),
+            "lnorm_key_decode": ([u64, i32p, P(ctypes.c_uint32)], ctypes.c_int),
             "lnorm_last_stats": ([P(Stats)], ctypes.c_int),
             "lnorm_compute_checkpointed": ([i32p, i32, i32, i32, i32, ctypes.c_char_p, i64, i32, i64p, i8p, i32p, i64p],
                                            ctypes.c_int),
@@ -432,6 +435,17 @@ def gray_change(d: int, j: int):
     a, b, c = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
     _check(load().lnorm_gray_change(d, j, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)), "lnorm_gray_change")
     return a.value, b.value, c.value
+
+
+def reduction_key(value: int, unit: int) -> int:
+    """The library's 8-byte max-reduction key (lnorm_reduction_key; csrc/common.cuh make_key)."""
+    return int(load().lnorm_reduction_key(value, unit))
+
+
+def key_decode(key: int):
+    v, u = ctypes.c_int32(), ctypes.c_uint32()
+    _check(load().lnorm_key_decode(key, ctypes.byref(v), ctypes.byref(u)), "lnorm_key_decode")
+    return v.value, u.value
 
 
 def partition(C: int, T: int, t: int):

@@ -1760,6 +1760,15 @@ int lnorm_partition(uint64_t C, int64_t T, int64_t t, int64_t* j_min, int64_t* j
   return LNORM_OK;
 }
 
+uint64_t lnorm_reduction_key(int32_t value, uint32_t unit) { return make_key(value, unit); }
+
+int lnorm_key_decode(uint64_t key, int32_t* value, uint32_t* unit) {
+  if (!value || !unit) return LNORM_EINVAL;
+  *value = key_value(key);
+  *unit = key_unit(key);
+  return LNORM_OK;
+}
+
 int lnorm_plan(const int32_t* M, int32_t n, int32_t m, int32_t d, int32_t with_marginals, int32_t world,
                lnorm_plan_info* out) {
   if (!out || world < 1) return LNORM_EINVAL;

@@ -3,11 +3,12 @@
 The N-GPU path shards the unit list with Algorithm 1 (PAPER.md:235-251,
 the library's lnorm_partition) and combines ranks with ONE max all-reduce of
 the 8-byte key (value biased to unsigned order in the high word, ~unit in the
-low word, csrc/common.cuh make_key).  Here each rank evaluates its slice's
-per-prefix maxima with the CPU oracle (the GPU is not needed for the
-decomposition logic), packs the key exactly as documented, and the gloo
-all-reduce must yield the global maximum and the SMALLEST unit attaining it
--- the unit that holds the lexicographically smallest optimum.
+low word: the library's lnorm_reduction_key, the kernels' make_key).  Here each
+rank evaluates its slice's per-prefix maxima with the CPU oracle (the GPU is not
+needed for the decomposition logic), packs them with the LIBRARY's key (checked
+against the documented layout), and the gloo all-reduce must yield the global
+maximum and the SMALLEST unit attaining it -- the unit that holds the
+lexicographically smallest optimum.
 """
 import os
 import socket
@@ -52,12 +53,14 @@ def _worker(rank, world, port, case, q):
     for u in range(lo, hi + 1):
         prefix = [0] + [(u >> (k - x)) & 1 for x in range(1, k + 1)]
         v, _ = oracle.prefix_max(M, prefix, d=1, with_marginals=marg)
-        key = pack_key(v, u)
+        key = L.reduction_key(v, u)          # the library's own key (csrc/common.cuh make_key)
+        assert key == pack_key(v, u)         # ... equal to the documented layout
         best = key if best is None or key > best else best
     # order-preserving u64 -> i64 map (flip the top bit) so gloo's int64 MAX reduces the key
     t = torch.tensor([best - (1 << 63)], dtype=torch.int64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     key = t.item() + (1 << 63)
+    assert L.key_decode(key) == unpack_key(key)
     if rank == 0:
         q.put((unpack_key(key), (lo, hi)))
     dist.barrier()
@@ -97,3 +100,17 @@ def test_partition_covers_units_for_every_world_size():
                 assert c == b + 1
             sizes = [b - a + 1 for a, b in rngs]
             assert max(sizes) - min(sizes) <= 1
+
+
+def test_library_reduction_key_order():
+    """lnorm_reduction_key (the kernels' make_key, host side): unsigned key order = (value, then the
+    SMALLER unit) for negative and positive values; lnorm_key_decode inverts it."""
+    import paper_2503_21596_b200 as L
+    vals = [-(2 ** 31), -5, -1, 0, 1, 17, 2 ** 31 - 1]
+    units = [0, 1, 7, 2 ** 32 - 1]
+    keys = {(v, u): L.reduction_key(v, u) for v in vals for u in units}
+    for (v, u), k in keys.items():
+        assert L.key_decode(k) == (v, u)
+        assert k == pack_key(v, u)
+    order = sorted(keys, key=lambda vu: keys[vu])
+    assert order == sorted(keys, key=lambda vu: (vu[0], -vu[1]))
