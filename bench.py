@@ -41,6 +41,7 @@ CONFIGS = {
     # config-5 sweep points used for profiles (not the headline)
     "l3_26x26": (26, 26, 3, False, 226, "L_3 of a random 26x26 matrix, entries in [-10,10], seed 226 (config 5b top)"),
     "l4_18x18": (18, 18, 4, False, 218, "L_4 of a random 18x18 matrix, entries in [-10,10], seed 218 (P:371)"),
+    "l4_22x22": (22, 22, 4, False, 222, "L_4 of a random 22x22 matrix, entries in [-10,10], seed 222 (a search long enough for the kernel's own rate)"),
     "l1_36x144": (36, 144, 1, False, 136, "L_1 of a random 36x144 matrix, entries in [-10,10], seed 136 (config 5a, m = 4n)"),
     "l1_40x160": (40, 160, 1, False, 140, "L_1 of a random 40x160 matrix, entries in [-10,10], seed 140 (config 5a, m = 4n)"),
 }
