@@ -580,3 +580,27 @@ def test_packed_two_unit_walk_every_unit(lib, d, n, c):
     assert st["packed_units"] == 2
     for i, gv in enumerate(got):
         assert gv == oracle.prefix_max(M, lst[i], d=d)[0], (i, lst[i])
+
+
+@pytest.mark.parametrize("d,n", [(3, 20), (4, 18)], ids=["L3_20x20", "L4_18x18"])
+def test_packed_walk_sliced_and_checkpointed(lib, tmp_path, d, n):
+    """The packed two-unit walk under Algorithm-1 slices (2/3/8 virtual ranks: slices start and end
+    inside a 64-unit chunk) and under checkpoint chunks of an odd unit count: bit-identical value and
+    argmax to the one-shot search, whose argmax attains the value (from-scratch oracle evaluation);
+    the one-shot search itself is checked against the oracle per sampled prefix in test_gpu_fullsize."""
+    M = synth.random_matrix(n, n, 4_200 + n + d)
+    v, arg = lib.compute(M, d=d)
+    assert lib.last_stats()["packed_units"] == 2
+    assert oracle.value(M, arg, d=d) == v
+    for slices in (2, 3, 8):
+        got = lib.compute_sliced(M, slices, d=d)
+        assert got[0] == v and list(got[1]) == list(arg), slices
+    units = lib.plan(M, d=d)["units"]
+    path = str(tmp_path / "ck.bin")
+    chunk = units // 5 + 33
+    while True:
+        done, cv, carg, _ = lib.compute_checkpointed(M, path, d=d, chunk_units=chunk, max_chunks=1)
+        if done:
+            break
+        assert cv <= v
+    assert cv == v and list(carg) == list(arg)
