@@ -586,6 +586,9 @@ walk_ldu8w_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const i
 #ifndef LN_LDU8W_PK_PR4
 #define LN_LDU8W_PK_PR4 0            // L_3 with four paired rows (short suffixes: small searches)
 #endif
+#ifndef LN_LDU8W_PK_BAT
+#define LN_LDU8W_PK_BAT 1
+#endif
 #ifndef LN_LDU8W_PK_MAXNW
 #define LN_LDU8W_PK_MAXNW 8
 #endif
@@ -598,7 +601,13 @@ __host__ __device__ constexpr bool w_has_pk() {
 // The walk with two units per lane and packed H (see sums_pk / op_add): same units, chunks, Gray
 // control and reduction key as walk_ldu8w_kernel; a chunk is 64 consecutive units (unit j of lane l
 // = chunk base + 32 j + l).
+// batched packed instances (f3, up to 24 columns): L_3 with four or five paired rows, L_4 with four
 template <int D, int NW, int PR>
+__host__ __device__ constexpr bool w_has_pk_bat() {
+  return LN_LDU8W_PK && LN_LDU8W_PK_BAT && NW <= 6 && ((D == 3 && (PR == 5 || PR == 4)) || (D == 4 && PR == 4));
+}
+
+template <int D, int NW, int PR, bool BAT = false>
 __global__ void __launch_bounds__(kBlockW, (w_minb<D, NW, PR>()))
 walk_ldu8w_pk_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int32_t* __restrict__ gInit) {
   using WK = LdW<D, NW, PR, true>;
@@ -613,32 +622,56 @@ walk_ldu8w_pk_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, cons
   const uint32_t k16 = p.one << 16;
   uint32_t nwords = 1;
   for (int i = 0; i < sw; ++i) nwords *= D;
-  {
-    const uint32_t* biasRec = reinterpret_cast<const uint32_t*>(gInit + (p.k + 3) * CW);
-    for (int i = lane; i < sw * RD; i += 32) sT[i] = gTab[i];
+  // matrix mb's delta table, set-major bias words and kappa sums -> shared memory
+  auto stage = [&](int mb) {
+    __syncwarp();
+    const uint32_t* biasRec = reinterpret_cast<const uint32_t*>(gInit + mb * p.init_stride + (p.k + 3) * CW);
+    const uint32_t* src = gTab + mb * p.tab_stride;
+    for (int i = lane; i < sw * RD; i += 32) sT[i] = src[i];
     for (int i = lane; i < NS * RW; i += 32) {
       const int m = i / RW, q = i % RW;
       sBias[i] = q < NW ? biasRec[m * NW + q] : 0u;
     }
     for (int m = lane; m < NS; m += 32) sBias[NS * RW + m] = biasRec[NS * NW + m];
     __syncwarp();
-  }
+  };
   int32_t best_all = INT32_MIN;
   uint32_t best_u = 0;
   bool have = false;
-  const int64_t nchunks = (p.units_per + 32 * P - 1) / (32 * P);
+  // BAT (batched launches): chunk ch -> matrix ch / CPM, as walk_ldu8w_kernel
+  const int64_t CPM = (p.units_per + 32 * P - 1) / (32 * P);
+  const int64_t nchunks = BAT ? CPM * p.batch : CPM;
+  int cur_b = BAT ? -1 : 0;
+  if constexpr (!BAT) stage(0);
   for (int64_t ch = blockIdx.x; ch < nchunks; ch = next_chunk(ch, p.chunk_ctr, lane)) {
+    int64_t lc = ch;
+    const int32_t* gI = gInit;
+    if constexpr (BAT) {
+      const int mb = (int)(ch / CPM);
+      lc = ch - (int64_t)mb * CPM;
+      gI = gInit + mb * p.init_stride;
+      if (mb != cur_b) {
+        if (cur_b >= 0) {                          // flush the previous matrix's key
+          unsigned long long key = have ? make_key(best_all, best_u) : 0ull;
+          key = warp_max_u64(key);
+          if (lane == 0 && key) atomicMax(p.key + cur_b, key);
+          best_all = INT32_MIN; have = false;
+        }
+        stage(mb);
+        cur_b = mb;
+      }
+    }
     uint32_t A[P][D][NW];
     int32_t H[NS][D];
 #pragma unroll
     for (int j = 0; j < P; ++j) {
-      const int64_t rel = ch * 32 * P + j * 32 + lane;
+      const int64_t rel = lc * 32 * P + j * 32 + lane;
       const int64_t u = p.unit_begin + (rel < p.units_per ? rel : 0);
       uint64_t lab = 0;
       if (p.prefix_table) lab = p.prefix_table[u - p.unit_begin];
       else for (int x = 0; x <= p.k; ++x) lab |= (uint64_t)prefix_digit(p, u, x) << (p.pbits * x);
       const uint64_t lmask = (1ull << p.pbits) - 1ull;
-      const uint32_t* pkRec = reinterpret_cast<const uint32_t*>(gInit + (p.k + 3) * CW) + NS * NW + NS;
+      const uint32_t* pkRec = reinterpret_cast<const uint32_t*>(gI + (p.k + 3) * CW) + NS * NW + NS;
       const uint32_t* stRec = pkRec + (p.k + 1) * NW;
 #pragma unroll
       for (int q = 0; q < NW; ++q) {
@@ -690,7 +723,7 @@ walk_ldu8w_pk_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, cons
     }
 #pragma unroll
     for (int j = 0; j < P; ++j) {
-      const int64_t rel = ch * 32 * P + j * 32 + lane;
+      const int64_t rel = lc * 32 * P + j * 32 + lane;
       const int32_t bj = (int32_t)(j == 0 ? ((uint32_t)best & 0xFFFFu) : ((uint32_t)best >> 16));
       if (rel < p.units_per) {
         if (p.unit_max) p.unit_max[rel] = bj;
@@ -700,7 +733,7 @@ walk_ldu8w_pk_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, cons
   }
   unsigned long long key = have ? make_key(best_all, best_u) : 0ull;
   key = warp_max_u64(key);
-  if (lane == 0 && key) atomicMax(p.key, key);
+  if (lane == 0 && key) atomicMax(p.key + (BAT && cur_b > 0 ? cur_b : 0), key);
 }
 
 template <int NW, int PR>
@@ -710,6 +743,12 @@ template <int D, int NW, int PR>
 cudaError_t launch_w(const WalkParams& p, const uint32_t* tab, const int32_t* init, int grid, cudaStream_t st) {
   const size_t sm = w_smem<NW, PR>(p.s);
   if (p.batch > 1) {                     // batched instances: <= 24 columns (the small-matrix regime)
+    if constexpr (w_has_pk_bat<D, NW, PR>()) {
+      cudaError_t e = ensure_dyn_smem((const void*)walk_ldu8w_pk_kernel<D, NW, PR, true>, sm);
+      if (e != cudaSuccess) return e;
+      walk_ldu8w_pk_kernel<D, NW, PR, true><<<grid, kBlockW, sm, st>>>(p, tab, init);
+      return cudaGetLastError();
+    }
     if constexpr (NW <= 6) {
       cudaError_t e = ensure_dyn_smem((const void*)walk_ldu8w_kernel<D, NW, PR, true>, sm);
       if (e != cudaSuccess) return e;
