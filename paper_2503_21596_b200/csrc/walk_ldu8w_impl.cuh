@@ -159,17 +159,22 @@ __device__ __forceinline__ int32_t w_max_tree(const int32_t (&v)[N]) {
 #ifndef LN_LDU8W_PK_IMAD
 #define LN_LDU8W_PK_IMAD 0
 #endif
-template <bool PK>
+// LN_LDU8W_PK_IMAD_LV: bit l-1 set = the adds of convolution level l (1: G_2 from H, 2: L_4's G_3,
+// 3: the last step) use the unfusable IMAD form (A/B knob; LN_LDU8W_PK_IMAD = all levels)
+#ifndef LN_LDU8W_PK_IMAD_LV
+#define LN_LDU8W_PK_IMAD_LV (LN_LDU8W_PK_IMAD ? 7 : 0)
+#endif
+template <bool PK, int LV = 1>
 __device__ __forceinline__ int32_t op_add(int32_t a, int32_t b, uint32_t one) {
   if constexpr (PK) {
-#if LN_LDU8W_PK_IMAD
-    uint32_t r;
-    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"((uint32_t)a), "r"(one), "r"((uint32_t)b));
-    return (int32_t)r;
-#else
-    (void)one;
-    return (int32_t)__vadd2((uint32_t)a, (uint32_t)b);
-#endif
+    if constexpr (((LN_LDU8W_PK_IMAD_LV >> (LV - 1)) & 1) != 0) {
+      uint32_t r;
+      asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"((uint32_t)a), "r"(one), "r"((uint32_t)b));
+      return (int32_t)r;
+    } else {
+      (void)one;
+      return (int32_t)__vadd2((uint32_t)a, (uint32_t)b);
+    }
   } else {
     return w_fadd(a, b, one);
   }
@@ -250,7 +255,7 @@ struct LdW {
   template <int U, int I>
   static __device__ __forceinline__ int32_t term2(const int32_t (&H)[NS][D], const int32_t (&g2)[NS], uint32_t one) {
     constexpr int T = std::integral_constant<int, w_submask(U, I)>::value;
-    return op_add<PK>(H[T][2], g2[U ^ T], one);
+    return op_add<PK, 2>(H[T][2], g2[U ^ T], one);
   }
   template <int U, int... Is>
   static __device__ __forceinline__ int32_t L2(const int32_t (&H)[NS][D], const int32_t (&g2)[NS], uint32_t one,
@@ -264,8 +269,8 @@ struct LdW {
   template <int T>
   static __device__ __forceinline__ int32_t last(const int32_t (&H)[NS][D], const int32_t (&g2)[NS], uint32_t one) {
     constexpr int U = (NS - 1) ^ T;
-    if constexpr (D == 3) return op_add<PK>(H[T][2], G2<U>(H, one), one);
-    else return op_add<PK>(H[T][3], L2<U>(H, g2, one, std::make_integer_sequence<int, (1 << w_popc(U))>{}), one);
+    if constexpr (D == 3) return op_add<PK, 3>(H[T][2], G2<U>(H, one), one);
+    else return op_add<PK, 3>(H[T][3], L2<U>(H, g2, one, std::make_integer_sequence<int, (1 << w_popc(U))>{}), one);
   }
   template <int... Us>
   static __device__ __forceinline__ void fill_g2(const int32_t (&H)[NS][D], int32_t (&g2)[NS], uint32_t one,
