@@ -265,7 +265,19 @@ struct U8Step {
         }
       }
     }
-    if (PK) {
+    if constexpr (PK && LPU == 2) {
+      // lane pairs (PKL): the unit's two strategy values (paired row +/-) as u16 halves -> ONE SHFL and
+      // one packed add join the two lanes' partial sums, one VIMNMX.U16x2 keeps both running maxima
+      static_assert(PR == 1 && MODE == MODE_L1 && G == 1, "packed lane-pair join");
+      const uint32_t k16 = one << 16;
+#pragma unroll
+      for (int j = 0; j < P; ++j) {
+        uint32_t w;
+        asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(w) : "r"(hs[j][1][0]), "r"(k16), "r"(hs[j][0][0]));
+        w += __shfl_xor_sync(0xffffffffu, w, 1);     // halves never carry: each is <= sum |M| <= 65535
+        best[j] = (int32_t)__vmaxu2((uint32_t)best[j], w);
+      }
+    } else if constexpr (PK) {
       static_assert(!PK || (PR == 1 && LPU == 1 && P % 2 == 0 && MODE != MODE_MARG), "packed maxima");
       const uint32_t k16 = one << 16;                 // 65536 from a kernel parameter: IMAD, not LEA
 #pragma unroll
@@ -501,7 +513,8 @@ walk_u8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int3
           if (G == 2) acc = sad4(A[j][q], B[h * G * NWL + NWL + q], acc);
         }
         if (LPU == 2) acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-        v0 = h == 0 ? (int32_t)acc : max(v0, (int32_t)acc);
+        if constexpr (PK && LPU == 2) v0 = h == 0 ? (int32_t)acc : (int32_t)((uint32_t)v0 | (acc << 16));
+        else v0 = h == 0 ? (int32_t)acc : max(v0, (int32_t)acc);
       }
       best[j] = v0;
     }
@@ -514,7 +527,7 @@ walk_u8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int3
 #pragma unroll
       for (int j = 0; j < P; j += 2) A[j][NWL - 1] = (A[j][NWL - 1] & 0xFFFFu) | (A[j + 1][NWL - 1] << 16);
     }
-    if constexpr (PK) {                                // two units' maxima per register (lo: unit 2i)
+    if constexpr (PK && LPU == 1) {                    // two units' maxima per register (lo: unit 2i)
 #pragma unroll
       for (int i = 0; i < P / 2; ++i) best[i] = (int32_t)(((uint32_t)best[2 * i + 1] << 16) | (uint32_t)best[2 * i]);
     }
@@ -552,13 +565,16 @@ walk_u8_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const int3
 #endif
       }
     }
-    if constexpr (PK) {                                // unpack (back to front: slot i holds units 2i, 2i+1)
+    if constexpr (PK && LPU == 1) {                    // unpack (back to front: slot i holds units 2i, 2i+1)
 #pragma unroll
       for (int i = P / 2 - 1; i >= 0; --i) {
         const uint32_t w = (uint32_t)best[i];
         best[2 * i + 1] = (int32_t)(w >> 16);
         best[2 * i] = (int32_t)(w & 0xFFFFu);
       }
+    } else if constexpr (PK) {                         // lane pairs: the max of the two signs' maxima
+#pragma unroll
+      for (int j = 0; j < P; ++j) best[j] = (int32_t)max((uint32_t)best[j] & 0xFFFFu, (uint32_t)best[j] >> 16);
     }
 #pragma unroll
     for (int j = 0; j < P; ++j) {
@@ -638,6 +654,12 @@ constexpr int kU8BatchMaxNW = 8;
 #define LN_U8_PACKMAX 0
 #endif
 constexpr int kU8PackMaxNW = LN_U8_PACKMAX ? 16 : 0;
+// packed lane-pair join (U8Step PK with LPU = 2, L_1 wide rows with sum |M| <= 65535): one SHFL and
+// one VIMNMX.U16x2 per unit instead of two SHFL + two VIADDMNMX.  Measured 1 % slower on 36x144
+// (81.7 vs 80.9 ms) and 2 % on 40x160 (1439 vs 1411 ms; profiles/r02/ab_u8_pkl.log): off
+#ifndef LN_U8_PKL
+#define LN_U8_PKL 0
+#endif
 
 // merged-last-word instances (MRG): 33-48 columns (the m = n sweep and the 42x42 headline)
 template <int MODE, int NW, int LPU>
@@ -667,6 +689,14 @@ cudaError_t launch_u8_l(const WalkParams& p, const uint32_t* tab, const int32_t*
       return cudaGetLastError();
     }
     return cudaErrorInvalidValue;
+  }
+  if constexpr (MODE == MODE_L1 && LPU == 2 && LN_U8_PKL) {
+    if (p.u8_pack_max) {                 // every value <= sum |M| <= 65535 (host): packed lane-pair join
+      cudaError_t e = ensure_dyn_smem((const void*)walk_u8_kernel<MODE, NW, P, LPU, false, true>, sm);
+      if (e != cudaSuccess) return e;
+      walk_u8_kernel<MODE, NW, P, LPU, false, true><<<grid, kBlockU8, sm, st>>>(p, tab, init);
+      return cudaGetLastError();
+    }
   }
   if constexpr (MODE != MODE_MARG && LPU == 1 && P % 2 == 0 && NW <= kU8PackMaxNW && u8_pr<MODE>() == 1) {
     if (p.u8_pack_max) {                 // every value <= sum |M| <= 65535 (host): packed maxima
