@@ -591,6 +591,9 @@ walk_ldu8w_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const i
 #ifndef LN_LDU8W_PK_PR4
 #define LN_LDU8W_PK_PR4 0            // L_3 with four paired rows (short suffixes: small searches)
 #endif
+#ifndef LN_LDU8W_PK_L4PR3
+#define LN_LDU8W_PK_L4PR3 1          // L_4 with three paired rows (short suffixes, batches of small matrices)
+#endif
 #ifndef LN_LDU8W_PK_BAT
 #define LN_LDU8W_PK_BAT 1
 #endif
@@ -600,7 +603,8 @@ walk_ldu8w_kernel(const WalkParams p, const uint32_t* __restrict__ gTab, const i
 template <int D, int NW, int PR>
 __host__ __device__ constexpr bool w_has_pk() {
   return LN_LDU8W_PK && NW <= LN_LDU8W_PK_MAXNW &&
-         ((D == 3 && PR == 5) || (D == 4 && PR == 4) || (LN_LDU8W_PK_PR4 && D == 3 && PR == 4));
+         ((D == 3 && PR == 5) || (D == 4 && PR == 4) || (LN_LDU8W_PK_PR4 && D == 3 && PR == 4) ||
+          (LN_LDU8W_PK_L4PR3 && D == 4 && PR == 3));
 }
 
 // The walk with two units per lane and packed H (see sums_pk / op_add): same units, chunks, Gray
@@ -609,7 +613,8 @@ __host__ __device__ constexpr bool w_has_pk() {
 // batched packed instances (f3, up to 24 columns): L_3 with four or five paired rows, L_4 with four
 template <int D, int NW, int PR>
 __host__ __device__ constexpr bool w_has_pk_bat() {
-  return LN_LDU8W_PK && LN_LDU8W_PK_BAT && NW <= 6 && ((D == 3 && (PR == 5 || PR == 4)) || (D == 4 && PR == 4));
+  return LN_LDU8W_PK && LN_LDU8W_PK_BAT && NW <= 6 &&
+         ((D == 3 && (PR == 5 || PR == 4)) || (D == 4 && (PR == 4 || (LN_LDU8W_PK_L4PR3 && PR == 3))));
 }
 
 template <int D, int NW, int PR, bool BAT = false>
